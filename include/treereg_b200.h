@@ -1,0 +1,211 @@
+/* treereg_b200.h — C-ABI of the B200-native HGMR hot path.
+ *
+ * Drop-in boundary for the reference's C++ hot-path API (namespace treereg,
+ * /root/reference/proj/core/include/treereg/*.hpp).  Each entry point below
+ * names the reference declaration it replaces.  Plain pointers and sizes
+ * only; all 3x3 matrices are ROW-MAJOR (the C++ adapter converts from
+ * Eigen's column-major).  Every function returns a trg_status; the detail
+ * string of the last failure on the calling thread is trg_last_error().
+ * There is no CPU fallback: without a CUDA device every compute call
+ * returns TRG_ECUDA.
+ *
+ * Error mapping: the reference's exception types map to
+ *   std::invalid_argument      -> TRG_EINVAL
+ *   std::domain_error          -> TRG_EDOMAIN
+ *   std::runtime_error         -> TRG_ERUNTIME
+ *   std::out_of_range          -> TRG_ERANGE
+ *   DegenerateGeometryError    -> TRG_EDEGENERATE  (mstep.hpp:14-16)
+ * and the adapter rethrows the same types. */
+#ifndef TREEREG_B200_H
+#define TREEREG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TRG_OK = 0,
+  TRG_EINVAL = 1,
+  TRG_EDOMAIN = 2,
+  TRG_ERUNTIME = 3,
+  TRG_ERANGE = 4,
+  TRG_EDEGENERATE = 5,
+  TRG_ECUDA = 6,
+  TRG_ENCCL = 7
+} trg_status;
+
+typedef struct trg_ctx trg_ctx;           /* device, stream, workspace arena */
+typedef struct trg_tree_dev trg_tree_dev; /* device-resident GMM tree */
+
+/* treereg::ModelConfig, gmm.hpp:34-41 */
+typedef struct {
+  int em_iterations_per_node;        /* 8 */
+  size_t min_points_per_node;        /* 32 */
+  double cov_regularization_epsilon; /* 1e-4 */
+  double cov_regularization_absolute;/* 1e-12 */
+  uint64_t rng_seed;                 /* 0 (flat GMM only) */
+  int max_level;                     /* 3 */
+} trg_model_config;
+
+/* treereg::AssocConfig, association.hpp:34-40 */
+typedef struct {
+  double lambda_c;      /* 0.01, in [0, 1/3] */
+  int max_level;        /* 0 = full tree depth */
+  double outlier_floor; /* 1e-300 */
+  int deterministic;    /* kept for interface parity; always deterministic */
+} trg_assoc_config;
+
+/* treereg::Variant::Kind, registration.hpp:19-20 */
+enum { TRG_VARIANT_ADAPTIVE = 0, TRG_VARIANT_TREE = 1 };
+
+/* treereg::RegistrationConfig, registration.hpp:27-36 */
+typedef struct {
+  int variant_kind;        /* TRG_VARIANT_ADAPTIVE | TRG_VARIANT_TREE */
+  int variant_param;       /* tree depth L */
+  double lambda_c;         /* 0.01 */
+  int max_em_iterations;   /* 50 */
+  double rotation_tol;     /* 1e-5 rad */
+  double translation_tol;  /* 1e-5 (fraction of target bbox diagonal) */
+  double initial_R[9];     /* identity */
+  double initial_t[3];     /* zero */
+  trg_model_config model_config;
+} trg_reg_config;
+
+/* Host-side tree: treereg::GmmTree (gmm.hpp:56-67) + cached eigen data of
+ * each GaussianComponent (gmm.hpp:12-23).  Arrays are caller-allocated with
+ * `capacity` >= trg_tree_capacity(max_level) nodes. */
+typedef struct {
+  int n_nodes, max_level, capacity;
+  double* weight;   /* [J] */
+  double* mean;     /* [J*3] */
+  double* cov;      /* [J*9] row-major */
+  double* lambdas;  /* [J*3] descending */
+  double* axes;     /* [J*9] row-major; column l = unit axis for lambdas[l] */
+  double* log_norm; /* [J] */
+  int* parent;      /* [J] -1 for level 0 */
+  int* first_child; /* [J] -1 for leaves */
+  int* child_count; /* [J] */
+  int* level;       /* [J] */
+} trg_tree;
+
+/* treereg::MomentSet, association.hpp:14-32 (m1 [J*3], m2 [J*9] or NULL) */
+typedef struct {
+  double* m0;
+  double* m1;
+  double* m2;
+  uint64_t total_points;
+  uint64_t outliers;
+  uint64_t density_evaluations;
+  double total_mass;
+} trg_moments;
+
+/* treereg::BuildDiagnostics (gmm.hpp:43-49) + the device counters that
+ * define the roofline bytes. */
+typedef struct {
+  uint64_t entries_per_round[8]; /* E_l */
+  int expanded_per_round[8];
+  int calibration_passes;
+  double calibration_drift;
+  uint64_t calib_density_evaluations;
+} trg_build_diag;
+
+/* treereg::MStepSolution, mstep.hpp:54-61 */
+typedef struct {
+  double omega[3];
+  double translation[3];
+  double delta_R[9];
+  double delta_t[3];
+  double criterion_before;
+  double criterion_after;
+  double condition_estimate;
+  int n_virtual_points;
+} trg_mstep_solution;
+
+/* treereg::RegistrationResult, registration.hpp:38-48.  Trace arrays are
+ * caller-allocated with `trace_capacity` >= max_em_iterations (or NULL). */
+typedef struct {
+  double R[9];
+  double t[3];
+  int iterations;
+  int converged;
+  double* criterion_trace;
+  double* criterion_after_trace;
+  uint64_t* eval_counts;
+  int trace_capacity;
+  double model_build_seconds;
+  double em_seconds;
+  size_t model_components;
+} trg_reg_result;
+
+/* ---- context ---------------------------------------------------------- */
+int trg_ctx_create(int device, trg_ctx** out);
+int trg_ctx_destroy(trg_ctx* ctx);
+const char* trg_last_error(void);
+int trg_device_sms(trg_ctx* ctx);
+/* Launch count of this library's kernels since ctx creation (bench evidence). */
+uint64_t trg_kernel_launches(trg_ctx* ctx);
+/* CUDA stream (cudaStream_t) all work of this context is ordered on. */
+void* trg_ctx_stream(trg_ctx* ctx);
+
+/* ---- model ------------------------------------------------------------ */
+int trg_tree_capacity(int max_level);
+/* Upload a host tree (e.g. a load_tree() result, gmm.cpp:798-896). */
+int trg_tree_upload(trg_ctx* ctx, const trg_tree* host, trg_tree_dev** out);
+int trg_tree_download(trg_ctx* ctx, const trg_tree_dev* tree, trg_tree* host);
+int trg_tree_free(trg_ctx* ctx, trg_tree_dev* tree);
+int trg_tree_size(const trg_tree_dev* tree);
+
+/* treereg::build_tree (gmm.hpp:69-70).  `xyz` is N*3 AoS doubles on the host
+ * (xyz_on_device = 0) or in device memory (1). */
+int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz_on_device,
+                   const trg_model_config* cfg, trg_tree_dev** out, trg_build_diag* diag);
+
+/* ---- E-step ----------------------------------------------------------- */
+/* treereg::associate_adaptive (association.hpp:54-56).  Moments are written
+ * to host memory.  point_node / point_weight (nullable, host, [N]) receive
+ * each point's deposit node (-1 = outlier) and path weight. */
+int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, size_t n,
+                  int xyz_on_device, const double R[9], const double t[3],
+                  const trg_assoc_config* cfg, trg_moments* out, int* point_node,
+                  double* point_weight);
+
+/* ---- M-step ----------------------------------------------------------- */
+/* treereg::make_virtual_points + treereg::solve_mstep (mstep.hpp:46-47, 67)
+ * on a host MomentSet (m0 [J], m1 [J*3]).  Returns TRG_EDEGENERATE where
+ * the reference throws DegenerateGeometryError. */
+int trg_solve_mstep(trg_ctx* ctx, const trg_tree_dev* tree, const double* m0, const double* m1,
+                    uint64_t total_points, trg_mstep_solution* out);
+
+/* ---- driver ----------------------------------------------------------- */
+/* treereg::register_with_tree (registration.hpp:59-62). */
+int trg_register_with_tree(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, size_t n,
+                           int xyz_on_device, const trg_reg_config* cfg, double target_diag,
+                           trg_reg_result* out);
+/* treereg::register_clouds (registration.hpp:53-55), adaptive:L / tree:L. */
+int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target, const double* source,
+                        size_t n_source, int on_device, const trg_reg_config* cfg,
+                        trg_reg_result* out);
+
+/* ---- host-side data (synthetic inputs; the reference's generators,
+ *      synthetic.cpp / cloud_io.cpp, restated + the new Kinect / LiDAR
+ *      frame-pair generators of SURVEY.md §8d) -------------------------- */
+int trg_synthetic(const char* kind, size_t n, uint64_t seed, double* out);
+int trg_unit_normalize(double* xyz, size_t n);
+double trg_bbox_diagonal(const double* xyz, size_t n);
+int trg_random_rigid_transform(double rot_range_deg, double trans_range, uint64_t seed, int trial,
+                               double R[9], double t[3]);
+/* 320x240 Kinect-style depth-frame pair (76,800 points each).  R_gt, t_gt map
+ * the source frame into the target frame. */
+int trg_synth_kinect_pair(uint64_t seed, double* target, double* source, double R_gt[9],
+                          double t_gt[3]);
+/* HDL-32-style sweep pair (72,000 points each). */
+int trg_synth_lidar_pair(uint64_t seed, double* target, double* source, double R_gt[9],
+                         double t_gt[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TREEREG_B200_H */

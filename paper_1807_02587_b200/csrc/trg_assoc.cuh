@@ -1,0 +1,290 @@
+// Device building blocks of the adaptive E-step (K7 associate_descend):
+// per-point log-time tree descent (association.cpp:91-157, Algorithm 1 of
+// the paper) and the deterministic per-CTA reduction of the deposits.
+//
+// Reduction scheme (no float atomics anywhere): each CTA processes tiles of
+// 256 points; per tile the (stop node, deposit) pairs are stably radix-sorted
+// by node inside the block, reduced by a segmented scan, and each segment
+// tail adds its sum into this CTA's private row of the partial table
+// partials[node][cta][NM] (epoch-stamped, so nothing is zeroed between
+// calls).  A combine pass then sums each node over CTAs in fixed order.
+#pragma once
+#include <cub/block/block_radix_sort.cuh>
+
+#include "trg_internal.cuh"
+
+namespace trg {
+
+constexpr int kAssocBlock = 256;
+
+// gmm.cpp:37-51 log_density / density, association.cpp:129 score.
+// Evaluation order is the reference's (see oracle/trg_oracle.c log_density).
+__device__ __forceinline__ double node_score(const DNode* __restrict__ g, double y0, double y1,
+                                             double y2, int* status) {
+  const double w = g->weight;
+  if (!(w > 0.0)) return 0.0;
+  if (!(g->lam[2] > 0.0)) {
+    atomicCAS(status, 0, kEDomain);  // log_density: covariance is not PD
+    return 0.0;
+  }
+  const double d0 = y0 - g->mean[0], d1 = y1 - g->mean[1], d2 = y2 - g->mean[2];
+  double p0 = g->axT[0] * d0;
+  p0 += g->axT[1] * d1;
+  p0 += g->axT[2] * d2;
+  double p1 = g->axT[3] * d0;
+  p1 += g->axT[4] * d1;
+  p1 += g->axT[5] * d2;
+  double p2 = g->axT[6] * d0;
+  p2 += g->axT[7] * d1;
+  p2 += g->axT[8] * d2;
+  const double q = p0 * p0 / g->lam[0] + p1 * p1 / g->lam[1] + p2 * p2 / g->lam[2];
+  return w * exp(g->log_norm - 0.5 * q);
+}
+
+struct Descent {
+  int node;       // stop node, -1 = outlier
+  double path;    // product of sibling-normalised responsibilities
+  uint32_t evals; // density evaluations
+};
+
+// association.cpp:117-150 for one transformed point y.
+__device__ __forceinline__ Descent descend(const DNode* __restrict__ nodes, int root_count,
+                                           int depth, double lambda_c, double outlier_floor,
+                                           double y0, double y1, double y2, int* status) {
+  Descent r{-1, 1.0, 0};
+  int node = -1;
+  for (int l = 0; l < depth; ++l) {
+    const int first = node < 0 ? 0 : nodes[node].first_child;
+    const int count = node < 0 ? root_count : nodes[node].child_count;
+    double sum = 0.0, best_s = 0.0;
+    int best = 0;
+    for (int k = 0; k < count; ++k) {
+      const double s = node_score(nodes + first + k, y0, y1, y2, status);
+      sum += s;
+      if (k == 0 || s > best_s) {  // strict '>' : lowest index wins ties
+        best_s = s;
+        best = k;
+      }
+    }
+    r.evals += count;
+    if (l == 0 && !(sum > outlier_floor)) {
+      r.node = -1;
+      return r;
+    }
+    if (!(sum > 0.0)) break;  // deeper underflow: keep the current node
+    node = first + best;
+    r.path *= best_s / sum;
+    const DNode* nd = nodes + node;
+    if (nd->child_count == 0) break;
+    if (nd->cplx < 0.0) {
+      atomicCAS(status, 0, kEDomain);  // node_complexity: no positive trace
+      break;
+    }
+    if (nd->cplx <= lambda_c) break;
+  }
+  r.node = node;
+  return r;
+}
+
+// Deposit vector of one point (association.cpp:20-23): NM = 4 -> (g, g y),
+// NM = 10 adds the 6 unique entries of g (y y^T).
+template <int NM>
+__device__ __forceinline__ void deposit_values(double g, double y0, double y1, double y2,
+                                               double v[NM]) {
+  v[0] = g;
+  v[1] = g * y0;
+  v[2] = g * y1;
+  v[3] = g * y2;
+  if constexpr (NM == 10) {
+    v[4] = g * (y0 * y0);
+    v[5] = g * (y0 * y1);
+    v[6] = g * (y0 * y2);
+    v[7] = g * (y1 * y1);
+    v[8] = g * (y1 * y2);
+    v[9] = g * (y2 * y2);
+  }
+}
+
+template <int NM>
+struct AssocSmem {
+  using Sort = cub::BlockRadixSort<unsigned, kAssocBlock, 1, int>;
+  typename Sort::TempStorage sort;
+  double vals_copy[kAssocBlock][NM];
+  unsigned skeys[kAssocBlock];
+  double warp_v[kAssocBlock / 32][NM];
+  int warp_f[kAssocBlock / 32];
+  double carry[kAssocBlock / 32][NM];
+  unsigned long long outliers, evals;
+};
+
+// Reduces one tile's deposits (key = node or >= J for "none") into the CTA's
+// row of the partial table.  Must be called by all threads of the block.
+template <int NM>
+__device__ void tile_reduce(AssocSmem<NM>& sm, unsigned key, const double v[NM], int J,
+                            int key_bits, double* __restrict__ partials,
+                            uint32_t* __restrict__ stamps, uint32_t epoch, int G, int cta) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int m = 0; m < NM; ++m) sm.vals_copy[tid][m] = v[m];
+  unsigned k1[1] = {key};
+  int i1[1] = {tid};
+  __syncthreads();
+  typename AssocSmem<NM>::Sort(sm.sort).Sort(k1, i1, 0, key_bits);
+  sm.skeys[tid] = k1[0];
+  __syncthreads();
+  const unsigned k = k1[0];
+  double x[NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) x[m] = sm.vals_copy[i1[0]][m];
+  const bool head = (tid == 0) || sm.skeys[tid - 1] != k;
+  const bool tail = (tid == kAssocBlock - 1) || sm.skeys[tid + 1] != k;
+  // warp-level inclusive segmented scan: (v, f) op: f_r ? v_r : v_l + v_r
+  int f = head ? 1 : 0;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    double o[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) o[m] = __shfl_up_sync(0xffffffffu, x[m], off);
+    const int of = __shfl_up_sync(0xffffffffu, f, off);
+    if (lane >= off) {
+      if (!f) {
+#pragma unroll
+        for (int m = 0; m < NM; ++m) x[m] = o[m] + x[m];
+      }
+      f |= of;
+    }
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int m = 0; m < NM; ++m) sm.warp_v[warp][m] = x[m];
+    sm.warp_f[warp] = f;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // carry into warp w = inclusive value at the last item of warp w-1
+#pragma unroll
+    for (int m = 0; m < NM; ++m) sm.carry[0][m] = 0.0;
+    for (int w = 1; w < kAssocBlock / 32; ++w)
+#pragma unroll
+      for (int m = 0; m < NM; ++m)
+        sm.carry[w][m] = sm.warp_f[w - 1] ? sm.warp_v[w - 1][m]
+                                          : sm.carry[w - 1][m] + sm.warp_v[w - 1][m];
+  }
+  __syncthreads();
+  if (!f && warp > 0) {
+#pragma unroll
+    for (int m = 0; m < NM; ++m) x[m] = sm.carry[warp][m] + x[m];
+  }
+  if (tail && k < (unsigned)J) {
+    const size_t row = (size_t)k * G + cta;
+    double* p = partials + row * NM;
+    if (stamps[row] == epoch) {
+#pragma unroll
+      for (int m = 0; m < NM; ++m) p[m] = p[m] + x[m];
+    } else {
+#pragma unroll
+      for (int m = 0; m < NM; ++m) p[m] = x[m];
+      stamps[row] = epoch;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int key_bits_for(int J) { return 32 - __clz((unsigned)J); }
+
+// Transform y = R p + t (geometry.hpp:31) in the reference's order.
+__device__ __forceinline__ void apply_rt(const double* Rt, double p0, double p1, double p2,
+                                         double& y0, double& y1, double& y2) {
+  if (Rt == nullptr) {
+    y0 = p0;
+    y1 = p1;
+    y2 = p2;
+    return;
+  }
+  double s = Rt[0] * p0;
+  s += Rt[1] * p1;
+  s += Rt[2] * p2;
+  y0 = s + Rt[9];
+  s = Rt[3] * p0;
+  s += Rt[4] * p1;
+  s += Rt[5] * p2;
+  y1 = s + Rt[10];
+  s = Rt[6] * p0;
+  s += Rt[7] * p1;
+  s += Rt[8] * p2;
+  y2 = s + Rt[11];
+}
+
+// Association pass of one CTA over tiles cta, cta+G, ... (persistent).
+template <int NM>
+__device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double* Rt_smem, int G,
+                           int cta) {
+  const int tid = threadIdx.x;
+  const int J = p.n_nodes;
+  const int kb = key_bits_for(J);
+  if (tid == 0) {
+    sm.outliers = 0;
+    sm.evals = 0;
+  }
+  __syncthreads();
+  unsigned long long my_out = 0, my_ev = 0;
+  const size_t ntiles = (p.n + kAssocBlock - 1) / kAssocBlock;
+  for (size_t tile = cta; tile < ntiles; tile += G) {
+    const size_t i = tile * kAssocBlock + tid;
+    unsigned key = (unsigned)J;
+    double v[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) v[m] = 0.0;
+    if (i < p.n) {
+      double y0, y1, y2;
+      apply_rt(Rt_smem, p.pts[3 * i], p.pts[3 * i + 1], p.pts[3 * i + 2], y0, y1, y2);
+      const Descent d = descend(p.nodes, p.root_count, p.depth, p.lambda_c, p.outlier_floor, y0,
+                                y1, y2, p.status);
+      my_ev += d.evals;
+      if (d.node < 0) {
+        ++my_out;
+      } else {
+        key = (unsigned)d.node;
+        deposit_values<NM>(d.path, y0, y1, y2, v);
+      }
+      if (p.point_node) {
+        p.point_node[i] = d.node;
+        p.point_w[i] = d.node < 0 ? 0.0 : d.path;
+      }
+    }
+    tile_reduce<NM>(sm, key, v, J, kb, p.partials, p.stamps, p.epoch, G, cta);
+  }
+  atomicAdd(&sm.outliers, my_out);
+  atomicAdd(&sm.evals, my_ev);
+  __syncthreads();
+  if (tid == 0) {
+    atomicAdd(&p.counters[0], sm.outliers);
+    atomicAdd(&p.counters[1], sm.evals);
+  }
+}
+
+// Sum node j's partial rows over CTAs in fixed order (one warp per node).
+template <int NM>
+__device__ __forceinline__ void combine_node(const double* __restrict__ partials,
+                                             const uint32_t* __restrict__ stamps, uint32_t epoch,
+                                             int G, int j, double out[NM]) {
+  const int lane = threadIdx.x & 31;
+  double acc[NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) acc[m] = 0.0;
+  for (int c = lane; c < G; c += 32) {
+    const size_t row = (size_t)j * G + c;
+    if (stamps[row] == epoch) {
+#pragma unroll
+      for (int m = 0; m < NM; ++m) acc[m] += partials[row * NM + m];
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int m = 0; m < NM; ++m) acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], off);
+#pragma unroll
+  for (int m = 0; m < NM; ++m) out[m] = acc[m];
+}
+
+}  // namespace trg

@@ -1,0 +1,351 @@
+// C-ABI entry points (include/treereg_b200.h): context, workspace, tree
+// upload/download and the E-step.  Host code here only validates, stages
+// and launches; all arithmetic on the hot path runs in the kernels.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "trg_internal.cuh"
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+namespace trg {
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out) {
+  if (bytes == 0) bytes = 16;
+  if (ctx->slot_size[slot] < bytes) {
+    if (ctx->slot_ptr[slot]) {
+      TRG_CU(cudaStreamSynchronize(ctx->stream));
+      TRG_CU(cudaFree(ctx->slot_ptr[slot]));
+      ctx->slot_ptr[slot] = nullptr;
+      ctx->slot_size[slot] = 0;
+    }
+    const size_t sz = bytes + bytes / 4;
+    TRG_CU(cudaMalloc(&ctx->slot_ptr[slot], sz));
+    ctx->slot_size[slot] = sz;
+    if (slot == kSlotStamps) TRG_CU(cudaMemset(ctx->slot_ptr[slot], 0, sz));
+  }
+  *out = ctx->slot_ptr[slot];
+  return TRG_OK;
+}
+
+int host_ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out) {
+  if (bytes == 0) bytes = 16;
+  if (ctx->host_slot_size[slot] < bytes) {
+    if (ctx->host_slot_ptr[slot]) {
+      TRG_CU(cudaStreamSynchronize(ctx->stream));
+      TRG_CU(cudaFreeHost(ctx->host_slot_ptr[slot]));
+    }
+    const size_t sz = bytes + bytes / 4;
+    TRG_CU(cudaMallocHost(&ctx->host_slot_ptr[slot], sz));
+    ctx->host_slot_size[slot] = sz;
+  }
+  *out = ctx->host_slot_ptr[slot];
+  return TRG_OK;
+}
+
+int check_status(trg_ctx* ctx, const char* where) {
+  int st = 0;
+  TRG_CU(cudaMemcpyAsync(&st, ctx->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  if (st != 0) {
+    TRG_CU(cudaMemsetAsync(ctx->status, 0, sizeof(int), ctx->stream));
+    const char* what = st == kEDomain   ? "covariance is not positive definite / no positive trace"
+                       : st == kEInval  ? "invalid argument"
+                       : st == kERuntime ? "no responsibility mass"
+                                         : "device error";
+    set_error(std::string(where) + ": " + what);
+    return st;
+  }
+  return TRG_OK;
+}
+
+int persistent_grid(trg_ctx* ctx, const void* kernel, int block, size_t smem) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+  if (per_sm < 1) per_sm = 1;
+  return ctx->sms * per_sm;
+}
+
+int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out) {
+  (void)ctx;
+  auto* t = new trg_tree_dev;
+  t->capacity = capacity;
+  if (cudaMalloc(&t->nodes, sizeof(DNode) * capacity) != cudaSuccess ||
+      cudaMalloc(&t->cov, sizeof(double) * 9 * capacity) != cudaSuccess) {
+    cudaFree(t->nodes);
+    cudaFree(t->cov);
+    delete t;
+    set_error("tree_alloc: cudaMalloc failed");
+    return TRG_ECUDA;
+  }
+  *out = t;
+  return TRG_OK;
+}
+
+}  // namespace trg
+
+using namespace trg;
+
+extern "C" {
+
+const char* trg_last_error(void) { return g_last_error.c_str(); }
+
+int trg_ctx_create(int device, trg_ctx** out) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    set_error("trg_ctx_create: no CUDA device (there is no CPU fallback)");
+    return TRG_ECUDA;
+  }
+  if (device < 0 || device >= n) {
+    set_error("trg_ctx_create: bad device index");
+    return TRG_EINVAL;
+  }
+  TRG_CU(cudaSetDevice(device));
+  auto* c = new trg_ctx;
+  c->device = device;
+  cudaDeviceProp prop;
+  TRG_CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    set_error("trg_ctx_create: this build targets sm_100a (B200) only");
+    delete c;
+    return TRG_ECUDA;
+  }
+  c->sms = prop.multiProcessorCount;
+  TRG_CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  TRG_CU(cudaMalloc(&c->status, sizeof(int)));
+  TRG_CU(cudaMemset(c->status, 0, sizeof(int)));
+  *out = c;
+  return TRG_OK;
+}
+
+int trg_ctx_destroy(trg_ctx* ctx) {
+  if (!ctx) return TRG_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (int i = 0; i < trg_ctx::kSlots; ++i) {
+    if (ctx->slot_ptr[i]) cudaFree(ctx->slot_ptr[i]);
+    if (ctx->host_slot_ptr[i]) cudaFreeHost(ctx->host_slot_ptr[i]);
+  }
+  cudaFree(ctx->status);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return TRG_OK;
+}
+
+int trg_device_sms(trg_ctx* ctx) { return ctx->sms; }
+uint64_t trg_kernel_launches(trg_ctx* ctx) { return ctx->launches; }
+void* trg_ctx_stream(trg_ctx* ctx) { return (void*)ctx->stream; }
+
+int trg_tree_capacity(int max_level) {
+  int cap = 0, p = 1;
+  for (int l = 0; l < max_level; ++l) {
+    p *= 8;
+    cap += p;
+  }
+  return cap;
+}
+
+int trg_tree_size(const trg_tree_dev* tree) { return tree ? tree->n_nodes : 0; }
+
+// Host tree -> packed device records.
+int trg_tree_upload(trg_ctx* ctx, const trg_tree* h, trg_tree_dev** out) {
+  if (!h || h->n_nodes <= 0 || h->max_level < 1) {
+    set_error("trg_tree_upload: empty model");
+    return TRG_EINVAL;
+  }
+  TRG_CU(cudaSetDevice(ctx->device));
+  const int J = h->n_nodes;
+  std::vector<DNode> nodes(J);
+  int root_count = 0;
+  while (root_count < J && h->level[root_count] == 0) ++root_count;
+  for (int i = 0; i < J; ++i) {
+    DNode& d = nodes[i];
+    for (int r = 0; r < 3; ++r) {
+      d.mean[r] = h->mean[3 * i + r];
+      d.lam[r] = h->lambdas[3 * i + r];
+      for (int k = 0; k < 3; ++k) d.axT[3 * r + k] = h->axes[9 * i + 3 * k + r];
+    }
+    d.log_norm = h->log_norm[i];
+    d.weight = h->weight[i];
+    const double tr = (d.lam[0] + d.lam[1]) + d.lam[2];
+    d.cplx = tr > 0.0 ? d.lam[2] / tr : -1.0;
+    d.first_child = h->first_child[i];
+    d.child_count = h->child_count[i];
+    d.level = h->level[i];
+    d.parent = h->parent[i];
+  }
+  trg_tree_dev* t = nullptr;
+  TRG_TRY(tree_alloc(ctx, std::max(J, trg_tree_capacity(h->max_level)), &t));
+  t->n_nodes = J;
+  t->max_level = h->max_level;
+  t->root_count = root_count;
+  TRG_CU(cudaMemcpyAsync(t->nodes, nodes.data(), sizeof(DNode) * J, cudaMemcpyHostToDevice,
+                         ctx->stream));
+  TRG_CU(cudaMemcpyAsync(t->cov, h->cov, sizeof(double) * 9 * J, cudaMemcpyHostToDevice,
+                         ctx->stream));
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  *out = t;
+  return TRG_OK;
+}
+
+int trg_tree_download(trg_ctx* ctx, const trg_tree_dev* t, trg_tree* h) {
+  if (!t || !h) {
+    set_error("trg_tree_download: null argument");
+    return TRG_EINVAL;
+  }
+  if (h->capacity < t->n_nodes) {
+    set_error("trg_tree_download: host capacity too small");
+    return TRG_EINVAL;
+  }
+  TRG_CU(cudaSetDevice(ctx->device));
+  const int J = t->n_nodes;
+  std::vector<DNode> nodes(J);
+  TRG_CU(cudaMemcpyAsync(nodes.data(), t->nodes, sizeof(DNode) * J, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+  TRG_CU(cudaMemcpyAsync(h->cov, t->cov, sizeof(double) * 9 * J, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  h->n_nodes = J;
+  h->max_level = t->max_level;
+  for (int i = 0; i < J; ++i) {
+    const DNode& d = nodes[i];
+    for (int r = 0; r < 3; ++r) {
+      h->mean[3 * i + r] = d.mean[r];
+      h->lambdas[3 * i + r] = d.lam[r];
+      for (int k = 0; k < 3; ++k) h->axes[9 * i + 3 * k + r] = d.axT[3 * r + k];
+    }
+    h->log_norm[i] = d.log_norm;
+    h->weight[i] = d.weight;
+    h->first_child[i] = d.first_child;
+    h->child_count[i] = d.child_count;
+    h->level[i] = d.level;
+    h->parent[i] = d.parent;
+  }
+  return TRG_OK;
+}
+
+int trg_tree_free(trg_ctx* ctx, trg_tree_dev* t) {
+  if (!t) return TRG_OK;
+  if (ctx) cudaSetDevice(ctx->device);
+  cudaFree(t->nodes);
+  cudaFree(t->cov);
+  delete t;
+  return TRG_OK;
+}
+
+// Stage N*3 points on the device (no-op when already there).
+static int stage_points(trg_ctx* ctx, const double* xyz, size_t n, int on_device, int slot,
+                        const double** dev) {
+  if (on_device) {
+    *dev = xyz;
+    return TRG_OK;
+  }
+  void* p = nullptr;
+  TRG_TRY(ws_get(ctx, slot, sizeof(double) * 3 * n, &p));
+  TRG_CU(cudaMemcpyAsync(p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+  *dev = static_cast<const double*>(p);
+  return TRG_OK;
+}
+
+int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, size_t n,
+                  int xyz_on_device, const double R[9], const double t[3],
+                  const trg_assoc_config* cfg, trg_moments* out, int* point_node,
+                  double* point_weight) {
+  // association.cpp:43-50 validate_inputs, :95-102
+  if (n == 0) {
+    set_error("association: empty point cloud");
+    return TRG_EINVAL;
+  }
+  if (!tree || tree->n_nodes == 0) {
+    set_error("association: empty model");
+    return TRG_EINVAL;
+  }
+  if (!(cfg->lambda_c >= 0.0 && cfg->lambda_c <= 1.0 / 3.0)) {
+    set_error("association: lambda_c outside [0, 1/3]");
+    return TRG_EINVAL;
+  }
+  const int depth = cfg->max_level == 0 ? tree->max_level : cfg->max_level;
+  if (depth < 1 || depth > tree->max_level) {
+    set_error("association: search depth exceeds tree depth");
+    return TRG_EINVAL;
+  }
+  TRG_CU(cudaSetDevice(ctx->device));
+  const int nm = out->m2 ? 10 : 4;
+  const int J = tree->n_nodes;
+  const int G = assoc_grid(ctx, nm);
+  AssocParams p{};
+  p.nodes = tree->nodes;
+  p.n_nodes = J;
+  p.root_count = tree->root_count;
+  p.depth = depth;
+  p.lambda_c = cfg->lambda_c;
+  p.outlier_floor = cfg->outlier_floor;
+  p.n = n;
+  p.epoch = ++ctx->epoch;
+  p.status = ctx->status;
+  TRG_TRY(stage_points(ctx, xyz, n, xyz_on_device, kSlotPoints, &p.pts));
+  void *part, *stamps, *mom, *cnt, *rt;
+  TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * nm * (size_t)J * G, &part));
+  TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)J * G, &stamps));
+  TRG_TRY(ws_get(ctx, kSlotMoments, sizeof(double) * nm * (size_t)J, &mom));
+  TRG_TRY(ws_get(ctx, kSlotCounters, 64 + 12 * sizeof(double), &cnt));
+  rt = static_cast<char*>(cnt) + 64;
+  p.partials = static_cast<double*>(part);
+  p.stamps = static_cast<uint32_t*>(stamps);
+  p.counters = static_cast<unsigned long long*>(cnt);
+  double hrt[12];
+  for (int k = 0; k < 9; ++k) hrt[k] = R[k];
+  for (int k = 0; k < 3; ++k) hrt[9 + k] = t[k];
+  TRG_CU(cudaMemcpyAsync(rt, hrt, sizeof hrt, cudaMemcpyHostToDevice, ctx->stream));
+  p.Rt = static_cast<const double*>(rt);
+  TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
+  if (point_node) {
+    void *pn, *pw;
+    TRG_TRY(ws_get(ctx, kSlotPointNode, sizeof(int) * n, &pn));
+    TRG_TRY(ws_get(ctx, kSlotPointW, sizeof(double) * n, &pw));
+    p.point_node = static_cast<int*>(pn);
+    p.point_w = static_cast<double*>(pw);
+  }
+  TRG_TRY(launch_associate(ctx, p, nm, static_cast<double*>(mom), G));
+  std::vector<double> hm((size_t)nm * J);
+  unsigned long long hc[2];
+  TRG_CU(cudaMemcpyAsync(hm.data(), mom, sizeof(double) * nm * J, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+  TRG_CU(cudaMemcpyAsync(hc, cnt, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
+  if (point_node) {
+    TRG_CU(cudaMemcpyAsync(point_node, p.point_node, sizeof(int) * n, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    TRG_CU(cudaMemcpyAsync(point_weight, p.point_w, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  }
+  TRG_TRY(check_status(ctx, "associate_adaptive"));
+  double mass = 0.0;
+  for (int j = 0; j < J; ++j) {
+    const double* v = &hm[(size_t)nm * j];
+    out->m0[j] = v[0];
+    for (int k = 0; k < 3; ++k) out->m1[3 * j + k] = v[1 + k];
+    if (nm == 10) {
+      double* m2 = out->m2 + 9 * j;
+      m2[0] = v[4];
+      m2[1] = m2[3] = v[5];
+      m2[2] = m2[6] = v[6];
+      m2[4] = v[7];
+      m2[5] = m2[7] = v[8];
+      m2[8] = v[9];
+    }
+    mass += v[0];
+  }
+  out->total_points = n;
+  out->outliers = hc[0];
+  out->density_evaluations = hc[1];
+  out->total_mass = mass;
+  return TRG_OK;
+}
+
+}  // extern "C"

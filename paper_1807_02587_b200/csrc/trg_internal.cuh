@@ -1,0 +1,124 @@
+// Internal declarations shared by the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/treereg_b200.h"
+#include "trg_math.cuh"
+
+namespace trg {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+#define TRG_CU(expr)                                                              \
+  do {                                                                            \
+    cudaError_t e_ = (expr);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      ::trg::set_error(std::string(#expr) + ": " + cudaGetErrorString(e_));       \
+      return TRG_ECUDA;                                                           \
+    }                                                                             \
+  } while (0)
+#define TRG_TRY(expr)            \
+  do {                           \
+    int rc_ = (expr);            \
+    if (rc_ != TRG_OK) return rc_; \
+  } while (0)
+
+// ------------------------------------------------------- device records
+// Packed per-node record used by every scoring loop (association, EM).
+// axT[3*l + k] = axes(k, l): row l is the unit axis of lam[l].
+struct __align__(16) DNode {
+  double mean[3];
+  double axT[9];
+  double lam[3];
+  double log_norm;
+  double weight;
+  double cplx;  // node_complexity (gmm.cpp:53-59); -1 when trace <= 0
+  int first_child, child_count;
+  int level, parent;
+};
+static_assert(sizeof(DNode) == 160, "DNode layout");
+
+}  // namespace trg
+
+struct trg_tree_dev {
+  int n_nodes = 0, max_level = 0, capacity = 0, root_count = 0;
+  trg::DNode* nodes = nullptr;  // [capacity]
+  double* cov = nullptr;        // [capacity*9] row-major
+  int* owner_ctx_device = nullptr;
+};
+
+struct trg_ctx {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  uint32_t epoch = 1;
+  static constexpr int kSlots = 32;
+  void* slot_ptr[kSlots] = {};
+  size_t slot_size[kSlots] = {};
+  void* host_slot_ptr[kSlots] = {};
+  size_t host_slot_size[kSlots] = {};
+  int* status = nullptr;  // device status word
+};
+
+namespace trg {
+
+// Workspace slots (device memory, grown on demand, never shrunk).
+enum Slot : int {
+  kSlotPoints = 0,
+  kSlotPartials,
+  kSlotStamps,
+  kSlotMoments,
+  kSlotCounters,
+  kSlotPointNode,
+  kSlotPointW,
+  kSlotSolve,
+  kSlotEm,
+  kSlotEmTrace,
+  kSlotBuild0,
+  kSlotBuild1,
+  kSlotBuild2,
+  kSlotBuild3,
+  kSlotBuild4,
+  kSlotBuild5,
+  kSlotBuild6,
+  kSlotBuild7,
+  kSlotBuild8,
+  kSlotBuild9,
+  kSlotBuild10,
+  kSlotBuild11,
+  kSlotPoints2,
+};
+
+int ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
+int host_ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
+int check_status(trg_ctx* ctx, const char* where);
+int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out);
+
+// Grid size for persistent kernels: SMs x resident CTAs.
+int persistent_grid(trg_ctx* ctx, const void* kernel, int block, size_t smem);
+
+// ---- association (trg_assoc.cu)
+struct AssocParams {
+  const DNode* nodes;
+  int n_nodes, root_count, depth;
+  double lambda_c, outlier_floor;
+  const double* pts;  // N*3 AoS
+  size_t n;
+  const double* Rt;  // device: R[9], t[3] (nullable => identity)
+  double* partials;  // [J][G][NM]
+  uint32_t* stamps;  // [J][G]
+  uint32_t epoch;
+  unsigned long long* counters;  // outliers, evals (atomic adds of integers)
+  int* point_node;               // nullable
+  double* point_w;               // nullable
+  int* status;
+};
+int launch_associate(trg_ctx* ctx, const AssocParams& p, int nm, double* moments /*[J][nm]*/,
+                     int grid);
+int assoc_grid(trg_ctx* ctx, int nm);
+
+}  // namespace trg

@@ -1,0 +1,512 @@
+"""Host-side mirror of the reference's hot-path API (namespace treereg).
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/core/include/treereg/{gmm,association,mstep,registration}.hpp,
+so parity tests read like the reference's own tests.  Every call goes
+through the C-ABI of libtrg_cuda.so (include/treereg_b200.h) and runs on the
+GPU; nothing here computes on the CPU beyond argument packing.
+
+Exceptions mirror the reference's C++ types:
+  std::invalid_argument   -> InvalidArgument (ValueError)
+  std::domain_error       -> DomainError (ArithmeticError)
+  std::runtime_error      -> RuntimeError
+  std::out_of_range       -> IndexError
+  DegenerateGeometryError -> DegenerateGeometryError (RuntimeError)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import (AssocConfigC, BuildDiagC, MomentsC, MStepSolutionC, ModelConfigC, RegConfigC,
+                   RegResultC, TreeC, dp, ip, u64p)
+
+
+class InvalidArgument(ValueError):
+    pass
+
+
+class DomainError(ArithmeticError):
+    pass
+
+
+class DegenerateGeometryError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _raise(rc: int):
+    msg = _lib.last_error()
+    if rc == _lib.TRG_EINVAL:
+        raise InvalidArgument(msg)
+    if rc == _lib.TRG_EDOMAIN:
+        raise DomainError(msg)
+    if rc == _lib.TRG_ERANGE:
+        raise IndexError(msg)
+    if rc == _lib.TRG_EDEGENERATE:
+        raise DegenerateGeometryError(msg)
+    if rc in (_lib.TRG_ECUDA, _lib.TRG_ENCCL):
+        raise CudaError(msg)
+    raise RuntimeError(msg)
+
+
+def _chk(rc: int):
+    if rc != 0:
+        _raise(rc)
+
+
+def _d(a: np.ndarray):
+    return a.ctypes.data_as(dp)
+
+
+def _i(a: np.ndarray):
+    return a.ctypes.data_as(ip)
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One CUDA device + stream + workspace (trg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        _chk(_lib.lib().trg_ctx_create(device, C.byref(self.h)))
+        self.device = device
+
+    def close(self):
+        if self.h:
+            _lib.lib().trg_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def sms(self) -> int:
+        return _lib.lib().trg_device_sms(self.h)
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(_lib.lib().trg_kernel_launches(self.h))
+
+    @property
+    def stream(self) -> int:
+        return int(_lib.lib().trg_ctx_stream(self.h) or 0)
+
+
+_DEFAULT: Context | None = None
+
+
+def default_context() -> Context:
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = Context(0)
+    return _DEFAULT
+
+
+# ------------------------------------------------------------------ configs
+@dataclass
+class ModelConfig:  # gmm.hpp:34-41
+    em_iterations_per_node: int = 8
+    min_points_per_node: int = 32
+    cov_regularization_epsilon: float = 1e-4
+    cov_regularization_absolute: float = 1e-12
+    rng_seed: int = 0
+    max_level: int = 3
+
+    def c(self) -> ModelConfigC:
+        return ModelConfigC(self.em_iterations_per_node, self.min_points_per_node,
+                            self.cov_regularization_epsilon, self.cov_regularization_absolute,
+                            self.rng_seed, self.max_level)
+
+
+@dataclass
+class AssocConfig:  # association.hpp:34-40
+    lambda_c: float = 0.01
+    max_level: int = 0
+    outlier_floor: float = 1e-300
+    deterministic: bool = True
+
+    def c(self) -> AssocConfigC:
+        return AssocConfigC(self.lambda_c, self.max_level, self.outlier_floor,
+                            1 if self.deterministic else 0)
+
+
+@dataclass
+class Variant:  # registration.hpp:17-25
+    kind: str = "adaptive"  # "adaptive" | "tree"
+    param: int = 3
+
+    @staticmethod
+    def parse(text: str) -> "Variant":
+        head, _, tail = text.partition(":")
+        if head not in ("adaptive", "tree"):
+            raise InvalidArgument(f"unsupported variant '{text}' (this path: adaptive:L, tree:L)")
+        if not tail:
+            raise InvalidArgument(f"variant '{head}' needs a parameter, e.g. {head}:3")
+        try:
+            p = int(tail)
+        except ValueError:
+            raise InvalidArgument(f"bad variant parameter in '{text}'") from None
+        if p < 1:
+            raise InvalidArgument("variant parameter must be >= 1")
+        return Variant(head, p)
+
+    def name(self) -> str:
+        return ("Adaptive L" if self.kind == "adaptive" else "GMM-Tree L") + str(self.param)
+
+
+@dataclass
+class RigidTransform:  # geometry.hpp:26-56
+    rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
+    translation: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    @staticmethod
+    def identity() -> "RigidTransform":
+        return RigidTransform()
+
+    def __call__(self, p):
+        return np.asarray(p) @ self.rotation.T + self.translation
+
+    def __mul__(self, rhs: "RigidTransform") -> "RigidTransform":
+        return RigidTransform(self.rotation @ rhs.rotation,
+                              self.rotation @ rhs.translation + self.translation)
+
+    def inverse(self) -> "RigidTransform":
+        rt = self.rotation.T
+        return RigidTransform(rt, -(rt @ self.translation))
+
+    def rotation_angle(self) -> float:
+        c = np.clip((np.trace(self.rotation) - 1.0) * 0.5, -1.0, 1.0)
+        return float(np.arccos(c))
+
+
+@dataclass
+class RegistrationConfig:  # registration.hpp:27-36
+    variant: Variant = field(default_factory=Variant)
+    lambda_c: float = 0.01
+    max_em_iterations: int = 50
+    rotation_tol: float = 1e-5
+    translation_tol: float = 1e-5
+    initial_transform: RigidTransform = field(default_factory=RigidTransform)
+    model_config: ModelConfig = field(default_factory=ModelConfig)
+    deterministic: bool = True
+
+    def c(self) -> RegConfigC:
+        r = RegConfigC()
+        r.variant_kind = 1 if self.variant.kind == "tree" else 0
+        r.variant_param = self.variant.param
+        r.lambda_c = self.lambda_c
+        r.max_em_iterations = self.max_em_iterations
+        r.rotation_tol = self.rotation_tol
+        r.translation_tol = self.translation_tol
+        R = np.ascontiguousarray(self.initial_transform.rotation, dtype=np.float64).ravel()
+        for k in range(9):
+            r.initial_R[k] = R[k]
+        for k in range(3):
+            r.initial_t[k] = float(self.initial_transform.translation[k])
+        r.model_config = self.model_config.c()
+        return r
+
+
+# ------------------------------------------------------------------ clouds
+def _points(cloud) -> np.ndarray:
+    p = np.ascontiguousarray(cloud, dtype=np.float64)
+    if p.ndim != 2 or p.shape[1] != 3:
+        raise InvalidArgument("point cloud must be an (N, 3) array")
+    return p
+
+
+def _cloud_ptr(cloud):
+    """(pointer, n, on_device) for a numpy (host) or torch CUDA tensor."""
+    if hasattr(cloud, "is_cuda") and cloud.is_cuda:
+        if cloud.dtype.__str__() != "torch.float64" or cloud.dim() != 2 or cloud.shape[1] != 3:
+            raise InvalidArgument("device point cloud must be a contiguous (N, 3) float64 tensor")
+        if not cloud.is_contiguous():
+            raise InvalidArgument("device point cloud must be contiguous")
+        return C.c_void_p(cloud.data_ptr()), int(cloud.shape[0]), 1, cloud
+    p = _points(cloud)
+    return p.ctypes.data_as(C.c_void_p), len(p), 0, p
+
+
+# ------------------------------------------------------------------ model
+class GmmTree:
+    """Device-resident GMM tree (gmm.hpp:56-67).  Host arrays are fetched
+    lazily (``.host()``) for inspection and parity checks."""
+
+    def __init__(self, handle: C.c_void_p, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+        self._host = None
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.lib().trg_tree_free(self.ctx.h, self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+    def size(self) -> int:
+        return _lib.lib().trg_tree_size(self.h)
+
+    def host(self) -> dict:
+        if self._host is None:
+            J = self.size()
+            t = dict(weight=np.zeros(J), mean=np.zeros((J, 3)), cov=np.zeros((J, 3, 3)),
+                     lambdas=np.zeros((J, 3)), axes=np.zeros((J, 3, 3)), log_norm=np.zeros(J),
+                     parent=np.zeros(J, np.int32), first_child=np.zeros(J, np.int32),
+                     child_count=np.zeros(J, np.int32), level=np.zeros(J, np.int32))
+            s = _tree_struct(t, 0, J)
+            _chk(_lib.lib().trg_tree_download(self.ctx.h, self.h, C.byref(s)))
+            t["max_level"] = s.max_level
+            self._host = t
+        return self._host
+
+    @property
+    def max_level(self) -> int:
+        return int(self.host()["max_level"])
+
+    @staticmethod
+    def from_host(t: dict, ctx: Context | None = None) -> "GmmTree":
+        """Upload a host tree (e.g. an oracle tree or a load_tree() result)."""
+        ctx = ctx or default_context()
+        a = {k: np.ascontiguousarray(v) for k, v in t.items() if isinstance(v, np.ndarray)}
+        a["level"] = a["level"].astype(np.int32)
+        for k in ("parent", "first_child", "child_count"):
+            a[k] = a[k].astype(np.int32)
+        s = _tree_struct(a, int(t["max_level"]), len(a["weight"]))
+        s.n_nodes = len(a["weight"])
+        h = C.c_void_p()
+        _chk(_lib.lib().trg_tree_upload(ctx.h, C.byref(s), C.byref(h)))
+        return GmmTree(h, ctx)
+
+
+def _tree_struct(t: dict, max_level: int, cap: int) -> TreeC:
+    s = TreeC()
+    s.n_nodes = 0
+    s.max_level = max_level
+    s.capacity = cap
+    for k in ("weight", "mean", "cov", "lambdas", "axes", "log_norm"):
+        setattr(s, k, _d(t[k]))
+    for k in ("parent", "first_child", "child_count", "level"):
+        setattr(s, k, _i(t[k]))
+    return s
+
+
+@dataclass
+class BuildDiagnostics:  # gmm.hpp:43-49 (+ device counters)
+    calibration_drift: float = 0.0
+    calibration_passes: int = 0
+    entries_per_round: list = field(default_factory=list)
+    expanded_per_round: list = field(default_factory=list)
+    calib_density_evaluations: int = 0
+
+
+def build_tree(cloud, config: ModelConfig = ModelConfig(),
+               diagnostics: BuildDiagnostics | None = None,
+               ctx: Context | None = None) -> GmmTree:
+    """gmm.hpp:69-70 build_tree, on the GPU."""
+    ctx = ctx or default_context()
+    ptr, n, on_dev, _keep = _cloud_ptr(cloud)
+    cfg = config.c()
+    h = C.c_void_p()
+    d = BuildDiagC()
+    _chk(_lib.lib().trg_build_tree(ctx.h, ptr, n, on_dev, C.byref(cfg), C.byref(h), C.byref(d)))
+    if diagnostics is not None:
+        diagnostics.calibration_drift = d.calibration_drift
+        diagnostics.calibration_passes = d.calibration_passes
+        L = config.max_level
+        diagnostics.entries_per_round = list(d.entries_per_round)[:L]
+        diagnostics.expanded_per_round = list(d.expanded_per_round)[:L]
+        diagnostics.calib_density_evaluations = int(d.calib_density_evaluations)
+    return GmmTree(h, ctx)
+
+
+# ------------------------------------------------------------------ E-step
+@dataclass
+class MomentSet:  # association.hpp:14-32
+    m0: np.ndarray
+    m1: np.ndarray
+    m2: np.ndarray | None
+    total_points: int = 0
+    total_mass: float = 0.0
+    outliers: int = 0
+    density_evaluations: int = 0
+
+    def components(self) -> int:
+        return len(self.m0)
+
+
+def associate_adaptive(cloud, tree: GmmTree, t: RigidTransform = None,
+                       config: AssocConfig = AssocConfig(), with_m2: bool = True,
+                       per_point: bool = False):
+    """association.hpp:54-56 associate_adaptive on the GPU.  With
+    ``per_point`` also returns each point's (deposit node, path weight)."""
+    t = t or RigidTransform.identity()
+    ptr, n, on_dev, _keep = _cloud_ptr(cloud)
+    J = tree.size()
+    m0, m1 = np.zeros(J), np.zeros((J, 3))
+    m2 = np.zeros((J, 3, 3)) if with_m2 else None
+    mc = MomentsC()
+    mc.m0, mc.m1 = _d(m0), _d(m1)
+    mc.m2 = _d(m2) if with_m2 else None
+    R = np.ascontiguousarray(t.rotation, dtype=np.float64)
+    tr = np.ascontiguousarray(t.translation, dtype=np.float64)
+    cfg = config.c()
+    node = np.zeros(n, np.int32) if per_point else None
+    w = np.zeros(n) if per_point else None
+    _chk(_lib.lib().trg_associate(tree.ctx.h, tree.h, ptr, n, on_dev, _d(R), _d(tr), C.byref(cfg),
+                                  C.byref(mc), _i(node) if per_point else None,
+                                  _d(w) if per_point else None))
+    ms = MomentSet(m0, m1, m2, int(mc.total_points), float(mc.total_mass), int(mc.outliers),
+                   int(mc.density_evaluations))
+    return (ms, node, w) if per_point else ms
+
+
+# ------------------------------------------------------------------ M-step
+@dataclass
+class VirtualPointSet:  # mstep.hpp:27-32 (moments + the model they refer to)
+    moments: MomentSet
+    tree: GmmTree
+
+
+@dataclass
+class MStepSolution:  # mstep.hpp:54-61
+    omega: np.ndarray
+    translation: np.ndarray
+    delta: RigidTransform
+    criterion_before: float
+    criterion_after: float
+    condition_estimate: float
+    n_virtual_points: int
+
+
+def make_virtual_points(moments: MomentSet, tree: GmmTree) -> VirtualPointSet:
+    """mstep.hpp:46-47.  The filter (m0 > 1e-8 N, pi* = m0/N, mu* = m1/m0)
+    runs on the device inside solve_mstep; validation mirrors mstep.cpp:11-17."""
+    if moments.components() != tree.size():
+        raise InvalidArgument("make_virtual_points: moment/component count mismatch")
+    if moments.total_points == 0:
+        raise InvalidArgument("make_virtual_points: no points were associated")
+    return VirtualPointSet(moments, tree)
+
+
+def solve_mstep(vps: VirtualPointSet) -> MStepSolution:
+    """mstep.hpp:67 solve_mstep on the GPU (single thread-block)."""
+    m = vps.moments
+    out = MStepSolutionC()
+    m0 = np.ascontiguousarray(m.m0, dtype=np.float64)
+    m1 = np.ascontiguousarray(m.m1, dtype=np.float64)
+    _chk(_lib.lib().trg_solve_mstep(vps.tree.ctx.h, vps.tree.h, _d(m0), _d(m1), m.total_points,
+                                    C.byref(out)))
+    R = np.array(out.delta_R[:]).reshape(3, 3)
+    return MStepSolution(np.array(out.omega[:]), np.array(out.translation[:]),
+                         RigidTransform(R, np.array(out.delta_t[:])), out.criterion_before,
+                         out.criterion_after, out.condition_estimate, out.n_virtual_points)
+
+
+# ------------------------------------------------------------------ driver
+@dataclass
+class RegistrationResult:  # registration.hpp:38-48
+    transform: RigidTransform
+    iterations: int
+    converged: bool
+    criterion_trace: np.ndarray
+    criterion_after_trace: np.ndarray
+    eval_counts: np.ndarray
+    model_build_seconds: float
+    em_seconds: float
+    model_components: int
+
+
+def _result(r: RegResultC, cb, ca, ev) -> RegistrationResult:
+    n = r.iterations
+    return RegistrationResult(
+        RigidTransform(np.array(r.R[:]).reshape(3, 3), np.array(r.t[:])), n, bool(r.converged),
+        cb[:n].copy(), ca[:n].copy(), ev[:n].copy(), r.model_build_seconds, r.em_seconds,
+        int(r.model_components))
+
+
+def _result_buffers(cfg: RegistrationConfig):
+    k = max(1, cfg.max_em_iterations)
+    cb, ca, ev = np.zeros(k), np.zeros(k), np.zeros(k, np.uint64)
+    r = RegResultC()
+    r.criterion_trace, r.criterion_after_trace = _d(cb), _d(ca)
+    r.eval_counts = ev.ctypes.data_as(u64p)
+    r.trace_capacity = k
+    return r, cb, ca, ev
+
+
+def register_with_tree(tree: GmmTree, source, config: RegistrationConfig = RegistrationConfig(),
+                       target_diag: float = 0.0) -> RegistrationResult:
+    """registration.hpp:59-62, EM loop resident on the GPU."""
+    ptr, n, on_dev, _keep = _cloud_ptr(source)
+    r, cb, ca, ev = _result_buffers(config)
+    cfg = config.c()
+    _chk(_lib.lib().trg_register_with_tree(tree.ctx.h, tree.h, ptr, n, on_dev, C.byref(cfg),
+                                           float(target_diag), C.byref(r)))
+    return _result(r, cb, ca, ev)
+
+
+def register_clouds(target, source, config: RegistrationConfig = RegistrationConfig(),
+                    ctx: Context | None = None) -> RegistrationResult:
+    """registration.hpp:53-55 (adaptive:L / tree:L): build + EM on the GPU."""
+    ctx = ctx or default_context()
+    pt, nt, dev_t, _k1 = _cloud_ptr(target)
+    ps, ns, dev_s, _k2 = _cloud_ptr(source)
+    if dev_t != dev_s:
+        raise InvalidArgument("register_clouds: target and source must live on the same side")
+    r, cb, ca, ev = _result_buffers(config)
+    cfg = config.c()
+    _chk(_lib.lib().trg_register_clouds(ctx.h, pt, nt, ps, ns, dev_t, C.byref(cfg), C.byref(r)))
+    return _result(r, cb, ca, ev)
+
+
+# ------------------------------------------------------------------ inputs
+def synthetic(kind: str, n: int, seed: int) -> np.ndarray:
+    """synthetic.cpp generators (bit-identical restatement)."""
+    out = np.zeros((n, 3))
+    _chk(_lib.lib().trg_synthetic(kind.encode(), n, seed, _d(out)))
+    return out
+
+
+def unit_normalized(cloud) -> np.ndarray:
+    p = _points(cloud).copy()
+    _chk(_lib.lib().trg_unit_normalize(_d(p), len(p)))
+    return p
+
+
+def bbox_diagonal(cloud) -> float:
+    p = _points(cloud)
+    return float(_lib.lib().trg_bbox_diagonal(_d(p), len(p)))
+
+
+def random_rigid_transform(rot_range_deg: float, trans_range: float, seed: int,
+                           trial: int = 0) -> RigidTransform:
+    R, t = np.zeros((3, 3)), np.zeros(3)
+    _chk(_lib.lib().trg_random_rigid_transform(rot_range_deg, trans_range, seed, trial, _d(R),
+                                               _d(t)))
+    return RigidTransform(R, t)
+
+
+def kinect_pair(seed: int):
+    """C2: 320x240 Kinect-style frame pair -> (target, source, gt source->target)."""
+    tg, sr, R, t = np.zeros((76800, 3)), np.zeros((76800, 3)), np.zeros((3, 3)), np.zeros(3)
+    _chk(_lib.lib().trg_synth_kinect_pair(seed, _d(tg), _d(sr), _d(R), _d(t)))
+    return tg, sr, RigidTransform(R, t)
+
+
+def lidar_pair(seed: int):
+    """C3: HDL-32-style sweep pair -> (target, source, gt source->target)."""
+    tg, sr, R, t = np.zeros((72000, 3)), np.zeros((72000, 3)), np.zeros((3, 3)), np.zeros(3)
+    _chk(_lib.lib().trg_synth_lidar_pair(seed, _d(tg), _d(sr), _d(R), _d(t)))
+    return tg, sr, RigidTransform(R, t)
