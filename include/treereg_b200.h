@@ -205,6 +205,14 @@ int trg_synth_kinect_pair(uint64_t seed, double* target, double* source, double 
 int trg_synth_lidar_pair(uint64_t seed, double* target, double* source, double R_gt[9],
                          double t_gt[3]);
 
+/* ---- diagnostics ------------------------------------------------------
+ * Runs the device eigensolvers on `count` row-major matrices: n = 6 is the
+ * 6x6 Jacobi of solve_mstep (mstep.cpp:77), n = 3 eig_sym3
+ * (geometry.cpp:40-79), n = -3 eig_sym3_floored at 1e-4 (:81-102).  Used by
+ * the tests to pin device math bit-for-bit to the CPU oracle. */
+int trg_debug_eig(trg_ctx* ctx, int n, const double* in, int count, double* evals,
+                  double* evecs, int* status);
+
 #ifdef __cplusplus
 }
 #endif

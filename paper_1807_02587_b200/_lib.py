@@ -105,6 +105,7 @@ SIGNATURES = {
                                              dp]),
     "trg_synth_kinect_pair": (C.c_int, [C.c_uint64, dp, dp, dp, dp]),
     "trg_synth_lidar_pair": (C.c_int, [C.c_uint64, dp, dp, dp, dp]),
+    "trg_debug_eig": (C.c_int, [C.c_void_p, C.c_int, dp, C.c_int, dp, dp, ip]),
 }
 
 _LIB = None

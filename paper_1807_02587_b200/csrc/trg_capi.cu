@@ -87,6 +87,20 @@ int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out) {
   return TRG_OK;
 }
 
+// Stage N*3 points on the device (no-op when already there).
+int stage_points_public(trg_ctx* ctx, const double* xyz, size_t n, int on_device, int slot,
+                        const double** dev) {
+  if (on_device) {
+    *dev = xyz;
+    return TRG_OK;
+  }
+  void* p = nullptr;
+  TRG_TRY(ws_get(ctx, slot, sizeof(double) * 3 * n, &p));
+  TRG_CU(cudaMemcpyAsync(p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+  *dev = static_cast<const double*>(p);
+  return TRG_OK;
+}
+
 }  // namespace trg
 
 using namespace trg;
@@ -239,19 +253,6 @@ int trg_tree_free(trg_ctx* ctx, trg_tree_dev* t) {
   return TRG_OK;
 }
 
-// Stage N*3 points on the device (no-op when already there).
-static int stage_points(trg_ctx* ctx, const double* xyz, size_t n, int on_device, int slot,
-                        const double** dev) {
-  if (on_device) {
-    *dev = xyz;
-    return TRG_OK;
-  }
-  void* p = nullptr;
-  TRG_TRY(ws_get(ctx, slot, sizeof(double) * 3 * n, &p));
-  TRG_CU(cudaMemcpyAsync(p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
-  *dev = static_cast<const double*>(p);
-  return TRG_OK;
-}
 
 int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, size_t n,
                   int xyz_on_device, const double R[9], const double t[3],
@@ -289,7 +290,7 @@ int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, siz
   p.n = n;
   p.epoch = ++ctx->epoch;
   p.status = ctx->status;
-  TRG_TRY(stage_points(ctx, xyz, n, xyz_on_device, kSlotPoints, &p.pts));
+  TRG_TRY(stage_points_public(ctx, xyz, n, xyz_on_device, kSlotPoints, &p.pts));
   void *part, *stamps, *mom, *cnt, *rt;
   TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * nm * (size_t)J * G, &part));
   TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)J * G, &stamps));

@@ -1,0 +1,371 @@
+// Registration EM resident on the GPU (registration.cpp:47-82, 140-209):
+// one persistent cooperative kernel runs every iteration -- E-step
+// (K7 descent + deterministic per-CTA reduction), node combine + virtual
+// point rows, single-block 6-DoF solve (K8), T <- delta o T, convergence and
+// degenerate-streak control -- with grid barriers between phases, so the
+// host never sees an iteration boundary.
+#include <cstdio>
+#include <vector>
+
+#include "trg_solve.cuh"
+
+namespace trg {
+
+struct EmState {
+  double Rt[12];        // running transform (R row-major, t)
+  double trans_limit;   // translation_tol * diag
+  int done, converged, iterations, fails;
+};
+
+struct EmParams {
+  AssocParams a;
+  double* moments;  // [J][4]
+  double* cta_acc;  // [G][kNormalEq + 2]
+  unsigned* bar;
+  EmState* st;
+  double* crit_before;
+  double* crit_after;
+  unsigned long long* evals;
+  int max_iters;
+  double rot_tol;
+  uint32_t epoch0;
+};
+
+constexpr int kAccStride = kNormalEq + 2;
+
+__global__ void __launch_bounds__(kAssocBlock, 2) k_register(EmParams p) {
+  __shared__ AssocSmem<4> sm;
+  __shared__ SolveSmem ss;
+  __shared__ double rt[12];
+  __shared__ int done;
+  __shared__ double red[kAccStride];
+  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int J = p.a.n_nodes;
+  const double n_total = (double)p.a.n;
+  for (int it = 0; it < p.max_iters; ++it) {
+    if (tid < 12) rt[tid] = ldcg(&p.st->Rt[tid]);
+    if (tid == 0) done = __ldcg(&p.st->done);
+    __syncthreads();
+    if (done) break;
+    // ---- P1: E-step over this CTA's point tiles
+    AssocParams a = p.a;
+    a.epoch = p.epoch0 + (uint32_t)it;
+    assoc_pass<4>(sm, a, rt, G, cta);
+    grid_sync(p.bar, G);
+    // ---- P2: per-node combine over CTAs + virtual-point rows
+    SolveAcc acc;
+    acc_zero(acc);
+    for (int j = cta * (kAssocBlock / 32) + warp; j < J; j += G * (kAssocBlock / 32)) {
+      double m[4];
+      combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p.moments[(size_t)j * 4 + k] = m[k];
+        vp_accumulate(a.nodes + j, m[0], m[1], m[2], m[3], n_total, acc, a.status);
+      }
+    }
+    block_reduce_acc(acc, ss);
+    if (tid == 0) {
+      double* o = p.cta_acc + (size_t)cta * kAccStride;
+#pragma unroll
+      for (int k = 0; k < kNormalEq; ++k) o[k] = acc.v[k];
+      o[kNormalEq] = acc.crit;
+      o[kNormalEq + 1] = (double)acc.nvp;
+    }
+    grid_sync(p.bar, G);
+    // ---- P3: CTA 0 solves and updates the transform
+    if (cta == 0) {
+      if (tid < kAccStride) {
+        double s = 0.0;
+        for (int c = 0; c < G; ++c) s += ldcg(p.cta_acc + (size_t)c * kAccStride + tid);
+        red[tid] = s;
+      }
+      __syncthreads();
+      __shared__ SolveOut so;
+      if (tid == 0) {
+        so.crit_before = red[kNormalEq];
+        solve_normal_eq(red, (int)red[kNormalEq + 1], &so);
+      }
+      __syncthreads();
+      double c = 0.0;
+      if (!so.degenerate) {
+        double dRt[12];
+        for (int i = 0; i < 9; ++i) dRt[i] = so.dR[i];
+        for (int i = 0; i < 3; ++i) dRt[9 + i] = so.dt[i];
+        for (int j = tid; j < J; j += blockDim.x) {
+          const double* m = p.moments + (size_t)j * 4;
+          c += crit_term(a.nodes + j, ldcg(m), ldcg(m + 1), ldcg(m + 2), ldcg(m + 3), n_total,
+                         dRt);
+        }
+      }
+      c = block_sum(c, ss);
+      if (tid == 0) {
+        EmState* st = p.st;
+        const unsigned long long ev = atomicExch(&a.counters[1], 0ull);
+        p.evals[it] = ev;
+        st->iterations = it + 1;
+        p.crit_before[it] = so.crit_before;
+        if (!so.degenerate) {
+          p.crit_after[it] = c;
+          // T = delta * T (geometry.hpp:42-47)
+          double nR[9], nt[3];
+          for (int i = 0; i < 3; ++i)
+            for (int jj = 0; jj < 3; ++jj) {
+              double s = so.dR[3 * i] * rt[jj];
+              s += so.dR[3 * i + 1] * rt[3 + jj];
+              s += so.dR[3 * i + 2] * rt[6 + jj];
+              nR[3 * i + jj] = s;
+            }
+          for (int i = 0; i < 3; ++i) {
+            double s = so.dR[3 * i] * rt[9];
+            s += so.dR[3 * i + 1] * rt[10];
+            s += so.dR[3 * i + 2] * rt[11];
+            nt[i] = s + so.dt[i];
+          }
+          for (int k = 0; k < 9; ++k) st->Rt[k] = nR[k];
+          for (int k = 0; k < 3; ++k) st->Rt[9 + k] = nt[k];
+          st->fails = 0;
+          // rotation_angle (geometry.cpp:17-20) and |t| (registration.cpp:68-69)
+          double cth = ((so.dR[0] + so.dR[4]) + so.dR[8] - 1.0) * 0.5;
+          cth = cth < -1.0 ? -1.0 : (cth > 1.0 ? 1.0 : cth);
+          double tn = so.trans[0] * so.trans[0];
+          tn += so.trans[1] * so.trans[1];
+          tn += so.trans[2] * so.trans[2];
+          if (acos(cth) < p.rot_tol && sqrt(tn) < st->trans_limit) {
+            st->converged = 1;
+            st->done = 1;
+          }
+        } else {
+          p.crit_after[it] = so.crit_before;
+          if (++st->fails >= 3) st->done = 1;
+        }
+        __threadfence();
+      }
+      __syncthreads();
+    }
+    grid_sync(p.bar, G);
+  }
+}
+
+// registration.cpp:140-151 tree_extent_estimate (single block; min/max are
+// exact, so the result is bit-identical to the reference).
+__global__ void k_extent(const DNode* __restrict__ nodes, int J, EmState* st, double diag,
+                         double tol) {
+  __shared__ double lo[3][256], hi[3][256];
+  double l[3] = {INFINITY, INFINITY, INFINITY}, h[3] = {-INFINITY, -INFINITY, -INFINITY};
+  if (!(diag > 0.0)) {
+    for (int j = threadIdx.x; j < J; j += blockDim.x) {
+      const DNode& g = nodes[j];
+      if (g.child_count != 0) continue;
+      const double r = 3.0 * sqrt(smax(g.lam[0], 0.0));
+      for (int k = 0; k < 3; ++k) {
+        l[k] = smin(l[k], g.mean[k] - r);
+        h[k] = smax(h[k], g.mean[k] + r);
+      }
+    }
+  }
+  for (int k = 0; k < 3; ++k) {
+    lo[k][threadIdx.x] = l[k];
+    hi[k][threadIdx.x] = h[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double d = diag;
+    if (!(diag > 0.0)) {
+      for (int t = 1; t < blockDim.x; ++t)
+        for (int k = 0; k < 3; ++k) {
+          l[k] = smin(l[k], lo[k][t]);
+          h[k] = smax(h[k], hi[k][t]);
+        }
+      double s = (h[0] - l[0]) * (h[0] - l[0]);
+      s += (h[1] - l[1]) * (h[1] - l[1]);
+      s += (h[2] - l[2]) * (h[2] - l[2]);
+      d = sqrt(s);
+    }
+    st->trans_limit = tol * d;
+  }
+}
+
+__global__ void k_check_finite(const double* __restrict__ p, size_t n3, int* status) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n3;
+       i += (size_t)gridDim.x * blockDim.x)
+    if (!isfinite(p[i])) atomicCAS(status, 0, kEInval);
+}
+
+__global__ void k_solve(const DNode* __restrict__ nodes, int J, const double* __restrict__ mom,
+                        double n_total, SolveOut* out, int* status) {
+  __shared__ SolveSmem ss;
+  block_solve(nodes, J, mom, 4, n_total, out, ss, status);
+}
+
+}  // namespace trg
+
+using namespace trg;
+
+namespace trg {
+int stage_points_public(trg_ctx* ctx, const double* xyz, size_t n, int on_device, int slot,
+                        const double** dev);
+}
+
+namespace {
+
+int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t n,
+           const trg_reg_config* cfg, double target_diag, trg_reg_result* out) {
+  const int J = tree->n_nodes;
+  const int G = persistent_grid(ctx, (const void*)k_register, kAssocBlock, 0);
+  EmParams p{};
+  p.a.nodes = tree->nodes;
+  p.a.n_nodes = J;
+  p.a.root_count = tree->root_count;
+  p.a.depth = tree->max_level;
+  p.a.lambda_c = cfg->variant_kind == TRG_VARIANT_TREE ? 0.0 : cfg->lambda_c;
+  p.a.outlier_floor = 1e-300;
+  p.a.pts = src_dev;
+  p.a.n = n;
+  p.a.status = ctx->status;
+  void *part, *stamps, *mom, *cnt, *em, *tr;
+  TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * 4 * (size_t)J * G, &part));
+  TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)J * G, &stamps));
+  TRG_TRY(ws_get(ctx, kSlotMoments, sizeof(double) * 4 * (size_t)J, &mom));
+  TRG_TRY(ws_get(ctx, kSlotCounters, 64, &cnt));
+  const size_t em_bytes = 256 + sizeof(EmState) + sizeof(double) * kAccStride * G;
+  TRG_TRY(ws_get(ctx, kSlotEm, em_bytes, &em));
+  const int K = cfg->max_em_iterations;
+  TRG_TRY(ws_get(ctx, kSlotEmTrace, (sizeof(double) * 2 + 8) * (size_t)K, &tr));
+  p.a.partials = static_cast<double*>(part);
+  p.a.stamps = static_cast<uint32_t*>(stamps);
+  p.a.counters = static_cast<unsigned long long*>(cnt);
+  p.moments = static_cast<double*>(mom);
+  p.bar = static_cast<unsigned*>(em);
+  p.st = reinterpret_cast<EmState*>(static_cast<char*>(em) + 64);
+  p.cta_acc = reinterpret_cast<double*>(static_cast<char*>(em) + 256);
+  p.crit_before = static_cast<double*>(tr);
+  p.crit_after = p.crit_before + K;
+  p.evals = reinterpret_cast<unsigned long long*>(p.crit_after + K);
+  p.max_iters = K;
+  p.rot_tol = cfg->rotation_tol;
+  p.epoch0 = ctx->epoch + 1;
+  ctx->epoch += (uint32_t)K + 1;
+  EmState st{};
+  for (int k = 0; k < 9; ++k) st.Rt[k] = cfg->initial_R[k];
+  for (int k = 0; k < 3; ++k) st.Rt[9 + k] = cfg->initial_t[k];
+  TRG_CU(cudaMemsetAsync(em, 0, 64, ctx->stream));
+  TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
+  TRG_CU(cudaMemcpyAsync(p.st, &st, sizeof st, cudaMemcpyHostToDevice, ctx->stream));
+  k_check_finite<<<64, 256, 0, ctx->stream>>>(src_dev, 3 * n, ctx->status);
+  k_extent<<<1, 256, 0, ctx->stream>>>(tree->nodes, J, p.st, target_diag, cfg->translation_tol);
+  cudaEvent_t e0, e1;
+  TRG_CU(cudaEventCreate(&e0));
+  TRG_CU(cudaEventCreate(&e1));
+  TRG_CU(cudaEventRecord(e0, ctx->stream));
+  void* args[] = {&p};
+  TRG_CU(cudaLaunchCooperativeKernel((const void*)k_register, G, kAssocBlock, args, 0,
+                                     ctx->stream));
+  TRG_CU(cudaEventRecord(e1, ctx->stream));
+  ctx->launches += 3;
+  TRG_CU(cudaMemcpyAsync(&st, p.st, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<double> cb(K), ca(K);
+  std::vector<unsigned long long> ev(K);
+  TRG_CU(cudaMemcpyAsync(cb.data(), p.crit_before, sizeof(double) * K, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+  TRG_CU(cudaMemcpyAsync(ca.data(), p.crit_after, sizeof(double) * K, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+  TRG_CU(cudaMemcpyAsync(ev.data(), p.evals, sizeof(unsigned long long) * K,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  TRG_TRY(check_status(ctx, "register_with_tree"));
+  for (int k = 0; k < 9; ++k) out->R[k] = st.Rt[k];
+  for (int k = 0; k < 3; ++k) out->t[k] = st.Rt[9 + k];
+  out->iterations = st.iterations;
+  out->converged = st.converged;
+  out->em_seconds = ms * 1e-3;
+  out->model_components = (size_t)J;
+  const int m = std::min(st.iterations, out->trace_capacity);
+  for (int i = 0; i < m; ++i) {
+    if (out->criterion_trace) out->criterion_trace[i] = cb[i];
+    if (out->criterion_after_trace) out->criterion_after_trace[i] = ca[i];
+    if (out->eval_counts) out->eval_counts[i] = ev[i];
+  }
+  return TRG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int trg_solve_mstep(trg_ctx* ctx, const trg_tree_dev* tree, const double* m0, const double* m1,
+                    uint64_t total_points, trg_mstep_solution* out) {
+  if (!tree || tree->n_nodes == 0) {
+    set_error("make_virtual_points: moment/component count mismatch");
+    return TRG_EINVAL;
+  }
+  if (total_points == 0) {
+    set_error("make_virtual_points: no points were associated");
+    return TRG_EINVAL;
+  }
+  TRG_CU(cudaSetDevice(ctx->device));
+  const int J = tree->n_nodes;
+  std::vector<double> h((size_t)J * 4);
+  for (int j = 0; j < J; ++j) {
+    h[4 * j] = m0[j];
+    for (int k = 0; k < 3; ++k) h[4 * j + 1 + k] = m1[3 * j + k];
+  }
+  void *mom, *so;
+  TRG_TRY(ws_get(ctx, kSlotMoments, sizeof(double) * 4 * (size_t)J, &mom));
+  TRG_TRY(ws_get(ctx, kSlotSolve, sizeof(SolveOut), &so));
+  TRG_CU(cudaMemcpyAsync(mom, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice,
+                         ctx->stream));
+  k_solve<<<1, 256, 0, ctx->stream>>>(tree->nodes, J, static_cast<double*>(mom),
+                                      (double)total_points, static_cast<SolveOut*>(so),
+                                      ctx->status);
+  ctx->launches += 1;
+  SolveOut o;
+  TRG_CU(cudaMemcpyAsync(&o, so, sizeof o, cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_TRY(check_status(ctx, "solve_mstep"));
+  out->n_virtual_points = o.nvp;
+  out->condition_estimate = o.cond;
+  if (o.degenerate) {
+    set_error(o.nvp < 3 ? "solve_mstep: fewer than 3 contributing components"
+                        : "solve_mstep: normal equations condition estimate exceeds limit");
+    return TRG_EDEGENERATE;
+  }
+  for (int k = 0; k < 3; ++k) {
+    out->omega[k] = o.omega[k];
+    out->translation[k] = o.trans[k];
+    out->delta_t[k] = o.dt[k];
+  }
+  for (int k = 0; k < 9; ++k) out->delta_R[k] = o.dR[k];
+  out->criterion_before = o.crit_before;
+  out->criterion_after = o.crit_after;
+  return TRG_OK;
+}
+
+int trg_register_with_tree(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, size_t n,
+                           int xyz_on_device, const trg_reg_config* cfg, double target_diag,
+                           trg_reg_result* out) {
+  if (n == 0 || !xyz) {
+    set_error("register: bad source cloud");
+    return TRG_EINVAL;
+  }
+  if (!tree || tree->n_nodes == 0) {
+    set_error("association: empty model");
+    return TRG_EINVAL;
+  }
+  if (cfg->max_em_iterations < 1) {
+    set_error("register: max_em_iterations must be >= 1");
+    return TRG_EINVAL;
+  }
+  TRG_CU(cudaSetDevice(ctx->device));
+  const double* dev = nullptr;
+  TRG_TRY(stage_points_public(ctx, xyz, n, xyz_on_device, kSlotPoints2, &dev));
+  const int rc = run_em(ctx, tree, dev, n, cfg, target_diag, out);
+  if (rc == TRG_EINVAL) set_error("register: bad source cloud");
+  return rc;
+}
+
+}  // extern "C"

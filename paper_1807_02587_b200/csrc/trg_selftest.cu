@@ -1,0 +1,55 @@
+// Diagnostic entry point: runs the device eigen/solve math on caller data so
+// tests can check it bit-for-bit against the host (oracle) arithmetic.
+#include "trg_internal.cuh"
+
+namespace trg {
+__global__ void k_eig_selftest(int n, const double* in, int count, double* evals, double* evecs,
+                               int* status3) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  if (n == 6) {
+    double a[6][6], ev[6], vec[6][6];
+    for (int r = 0; r < 6; ++r)
+      for (int c = 0; c < 6; ++c) a[r][c] = in[36 * i + 6 * r + c];
+    jacobi_eig<6>(a, ev, vec);
+    for (int r = 0; r < 6; ++r) {
+      evals[6 * i + r] = ev[r];
+      for (int c = 0; c < 6; ++c) evecs[36 * i + 6 * r + c] = vec[r][c];
+    }
+  } else {
+    // n == 3: strict eig_sym3 (geometry.cpp:40-79); n == -3: floored at 1e-4
+    double m[3][3], lam[3], ax[3][3];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) m[r][c] = in[9 * i + 3 * r + c];
+    status3[i] = n == 3 ? eig_sym3(m, lam, ax) : eig_sym3_floored(m, 1e-4, lam, ax);
+    for (int r = 0; r < 3; ++r) {
+      evals[3 * i + r] = lam[r];
+      for (int c = 0; c < 3; ++c) evecs[9 * i + 3 * r + c] = ax[r][c];
+    }
+  }
+}
+}  // namespace trg
+
+using namespace trg;
+extern "C" int trg_debug_eig(trg_ctx* ctx, int n, const double* in, int count, double* evals,
+                             double* evecs, int* status3) {
+  const int k = n == 6 ? 6 : 3;
+  double *din, *dev, *dvec;
+  int* dst;
+  TRG_CU(cudaSetDevice(ctx->device));
+  TRG_CU(cudaMalloc(&din, sizeof(double) * k * k * count));
+  TRG_CU(cudaMalloc(&dev, sizeof(double) * k * count));
+  TRG_CU(cudaMalloc(&dvec, sizeof(double) * k * k * count));
+  TRG_CU(cudaMalloc(&dst, sizeof(int) * count));
+  TRG_CU(cudaMemcpy(din, in, sizeof(double) * k * k * count, cudaMemcpyHostToDevice));
+  k_eig_selftest<<<(count + 127) / 128, 128, 0, ctx->stream>>>(n, din, count, dev, dvec, dst);
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  TRG_CU(cudaMemcpy(evals, dev, sizeof(double) * k * count, cudaMemcpyDeviceToHost));
+  TRG_CU(cudaMemcpy(evecs, dvec, sizeof(double) * k * k * count, cudaMemcpyDeviceToHost));
+  if (status3) TRG_CU(cudaMemcpy(status3, dst, sizeof(int) * count, cudaMemcpyDeviceToHost));
+  cudaFree(din);
+  cudaFree(dev);
+  cudaFree(dvec);
+  cudaFree(dst);
+  return TRG_OK;
+}

@@ -7,16 +7,6 @@ int trg_build_tree(trg_ctx*, const double*, size_t, int, const trg_model_config*
   set_error("trg_build_tree: not built yet");
   return TRG_ERUNTIME;
 }
-int trg_solve_mstep(trg_ctx*, const trg_tree_dev*, const double*, const double*, uint64_t,
-                    trg_mstep_solution*) {
-  set_error("trg_solve_mstep: not built yet");
-  return TRG_ERUNTIME;
-}
-int trg_register_with_tree(trg_ctx*, const trg_tree_dev*, const double*, size_t, int,
-                           const trg_reg_config*, double, trg_reg_result*) {
-  set_error("trg_register_with_tree: not built yet");
-  return TRG_ERUNTIME;
-}
 int trg_register_clouds(trg_ctx*, const double*, size_t, const double*, size_t, int,
                         const trg_reg_config*, trg_reg_result*) {
   set_error("trg_register_clouds: not built yet");
