@@ -1,0 +1,1419 @@
+// Tree construction (build_tree, gmm.cpp:584-657) as ONE persistent
+// cooperative kernel: every expansion round processes all frontier nodes of
+// a level at once over a level-wide, node-sorted entry buffer (K1..K6 of
+// SURVEY.md §2b), then leaf calibration (gmm.cpp:523-580) reuses the K7
+// association code.  No float atomics: per-tile partials are combined in
+// tile order by the last-arriving CTA of each node ("last arriver").
+//
+// Round r expands K_r nodes (r = 0: the virtual root over all N points).
+// Phase schedule of a round (I = em_iterations_per_node, default 8):
+//   p = 0          list_moments pass 1 (+ heaviest entry = FPS seed 0)
+//   p = 1          list_moments pass 2; corner seeds + corner init; FPS round 1
+//   p = 2..7       FPS rounds 2..7 (farthest_point_seeds, gmm.cpp:267-303)
+//   corner fit     EM iterations at p = 2..I+1, final pass at p = I+2
+//   FPS fit        init after p = 7, EM at p = 8..I+7, final pass at p = I+8
+//   p = I+9        candidate choice + survivors done; partition count pass
+//   p = I+10       layout: create tree nodes, next round's segments (CTA 0)
+//   p = I+11       partition write pass (skipped in the last round)
+#include <cub/block/block_scan.cuh>
+#include <vector>
+
+#include "trg_solve.cuh"
+
+namespace trg {
+
+constexpr int kTile = 256;     // entries per tile (tiles never span nodes)
+constexpr int kRec = 210;      // doubles per tile partial record
+constexpr int kOffEm = 0;      // EM moments: cand c at c*81: comp*10 + {m0,m1[3],m2[6]}, ll at 80
+constexpr int kOffFin = 162;   // final pass: cand c at 162 + 9c: ll, child_mass[8]
+constexpr int kOffFps = 180;   // FPS argmax: score, index
+constexpr int kOffMom1 = 182;  // m0, m1[3], wmax, wmax index
+constexpr int kOffMom2 = 188;  // m2[6]
+constexpr int kOffCnt = 194;   // partition: count[8], mass[8]
+
+// One mixture component during a node fit (gmm.hpp:12-23 + log weight).
+struct GComp {
+  double w, lw;
+  double mean[3];
+  double axT[9];
+  double lam[3];
+  double log_norm;
+  double cov[9];
+  double pad[3];
+};
+static_assert(sizeof(GComp) == 240, "GComp layout");
+
+struct RoundNodes {  // per expanding node k of a round (ping-pong by round parity)
+  int* tree_id;      // tree node being expanded (-1: virtual root)
+  int* seg;          // entry segment start
+  int* len;          // entry count
+  int* tile0;        // first tile
+  int* ntiles;
+};
+
+struct NodeFit {  // per expanding node k (current round only)
+  double* mass;      // [K]
+  double* ref;       // [K][3]  first entry's point
+  double* mean;      // [K][3]
+  double* scatter;   // [K][9]
+  double* floorv;    // [K]
+  double* seeds;     // [K][8][3] FPS seeds
+  int* wmax_idx;     // [K]
+  GComp* comps;      // [K][2][8]
+  double* final_ll;  // [K][2]
+  double* cmass;     // [K][2][8]
+  int* kept;         // [K]
+  int* ok;           // [K]
+  int* ns;           // [K]
+  int* surv;         // [K][8]
+  double* smass;     // [K][8]  survivor (child) masses
+  double* stotal;    // [K]
+  int* next_seg;     // [K][8]  child segment start in next round (-1: not expanded)
+  unsigned* arrive;  // [K]
+};
+
+struct BuildState {
+  int round, J, done;
+  int Kp[2], Tp[2], Ep[2];  // round sizes by parity
+  int status_overflow;
+  int need_E, need_K, need_T;
+  // calibration
+  int cal_pass;
+  double drift;
+  unsigned long long cal_evals;
+  unsigned long long E_round[8];
+  int K_round[8];
+};
+
+struct BuildParams {
+  const double* pts;
+  size_t n;
+  int L, em_iters;
+  double min_points, eps, abs_floor;
+  // capacities
+  int Kmax, Tmax, Emax;
+  // round buffers (index by parity)
+  double* ex[2];
+  double* ey[2];
+  double* ez[2];
+  double* ew[2];
+  RoundNodes rn[2];
+  int* tile_node[2];
+  int* tile_start[2];
+  int* tile_len[2];
+  NodeFit nf;
+  double* partial;    // [Tmax][kRec]
+  double* nodered;    // [Kmax][kRec] per-node reduced record
+  unsigned* fdone;    // [Kmax] fields reduced (per phase)
+  double* tile_base;  // [Tmax][8] child base offsets within node's child segment
+  double* min_d2;     // [Emax]
+  double* emit;       // [Emax][8]
+  // tree
+  DNode* nodes;
+  double* cov;
+  int capacity;
+  // calibration association
+  AssocParams a;
+  double* cal_moments;  // [J][10]
+  double* cta_drift;    // [G]
+  unsigned* bar;
+  BuildState* st;
+  int* status;
+};
+
+// ----------------------------------------------------------------- helpers
+__device__ __forceinline__ void comp_to_regs(const GComp& c, double r[18]) {
+  r[0] = c.w;
+  r[1] = c.lw;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r[2 + i] = c.mean[i];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) r[5 + i] = c.axT[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r[14 + i] = c.lam[i];
+  r[17] = c.log_norm;
+}
+
+// gmm.cpp:176-178: log w + log_density, or -inf when w == 0.
+__device__ __forceinline__ double comp_log(const double r[18], double x0, double x1, double x2,
+                                           int* status) {
+  if (!(r[0] > 0.0)) return -INFINITY;
+  if (!(r[16] > 0.0)) {
+    atomicCAS(status, 0, kEDomain);
+    return -INFINITY;
+  }
+  const double d0 = x0 - r[2], d1 = x1 - r[3], d2 = x2 - r[4];
+  double p0 = r[5] * d0;
+  p0 += r[6] * d1;
+  p0 += r[7] * d2;
+  double p1 = r[8] * d0;
+  p1 += r[9] * d1;
+  p1 += r[10] * d2;
+  double p2 = r[11] * d0;
+  p2 += r[12] * d1;
+  p2 += r[13] * d2;
+  const double q = p0 * p0 / r[14] + p1 * p1 / r[15] + p2 * p2 / r[16];
+  return r[1] + (r[17] - 0.5 * q);
+}
+
+// set_floored_cov (gmm.cpp:143-150) into a GComp.
+__device__ __forceinline__ int comp_set_cov(GComp& g, const double sc[3][3], double floor_value) {
+  double lam[3], ax[3][3], cov[3][3];
+  const int rc = eig_sym3_floored(sc, floor_value, lam, ax);
+  if (rc) return rc;
+  reconstruct(lam, ax, cov);
+  for (int i = 0; i < 3; ++i) {
+    g.lam[i] = lam[i];
+    for (int j = 0; j < 3; ++j) {
+      g.axT[3 * i + j] = ax[j][i];
+      g.cov[3 * i + j] = cov[i][j];
+    }
+  }
+  g.log_norm = log_norm_of(lam);
+  return kOk;
+}
+
+__device__ __forceinline__ void write_dnode_from_comp(DNode& d, double* cov9, const GComp& g,
+                                                      double w, int level, int parent) {
+  for (int i = 0; i < 3; ++i) d.mean[i] = g.mean[i];
+  for (int i = 0; i < 9; ++i) {
+    d.axT[i] = g.axT[i];
+    cov9[i] = g.cov[i];
+  }
+  for (int i = 0; i < 3; ++i) d.lam[i] = g.lam[i];
+  d.log_norm = g.log_norm;
+  d.weight = w;
+  const double tr = (g.lam[0] + g.lam[1]) + g.lam[2];
+  d.cplx = tr > 0.0 ? g.lam[2] / tr : -1.0;
+  d.first_child = -1;
+  d.child_count = 0;
+  d.level = level;
+  d.parent = parent;
+}
+
+// refresh_eig (gmm.cpp:31-35) of a tree node from its cov.
+__device__ __forceinline__ int refresh_node(DNode& d, const double* cov9) {
+  double m[3][3], lam[3], ax[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) m[i][j] = cov9[3 * i + j];
+  const int rc = eig_sym3(m, lam, ax);
+  if (rc) return rc;
+  for (int i = 0; i < 3; ++i) {
+    d.lam[i] = lam[i];
+    for (int j = 0; j < 3; ++j) d.axT[3 * i + j] = ax[j][i];
+  }
+  d.log_norm = log_norm_of(lam);
+  const double tr = (lam[0] + lam[1]) + lam[2];
+  d.cplx = tr > 0.0 ? lam[2] / tr : -1.0;
+  return kOk;
+}
+
+// Deterministic block sum of NV values per thread; results in out[0..NV) (smem).
+template <int NV>
+__device__ __forceinline__ void block_sum_vec(double v[NV], double (*wsum)[NV], double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) wsum[warp][k] = v[k];
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double s = wsum[0][threadIdx.x];
+    for (int w = 1; w < kTile / 32; ++w) s += wsum[w][threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// (score, index) argmax: larger score, then lower index.
+__device__ __forceinline__ void argmax_merge(double& s, double& i, double s2, double i2) {
+  if (s2 > s || (s2 == s && i2 < i)) {
+    s = s2;
+    i = i2;
+  }
+}
+
+__device__ __forceinline__ void block_argmax(double s, double i, double (*ws)[2], double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double s2 = __shfl_xor_sync(0xffffffffu, s, off);
+    const double i2 = __shfl_xor_sync(0xffffffffu, i, off);
+    argmax_merge(s, i, s2, i2);
+  }
+  if (lane == 0) {
+    ws[warp][0] = s;
+    ws[warp][1] = i;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bs = ws[0][0], bi = ws[0][1];
+    for (int w = 1; w < kTile / 32; ++w) argmax_merge(bs, bi, ws[w][0], ws[w][1]);
+    out[0] = bs;
+    out[1] = bi;
+  }
+  __syncthreads();
+}
+
+struct Phase {
+  bool mom1, mom2, pcount, pwrite, layout;
+  int fps;      // FPS round 1..7 (0 = none)
+  int mode[2];  // per candidate: 0 none, 1 EM, 2 final
+  int em_it[2];
+};
+
+__device__ __forceinline__ Phase phase_of(int p, int I, bool last_round) {
+  Phase ph{};
+  if (p == 0) ph.mom1 = true;
+  if (p == 1) ph.mom2 = true;
+  if (p >= 1 && p <= 7) ph.fps = p;
+  if (p >= 2 && p <= I + 1) {
+    ph.mode[0] = 1;
+    ph.em_it[0] = p - 1;
+  }
+  if (p == I + 2) ph.mode[0] = 2;
+  if (p >= 8 && p <= I + 7) {
+    ph.mode[1] = 1;
+    ph.em_it[1] = p - 7;
+  }
+  if (p == I + 8) ph.mode[1] = 2;
+  if (p == I + 9) ph.pcount = true;
+  if (p == I + 10) ph.layout = true;
+  if (p == I + 11 && !last_round) ph.pwrite = true;
+  return ph;
+}
+
+struct BuildSmem {
+  union {
+    struct {
+      double wsum[kTile / 32][16];
+      double ws2[kTile / 32][2];
+      double red[16];
+      double am[2];
+    } s;
+    struct {
+      double acc[kTile / 32][2][8][11];
+    } e;
+    typename cub::BlockScan<unsigned long long, kTile>::TempStorage scan;
+  } u;
+  int nitems;
+  int item_off[192];
+  int item_kind[192];
+  int tnode, tstart, tlen, tidx;
+  double nref[3], nmean[3], seed[3];
+  GComp comp[2][8];
+  int cand_list[2];
+  int ncand;
+  int surv[8];
+  int ns, kept;
+  double floorv;
+  double drift;
+};
+
+// ----------------------------------------------------------------- tile work
+// Thread-per-entry passes: list_moments 1/2 and one FPS round.
+__device__ void tile_entry_pass(const BuildParams& p, BuildSmem& sm, const Phase& ph, int par,
+                                double* rec) {
+  const int tid = threadIdx.x;
+  const int e = sm.tstart + tid;
+  const bool act = tid < sm.tlen;
+  double x0 = 0, x1 = 0, x2 = 0, w = 0;
+  if (act) {
+    x0 = p.ex[par][e];
+    x1 = p.ey[par][e];
+    x2 = p.ez[par][e];
+    w = p.ew[par][e];
+  }
+  if (ph.mom1) {
+    double v[4] = {0, 0, 0, 0};
+    if (act) {
+      v[0] = w;
+      v[1] = w * (x0 - sm.nref[0]);
+      v[2] = w * (x1 - sm.nref[1]);
+      v[3] = w * (x2 - sm.nref[2]);
+    }
+    block_sum_vec<4>(v, (double(*)[4])sm.u.s.wsum, sm.u.s.red);
+    if (tid < 4) rec[kOffMom1 + tid] = sm.u.s.red[tid];
+    __syncthreads();
+    block_argmax(act ? w : -INFINITY, act ? (double)e : 1e300, sm.u.s.ws2, sm.u.s.am);
+    if (tid == 0) {
+      rec[kOffMom1 + 4] = sm.u.s.am[0];
+      rec[kOffMom1 + 5] = sm.u.s.am[1];
+    }
+    __syncthreads();
+  }
+  if (ph.mom2) {
+    double v[6] = {0, 0, 0, 0, 0, 0};
+    if (act) {
+      const double d0 = x0 - sm.nmean[0], d1 = x1 - sm.nmean[1], d2 = x2 - sm.nmean[2];
+      v[0] = w * (d0 * d0);
+      v[1] = w * (d0 * d1);
+      v[2] = w * (d0 * d2);
+      v[3] = w * (d1 * d1);
+      v[4] = w * (d1 * d2);
+      v[5] = w * (d2 * d2);
+    }
+    block_sum_vec<6>(v, (double(*)[6])sm.u.s.wsum, sm.u.s.red);
+    if (tid < 6) rec[kOffMom2 + tid] = sm.u.s.red[tid];
+    __syncthreads();
+  }
+  if (ph.fps) {
+    double sc = -INFINITY;
+    if (act) {
+      const double a = x0 - sm.seed[0], b = x1 - sm.seed[1], c = x2 - sm.seed[2];
+      double d2 = a * a;
+      d2 += b * b;
+      d2 += c * c;
+      const double md = ph.fps == 1 ? d2 : smin(p.min_d2[e], d2);
+      p.min_d2[e] = md;
+      sc = w * md;
+    }
+    block_argmax(sc, act ? (double)e : 1e300, sm.u.s.ws2, sm.u.s.am);
+    if (tid == 0) {
+      rec[kOffFps] = sm.u.s.am[0];
+      rec[kOffFps + 1] = sm.u.s.am[1];
+    }
+    __syncthreads();
+  }
+}
+
+// Lane-per-component E-step over the tile for the active candidates
+// (e_step_moments gmm.cpp:159-206, final pass :331-358, partition :430-454).
+// mode_pc: 0 = per phase modes, 3 = partition count (kept candidate).
+__device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase& ph, int par,
+                               double* rec, bool pcount) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nc = pcount ? 1 : sm.ncand;
+  const int gsz = 8 * nc;          // lanes per entry
+  const int per_step = 32 / gsz;   // entries per warp step
+  const int comp = lane & 7;
+  const int ci = (lane >> 3) % nc;  // index into active candidate list
+  const int cand = pcount ? sm.kept : sm.cand_list[ci];
+  const int mode = pcount ? 3 : ph.mode[cand];
+  const int gbase = lane & ~7;  // first lane of my 8-lane group
+  double r[18];
+  comp_to_regs(sm.comp[cand][comp], r);
+  // survivor slot of my component (partition)
+  int my_s = -1;
+  if (pcount)
+    for (int s = 0; s < sm.ns; ++s)
+      if (sm.surv[s] == comp) my_s = s;
+  double acc[11];
+#pragma unroll
+  for (int k = 0; k < 11; ++k) acc[k] = 0.0;
+  const int slot = lane / gsz;
+  // entries of this warp: [warp*32, warp*32+32) of the tile
+  for (int base = warp * 32; base < warp * 32 + 32; base += per_step) {
+    const int ei = base + slot;
+    const bool act = ei < sm.tlen;
+    const int e = sm.tstart + ei;
+    double x0 = 0, x1 = 0, x2 = 0, w = 0;
+    if (act) {
+      x0 = p.ex[par][e];
+      x1 = p.ey[par][e];
+      x2 = p.ez[par][e];
+      w = p.ew[par][e];
+    }
+    const double lg = act ? comp_log(r, x0, x1, x2, p.status) : -INFINITY;
+    // max over the 8 components (order-free)
+    double m = lg;
+#pragma unroll
+    for (int off = 1; off < 8; off <<= 1) m = smax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    // gather the 8 log-terms; sum exps in component order (gmm.cpp:183)
+    double lgs[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) lgs[k] = __shfl_sync(0xffffffffu, lg, gbase + k);
+    if (!act) continue;
+    if (!isfinite(m)) {
+      // gmm.cpp:348: the entry keeps gamma = 0; the partition then hands it
+      // whole to the heaviest survivor (gmm.cpp:444-453)
+      if (mode == 3 && my_s >= 0) {
+        int best = 0;
+        for (int s2 = 1; s2 < sm.ns; ++s2)
+          if (p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[s2]] >
+              p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[best]])
+            best = s2;
+        p.emit[(size_t)e * 8 + my_s] = my_s == best ? w : 0.0;
+        if (my_s == best) {
+          acc[0] += 1.0;
+          acc[1] += w;
+        }
+      }
+      continue;  // uniform within the 8-lane group
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += exp(lgs[k] - m);
+    const double lt = m + log(s);
+    const double gam = exp(lg - lt);
+    if (mode == 1) {
+      if (comp == 0) acc[10] += w * lt;
+      const double g = gam * w;
+      if (g > 0.0) {
+        const double d0 = x0 - sm.nmean[0], d1 = x1 - sm.nmean[1], d2 = x2 - sm.nmean[2];
+        acc[0] += g;
+        acc[1] += g * d0;
+        acc[2] += g * d1;
+        acc[3] += g * d2;
+        acc[4] += g * (d0 * d0);
+        acc[5] += g * (d0 * d1);
+        acc[6] += g * (d0 * d2);
+        acc[7] += g * (d1 * d1);
+        acc[8] += g * (d1 * d2);
+        acc[9] += g * (d2 * d2);
+      }
+    } else if (mode == 2) {
+      if (comp == 0) acc[10] += w * lt;
+      acc[0] += w * gam;
+    } else if (mode == 3) {
+      // survivor-normalised soft partition (gmm.cpp:434-454)
+      double denom = 0.0;
+      for (int s2 = 0; s2 < sm.ns; ++s2) denom += exp(lgs[sm.surv[s2]] - lt);
+      double* em = p.emit + (size_t)e * 8;
+      if (denom > 0.0) {
+        if (my_s >= 0) {
+          const double g = gam / denom;
+          double out = 0.0;
+          if (!(g < 1e-12)) {
+            out = w * g;
+            acc[0] += 1.0;
+            acc[1] += out;
+          }
+          em[my_s] = out;
+        }
+      } else {
+        int best = 0;
+        for (int s2 = 1; s2 < sm.ns; ++s2)
+          if (p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[s2]] >
+              p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[best]])
+            best = s2;
+        if (my_s >= 0) {
+          const double out = my_s == best ? w : 0.0;
+          if (my_s == best) {
+            acc[0] += 1.0;
+            acc[1] += w;
+          }
+          em[my_s] = out;
+        }
+      }
+    }
+  }
+  // reduce over entry slots (lanes with the same (cand, comp))
+#pragma unroll
+  for (int off = gsz; off < 32; off <<= 1)
+#pragma unroll
+    for (int k = 0; k < 11; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+  if (lane < gsz)
+#pragma unroll
+    for (int k = 0; k < 11; ++k) sm.u.e.acc[warp][ci][comp][k] = acc[k];
+  __syncthreads();
+  // combine warps in order
+  for (int idx = tid; idx < nc * 8 * 11; idx += blockDim.x) {
+    const int c2 = idx / 88, cm = (idx / 11) % 8, k = idx % 11;
+    double s = sm.u.e.acc[0][c2][cm][k];
+    for (int w2 = 1; w2 < kTile / 32; ++w2) s += sm.u.e.acc[w2][c2][cm][k];
+    const int cand2 = pcount ? sm.kept : sm.cand_list[c2];
+    const int md = pcount ? 3 : ph.mode[cand2];
+    if (md == 1) {
+      if (k < 10) rec[kOffEm + cand2 * 81 + cm * 10 + k] = s;
+      else if (cm == 0) rec[kOffEm + cand2 * 81 + 80] = s;
+    } else if (md == 2) {
+      if (k == 0) rec[kOffFin + cand2 * 9 + 1 + cm] = s;
+      else if (k == 10 && cm == 0) rec[kOffFin + cand2 * 9] = s;
+    } else if (md == 3) {
+      if (k == 0) rec[kOffCnt + cm] = s;      // indexed by comp; remapped below
+      else if (k == 1) rec[kOffCnt + 8 + cm] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// ----------------------------------------------------------------- node work
+// M-step for candidate c of node k (thread `comp` of the last arriver).
+__device__ void node_mstep(const BuildParams& p, int k, int c, const double* red, int comp) {
+  GComp* comps = p.nf.comps + ((size_t)k * 2 + c) * 8;
+  const double* ac = red + kOffEm + c * 81;
+  double total = 0.0;
+  for (int j = 0; j < 8; ++j) total += __ldcg(ac + j * 10);
+  if (!(total > 0.0)) {
+    atomicCAS(p.status, 0, kERuntime);  // m_step: no responsibility mass
+    return;
+  }
+  double a[10];
+  for (int q = 0; q < 10; ++q) a[q] = __ldcg(ac + comp * 10 + q);
+  GComp& g = comps[comp];
+  if (a[0] <= total * 1e-12) {
+    g.w = 0.0;
+    return;
+  }
+  const double m0 = a[0];
+  const double d[3] = {a[1] / m0, a[2] / m0, a[3] / m0};
+  const double m2[3][3] = {{a[4], a[5], a[6]}, {a[5], a[7], a[8]}, {a[6], a[8], a[9]}};
+  double sc[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) sc[i][j] = m2[i][j] / m0 - d[i] * d[j];
+  g.w = m0 / total;
+  g.lw = log(g.w);
+  const double* mean = p.nf.mean + 3 * k;
+  for (int i = 0; i < 3; ++i) g.mean[i] = mean[i] + d[i];
+  if (comp_set_cov(g, sc, p.nf.floorv[k])) atomicCAS(p.status, 0, kEInval);
+}
+
+// Candidate init (fit_candidate gmm.cpp:319-326) for component `comp`.
+__device__ void cand_init(const BuildParams& p, int k, int c, const double seed[3], int comp) {
+  GComp& g = p.nf.comps[((size_t)k * 2 + c) * 8 + comp];
+  g.w = 1.0 / 8.0;
+  g.lw = log(g.w);
+  for (int i = 0; i < 3; ++i) g.mean[i] = seed[i];
+  double cs[3][3];
+  const double* S = p.nf.scatter + 9 * k;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) cs[i][j] = S[3 * i + j] / 4.0;
+  if (comp_set_cov(g, cs, p.nf.floorv[k])) atomicCAS(p.status, 0, kEInval);
+}
+
+// Node work after phase ph, done by ONE warp (the warp that reduced the
+// node's last field); `red` is the node's reduced record (global, L2).
+__device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, int par,
+                                 const double* red, int round) {
+  const int lane = threadIdx.x & 31;
+  const NodeFit& nf = p.nf;
+  if (ph.mom1 && lane == 0) {
+    const double mass = __ldcg(red + kOffMom1);
+    nf.mass[k] = mass;
+    if (!(mass > 0.0)) atomicCAS(p.status, 0, kEInval);  // list_moments: no mass
+    for (int i = 0; i < 3; ++i)
+      nf.mean[3 * k + i] = nf.ref[3 * k + i] + __ldcg(red + kOffMom1 + 1 + i) / mass;
+    const int e0 = (int)__ldcg(red + kOffMom1 + 5);
+    nf.wmax_idx[k] = e0;
+    nf.seeds[24 * k + 0] = p.ex[par][e0];
+    nf.seeds[24 * k + 1] = p.ey[par][e0];
+    nf.seeds[24 * k + 2] = p.ez[par][e0];
+  }
+  if (ph.mom2) {
+    if (lane == 0) {
+      const double mass = nf.mass[k];
+      double m[6];
+      for (int q = 0; q < 6; ++q) m[q] = __ldcg(red + kOffMom2 + q);
+      const double M[3][3] = {{m[0], m[1], m[2]}, {m[1], m[3], m[4]}, {m[2], m[4], m[5]}};
+      double S[3][3];
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+          S[i][j] = M[i][j] / mass;
+          nf.scatter[9 * k + 3 * i + j] = S[i][j];
+        }
+      nf.floorv[k] = cov_floor(S, p.eps, p.abs_floor);
+    }
+    __syncwarp();
+    // corner seeds (gmm.cpp:248-261): lane c computes seed c
+    if (lane < 8) {
+      double S[3][3], lam[3], ax[3][3];
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) S[i][j] = nf.scatter[9 * k + 3 * i + j];
+      if (eig_sym3_floored(S, nf.floorv[k], lam, ax)) atomicCAS(p.status, 0, kEInval);
+      double off[3] = {0.0, 0.0, 0.0};
+      for (int l = 0; l < 3; ++l) {
+        const double sign = ((lane >> l) & 1) != 0 ? 1.0 : -1.0;
+        const double sc = sign * 0.5 * sqrt(lam[l]);
+        for (int i = 0; i < 3; ++i) off[i] = off[i] + sc * ax[i][l];
+      }
+      double seed[3];
+      for (int i = 0; i < 3; ++i) seed[i] = nf.mean[3 * k + i] + off[i];
+      cand_init(p, k, 0, seed, lane);
+    }
+    __syncwarp();
+  }
+  if (ph.fps && lane == 0) {
+    const double bs = __ldcg(red + kOffFps);
+    double* sd = nf.seeds + 24 * k;
+    if (!(bs > 0.0)) {  // degenerate support: duplicate seed 0 (gmm.cpp:291-294)
+      for (int i = 0; i < 3; ++i) sd[3 * ph.fps + i] = sd[i];
+    } else {
+      const int e = (int)__ldcg(red + kOffFps + 1);
+      sd[3 * ph.fps + 0] = p.ex[par][e];
+      sd[3 * ph.fps + 1] = p.ey[par][e];
+      sd[3 * ph.fps + 2] = p.ez[par][e];
+    }
+  }
+  __syncwarp();
+  if (ph.fps == 7 && lane < 8) {
+    double seed[3];
+    for (int i = 0; i < 3; ++i) seed[i] = nf.seeds[24 * k + 3 * lane + i];
+    cand_init(p, k, 1, seed, lane);
+  }
+  // M-steps: lanes 0-7 candidate 0, lanes 8-15 candidate 1
+  if (lane < 16) {
+    const int c = lane >> 3;
+    if (ph.mode[c] == 1) node_mstep(p, k, c, red, lane & 7);
+  }
+  if (lane < 2 && ph.mode[lane] == 2) {
+    const int c = lane;
+    nf.final_ll[2 * k + c] = __ldcg(red + kOffFin + 9 * c);
+    for (int j = 0; j < 8; ++j) nf.cmass[16 * k + 8 * c + j] = __ldcg(red + kOffFin + 9 * c + 1 + j);
+  }
+  __syncwarp();
+  if (ph.mode[1] == 2 && lane == 0) {
+    // candidate choice (gmm.cpp:394) and survivors (gmm.cpp:414-428)
+    const int kept = (nf.final_ll[2 * k + 1] > nf.final_ll[2 * k + 0]) ? 1 : 0;
+    nf.kept[k] = kept;
+    const double* cm = nf.cmass + 16 * k + 8 * kept;
+    const double thr = smax(4.0, nf.mass[k] * 1e-6);
+    int ns = 0;
+    for (int j = 0; j < 8; ++j)
+      if (cm[j] > thr) nf.surv[8 * k + ns++] = j;
+    int ok = 1;
+    if (ns == 0) {
+      if (round != 0) {
+        ok = 0;
+      } else {
+        int best = 0;
+        for (int j = 1; j < 8; ++j)
+          if (cm[j] > cm[best]) best = j;
+        nf.surv[8 * k + ns++] = best;
+      }
+    }
+    nf.ns[k] = ok ? ns : 0;
+    nf.ok[k] = ok;
+  }
+  if (ph.pcount) {
+    // per-child totals + per-tile child base offsets (stable order); lane s
+    const int ns = nf.ns[k];
+    if (lane < ns) {
+      const int s = lane;
+      const int comp = nf.surv[8 * k + s];
+      const int t0 = p.rn[par].tile0[k], nt = p.rn[par].ntiles[k];
+      double base = 0.0;
+      for (int t = 0; t < nt; ++t) {
+        p.tile_base[(size_t)(t0 + t) * 8 + s] = base;
+        base += __ldcg(p.partial + (size_t)(t0 + t) * kRec + kOffCnt + comp);
+      }
+      nf.next_seg[8 * k + s] = (int)base;  // child entry count (layout turns it into a segment)
+      nf.smass[8 * k + s] = __ldcg(red + kOffCnt + 8 + comp);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double total = 0.0;
+      for (int s = 0; s < ns; ++s) total += nf.smass[8 * k + s];
+      nf.stotal[k] = total;
+    }
+  }
+  __syncwarp();
+}
+
+// Node-level context of the tile about to be processed (smem).
+__device__ void load_tile_ctx(const BuildParams& p, BuildSmem& sm, const Phase& ph, int par,
+                              int t) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    sm.tidx = t;
+    sm.tnode = p.tile_node[par][t];
+    sm.tstart = p.tile_start[par][t];
+    sm.tlen = p.tile_len[par][t];
+  }
+  __syncthreads();
+  const int k = sm.tnode;
+  if (tid < 3) {
+    if (ph.mom1) {
+      const int e0 = p.rn[par].seg[k];
+      const double v = tid == 0 ? p.ex[par][e0] : (tid == 1 ? p.ey[par][e0] : p.ez[par][e0]);
+      sm.nref[tid] = v;
+      p.nf.ref[3 * k + tid] = v;
+    }
+    sm.nmean[tid] = p.nf.mean[3 * k + tid];
+    if (ph.fps) sm.seed[tid] = p.nf.seeds[24 * k + 3 * (ph.fps - 1) + tid];
+  }
+  if (tid == 0) {
+    int nc = 0;
+    for (int c = 0; c < 2; ++c)
+      if (ph.mode[c]) sm.cand_list[nc++] = c;
+    sm.ncand = nc;
+    if (ph.pcount) {
+      sm.kept = p.nf.kept[k];
+      sm.ns = p.nf.ns[k];
+      for (int s = 0; s < sm.ns; ++s) sm.surv[s] = p.nf.surv[8 * k + s];
+    }
+  }
+  const bool need_comps = ph.mode[0] || ph.mode[1] || ph.pcount;
+  if (need_comps) {
+    // 2 x 8 components
+    constexpr int kD = (int)(sizeof(GComp) / sizeof(double));
+    const double* src = reinterpret_cast<const double*>(p.nf.comps + (size_t)k * 16);
+    double* dst = reinterpret_cast<double*>(&sm.comp[0][0]);
+    for (int i = tid; i < 16 * kD; i += blockDim.x) dst[i] = __ldcg(src + i);
+  }
+  __syncthreads();
+}
+
+// Partition write (gmm.cpp:441-442): stable compaction of one tile into the
+// next round's node-sorted entry buffer.
+__device__ void tile_pwrite(const BuildParams& p, BuildSmem& sm, int par, int t) {
+  const int tid = threadIdx.x;
+  const int k = sm.tnode;
+  const int ns = p.nf.ns[k];
+  const bool act = tid < sm.tlen;
+  const int e = sm.tstart + tid;
+  double em[8];
+  unsigned long long f0 = 0, f1 = 0;
+  for (int s = 0; s < 8; ++s) {
+    em[s] = (act && s < ns) ? p.emit[(size_t)e * 8 + s] : 0.0;
+    const unsigned long long bit = em[s] > 0.0 ? 1ull : 0ull;
+    if (s < 4) f0 |= bit << (16 * s);
+    else f1 |= bit << (16 * (s - 4));
+  }
+  using Scan = cub::BlockScan<unsigned long long, kTile>;
+  unsigned long long r0, r1;
+  Scan(sm.u.scan).ExclusiveSum(f0, r0);
+  __syncthreads();
+  Scan(sm.u.scan).ExclusiveSum(f1, r1);
+  __syncthreads();
+  if (!act) return;
+  const int npar = par ^ 1;
+  for (int s = 0; s < ns; ++s) {
+    if (!(em[s] > 0.0)) continue;
+    const int cs = p.nf.next_seg[8 * k + s];
+    if (cs < 0) continue;
+    const unsigned long long rr = s < 4 ? r0 : r1;
+    const int rank = (int)((rr >> (16 * (s & 3))) & 0xffffull);
+    const int pos = cs + (int)p.tile_base[(size_t)t * 8 + s] + rank;
+    p.ex[npar][pos] = p.ex[par][e];
+    p.ey[npar][pos] = p.ey[par][e];
+    p.ez[npar][pos] = p.ez[par][e];
+    p.ew[npar][pos] = em[s];
+  }
+}
+
+// Layout (CTA 0): create this round's child tree nodes, choose the next
+// round's expanding set (mass gate gmm.cpp:621-623), segments and tiles.
+__device__ void round_layout(const BuildParams& p, int par, int round, BuildSmem& sm) {
+  if (threadIdx.x != 0) return;
+  BuildState* st = p.st;
+  const int K = st->Kp[par];
+  int J = st->J;
+  const int npar = par ^ 1;
+  int K2 = 0, E2 = 0, T2 = 0, needK = 0, needE = 0, needT = 0;
+  const bool last = round + 1 >= p.L;
+  for (int k = 0; k < K; ++k) {
+    const int ns = p.nf.ns[k];
+    if (!p.nf.ok[k] || ns == 0) continue;
+    const int parent = p.rn[par].tree_id[k];
+    if (J + ns > p.capacity) {
+      atomicCAS(p.status, 0, kERuntime);
+      return;
+    }
+    if (parent >= 0) {
+      p.nodes[parent].first_child = J;
+      p.nodes[parent].child_count = ns;
+    }
+    const int kept = p.nf.kept[k];
+    for (int s = 0; s < ns; ++s) {
+      const GComp& g = p.nf.comps[((size_t)k * 2 + kept) * 8 + p.nf.surv[8 * k + s]];
+      const double w = p.nf.smass[8 * k + s] / p.nf.stotal[k];
+      write_dnode_from_comp(p.nodes[J], p.cov + 9 * (size_t)J, g, w, round, parent);
+      const int cnt = p.nf.next_seg[8 * k + s];  // child entry count (from pcount)
+      int seg = -1;
+      if (!last && !(p.nf.smass[8 * k + s] < p.min_points)) {
+        needK += 1;
+        needE += cnt;
+        needT += (cnt + kTile - 1) / kTile;
+        if (K2 >= p.Kmax || E2 + cnt > p.Emax) {
+          st->status_overflow = 1;
+        } else {
+          seg = E2;
+          const int nt = (cnt + kTile - 1) / kTile;
+          p.rn[npar].tree_id[K2] = J;
+          p.rn[npar].seg[K2] = E2;
+          p.rn[npar].len[K2] = cnt;
+          p.rn[npar].tile0[K2] = T2;
+          p.rn[npar].ntiles[K2] = nt;
+          if (T2 + nt > p.Tmax) st->status_overflow = 1;
+          else
+            for (int t = 0; t < nt; ++t) {
+              p.tile_node[npar][T2 + t] = K2;
+              p.tile_start[npar][T2 + t] = E2 + t * kTile;
+              p.tile_len[npar][T2 + t] = min(kTile, cnt - t * kTile);
+            }
+          ++K2;
+          E2 += cnt;
+          T2 += nt;
+        }
+      }
+      p.nf.next_seg[8 * k + s] = seg;
+      ++J;
+    }
+  }
+  st->J = J;
+  if (!last && st->status_overflow) {
+    st->need_K = needK;
+    st->need_E = needE;
+    st->need_T = needT;
+  }
+  st->round = round + 1;
+  st->Kp[npar] = K2;
+  st->Ep[npar] = E2;
+  st->Tp[npar] = T2;
+  if (round + 1 < 8) {
+    st->E_round[round + 1] = (unsigned long long)E2;
+    st->K_round[round + 1] = K2;
+  }
+  if (last || K2 == 0) st->done = 1;
+  __threadfence();
+  (void)sm;
+}
+
+// reset_parents_to_child_moments (gmm.cpp:489-513), CTA 0, thread 0.
+__device__ void reset_parents(const BuildParams& p, int J) {
+  for (int l = p.L - 2; l >= 0; --l)
+    for (int i = 0; i < J; ++i) {
+      DNode& nd = p.nodes[i];
+      if (nd.level != l || nd.child_count == 0) continue;
+      double w = 0.0, mu[3] = {0.0, 0.0, 0.0};
+      for (int c = 0; c < nd.child_count; ++c) {
+        const DNode& ch = p.nodes[nd.first_child + c];
+        w += ch.weight;
+        for (int k = 0; k < 3; ++k) mu[k] = mu[k] + ch.weight * ch.mean[k];
+      }
+      if (!(w > 0.0)) continue;
+      for (int k = 0; k < 3; ++k) mu[k] = mu[k] / w;
+      double cov[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int c = 0; c < nd.child_count; ++c) {
+        const int ci = nd.first_child + c;
+        const DNode& ch = p.nodes[ci];
+        const double d[3] = {ch.mean[0] - mu[0], ch.mean[1] - mu[1], ch.mean[2] - mu[2]};
+        for (int r = 0; r < 3; ++r)
+          for (int s = 0; s < 3; ++s)
+            cov[3 * r + s] = cov[3 * r + s] + ch.weight * (p.cov[9 * (size_t)ci + 3 * r + s] + d[r] * d[s]);
+      }
+      for (int k = 0; k < 9; ++k) p.cov[9 * (size_t)i + k] = cov[k] / w;
+      for (int k = 0; k < 3; ++k) nd.mean[k] = mu[k];
+    }
+}
+
+// ----------------------------------------------------------------- kernel
+// Field items reduced per node after a phase: (offset, kind 0 = sum,
+// kind 1 = (score, index) argmax pair).
+__device__ int phase_items(const Phase& ph, int* off, int* kind) {
+  int n = 0;
+  auto sum_range = [&](int o, int c) {
+    for (int i = 0; i < c; ++i) {
+      off[n] = o + i;
+      kind[n++] = 0;
+    }
+  };
+  if (ph.mom1) {
+    sum_range(kOffMom1, 4);
+    off[n] = kOffMom1 + 4;
+    kind[n++] = 1;
+  }
+  if (ph.mom2) sum_range(kOffMom2, 6);
+  if (ph.fps) {
+    off[n] = kOffFps;
+    kind[n++] = 1;
+  }
+  for (int c = 0; c < 2; ++c) {
+    if (ph.mode[c] == 1) sum_range(kOffEm + 81 * c, 81);
+    if (ph.mode[c] == 2) sum_range(kOffFin + 9 * c, 9);
+  }
+  if (ph.pcount) sum_range(kOffCnt + 8, 8);
+  return n;
+}
+
+// Sum (or argmax-merge) field item `f` of node k over its tiles, one warp;
+// lane-strided then butterfly: fixed order, deterministic.
+__device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k, int off,
+                                            int kind) {
+  const int lane = threadIdx.x & 31;
+  const int t0 = p.rn[par].tile0[k], nt = p.rn[par].ntiles[k];
+  double* out = p.nodered + (size_t)k * kRec;
+  if (kind == 0) {
+    double v = 0.0;
+    for (int q = lane; q < nt; q += 32) v += __ldcg(p.partial + (size_t)(t0 + q) * kRec + off);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) out[off] = v;
+  } else {
+    double bs = -INFINITY, bi = 1e300;
+    for (int q = lane; q < nt; q += 32)
+      argmax_merge(bs, bi, __ldcg(p.partial + (size_t)(t0 + q) * kRec + off),
+                   __ldcg(p.partial + (size_t)(t0 + q) * kRec + off + 1));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+      const double i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      argmax_merge(bs, bi, s2, i2);
+    }
+    if (lane == 0) {
+      out[off] = bs;
+      out[off + 1] = bi;
+    }
+  }
+}
+
+constexpr size_t kBuildSmemBytes =
+    sizeof(BuildSmem) > sizeof(AssocSmem<10>) ? sizeof(BuildSmem) : sizeof(AssocSmem<10>);
+
+__global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
+  __shared__ __align__(16) unsigned char smem_raw[kBuildSmemBytes];
+  BuildSmem& sm = *reinterpret_cast<BuildSmem*>(smem_raw);
+  AssocSmem<10>& asm_ = *reinterpret_cast<AssocSmem<10>*>(smem_raw);
+  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  BuildState* st = p.st;
+  // ------------------------------------------------ expansion rounds
+  for (int round = 0; round < p.L; ++round) {
+    const int par = round & 1;
+    const bool last_round = round + 1 >= p.L;
+    const int nphase = p.em_iters + 12;
+    for (int ph_i = 0; ph_i < nphase; ++ph_i) {
+      const Phase ph = phase_of(ph_i, p.em_iters, last_round);
+      if (!(ph.mom1 || ph.mom2 || ph.fps || ph.mode[0] || ph.mode[1] || ph.pcount || ph.layout ||
+            ph.pwrite))
+        continue;
+      if (ph.layout) {
+        if (cta == 0) round_layout(p, par, round, sm);
+        grid_sync(p.bar, G);
+        continue;
+      }
+      // (a) tile pass
+      const int T = __ldcg(&st->Tp[par]);
+      for (int t = cta; t < T; t += G) {
+        load_tile_ctx(p, sm, ph, par, t);
+        if (ph.pwrite) {
+          tile_pwrite(p, sm, par, t);
+        } else {
+          double* rec = p.partial + (size_t)t * kRec;
+          tile_entry_pass(p, sm, ph, par, rec);
+          if (ph.mode[0] || ph.mode[1]) tile_comp_pass(p, sm, ph, par, rec, false);
+          if (ph.pcount) tile_comp_pass(p, sm, ph, par, rec, true);
+        }
+        __syncthreads();
+      }
+      grid_sync(p.bar, G);
+      if (ph.pwrite) continue;
+      // (b) per-node reduction of the tile records + node update
+      if (tid == 0) sm.nitems = phase_items(ph, sm.item_off, sm.item_kind);
+      __syncthreads();
+      const int NI = sm.nitems;
+      const int K = __ldcg(&st->Kp[par]);
+      for (int it = cta * (kTile / 32) + warp; it < K * NI; it += G * (kTile / 32)) {
+        const int k = it / NI, f = it % NI;
+        reduce_item(p, par, k, sm.item_off[f], sm.item_kind[f]);
+        unsigned last = 0;
+        if (lane == 0) {
+          __threadfence();
+          last = (atomicAdd(&p.fdone[k], 1u) == (unsigned)NI - 1) ? 1u : 0u;
+          if (last) {
+            p.fdone[k] = 0u;
+            __threadfence();
+          }
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
+      }
+      grid_sync(p.bar, G);
+    }
+    if (__ldcg(&st->done) || __ldcg(&st->status_overflow)) break;
+  }
+  if (__ldcg(&st->status_overflow)) return;
+  const int J = __ldcg(&st->J);
+  // ------------------------------------------------ rematch + refresh_eig
+  if (cta == 0 && tid == 0) reset_parents(p, J);
+  grid_sync(p.bar, G);
+  for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x)
+    if (refresh_node(p.nodes[j], p.cov + 9 * (size_t)j)) atomicCAS(p.status, 0, kEInval);
+  grid_sync(p.bar, G);
+  // ------------------------------------------------ leaf calibration
+  int root_count = 0;
+  {
+    // level-0 prefix
+    __shared__ int rc;
+    if (tid == 0) {
+      int c = 0;
+      while (c < J && p.nodes[c].level == 0) ++c;
+      rc = c;
+    }
+    __syncthreads();
+    root_count = rc;
+  }
+  for (int pass = 0; pass < 40; ++pass) {
+    if (!(__ldcg(&st->drift) > 1e-13)) break;  // gmm.cpp:652
+    AssocParams a = p.a;
+    a.n_nodes = J;
+    a.root_count = root_count;
+    a.epoch = p.a.epoch + (uint32_t)pass;
+    assoc_pass<10>(asm_, a, nullptr, G, cta);
+    grid_sync(p.bar, G);
+    // combine + leaf refit (calibrate_pass gmm.cpp:532-545)
+    const int lane = tid & 31, warp = tid >> 5;
+    double drift = 0.0;
+    for (int j = cta * (kTile / 32) + warp; j < J; j += G * (kTile / 32)) {
+      double m[10];
+      combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
+      if (lane == 0) {
+        for (int q = 0; q < 10; ++q) p.cal_moments[(size_t)j * 10 + q] = m[q];
+        DNode& nd = p.nodes[j];
+        if (nd.child_count == 0 && m[0] > 0.0) {
+          const double mu[3] = {m[1] / m[0], m[2] / m[0], m[3] / m[0]};
+          const double M[3][3] = {{m[4], m[5], m[6]}, {m[5], m[7], m[8]}, {m[6], m[8], m[9]}};
+          double S[3][3], S2[3][3];
+          for (int r = 0; r < 3; ++r)
+            for (int s = 0; s < 3; ++s) S[r][s] = M[r][s] / m[0] - mu[r] * mu[s];
+          for (int r = 0; r < 3; ++r)
+            for (int s = 0; s < 3; ++s) S2[r][s] = 0.5 * (S[r][s] + S[s][r]);
+          double dm = (nd.mean[0] - mu[0]) * (nd.mean[0] - mu[0]);
+          dm += (nd.mean[1] - mu[1]) * (nd.mean[1] - mu[1]);
+          dm += (nd.mean[2] - mu[2]) * (nd.mean[2] - mu[2]);
+          drift = smax(drift, sqrt(dm));
+          double before[3][3];
+          for (int r = 0; r < 3; ++r)
+            for (int s = 0; s < 3; ++s) before[r][s] = p.cov[9 * (size_t)j + 3 * r + s];
+          GComp g;
+          g.w = nd.weight;
+          for (int q = 0; q < 3; ++q) g.mean[q] = mu[q];
+          if (comp_set_cov(g, S2, cov_floor(S2, p.eps, p.abs_floor))) atomicCAS(p.status, 0, kEInval);
+          double dc[3][3];
+          for (int r = 0; r < 3; ++r)
+            for (int s = 0; s < 3; ++s) dc[r][s] = g.cov[3 * r + s] - before[r][s];
+          drift = smax(drift, norm33(dc));
+          write_dnode_from_comp(nd, p.cov + 9 * (size_t)j, g, nd.weight, nd.level, nd.parent);
+          nd.child_count = 0;
+          nd.first_child = -1;
+        }
+      }
+    }
+    // CTA max of drift (order-free)
+    {
+      __shared__ double dmax[kTile / 32];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) drift = smax(drift, __shfl_xor_sync(0xffffffffu, drift, off));
+      if (lane == 0) dmax[warp] = drift;
+      __syncthreads();
+      if (tid == 0) {
+        double d = dmax[0];
+        for (int w = 1; w < kTile / 32; ++w) d = smax(d, dmax[w]);
+        p.cta_drift[cta] = d;
+      }
+    }
+    grid_sync(p.bar, G);
+    if (cta == 0) {
+      if (tid == 0) {
+        double drift_all = 0.0;
+        for (int c = 0; c < G; ++c) drift_all = smax(drift_all, __ldcg(&p.cta_drift[c]));
+        // branch masses (gmm.cpp:547-556) in place of a scratch array: use
+        // cal_moments[j*10] for leaves, accumulate parents level by level.
+        double* branch = p.cal_moments;  // reuse slot 0 of each node
+        for (int j = 0; j < J; ++j)
+          if (p.nodes[j].child_count != 0) branch[(size_t)j * 10] = 0.0;
+        for (int l = p.L - 2; l >= 0; --l)
+          for (int j = 0; j < J; ++j) {
+            const DNode& nd = p.nodes[j];
+            if (nd.level != l || nd.child_count == 0) continue;
+            double s = 0.0;
+            for (int c = 0; c < nd.child_count; ++c) s += branch[(size_t)(nd.first_child + c) * 10];
+            branch[(size_t)j * 10] = s;
+          }
+        auto reweight = [&](int first, int count) {
+          double s = 0.0;
+          for (int c = 0; c < count; ++c) s += branch[(size_t)(first + c) * 10];
+          if (!(s > 0.0)) return;
+          for (int c = 0; c < count; ++c) {
+            const double w = branch[(size_t)(first + c) * 10] / s;
+            drift_all = smax(drift_all, fabs(p.nodes[first + c].weight - w));
+            p.nodes[first + c].weight = w;
+          }
+        };
+        reweight(0, root_count);
+        for (int j = 0; j < J; ++j)
+          if (p.nodes[j].child_count != 0) reweight(p.nodes[j].first_child, p.nodes[j].child_count);
+        reset_parents(p, J);
+        st->drift = drift_all;
+        st->cal_pass = pass + 1;
+        __threadfence();
+      }
+      __syncthreads();
+      // refresh_eig of internal nodes (gmm.cpp:576-578)
+      for (int j = tid; j < J; j += blockDim.x)
+        if (p.nodes[j].child_count != 0)
+          if (refresh_node(p.nodes[j], p.cov + 9 * (size_t)j)) atomicCAS(p.status, 0, kEInval);
+      __threadfence();
+    }
+    grid_sync(p.bar, G);
+  }
+  if (cta == 0 && tid == 0) st->cal_evals = __ldcg(&p.a.counters[1]);
+}
+
+__global__ void k_init_entries(const double* __restrict__ pts, size_t n, double* ex, double* ey,
+                               double* ez, double* ew, int* tile_node, int* tile_start,
+                               int* tile_len, int* status) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+    if (!isfinite(x) || !isfinite(y) || !isfinite(z)) atomicCAS(status, 0, kEInval);
+    ex[i] = x;
+    ey[i] = y;
+    ez[i] = z;
+    ew[i] = 1.0;
+    if (i % kTile == 0) {
+      const size_t t = i / kTile;
+      tile_node[t] = 0;
+      tile_start[t] = (int)i;
+      tile_len[t] = (int)min((size_t)kTile, n - i);
+    }
+  }
+}
+
+}  // namespace trg
+
+using namespace trg;
+
+namespace trg {
+int stage_points_public(trg_ctx* ctx, const double* xyz, size_t n, int on_device, int slot,
+                        const double** dev);
+}
+
+namespace {
+
+struct BuildAlloc {
+  int Kmax, Tmax, Emax;
+};
+
+int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config* cfg,
+              BuildAlloc al, trg_tree_dev** out, trg_build_diag* diag, bool* overflow,
+              BuildAlloc* need) {
+  const int L = cfg->max_level;
+  const int cap = trg_tree_capacity(L);
+  BuildParams p{};
+  p.pts = pts;
+  p.n = n;
+  p.L = L;
+  p.em_iters = cfg->em_iterations_per_node;
+  p.min_points = (double)cfg->min_points_per_node;
+  p.eps = cfg->cov_regularization_epsilon;
+  p.abs_floor = cfg->cov_regularization_absolute;
+  p.Kmax = al.Kmax;
+  p.Tmax = al.Tmax;
+  p.Emax = al.Emax;
+  p.capacity = cap;
+  // ---- one arena for everything
+  const size_t E = (size_t)al.Emax, T = (size_t)al.Tmax, K = (size_t)al.Kmax;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  size_t o_e[2][4], o_rn[2][5], o_tl[2][3];
+  for (int b = 0; b < 2; ++b) {
+    for (int q = 0; q < 4; ++q) o_e[b][q] = carve(sizeof(double) * E);
+    for (int q = 0; q < 5; ++q) o_rn[b][q] = carve(sizeof(int) * K);
+    for (int q = 0; q < 3; ++q) o_tl[b][q] = carve(sizeof(int) * T);
+  }
+  const size_t o_mass = carve(sizeof(double) * K), o_ref = carve(sizeof(double) * 3 * K),
+               o_mean = carve(sizeof(double) * 3 * K), o_sc = carve(sizeof(double) * 9 * K),
+               o_fl = carve(sizeof(double) * K), o_seeds = carve(sizeof(double) * 24 * K),
+               o_wmi = carve(sizeof(int) * K), o_comps = carve(sizeof(GComp) * 16 * K),
+               o_fll = carve(sizeof(double) * 2 * K), o_cm = carve(sizeof(double) * 16 * K),
+               o_kept = carve(sizeof(int) * K), o_ok = carve(sizeof(int) * K),
+               o_ns = carve(sizeof(int) * K), o_surv = carve(sizeof(int) * 8 * K),
+               o_sm = carve(sizeof(double) * 8 * K), o_st = carve(sizeof(double) * K),
+               o_nseg = carve(sizeof(int) * 8 * K), o_arr = carve(sizeof(unsigned) * K),
+               o_part = carve(sizeof(double) * kRec * T),
+               o_nred = carve(sizeof(double) * kRec * K), o_fd = carve(sizeof(unsigned) * K),
+               o_tb = carve(sizeof(double) * 8 * T),
+               o_md = carve(sizeof(double) * E), o_emit = carve(sizeof(double) * 8 * E),
+               o_calm = carve(sizeof(double) * 10 * cap), o_bar = carve(64),
+               o_state = carve(sizeof(BuildState));
+  const int G = persistent_grid(ctx, (const void*)k_build, kTile, 0);
+  const size_t o_cd = carve(sizeof(double) * G);
+  void* arena = nullptr;
+  TRG_TRY(ws_get(ctx, kSlotBuild0, off, &arena));
+  char* A = static_cast<char*>(arena);
+  for (int b = 0; b < 2; ++b) {
+    p.ex[b] = (double*)(A + o_e[b][0]);
+    p.ey[b] = (double*)(A + o_e[b][1]);
+    p.ez[b] = (double*)(A + o_e[b][2]);
+    p.ew[b] = (double*)(A + o_e[b][3]);
+    p.rn[b].tree_id = (int*)(A + o_rn[b][0]);
+    p.rn[b].seg = (int*)(A + o_rn[b][1]);
+    p.rn[b].len = (int*)(A + o_rn[b][2]);
+    p.rn[b].tile0 = (int*)(A + o_rn[b][3]);
+    p.rn[b].ntiles = (int*)(A + o_rn[b][4]);
+    p.tile_node[b] = (int*)(A + o_tl[b][0]);
+    p.tile_start[b] = (int*)(A + o_tl[b][1]);
+    p.tile_len[b] = (int*)(A + o_tl[b][2]);
+  }
+  p.nf.mass = (double*)(A + o_mass);
+  p.nf.ref = (double*)(A + o_ref);
+  p.nf.mean = (double*)(A + o_mean);
+  p.nf.scatter = (double*)(A + o_sc);
+  p.nf.floorv = (double*)(A + o_fl);
+  p.nf.seeds = (double*)(A + o_seeds);
+  p.nf.wmax_idx = (int*)(A + o_wmi);
+  p.nf.comps = (GComp*)(A + o_comps);
+  p.nf.final_ll = (double*)(A + o_fll);
+  p.nf.cmass = (double*)(A + o_cm);
+  p.nf.kept = (int*)(A + o_kept);
+  p.nf.ok = (int*)(A + o_ok);
+  p.nf.ns = (int*)(A + o_ns);
+  p.nf.surv = (int*)(A + o_surv);
+  p.nf.smass = (double*)(A + o_sm);
+  p.nf.stotal = (double*)(A + o_st);
+  p.nf.next_seg = (int*)(A + o_nseg);
+  p.nf.arrive = (unsigned*)(A + o_arr);
+  p.partial = (double*)(A + o_part);
+  p.nodered = (double*)(A + o_nred);
+  p.fdone = (unsigned*)(A + o_fd);
+  p.tile_base = (double*)(A + o_tb);
+  p.min_d2 = (double*)(A + o_md);
+  p.emit = (double*)(A + o_emit);
+  p.cal_moments = (double*)(A + o_calm);
+  p.bar = (unsigned*)(A + o_bar);
+  p.st = (BuildState*)(A + o_state);
+  p.cta_drift = (double*)(A + o_cd);
+  p.status = ctx->status;
+  // tree
+  trg_tree_dev* tree = nullptr;
+  TRG_TRY(tree_alloc(ctx, cap, &tree));
+  tree->max_level = L;
+  p.nodes = tree->nodes;
+  p.cov = tree->cov;
+  // calibration association (NM = 10, identity, lambda_c = 0, full depth)
+  void *part, *stamps, *cnt;
+  TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * 10 * (size_t)cap * G, &part));
+  TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)cap * G, &stamps));
+  TRG_TRY(ws_get(ctx, kSlotCounters, 64, &cnt));
+  p.a.nodes = tree->nodes;
+  p.a.depth = L;
+  p.a.lambda_c = 0.0;
+  p.a.outlier_floor = 1e-300;
+  p.a.pts = pts;
+  p.a.n = n;
+  p.a.Rt = nullptr;
+  p.a.partials = (double*)part;
+  p.a.stamps = (uint32_t*)stamps;
+  p.a.counters = (unsigned long long*)cnt;
+  p.a.status = ctx->status;
+  p.a.epoch = ctx->epoch + 1;
+  ctx->epoch += 41;
+  // ---- initial state
+  BuildState st{};
+  st.Kp[0] = 1;
+  st.Tp[0] = (int)((n + kTile - 1) / kTile);
+  st.Ep[0] = (int)n;
+  st.J = 0;
+  st.drift = INFINITY;
+  st.E_round[0] = n;
+  st.K_round[0] = 1;
+  TRG_CU(cudaMemsetAsync(A + o_bar, 0, 64, ctx->stream));
+  TRG_CU(cudaMemsetAsync(A + o_arr, 0, sizeof(unsigned) * K, ctx->stream));
+  TRG_CU(cudaMemsetAsync(A + o_fd, 0, sizeof(unsigned) * K, ctx->stream));
+  TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
+  TRG_CU(cudaMemcpyAsync(p.st, &st, sizeof st, cudaMemcpyHostToDevice, ctx->stream));
+  const int h_rn[5] = {-1, 0, (int)n, 0, st.Tp[0]};
+  for (int q = 0; q < 5; ++q)
+    TRG_CU(cudaMemcpyAsync(A + o_rn[0][q], &h_rn[q], sizeof(int), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  k_init_entries<<<256, 256, 0, ctx->stream>>>(pts, n, p.ex[0], p.ey[0], p.ez[0], p.ew[0],
+                                               p.tile_node[0], p.tile_start[0], p.tile_len[0],
+                                               ctx->status);
+  void* args[] = {&p};
+  TRG_CU(cudaLaunchCooperativeKernel((const void*)k_build, G, kTile, args, 0, ctx->stream));
+  ctx->launches += 2;
+  TRG_CU(cudaMemcpyAsync(&st, p.st, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+  int rc = check_status(ctx, "build_tree");
+  if (rc == TRG_OK && st.status_overflow) {
+    *overflow = true;
+    need->Emax = std::max(al.Emax, st.need_E);
+    need->Kmax = std::max(al.Kmax, st.need_K);
+    need->Tmax = std::max(al.Tmax, st.need_T);
+    trg_tree_free(ctx, tree);
+    return TRG_OK;
+  }
+  if (rc != TRG_OK) {
+    trg_tree_free(ctx, tree);
+    return rc;
+  }
+  tree->n_nodes = st.J;
+  {
+    // root_count: level-0 prefix (from the host copy of levels)
+    std::vector<DNode> h(st.J);
+    TRG_CU(cudaMemcpy(h.data(), tree->nodes, sizeof(DNode) * st.J, cudaMemcpyDeviceToHost));
+    int rcnt = 0;
+    while (rcnt < st.J && h[rcnt].level == 0) ++rcnt;
+    tree->root_count = rcnt;
+  }
+  if (diag) {
+    for (int r = 0; r < 8; ++r) {
+      diag->entries_per_round[r] = r < L ? st.E_round[r] : 0;
+      diag->expanded_per_round[r] = r < L ? st.K_round[r] : 0;
+    }
+    diag->calibration_passes = st.cal_pass;
+    diag->calibration_drift = st.drift;
+    diag->calib_density_evaluations = st.cal_evals;
+  }
+  *out = tree;
+  return TRG_OK;
+}
+
+}  // namespace
+
+extern "C" int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz_on_device,
+                              const trg_model_config* cfg, trg_tree_dev** out,
+                              trg_build_diag* diag) {
+  // validate_config gmm.cpp:465-477, validate_cloud :479-484
+  if (cfg->max_level < 1) {
+    set_error("max_level must be >= 1");
+    return TRG_EINVAL;
+  }
+  if (cfg->max_level > 7) {
+    set_error("max_level above 7 is not supported by this build");
+    return TRG_EINVAL;
+  }
+  if (cfg->em_iterations_per_node < 1) {
+    set_error("em_iterations_per_node must be >= 1");
+    return TRG_EINVAL;
+  }
+  if (cfg->min_points_per_node < 1) {
+    set_error("min_points_per_node must be >= 1");
+    return TRG_EINVAL;
+  }
+  if (!(cfg->cov_regularization_epsilon >= 0.0) || !(cfg->cov_regularization_absolute > 0.0)) {
+    set_error("covariance regularization must be positive");
+    return TRG_EINVAL;
+  }
+  if (n == 0 || !xyz) {
+    set_error("point cloud is empty");
+    return TRG_EINVAL;
+  }
+  if (n > (size_t)INT32_MAX / 8) {
+    set_error("point cloud too large for int32 entry indexing");
+    return TRG_EINVAL;
+  }
+  TRG_CU(cudaSetDevice(ctx->device));
+  const double* dev = nullptr;
+  TRG_TRY(stage_points_public(ctx, xyz, n, xyz_on_device, kSlotPoints, &dev));
+  const int L = cfg->max_level;
+  int kmax = 1;
+  for (int l = 0; l + 1 < L; ++l) kmax *= 8;
+  BuildAlloc al;
+  al.Kmax = std::max(1, kmax);
+  al.Emax = (int)std::min<size_t>((size_t)INT32_MAX / 16, n * (L > 1 ? 4 : 1) + 1024);
+  al.Tmax = al.Emax / kTile + al.Kmax + 8;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    bool overflow = false;
+    BuildAlloc need = al;
+    const int rc = run_build(ctx, dev, n, cfg, al, out, diag, &overflow, &need);
+    if (rc != TRG_OK) {
+      if (rc == TRG_EINVAL && trg_last_error()[0] == 'b') set_error("point cloud has non-finite coordinates or no mass");
+      return rc;
+    }
+    if (!overflow) return TRG_OK;
+    al.Emax = std::max(al.Emax * 2, need.Emax + 1024);
+    al.Kmax = std::max(al.Kmax, need.Kmax);
+    al.Tmax = al.Emax / kTile + al.Kmax + 8;
+  }
+  set_error("build_tree: entry buffer growth did not converge");
+  return TRG_ERUNTIME;
+}

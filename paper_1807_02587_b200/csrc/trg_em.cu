@@ -4,6 +4,7 @@
 // point rows, single-block 6-DoF solve (K8), T <- delta o T, convergence and
 // degenerate-streak control -- with grid barriers between phases, so the
 // host never sees an iteration boundary.
+#include <cmath>
 #include <cstdio>
 #include <vector>
 
@@ -294,6 +295,47 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   return TRG_OK;
 }
 
+// Bounding-box diagonal of a cloud (cloud_io.cpp:21-33).  min/max are exact,
+// so the device reduction is bit-identical to the reference.
+__global__ void k_bbox(const double* __restrict__ p, size_t n, double* out) {
+  __shared__ double lo[3][256], hi[3][256];
+  double l[3] = {p[0], p[1], p[2]}, h[3] = {p[0], p[1], p[2]};
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x)
+    for (int k = 0; k < 3; ++k) {
+      const double v = p[3 * i + k];
+      l[k] = (v < l[k]) ? v : l[k];
+      h[k] = (h[k] < v) ? v : h[k];
+    }
+  for (int k = 0; k < 3; ++k) {
+    lo[k][threadIdx.x] = l[k];
+    hi[k][threadIdx.x] = h[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < blockDim.x; ++t)
+      for (int k = 0; k < 3; ++k) {
+        l[k] = (lo[k][t] < l[k]) ? lo[k][t] : l[k];
+        h[k] = (h[k] < hi[k][t]) ? hi[k][t] : h[k];
+      }
+    double s = (h[0] - l[0]) * (h[0] - l[0]);
+    s += (h[1] - l[1]) * (h[1] - l[1]);
+    s += (h[2] - l[2]) * (h[2] - l[2]);
+    *out = sqrt(s);
+  }
+}
+
+double target_bbox_diagonal(trg_ctx* ctx, const double* dev_or_null, const double* host, size_t n) {
+  if (!dev_or_null) return trg_bbox_diagonal(host, n);
+  void* o = nullptr;
+  if (ws_get(ctx, kSlotSolve, 64, &o) != TRG_OK) return 0.0;
+  k_bbox<<<1, 256, 0, ctx->stream>>>(dev_or_null, n, static_cast<double*>(o));
+  ctx->launches += 1;
+  double d = 0.0;
+  cudaMemcpyAsync(&d, o, sizeof d, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  return d;
+}
+
 }  // namespace
 
 extern "C" {
@@ -365,6 +407,77 @@ int trg_register_with_tree(trg_ctx* ctx, const trg_tree_dev* tree, const double*
   TRG_TRY(stage_points_public(ctx, xyz, n, xyz_on_device, kSlotPoints2, &dev));
   const int rc = run_em(ctx, tree, dev, n, cfg, target_diag, out);
   if (rc == TRG_EINVAL) set_error("register: bad source cloud");
+  return rc;
+}
+
+// registration.cpp:174-209 register_clouds (adaptive:L / tree:L):
+// validate, build the tree on the target, then the EM loop.
+int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
+                        const double* source, size_t n_source, int on_device,
+                        const trg_reg_config* cfg, trg_reg_result* out) {
+  if (n_target == 0 || n_source == 0 || !target || !source) {
+    set_error("register: empty cloud");
+    return TRG_EINVAL;
+  }
+  if (!(cfg->rotation_tol > 0.0) || !(cfg->translation_tol > 0.0)) {
+    set_error("register: tolerances must be positive");
+    return TRG_EINVAL;
+  }
+  if (cfg->max_em_iterations < 1) {
+    set_error("register: max_em_iterations must be >= 1");
+    return TRG_EINVAL;
+  }
+  if (cfg->variant_param < 1) {
+    set_error("register: variant parameter must be >= 1");
+    return TRG_EINVAL;
+  }
+  if (cfg->variant_kind != TRG_VARIANT_ADAPTIVE && cfg->variant_kind != TRG_VARIANT_TREE) {
+    set_error("register: this path implements adaptive:L and tree:L");
+    return TRG_EINVAL;
+  }
+  {  // initial_transform.is_valid(1e-9) (geometry.cpp:22-38)
+    const double* R = cfg->initial_R;
+    double o = 0.0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double s = R[i] * R[j];
+        s += R[3 + i] * R[3 + j];
+        s += R[6 + i] * R[6 + j];
+        const double d = s - (i == j ? 1.0 : 0.0);
+        o += d * d;
+      }
+    const double det = R[0] * (R[4] * R[8] - R[7] * R[5]) - R[3] * (R[1] * R[8] - R[7] * R[2]) +
+                       R[6] * (R[1] * R[5] - R[4] * R[2]);
+    bool fin = true;
+    for (int k = 0; k < 9; ++k) fin = fin && std::isfinite(R[k]);
+    for (int k = 0; k < 3; ++k) fin = fin && std::isfinite(cfg->initial_t[k]);
+    if (!fin || !(std::sqrt(o) <= 1e-9) || !(std::fabs(det - 1.0) <= 1e-9)) {
+      set_error("register: invalid initial transform");
+      return TRG_EINVAL;
+    }
+  }
+  TRG_CU(cudaSetDevice(ctx->device));
+  const double* src = nullptr;
+  TRG_TRY(stage_points_public(ctx, source, n_source, on_device, kSlotPoints2, &src));
+  cudaEvent_t e0, e1;
+  TRG_CU(cudaEventCreate(&e0));
+  TRG_CU(cudaEventCreate(&e1));
+  TRG_CU(cudaEventRecord(e0, ctx->stream));
+  trg_model_config mc = cfg->model_config;
+  mc.max_level = cfg->variant_param;
+  trg_tree_dev* tree = nullptr;
+  int rc = trg_build_tree(ctx, target, n_target, on_device, &mc, &tree, nullptr);
+  if (rc != TRG_OK) return rc;
+  TRG_CU(cudaEventRecord(e1, ctx->stream));
+  const double diag = target_bbox_diagonal(ctx, on_device ? target : nullptr, target, n_target);
+  rc = run_em(ctx, tree, src, n_source, cfg, diag, out);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  out->model_build_seconds = ms * 1e-3;
+  trg_tree_free(ctx, tree);
+  if (rc == TRG_EINVAL) set_error("register: non-finite coordinates");
   return rc;
 }
 

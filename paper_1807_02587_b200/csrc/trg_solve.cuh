@@ -173,7 +173,7 @@ struct SolveOut {
 // Thread-0 part of solve_mstep (mstep.cpp:76-98) from the reduced normal
 // equations.  __noinline__ keeps its 6x6 working set out of the callers'
 // register budget.
-__device__ __noinline__ void solve_normal_eq(const double* v, int nvp, SolveOut* o) {
+static __device__ __noinline__ void solve_normal_eq(const double* v, int nvp, SolveOut* o) {
   o->nvp = nvp;
   o->degenerate = 0;
   if (nvp < 3) {
@@ -210,7 +210,7 @@ __device__ __noinline__ void solve_normal_eq(const double* v, int nvp, SolveOut*
 }
 
 // Whole solve on one block from device moments (stride nm, m0 at 0, m1 at 1..3).
-__device__ void block_solve(const DNode* __restrict__ nodes, int J, const double* __restrict__ mom,
+static __device__ void block_solve(const DNode* __restrict__ nodes, int J, const double* __restrict__ mom,
                             int nm, double n_total, SolveOut* out, SolveSmem& sm, int* status) {
   SolveAcc a;
   acc_zero(a);

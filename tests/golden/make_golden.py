@@ -30,6 +30,9 @@ def cases(ref):
     from paper_1807_02587_b200 import treereg  # host-side generator only
     tg, _, _ = treereg.kinect_pair(2)
     yield "kinect4k_L3", np.ascontiguousarray(tg[::19][:4000]), 3, (5.0, 0.05, 2)
+    # BASELINE config C1: unit_normalized(synthetic_lumpy(10000, 1)), L = 2,
+    # pose random_rigid_transform({15 deg, 0.05, seed 1}, 0)
+    yield "c1_lumpy10k_L2", ref.unit_normalized(ref.synthetic("lumpy", 10000, 1)), 2, (15.0, 0.05, 1)
 
 
 def main():
@@ -62,6 +65,9 @@ def main():
         out["reg_meta"] = np.array([reg["iterations"], int(reg["converged"]), diag])
         out["reg_crit_before"], out["reg_crit_after"] = reg["criterion_before"], reg["criterion_after"]
         out["reg_evals"] = reg["eval_counts"]
+        rc = ref.register_clouds(pts, src, level=L)
+        out["rc_R"], out["rc_t"] = rc["R"], rc["t"]
+        out["rc_meta"] = np.array([rc["iterations"], int(rc["converged"])])
         np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
         print(name, len(pts), "nodes", len(tree["weight"]), "reg iters", reg["iterations"],
               "converged", reg["converged"])
