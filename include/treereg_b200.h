@@ -201,6 +201,10 @@ int trg_random_rigid_transform(double rot_range_deg, double trans_range, uint64_
  * the source frame into the target frame. */
 int trg_synth_kinect_pair(uint64_t seed, double* target, double* source, double R_gt[9],
                           double t_gt[3]);
+/* Same with explicit axial-noise scale and camera-motion ranges. */
+int trg_synth_kinect_pair_ex(uint64_t seed, double noise_scale, double rot_range_deg,
+                             double trans_range, double* target, double* source, double R_gt[9],
+                             double t_gt[3]);
 /* HDL-32-style sweep pair (72,000 points each). */
 int trg_synth_lidar_pair(uint64_t seed, double* target, double* source, double R_gt[9],
                          double t_gt[3]);

@@ -104,6 +104,8 @@ SIGNATURES = {
     "trg_random_rigid_transform": (C.c_int, [C.c_double, C.c_double, C.c_uint64, C.c_int, dp,
                                              dp]),
     "trg_synth_kinect_pair": (C.c_int, [C.c_uint64, dp, dp, dp, dp]),
+    "trg_synth_kinect_pair_ex": (C.c_int, [C.c_uint64, C.c_double, C.c_double, C.c_double, dp, dp,
+                                           dp, dp]),
     "trg_synth_lidar_pair": (C.c_int, [C.c_uint64, dp, dp, dp, dp]),
     "trg_debug_eig": (C.c_int, [C.c_void_p, C.c_int, dp, C.c_int, dp, dp, ip]),
 }

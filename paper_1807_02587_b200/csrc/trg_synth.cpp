@@ -295,11 +295,11 @@ double hit_box_inside(const Ray& r, V3 lo, V3 hi) {
 
 double hit_sphere(const Ray& r, V3 c, double rad) {
   const V3 oc = sub(r.o, c);
+  const double a = dot(r.d, r.d);  // ray directions are not unit length
   const double b = dot(oc, r.d), cc = dot(oc, oc) - rad * rad;
-  const double disc = b * b - cc;
+  const double disc = b * b - a * cc;
   if (disc < 0) return kInf;
-  const double s = std::sqrt(disc);
-  const double t = -b - s;
+  const double t = (-b - std::sqrt(disc)) / a;
   return t > 1e-9 ? t : kInf;
 }
 
@@ -345,7 +345,8 @@ void look_at(V3 eye, V3 target, double R[9], double t[3]) {
 
 // Renders one 320x240 frame from camera pose (Rwc, twc); points in camera
 // coordinates, axial noise sigma_z = 0.0012 + 0.0019 (z - 0.4)^2.
-void render_kinect(const double Rwc[9], const double twc[3], Rng& rng, double* out) {
+void render_kinect(const double Rwc[9], const double twc[3], Rng& rng, double* out,
+                   double noise_scale) {
   const double fx = 262.5, fy = 262.5, cx = 159.5, cy = 119.5;
   std::normal_distribution<double> g(0.0, 1.0);
   std::size_t k = 0;
@@ -359,7 +360,7 @@ void render_kinect(const double Rwc[9], const double twc[3], Rng& rng, double* o
       const double t = cast_room(r);  // z = t since dc.z == 1
       const double z = std::isfinite(t) ? t : 6.0;
       const double sz = 0.0012 + 0.0019 * (z - 0.4) * (z - 0.4);
-      const double zn = z + sz * g(rng);
+      const double zn = z + noise_scale * sz * g(rng);
       out[k++] = dc.x * zn;
       out[k++] = dc.y * zn;
       out[k++] = zn;
@@ -492,21 +493,26 @@ int trg_random_rigid_transform(double rot_deg, double trans, uint64_t seed, int 
   return TRG_OK;
 }
 
-int trg_synth_kinect_pair(uint64_t seed, double* target, double* source, double R_gt[9],
-                          double t_gt[3]) {
+int trg_synth_kinect_pair_ex(uint64_t seed, double noise_scale, double rot_deg, double trans,
+                             double* target, double* source, double R_gt[9], double t_gt[3]) {
   double R1[9], t1[3];
   look_at({3.4, 1.5, 2.6}, {1.2, 0.7, 0.9}, R1, t1);
   double dR[9], dt[3];
-  rigid(5.0, 0.05, seed, 0, dR, dt);
+  rigid(rot_deg, trans, seed, 0, dR, dt);
   double R2[9], t2[3];  // camera 2 = camera 1 moved by (dR, dt) in its own frame
   matmul(R1, dR, R2);
   for (int i = 0; i < 3; ++i)
     t2[i] = t1[i] + R1[3 * i] * dt[0] + R1[3 * i + 1] * dt[1] + R1[3 * i + 2] * dt[2];
   Rng rng(splitmix64(seed + 0x4b696e656374ull));
-  render_kinect(R1, t1, rng, target);
-  render_kinect(R2, t2, rng, source);
+  render_kinect(R1, t1, rng, target, noise_scale);
+  render_kinect(R2, t2, rng, source, noise_scale);
   relative(R1, t1, R2, t2, R_gt, t_gt);
   return TRG_OK;
+}
+
+int trg_synth_kinect_pair(uint64_t seed, double* target, double* source, double R_gt[9],
+                          double t_gt[3]) {
+  return trg_synth_kinect_pair_ex(seed, 1.0, 5.0, 0.05, target, source, R_gt, t_gt);
 }
 
 int trg_synth_lidar_pair(uint64_t seed, double* target, double* source, double R_gt[9],
