@@ -1,0 +1,339 @@
+"""bench.py — HGMR registration throughput on B200 (contract: one JSON line).
+
+Workload (N = 1): BASELINE.json configs[1] = C2, a Kinect-sized 320x240
+synthetic depth-frame pair (76,800 points each), adaptive:3 (depth-3 GMM
+tree, lambda_c = 0.01).  One STEP = one full frame-pair registration through
+the reference's public API (register_clouds: tree build on the target + EM
+on the source), as the paper times it.
+
+* value  : registrations/s over all ranks, inputs already resident in HBM
+           (device pointers), CUDA-event time per step on the library's stream,
+           L2 flushed (256 MB write) before every timed step.
+* e2e    : the same metric through the same C-ABI call with pinned HOST
+           buffers: H2D of both clouds + all D2H result reads inside the timed
+           region (host wall clock around each synchronous call).
+* N > 1  : one process per GPU (torchrun), every rank registers its own copy of
+           the C2 pair (independent pairs shard with no collective), weak
+           scaling; value = N*K / max-over-ranks time.
+* --impl reference: the reference's own CPU implementation (oracle/_ref =
+           /root/reference sources built with the test shims) on the host's
+           cores, same workload and metric; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "registrations/sec + tree-build Mpoints/sec at 1/2/4/8 B200; HBM roofline frac"
+UNIT = "registrations/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload(cfg_name: str):
+    from paper_1807_02587_b200 import treereg as tr
+    if cfg_name == "c2":
+        tg, sr, gt = tr.kinect_pair(2)
+        return tg, sr, gt, 3, "C2 Kinect 320x240 synthetic depth-frame pair (76,800 pts each), adaptive:3"
+    if cfg_name == "c3":
+        tg, sr, gt = tr.lidar_pair(3)
+        return tg, sr, gt, 3, "C3 HDL-32-style synthetic sweep pair (72,000 pts each), adaptive:3"
+    if cfg_name == "c1":
+        tg = tr.unit_normalized(tr.synthetic("lumpy", 10000, 1))
+        T = tr.random_rigid_transform(15.0, 0.05, 1)
+        sr = T(tg)
+        return tg, sr, T.inverse(), 2, "C1 unit-normalized lumpy 10k pair, adaptive:2"
+    raise SystemExit(f"unknown config {cfg_name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def algorithmic_bytes(diag, n_target: int, n_source: int, J: int, em_iters: int):
+    """FP64 (s = 8), entry = idx 4 B + w 8 B + point 24 B.
+    Build: per round 36 passes over E_l entries + the partition write of
+    E_{l+1}, plus P_cal calibration associations.  Registration: I_em E-steps."""
+    s = 8
+    ent = 12 + 3 * s
+    E = list(diag.entries_per_round) + [0]
+    L = len(diag.entries_per_round)
+    b_rounds = sum(36 * E[l] * ent + E[l + 1] * ent for l in range(L))
+    b_assoc_cal = n_target * 3 * s + J * 136 + J * 104
+    b_build = b_rounds + diag.calibration_passes * b_assoc_cal
+    b_assoc_reg = n_source * 3 * s + J * 136 + J * 32
+    return b_build, em_iters * b_assoc_reg
+
+
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if os.environ.get("TRG_BENCH_BACKEND", "nccl") == "nccl" else "gloo"
+        dist.init_process_group(backend)
+    return world, rank, local, dist
+
+
+def max_over_ranks(x: float, dist, device=None):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist, device=None):
+    if dist is not None:
+        import torch
+        t = torch.zeros(1, device=device)
+        dist.all_reduce(t)
+
+
+# --------------------------------------------------------------- reference
+def run_reference(args):
+    world, rank, local, dist = dist_setup(args.gpus)
+    if rank != 0:
+        return 0
+    from oracle.oracle import Ref  # the reference's own CPU implementation
+    tg, sr, gt, L, wl = workload(args.config)
+    ref = Ref()
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    for _ in range(args.warmup):
+        ref.register_clouds(tg, sr, level=L)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ref.register_clouds(tg, sr, level=L)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    v = args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": wl, "l2": "inputs 3.7 MB < L2; CPU run"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} full registrations (build+EM) of the {args.config.upper()} pair"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- B200 arm
+def run_b200(args):
+    import torch
+    world, rank, local, dist = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1807_02587_b200 import treereg as tr
+    ctx = tr.Context(local)
+    tg, sr, gt, L, wl = workload(args.config)
+    cfg = tr.RegistrationConfig(variant=tr.Variant("adaptive", L))
+    tg_d = torch.from_numpy(tg).to(dev).contiguous()
+    sr_d = torch.from_numpy(sr).to(dev).contiguous()
+    tg_h = torch.from_numpy(tg).pin_memory()
+    sr_h = torch.from_numpy(sr).pin_memory()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+
+    def step_dev():
+        return tr.register_clouds(tg_d, sr_d, cfg, ctx)
+
+    def step_host():
+        return tr.register_clouds(tg_h.numpy(), sr_h.numpy(), cfg, ctx)
+
+    for _ in range(args.warmup):
+        res = step_dev()
+        step_host()
+    torch.cuda.synchronize()
+    # accuracy of the measured registration (vs the generator's ground truth)
+    rot_err = float(np.degrees(np.arccos(np.clip(
+        (np.trace(res.transform.rotation.T @ gt.rotation) - 1) / 2, -1, 1))))
+    # ---- device-resident timing
+    launches0 = ctx.kernel_launches
+    step_ms, build_s, em_s = [], [], []
+    barrier(dist, dev)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = step_dev()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            build_s.append(r.model_build_seconds)
+            em_s.append(r.em_seconds)
+        torch.cuda.synchronize()
+    barrier(dist, dev)
+    launches = (ctx.kernel_launches - launches0) / args.steps
+    t_dev = max_over_ranks(sum(step_ms) / 1e3, dist, dev)
+    # ---- end-to-end through the C-ABI with host buffers
+    h0, d0 = ctx.transfer_bytes()
+    e2e_s = []
+    barrier(dist, dev)
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step_host()
+        e2e_s.append(time.perf_counter() - t0)
+    h1, d1 = ctx.transfer_bytes()
+    t_e2e = max_over_ranks(sum(e2e_s), dist, dev)
+    n_total = world * args.steps
+    value = n_total / t_dev
+    e2e = n_total / t_e2e
+    # ---- roofline of the dominant kernel (the build, k_build)
+    diag = tr.BuildDiagnostics()
+    tree = tr.build_tree(tg_d, tr.ModelConfig(max_level=L), diag, ctx)
+    J = tree.size()
+    b_build, b_em = algorithmic_bytes(diag, len(tg), len(sr), J, res.iterations)
+    t_build = float(np.median(build_s))
+    t_em = float(np.median(em_s))
+    peak, peak_kind = load_peaks()
+    achieved = b_build / t_build / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "k_build_dram_bytes.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl, "pairs_per_rank_per_step": 1,
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "parallelism": f"batch-sharded pairs x{world}, no collectives"},
+        "tree_build_mpoints_per_s": world * len(tg) / t_build / 1e6,
+        "phase_ms": {"build": 1e3 * t_build, "em": 1e3 * t_em,
+                     "em_iterations": res.iterations, "converged": res.converged},
+        "rot_err_deg_vs_gt": rot_err,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_build (tree build + leaf calibration)",
+                     "algorithmic_bytes": b_build, "peak_kind": peak_kind,
+                     "E_per_round": list(diag.entries_per_round),
+                     "calibration_passes": diag.calibration_passes},
+        "e2e": {"value": e2e, "unit": UNIT,
+                "h2d_bytes_per_step": (h1 - h0) // args.steps,
+                "d2h_bytes_per_step": (d1 - d0) // args.steps},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.config)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(cfg_name):
+    """The reference implementation (oracle/_ref) on this host's cores, one
+    full registration of the same pair (a bounded ~5-10 s sample)."""
+    try:
+        from oracle.oracle import Ref
+        tg, sr, gt, L, wl = workload(cfg_name)
+        ref = Ref()
+        cores = os.cpu_count() or 1
+        ref.set_threads(cores)
+        t0 = time.perf_counter()
+        ref.register_clouds(tg, sr, level=L)
+        dt = time.perf_counter() - t0
+        return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"1 full registration (build+EM) of the {cfg_name.upper()} pair, "
+                          f"{cores} threads, {dt:.2f} s"}
+    except Exception as e:  # the oracle build is test infrastructure; report, don't fail
+        return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -147,6 +147,8 @@ const char* trg_last_error(void);
 int trg_device_sms(trg_ctx* ctx);
 /* Launch count of this library's kernels since ctx creation (bench evidence). */
 uint64_t trg_kernel_launches(trg_ctx* ctx);
+/* Bytes copied host->device / device->host by this context so far. */
+void trg_ctx_transfer_bytes(trg_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 /* CUDA stream (cudaStream_t) all work of this context is ordered on. */
 void* trg_ctx_stream(trg_ctx* ctx);
 
@@ -214,6 +216,11 @@ int trg_synth_lidar_pair(uint64_t seed, double* target, double* source, double R
  * 6x6 Jacobi of solve_mstep (mstep.cpp:77), n = 3 eig_sym3
  * (geometry.cpp:40-79), n = -3 eig_sym3_floored at 1e-4 (:81-102).  Used by
  * the tests to pin device math bit-for-bit to the CPU oracle. */
+/* Device timeline of the last trg_build_tree on this context: globaltimer
+ * (ns) at each grid barrier and a phase label (round*100 + phase; +50 for
+ * the node-reduction half; 900-902 rematch; 1000+10*pass+stage calibration).
+ * Returns the number of marks. */
+int trg_debug_build_timeline(trg_ctx* ctx, uint64_t* t_ns, int* labels, int cap);
 int trg_debug_eig(trg_ctx* ctx, int n, const double* in, int count, double* evals,
                   double* evecs, int* status);
 

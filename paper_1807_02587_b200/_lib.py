@@ -80,6 +80,7 @@ SIGNATURES = {
     "trg_device_sms": (C.c_int, [C.c_void_p]),
     "trg_kernel_launches": (C.c_uint64, [C.c_void_p]),
     "trg_ctx_stream": (C.c_void_p, [C.c_void_p]),
+    "trg_ctx_transfer_bytes": (None, [C.c_void_p, u64p, u64p]),
     "trg_tree_capacity": (C.c_int, [C.c_int]),
     "trg_tree_upload": (C.c_int, [C.c_void_p, C.POINTER(TreeC), C.POINTER(C.c_void_p)]),
     "trg_tree_download": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(TreeC)]),
@@ -107,6 +108,7 @@ SIGNATURES = {
     "trg_synth_kinect_pair_ex": (C.c_int, [C.c_uint64, C.c_double, C.c_double, C.c_double, dp, dp,
                                            dp, dp]),
     "trg_synth_lidar_pair": (C.c_int, [C.c_uint64, dp, dp, dp, dp]),
+    "trg_debug_build_timeline": (C.c_int, [C.c_void_p, u64p, ip, C.c_int]),
     "trg_debug_eig": (C.c_int, [C.c_void_p, C.c_int, dp, C.c_int, dp, dp, ip]),
 }
 

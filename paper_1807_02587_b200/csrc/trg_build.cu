@@ -79,11 +79,23 @@ struct BuildState {
   int need_E, need_K, need_T;
   // calibration
   int cal_pass;
+  int root_count;
+  int lvl_start[9];
   double drift;
   unsigned long long cal_evals;
   unsigned long long E_round[8];
   int K_round[8];
+  // device timeline (CTA 0 after each grid barrier): label, globaltimer ns
+  int tl_n;
+  int tl_lab[1024];
+  unsigned long long tl_t[1024];
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct BuildParams {
   const double* pts;
@@ -116,12 +128,23 @@ struct BuildParams {
   AssocParams a;
   double* cal_moments;  // [J][10]
   double* cta_drift;    // [G]
+  int* layout_scratch;  // [6 * 8 * Kmax]
   unsigned* bar;
   BuildState* st;
   int* status;
 };
 
 // ----------------------------------------------------------------- helpers
+__device__ __forceinline__ void tl_mark(BuildState* st, int label) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int i = st->tl_n;
+    if (i < 1024) {
+      st->tl_lab[i] = label;
+      st->tl_t[i] = gtimer();
+      st->tl_n = i + 1;
+    }
+  }
+}
 __device__ __forceinline__ void comp_to_regs(const GComp& c, double r[18]) {
   r[0] = c.w;
   r[1] = c.lw;
@@ -785,90 +808,177 @@ __device__ void tile_pwrite(const BuildParams& p, BuildSmem& sm, int par, int t)
   }
 }
 
-// Layout (CTA 0): create this round's child tree nodes, choose the next
-// round's expanding set (mass gate gmm.cpp:621-623), segments and tiles.
-__device__ void round_layout(const BuildParams& p, int par, int round, BuildSmem& sm) {
-  if (threadIdx.x != 0) return;
-  BuildState* st = p.st;
-  const int K = st->Kp[par];
-  int J = st->J;
-  const int npar = par ^ 1;
-  int K2 = 0, E2 = 0, T2 = 0, needK = 0, needE = 0, needT = 0;
-  const bool last = round + 1 >= p.L;
-  for (int k = 0; k < K; ++k) {
-    const int ns = p.nf.ns[k];
-    if (!p.nf.ok[k] || ns == 0) continue;
-    const int parent = p.rn[par].tree_id[k];
-    if (J + ns > p.capacity) {
-      atomicCAS(p.status, 0, kERuntime);
-      return;
+// Block-wide exclusive scan of n ints in place (one CTA, any n); returns
+// the total.  Chunked per thread, then a warp/smem scan of chunk totals.
+__device__ int block_exscan(int* a, int n, int* wtmp /* >= 33 ints smem */) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (n + nt - 1) / nt;
+  const int b = min(n, tid * per), e = min(n, b + per);
+  int sum = 0;
+  for (int i = b; i < e; ++i) sum += a[i];
+  int x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wtmp[warp] = x;
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0;
+    for (int w = 0; w < nt / 32; ++w) {
+      const int v = wtmp[w];
+      wtmp[w] = run;
+      run += v;
     }
+    wtmp[32] = run;
+  }
+  __syncthreads();
+  int run = wtmp[warp] + x - sum;
+  for (int i = b; i < e; ++i) {
+    const int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  const int total = wtmp[32];
+  __syncthreads();
+  return total;
+}
+
+// Layout (CTA 0, all threads): create this round's child tree nodes, choose
+// the next round's expanding set (mass gate gmm.cpp:621-623), its entry
+// segments and tiles.  Children are numbered node by node, survivor by
+// survivor, exactly like build_tree's push_back order (gmm.cpp:629-641).
+__device__ void round_layout(const BuildParams& p, int par, int round, int* scratch) {
+  BuildState* st = p.st;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ int wtmp[33];
+  __shared__ int sJ0, sK2, sE2, sT2, sNC, sOvf;
+  const int K = st->Kp[par];
+  const int J0 = st->J;
+  const int npar = par ^ 1;
+  const bool last = round + 1 >= p.L;
+  // (1) child-id base per expanding node
+  int* nbase = scratch;           // [K]
+  int* cgate = scratch + K;       // [NC] gated flag -> K2 position
+  int* ngate = cgate + 8 * K;     // [NC] gated flag (kept)
+  int* ccnt = ngate + 8 * K;      // [NC] entry count -> E2 offset
+  int* ctil = ccnt + 8 * K;       // [NC] tile count -> T2 offset
+  int* cidx = ctil + 8 * K;       // [NC] (k << 3 | s)
+  for (int k = tid; k < K; k += nt) nbase[k] = p.nf.ok[k] ? p.nf.ns[k] : 0;
+  __syncthreads();
+  const int NC = block_exscan(nbase, K, wtmp);
+  if (tid == 0) {
+    sJ0 = J0;
+    sNC = NC;
+    sOvf = (J0 + NC > p.capacity) ? 1 : 0;
+  }
+  __syncthreads();
+  if (sOvf) {
+    if (tid == 0) atomicCAS(p.status, 0, kERuntime);
+    return;
+  }
+  // (2) create child nodes, link parents; gather per-child gate/count/tiles
+  for (int k = tid; k < K; k += nt) {
+    const int ns = p.nf.ok[k] ? p.nf.ns[k] : 0;
+    if (ns == 0) continue;
+    const int parent = p.rn[par].tree_id[k];
+    const int id0 = J0 + nbase[k];
     if (parent >= 0) {
-      p.nodes[parent].first_child = J;
+      p.nodes[parent].first_child = id0;
       p.nodes[parent].child_count = ns;
     }
     const int kept = p.nf.kept[k];
-    for (int s = 0; s < ns; ++s) {
-      const GComp& g = p.nf.comps[((size_t)k * 2 + kept) * 8 + p.nf.surv[8 * k + s]];
-      const double w = p.nf.smass[8 * k + s] / p.nf.stotal[k];
-      write_dnode_from_comp(p.nodes[J], p.cov + 9 * (size_t)J, g, w, round, parent);
-      const int cnt = p.nf.next_seg[8 * k + s];  // child entry count (from pcount)
-      int seg = -1;
-      if (!last && !(p.nf.smass[8 * k + s] < p.min_points)) {
-        needK += 1;
-        needE += cnt;
-        needT += (cnt + kTile - 1) / kTile;
-        if (K2 >= p.Kmax || E2 + cnt > p.Emax) {
-          st->status_overflow = 1;
-        } else {
-          seg = E2;
-          const int nt = (cnt + kTile - 1) / kTile;
-          p.rn[npar].tree_id[K2] = J;
-          p.rn[npar].seg[K2] = E2;
-          p.rn[npar].len[K2] = cnt;
-          p.rn[npar].tile0[K2] = T2;
-          p.rn[npar].ntiles[K2] = nt;
-          if (T2 + nt > p.Tmax) st->status_overflow = 1;
-          else
-            for (int t = 0; t < nt; ++t) {
-              p.tile_node[npar][T2 + t] = K2;
-              p.tile_start[npar][T2 + t] = E2 + t * kTile;
-              p.tile_len[npar][T2 + t] = min(kTile, cnt - t * kTile);
-            }
-          ++K2;
-          E2 += cnt;
-          T2 += nt;
-        }
-      }
-      p.nf.next_seg[8 * k + s] = seg;
-      ++J;
+    for (int s2 = 0; s2 < ns; ++s2) {
+      const int c = nbase[k] + s2;
+      const GComp& g = p.nf.comps[((size_t)k * 2 + kept) * 8 + p.nf.surv[8 * k + s2]];
+      const double w = p.nf.smass[8 * k + s2] / p.nf.stotal[k];
+      write_dnode_from_comp(p.nodes[id0 + s2], p.cov + 9 * (size_t)(id0 + s2), g, w, round, parent);
+      const int cnt = p.nf.next_seg[8 * k + s2];  // child entry count (from pcount)
+      const bool gate = !last && !(p.nf.smass[8 * k + s2] < p.min_points);
+      cgate[c] = gate ? 1 : 0;
+      ccnt[c] = gate ? cnt : 0;
+      ctil[c] = gate ? (cnt + kTile - 1) / kTile : 0;
+      cidx[c] = (k << 3) | s2;
     }
   }
-  st->J = J;
-  if (!last && st->status_overflow) {
-    st->need_K = needK;
-    st->need_E = needE;
-    st->need_T = needT;
+  __syncthreads();
+  // (3) next round's expanding list: positions, entry offsets, tile offsets
+  for (int c = tid; c < NC; c += nt) ngate[c] = cgate[c];
+  __syncthreads();
+  const int K2 = block_exscan(cgate, NC, wtmp);
+  const int E2 = block_exscan(ccnt, NC, wtmp);
+  const int T2 = block_exscan(ctil, NC, wtmp);
+  if (tid == 0) {
+    sK2 = K2;
+    sE2 = E2;
+    sT2 = T2;
+    sOvf = (!last && (K2 > p.Kmax || E2 > p.Emax || T2 > p.Tmax)) ? 1 : 0;
   }
-  st->round = round + 1;
-  st->Kp[npar] = K2;
-  st->Ep[npar] = E2;
-  st->Tp[npar] = T2;
-  if (round + 1 < 8) {
-    st->E_round[round + 1] = (unsigned long long)E2;
-    st->K_round[round + 1] = K2;
+  __syncthreads();
+  if (sOvf) {
+    if (tid == 0) {
+      st->status_overflow = 1;
+      st->need_K = K2;
+      st->need_E = E2;
+      st->need_T = T2;
+      st->done = 1;
+      __threadfence();
+    }
+    return;
   }
-  if (last || K2 == 0) st->done = 1;
-  __threadfence();
-  (void)sm;
+  for (int c = tid; c < NC; c += nt) {
+    const int k = cidx[c] >> 3, s2 = cidx[c] & 7;
+    if (!ngate[c]) {
+      p.nf.next_seg[8 * k + s2] = -1;
+      continue;
+    }
+    const int k2 = cgate[c], e2 = ccnt[c], t2 = ctil[c];
+    const int cnt = p.nf.next_seg[8 * k + s2];
+    const int ntl = (cnt + kTile - 1) / kTile;
+    p.rn[npar].tree_id[k2] = J0 + c;
+    p.rn[npar].seg[k2] = e2;
+    p.rn[npar].len[k2] = cnt;
+    p.rn[npar].tile0[k2] = t2;
+    p.rn[npar].ntiles[k2] = ntl;
+    for (int q = 0; q < ntl; ++q) {
+      p.tile_node[npar][t2 + q] = k2;
+      p.tile_start[npar][t2 + q] = e2 + q * kTile;
+      p.tile_len[npar][t2 + q] = min(kTile, cnt - q * kTile);
+    }
+    p.nf.next_seg[8 * k + s2] = e2;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    st->J = J0 + NC;
+    if (round == 0) st->root_count = NC;
+    if (round < 8) st->lvl_start[round] = J0;
+    st->lvl_start[round + 1] = J0 + NC;
+    st->round = round + 1;
+    st->Kp[npar] = K2;
+    st->Ep[npar] = E2;
+    st->Tp[npar] = T2;
+    if (round + 1 < 8) {
+      st->E_round[round + 1] = (unsigned long long)E2;
+      st->K_round[round + 1] = K2;
+    }
+    if (last || K2 == 0) {
+      st->done = 1;
+      for (int l = round + 1; l < 9; ++l) st->lvl_start[l] = J0 + NC;
+    }
+    __threadfence();
+  }
+  __syncthreads();
 }
 
-// reset_parents_to_child_moments (gmm.cpp:489-513), CTA 0, thread 0.
-__device__ void reset_parents(const BuildParams& p, int J) {
-  for (int l = p.L - 2; l >= 0; --l)
-    for (int i = 0; i < J; ++i) {
+// reset_parents_to_child_moments (gmm.cpp:489-513), one CTA: levels bottom
+// up, the parents of a level in parallel (each parent's sums run over its
+// children in order, as in the reference).
+__device__ void reset_parents(const BuildParams& p, const int* lvl_start) {
+  for (int l = p.L - 2; l >= 0; --l) {
+    for (int i = lvl_start[l] + threadIdx.x; i < lvl_start[l + 1]; i += blockDim.x) {
       DNode& nd = p.nodes[i];
-      if (nd.level != l || nd.child_count == 0) continue;
+      if (nd.child_count == 0) continue;
       double w = 0.0, mu[3] = {0.0, 0.0, 0.0};
       for (int c = 0; c < nd.child_count; ++c) {
         const DNode& ch = p.nodes[nd.first_child + c];
@@ -889,6 +999,8 @@ __device__ void reset_parents(const BuildParams& p, int J) {
       for (int k = 0; k < 9; ++k) p.cov[9 * (size_t)i + k] = cov[k] / w;
       for (int k = 0; k < 3; ++k) nd.mean[k] = mu[k];
     }
+    __syncthreads();
+  }
 }
 
 // ----------------------------------------------------------------- kernel
@@ -961,6 +1073,7 @@ __global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   BuildState* st = p.st;
+  tl_mark(st, -1);
   // ------------------------------------------------ expansion rounds
   for (int round = 0; round < p.L; ++round) {
     const int par = round & 1;
@@ -972,8 +1085,9 @@ __global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
             ph.pwrite))
         continue;
       if (ph.layout) {
-        if (cta == 0) round_layout(p, par, round, sm);
+        if (cta == 0) round_layout(p, par, round, p.layout_scratch);
         grid_sync(p.bar, G);
+        tl_mark(st, round * 100 + ph_i);
         continue;
       }
       // (a) tile pass
@@ -991,6 +1105,7 @@ __global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
         __syncthreads();
       }
       grid_sync(p.bar, G);
+      tl_mark(st, round * 100 + ph_i);
       if (ph.pwrite) continue;
       // (b) per-node reduction of the tile records + node update
       if (tid == 0) sm.nitems = phase_items(ph, sm.item_off, sm.item_kind);
@@ -1013,30 +1128,26 @@ __global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
         if (last) node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
       }
       grid_sync(p.bar, G);
+      tl_mark(st, round * 100 + 50 + ph_i);
     }
     if (__ldcg(&st->done) || __ldcg(&st->status_overflow)) break;
   }
   if (__ldcg(&st->status_overflow)) return;
   const int J = __ldcg(&st->J);
+  __shared__ int lvl[9];
+  if (tid < 9) lvl[tid] = __ldcg(&st->lvl_start[tid]);
+  __syncthreads();
   // ------------------------------------------------ rematch + refresh_eig
-  if (cta == 0 && tid == 0) reset_parents(p, J);
+  tl_mark(st, 900);
+  if (cta == 0) reset_parents(p, lvl);
   grid_sync(p.bar, G);
+  tl_mark(st, 901);
   for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x)
     if (refresh_node(p.nodes[j], p.cov + 9 * (size_t)j)) atomicCAS(p.status, 0, kEInval);
   grid_sync(p.bar, G);
+  tl_mark(st, 902);
   // ------------------------------------------------ leaf calibration
-  int root_count = 0;
-  {
-    // level-0 prefix
-    __shared__ int rc;
-    if (tid == 0) {
-      int c = 0;
-      while (c < J && p.nodes[c].level == 0) ++c;
-      rc = c;
-    }
-    __syncthreads();
-    root_count = rc;
-  }
+  const int root_count = lvl[1] - lvl[0];
   for (int pass = 0; pass < 40; ++pass) {
     if (!(__ldcg(&st->drift) > 1e-13)) break;  // gmm.cpp:652
     AssocParams a = p.a;
@@ -1045,14 +1156,14 @@ __global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
     a.epoch = p.a.epoch + (uint32_t)pass;
     assoc_pass<10>(asm_, a, nullptr, G, cta);
     grid_sync(p.bar, G);
+    tl_mark(st, 1000 + pass * 10 + 1);
     // combine + leaf refit (calibrate_pass gmm.cpp:532-545)
-    const int lane = tid & 31, warp = tid >> 5;
     double drift = 0.0;
     for (int j = cta * (kTile / 32) + warp; j < J; j += G * (kTile / 32)) {
       double m[10];
       combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
       if (lane == 0) {
-        for (int q = 0; q < 10; ++q) p.cal_moments[(size_t)j * 10 + q] = m[q];
+        p.cal_moments[(size_t)j * 10] = m[0];  // branch mass seed (leaves)
         DNode& nd = p.nodes[j];
         if (nd.child_count == 0 && m[0] > 0.0) {
           const double mu[3] = {m[1] / m[0], m[2] / m[0], m[3] / m[0]};
@@ -1078,13 +1189,10 @@ __global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
             for (int s = 0; s < 3; ++s) dc[r][s] = g.cov[3 * r + s] - before[r][s];
           drift = smax(drift, norm33(dc));
           write_dnode_from_comp(nd, p.cov + 9 * (size_t)j, g, nd.weight, nd.level, nd.parent);
-          nd.child_count = 0;
-          nd.first_child = -1;
         }
       }
     }
-    // CTA max of drift (order-free)
-    {
+    {  // CTA max of drift (order-free)
       __shared__ double dmax[kTile / 32];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) drift = smax(drift, __shfl_xor_sync(0xffffffffu, drift, off));
@@ -1097,42 +1205,57 @@ __global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
       }
     }
     grid_sync(p.bar, G);
+    tl_mark(st, 1000 + pass * 10 + 2);
     if (cta == 0) {
-      if (tid == 0) {
-        double drift_all = 0.0;
-        for (int c = 0; c < G; ++c) drift_all = smax(drift_all, __ldcg(&p.cta_drift[c]));
-        // branch masses (gmm.cpp:547-556) in place of a scratch array: use
-        // cal_moments[j*10] for leaves, accumulate parents level by level.
-        double* branch = p.cal_moments;  // reuse slot 0 of each node
-        for (int j = 0; j < J; ++j)
-          if (p.nodes[j].child_count != 0) branch[(size_t)j * 10] = 0.0;
-        for (int l = p.L - 2; l >= 0; --l)
-          for (int j = 0; j < J; ++j) {
-            const DNode& nd = p.nodes[j];
-            if (nd.level != l || nd.child_count == 0) continue;
-            double s = 0.0;
-            for (int c = 0; c < nd.child_count; ++c) s += branch[(size_t)(nd.first_child + c) * 10];
-            branch[(size_t)j * 10] = s;
-          }
-        auto reweight = [&](int first, int count) {
-          double s = 0.0;
-          for (int c = 0; c < count; ++c) s += branch[(size_t)(first + c) * 10];
-          if (!(s > 0.0)) return;
-          for (int c = 0; c < count; ++c) {
-            const double w = branch[(size_t)(first + c) * 10] / s;
-            drift_all = smax(drift_all, fabs(p.nodes[first + c].weight - w));
-            p.nodes[first + c].weight = w;
-          }
-        };
-        reweight(0, root_count);
-        for (int j = 0; j < J; ++j)
-          if (p.nodes[j].child_count != 0) reweight(p.nodes[j].first_child, p.nodes[j].child_count);
-        reset_parents(p, J);
-        st->drift = drift_all;
-        st->cal_pass = pass + 1;
-        __threadfence();
+      // branch masses bottom-up (gmm.cpp:547-556), level-parallel
+      double* branch = p.cal_moments;  // slot 0 of each node
+      for (int l = p.L - 2; l >= 0; --l) {
+        for (int j = lvl[l] + tid; j < lvl[l + 1]; j += blockDim.x) {
+          const DNode& nd = p.nodes[j];
+          if (nd.child_count == 0) continue;
+          double sb = 0.0;
+          for (int c = 0; c < nd.child_count; ++c) sb += branch[(size_t)(nd.first_child + c) * 10];
+          branch[(size_t)j * 10] = sb;
+        }
+        __syncthreads();
       }
-      __syncthreads();
+      // sibling reweight per octet (gmm.cpp:557-574), octets in parallel
+      double drift2 = 0.0;
+      for (int j = tid - 1; j < J; j += blockDim.x) {
+        int first, count;
+        if (j < 0) {
+          first = 0;
+          count = root_count;
+        } else {
+          if (p.nodes[j].child_count == 0) continue;
+          first = p.nodes[j].first_child;
+          count = p.nodes[j].child_count;
+        }
+        double sb = 0.0;
+        for (int c = 0; c < count; ++c) sb += branch[(size_t)(first + c) * 10];
+        if (!(sb > 0.0)) continue;  // shadowed octet keeps the fitted shares
+        for (int c = 0; c < count; ++c) {
+          const double w = branch[(size_t)(first + c) * 10] / sb;
+          drift2 = smax(drift2, fabs(p.nodes[first + c].weight - w));
+          p.nodes[first + c].weight = w;
+        }
+      }
+      {
+        __shared__ double dmx[kTile / 32];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) drift2 = smax(drift2, __shfl_xor_sync(0xffffffffu, drift2, off));
+        if (lane == 0) dmx[warp] = drift2;
+        __syncthreads();
+        if (tid == 0) {
+          double d = 0.0;
+          for (int c = 0; c < G; ++c) d = smax(d, __ldcg(&p.cta_drift[c]));
+          for (int w = 0; w < kTile / 32; ++w) d = smax(d, dmx[w]);
+          st->drift = d;
+          st->cal_pass = pass + 1;
+        }
+        __syncthreads();
+      }
+      reset_parents(p, lvl);
       // refresh_eig of internal nodes (gmm.cpp:576-578)
       for (int j = tid; j < J; j += blockDim.x)
         if (p.nodes[j].child_count != 0)
@@ -1140,6 +1263,7 @@ __global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
       __threadfence();
     }
     grid_sync(p.bar, G);
+    tl_mark(st, 1000 + pass * 10 + 3);
   }
   if (cta == 0 && tid == 0) st->cal_evals = __ldcg(&p.a.counters[1]);
 }
@@ -1224,6 +1348,7 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
                o_tb = carve(sizeof(double) * 8 * T),
                o_md = carve(sizeof(double) * E), o_emit = carve(sizeof(double) * 8 * E),
                o_calm = carve(sizeof(double) * 10 * cap), o_bar = carve(64),
+               o_lay = carve(sizeof(int) * 48 * K),
                o_state = carve(sizeof(BuildState));
   const int G = persistent_grid(ctx, (const void*)k_build, kTile, 0);
   const size_t o_cd = carve(sizeof(double) * G);
@@ -1269,6 +1394,7 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   p.min_d2 = (double*)(A + o_md);
   p.emit = (double*)(A + o_emit);
   p.cal_moments = (double*)(A + o_calm);
+  p.layout_scratch = (int*)(A + o_lay);
   p.bar = (unsigned*)(A + o_bar);
   p.st = (BuildState*)(A + o_state);
   p.cta_drift = (double*)(A + o_cd);
@@ -1310,18 +1436,17 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   TRG_CU(cudaMemsetAsync(A + o_arr, 0, sizeof(unsigned) * K, ctx->stream));
   TRG_CU(cudaMemsetAsync(A + o_fd, 0, sizeof(unsigned) * K, ctx->stream));
   TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
-  TRG_CU(cudaMemcpyAsync(p.st, &st, sizeof st, cudaMemcpyHostToDevice, ctx->stream));
+  TRG_CU(trg_memcpy(ctx, p.st, &st, sizeof st, cudaMemcpyHostToDevice));
   const int h_rn[5] = {-1, 0, (int)n, 0, st.Tp[0]};
   for (int q = 0; q < 5; ++q)
-    TRG_CU(cudaMemcpyAsync(A + o_rn[0][q], &h_rn[q], sizeof(int), cudaMemcpyHostToDevice,
-                           ctx->stream));
+    TRG_CU(trg_memcpy(ctx, A + o_rn[0][q], &h_rn[q], sizeof(int), cudaMemcpyHostToDevice));
   k_init_entries<<<256, 256, 0, ctx->stream>>>(pts, n, p.ex[0], p.ey[0], p.ez[0], p.ew[0],
                                                p.tile_node[0], p.tile_start[0], p.tile_len[0],
                                                ctx->status);
   void* args[] = {&p};
   TRG_CU(cudaLaunchCooperativeKernel((const void*)k_build, G, kTile, args, 0, ctx->stream));
   ctx->launches += 2;
-  TRG_CU(cudaMemcpyAsync(&st, p.st, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(trg_memcpy(ctx, &st, p.st, sizeof st, cudaMemcpyDeviceToHost));
   int rc = check_status(ctx, "build_tree");
   if (rc == TRG_OK && st.status_overflow) {
     *overflow = true;
@@ -1336,14 +1461,9 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
     return rc;
   }
   tree->n_nodes = st.J;
-  {
-    // root_count: level-0 prefix (from the host copy of levels)
-    std::vector<DNode> h(st.J);
-    TRG_CU(cudaMemcpy(h.data(), tree->nodes, sizeof(DNode) * st.J, cudaMemcpyDeviceToHost));
-    int rcnt = 0;
-    while (rcnt < st.J && h[rcnt].level == 0) ++rcnt;
-    tree->root_count = rcnt;
-  }
+  tree->root_count = st.root_count;
+  ctx->timeline.assign(st.tl_t, st.tl_t + std::min(st.tl_n, 1024));
+  ctx->timeline_lab.assign(st.tl_lab, st.tl_lab + std::min(st.tl_n, 1024));
   if (diag) {
     for (int r = 0; r < 8; ++r) {
       diag->entries_per_round[r] = r < L ? st.E_round[r] : 0;

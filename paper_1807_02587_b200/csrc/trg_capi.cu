@@ -50,7 +50,7 @@ int host_ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out) {
 
 int check_status(trg_ctx* ctx, const char* where) {
   int st = 0;
-  TRG_CU(cudaMemcpyAsync(&st, ctx->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(trg_memcpy(ctx, &st, ctx->status, sizeof(int), cudaMemcpyDeviceToHost));
   TRG_CU(cudaStreamSynchronize(ctx->stream));
   if (st != 0) {
     TRG_CU(cudaMemsetAsync(ctx->status, 0, sizeof(int), ctx->stream));
@@ -96,7 +96,7 @@ int stage_points_public(trg_ctx* ctx, const double* xyz, size_t n, int on_device
   }
   void* p = nullptr;
   TRG_TRY(ws_get(ctx, slot, sizeof(double) * 3 * n, &p));
-  TRG_CU(cudaMemcpyAsync(p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+  TRG_CU(trg_memcpy(ctx, p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
   *dev = static_cast<const double*>(p);
   return TRG_OK;
 }
@@ -153,6 +153,18 @@ int trg_ctx_destroy(trg_ctx* ctx) {
 }
 
 int trg_device_sms(trg_ctx* ctx) { return ctx->sms; }
+int trg_debug_build_timeline(trg_ctx* ctx, uint64_t* t_ns, int* labels, int cap) {
+  const int n = (int)ctx->timeline.size();
+  for (int i = 0; i < n && i < cap; ++i) {
+    t_ns[i] = ctx->timeline[i];
+    labels[i] = ctx->timeline_lab[i];
+  }
+  return n;
+}
+void trg_ctx_transfer_bytes(trg_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
+  *h2d = ctx->bytes_h2d;
+  *d2h = ctx->bytes_d2h;
+}
 uint64_t trg_kernel_launches(trg_ctx* ctx) { return ctx->launches; }
 void* trg_ctx_stream(trg_ctx* ctx) { return (void*)ctx->stream; }
 
@@ -199,10 +211,8 @@ int trg_tree_upload(trg_ctx* ctx, const trg_tree* h, trg_tree_dev** out) {
   t->n_nodes = J;
   t->max_level = h->max_level;
   t->root_count = root_count;
-  TRG_CU(cudaMemcpyAsync(t->nodes, nodes.data(), sizeof(DNode) * J, cudaMemcpyHostToDevice,
-                         ctx->stream));
-  TRG_CU(cudaMemcpyAsync(t->cov, h->cov, sizeof(double) * 9 * J, cudaMemcpyHostToDevice,
-                         ctx->stream));
+  TRG_CU(trg_memcpy(ctx, t->nodes, nodes.data(), sizeof(DNode) * J, cudaMemcpyHostToDevice));
+  TRG_CU(trg_memcpy(ctx, t->cov, h->cov, sizeof(double) * 9 * J, cudaMemcpyHostToDevice));
   TRG_CU(cudaStreamSynchronize(ctx->stream));
   *out = t;
   return TRG_OK;
@@ -220,10 +230,8 @@ int trg_tree_download(trg_ctx* ctx, const trg_tree_dev* t, trg_tree* h) {
   TRG_CU(cudaSetDevice(ctx->device));
   const int J = t->n_nodes;
   std::vector<DNode> nodes(J);
-  TRG_CU(cudaMemcpyAsync(nodes.data(), t->nodes, sizeof(DNode) * J, cudaMemcpyDeviceToHost,
-                         ctx->stream));
-  TRG_CU(cudaMemcpyAsync(h->cov, t->cov, sizeof(double) * 9 * J, cudaMemcpyDeviceToHost,
-                         ctx->stream));
+  TRG_CU(trg_memcpy(ctx, nodes.data(), t->nodes, sizeof(DNode) * J, cudaMemcpyDeviceToHost));
+  TRG_CU(trg_memcpy(ctx, h->cov, t->cov, sizeof(double) * 9 * J, cudaMemcpyDeviceToHost));
   TRG_CU(cudaStreamSynchronize(ctx->stream));
   h->n_nodes = J;
   h->max_level = t->max_level;
@@ -303,7 +311,7 @@ int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, siz
   double hrt[12];
   for (int k = 0; k < 9; ++k) hrt[k] = R[k];
   for (int k = 0; k < 3; ++k) hrt[9 + k] = t[k];
-  TRG_CU(cudaMemcpyAsync(rt, hrt, sizeof hrt, cudaMemcpyHostToDevice, ctx->stream));
+  TRG_CU(trg_memcpy(ctx, rt, hrt, sizeof hrt, cudaMemcpyHostToDevice));
   p.Rt = static_cast<const double*>(rt);
   TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
   if (point_node) {
@@ -316,14 +324,11 @@ int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, siz
   TRG_TRY(launch_associate(ctx, p, nm, static_cast<double*>(mom), G));
   std::vector<double> hm((size_t)nm * J);
   unsigned long long hc[2];
-  TRG_CU(cudaMemcpyAsync(hm.data(), mom, sizeof(double) * nm * J, cudaMemcpyDeviceToHost,
-                         ctx->stream));
-  TRG_CU(cudaMemcpyAsync(hc, cnt, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(trg_memcpy(ctx, hm.data(), mom, sizeof(double) * nm * J, cudaMemcpyDeviceToHost));
+  TRG_CU(trg_memcpy(ctx, hc, cnt, sizeof hc, cudaMemcpyDeviceToHost));
   if (point_node) {
-    TRG_CU(cudaMemcpyAsync(point_node, p.point_node, sizeof(int) * n, cudaMemcpyDeviceToHost,
-                           ctx->stream));
-    TRG_CU(cudaMemcpyAsync(point_weight, p.point_w, sizeof(double) * n, cudaMemcpyDeviceToHost,
-                           ctx->stream));
+    TRG_CU(trg_memcpy(ctx, point_node, p.point_node, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    TRG_CU(trg_memcpy(ctx, point_weight, p.point_w, sizeof(double) * n, cudaMemcpyDeviceToHost));
   }
   TRG_TRY(check_status(ctx, "associate_adaptive"));
   double mass = 0.0;

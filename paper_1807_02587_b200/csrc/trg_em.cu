@@ -253,7 +253,7 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   for (int k = 0; k < 3; ++k) st.Rt[9 + k] = cfg->initial_t[k];
   TRG_CU(cudaMemsetAsync(em, 0, 64, ctx->stream));
   TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
-  TRG_CU(cudaMemcpyAsync(p.st, &st, sizeof st, cudaMemcpyHostToDevice, ctx->stream));
+  TRG_CU(trg_memcpy(ctx, p.st, &st, sizeof st, cudaMemcpyHostToDevice));
   k_check_finite<<<64, 256, 0, ctx->stream>>>(src_dev, 3 * n, ctx->status);
   k_extent<<<1, 256, 0, ctx->stream>>>(tree->nodes, J, p.st, target_diag, cfg->translation_tol);
   cudaEvent_t e0, e1;
@@ -265,15 +265,12 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
                                      ctx->stream));
   TRG_CU(cudaEventRecord(e1, ctx->stream));
   ctx->launches += 3;
-  TRG_CU(cudaMemcpyAsync(&st, p.st, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(trg_memcpy(ctx, &st, p.st, sizeof st, cudaMemcpyDeviceToHost));
   std::vector<double> cb(K), ca(K);
   std::vector<unsigned long long> ev(K);
-  TRG_CU(cudaMemcpyAsync(cb.data(), p.crit_before, sizeof(double) * K, cudaMemcpyDeviceToHost,
-                         ctx->stream));
-  TRG_CU(cudaMemcpyAsync(ca.data(), p.crit_after, sizeof(double) * K, cudaMemcpyDeviceToHost,
-                         ctx->stream));
-  TRG_CU(cudaMemcpyAsync(ev.data(), p.evals, sizeof(unsigned long long) * K,
-                         cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(trg_memcpy(ctx, cb.data(), p.crit_before, sizeof(double) * K, cudaMemcpyDeviceToHost));
+  TRG_CU(trg_memcpy(ctx, ca.data(), p.crit_after, sizeof(double) * K, cudaMemcpyDeviceToHost));
+  TRG_CU(trg_memcpy(ctx, ev.data(), p.evals, sizeof(unsigned long long) * K, cudaMemcpyDeviceToHost));
   TRG_CU(cudaEventSynchronize(e1));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
@@ -331,7 +328,7 @@ double target_bbox_diagonal(trg_ctx* ctx, const double* dev_or_null, const doubl
   k_bbox<<<1, 256, 0, ctx->stream>>>(dev_or_null, n, static_cast<double*>(o));
   ctx->launches += 1;
   double d = 0.0;
-  cudaMemcpyAsync(&d, o, sizeof d, cudaMemcpyDeviceToHost, ctx->stream);
+  trg_memcpy(ctx, &d, o, sizeof d, cudaMemcpyDeviceToHost);
   cudaStreamSynchronize(ctx->stream);
   return d;
 }
@@ -360,14 +357,13 @@ int trg_solve_mstep(trg_ctx* ctx, const trg_tree_dev* tree, const double* m0, co
   void *mom, *so;
   TRG_TRY(ws_get(ctx, kSlotMoments, sizeof(double) * 4 * (size_t)J, &mom));
   TRG_TRY(ws_get(ctx, kSlotSolve, sizeof(SolveOut), &so));
-  TRG_CU(cudaMemcpyAsync(mom, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice,
-                         ctx->stream));
+  TRG_CU(trg_memcpy(ctx, mom, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
   k_solve<<<1, 256, 0, ctx->stream>>>(tree->nodes, J, static_cast<double*>(mom),
                                       (double)total_points, static_cast<SolveOut*>(so),
                                       ctx->status);
   ctx->launches += 1;
   SolveOut o;
-  TRG_CU(cudaMemcpyAsync(&o, so, sizeof o, cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(trg_memcpy(ctx, &o, so, sizeof o, cudaMemcpyDeviceToHost));
   TRG_TRY(check_status(ctx, "solve_mstep"));
   out->n_virtual_points = o.nvp;
   out->condition_estimate = o.cond;

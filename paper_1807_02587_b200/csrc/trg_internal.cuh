@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/treereg_b200.h"
 #include "trg_math.cuh"
@@ -52,6 +53,7 @@ struct trg_tree_dev {
 
 struct trg_ctx {
   int device = 0;
+  uint64_t bytes_h2d = 0, bytes_d2h = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
@@ -62,6 +64,8 @@ struct trg_ctx {
   void* host_slot_ptr[kSlots] = {};
   size_t host_slot_size[kSlots] = {};
   int* status = nullptr;  // device status word
+  std::vector<unsigned long long> timeline;  // last build: globaltimer ns per barrier
+  std::vector<int> timeline_lab;
 };
 
 namespace trg {
@@ -94,6 +98,15 @@ enum Slot : int {
 };
 
 int ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
+
+// Every host<->device copy of the library goes through here (byte counters
+// back the e2e h2d/d2h figures of bench.py).
+inline cudaError_t trg_memcpy(trg_ctx* ctx, void* dst, const void* src, size_t bytes,
+                              cudaMemcpyKind kind) {
+  if (kind == cudaMemcpyHostToDevice) ctx->bytes_h2d += bytes;
+  if (kind == cudaMemcpyDeviceToHost) ctx->bytes_d2h += bytes;
+  return cudaMemcpyAsync(dst, src, bytes, kind, ctx->stream);
+}
 int host_ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
 int check_status(trg_ctx* ctx, const char* where);
 int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out);

@@ -97,6 +97,12 @@ class Context:
     def kernel_launches(self) -> int:
         return int(_lib.lib().trg_kernel_launches(self.h))
 
+    def transfer_bytes(self):
+        """(host->device, device->host) bytes copied by this context so far."""
+        a, b = C.c_uint64(), C.c_uint64()
+        _lib.lib().trg_ctx_transfer_bytes(self.h, C.byref(a), C.byref(b))
+        return int(a.value), int(b.value)
+
     @property
     def stream(self) -> int:
         return int(_lib.lib().trg_ctx_stream(self.h) or 0)
