@@ -445,12 +445,20 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     double m = lg;
 #pragma unroll
     for (int off = 1; off < 8; off <<= 1) m = smax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    // gather the 8 log-terms; sum exps in component order (gmm.cpp:183)
-    double lgs[8];
+    const bool fin = act && isfinite(m);  // uniform within the 8-lane group
+    // each lane exponentiates its own term; the sum runs in component
+    // order like gmm.cpp:183 (all lanes take part in every shuffle)
+    const double ek = fin ? exp(lg - m) : 0.0;
+    double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) lgs[k] = __shfl_sync(0xffffffffu, lg, gbase + k);
+    for (int k = 0; k < 8; ++k) s += __shfl_sync(0xffffffffu, ek, gbase + k);
+    const double lt = fin ? m + log(s) : 0.0;
+    const double gam = fin ? exp(lg - lt) : 0.0;
+    double denom = 0.0;
+    if (mode == 3)
+      for (int s2 = 0; s2 < sm.ns; ++s2) denom += __shfl_sync(0xffffffffu, gam, gbase + sm.surv[s2]);
     if (!act) continue;
-    if (!isfinite(m)) {
+    if (!fin) {
       // gmm.cpp:348: the entry keeps gamma = 0; the partition then hands it
       // whole to the heaviest survivor (gmm.cpp:444-453)
       if (mode == 3 && my_s >= 0) {
@@ -465,13 +473,8 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
           acc[1] += w;
         }
       }
-      continue;  // uniform within the 8-lane group
+      continue;
     }
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) s += exp(lgs[k] - m);
-    const double lt = m + log(s);
-    const double gam = exp(lg - lt);
     if (mode == 1) {
       if (comp == 0) acc[10] += w * lt;
       const double g = gam * w;
@@ -493,8 +496,6 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
       acc[0] += w * gam;
     } else if (mode == 3) {
       // survivor-normalised soft partition (gmm.cpp:434-454)
-      double denom = 0.0;
-      for (int s2 = 0; s2 < sm.ns; ++s2) denom += exp(lgs[sm.surv[s2]] - lt);
       double* em = p.emit + (size_t)e * 8;
       if (denom > 0.0) {
         if (my_s >= 0) {
@@ -1066,7 +1067,7 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
 constexpr size_t kBuildSmemBytes =
     sizeof(BuildSmem) > sizeof(AssocSmem<10>) ? sizeof(BuildSmem) : sizeof(AssocSmem<10>);
 
-__global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
+__global__ void __launch_bounds__(kTile, 2) k_build(BuildParams p) {
   __shared__ __align__(16) unsigned char smem_raw[kBuildSmemBytes];
   BuildSmem& sm = *reinterpret_cast<BuildSmem*>(smem_raw);
   AssocSmem<10>& asm_ = *reinterpret_cast<AssocSmem<10>*>(smem_raw);
@@ -1246,10 +1247,16 @@ __global__ void __launch_bounds__(kTile, 1) k_build(BuildParams p) {
         for (int off = 16; off > 0; off >>= 1) drift2 = smax(drift2, __shfl_xor_sync(0xffffffffu, drift2, off));
         if (lane == 0) dmx[warp] = drift2;
         __syncthreads();
+        double dc = 0.0;
+        for (int c = tid; c < G; c += blockDim.x) dc = smax(dc, __ldcg(&p.cta_drift[c]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) dc = smax(dc, __shfl_xor_sync(0xffffffffu, dc, off));
+        __shared__ double dcw[kTile / 32];
+        if (lane == 0) dcw[warp] = dc;
+        __syncthreads();
         if (tid == 0) {
           double d = 0.0;
-          for (int c = 0; c < G; ++c) d = smax(d, __ldcg(&p.cta_drift[c]));
-          for (int w = 0; w < kTile / 32; ++w) d = smax(d, dmx[w]);
+          for (int w = 0; w < kTile / 32; ++w) d = smax(d, smax(dmx[w], dcw[w]));
           st->drift = d;
           st->cal_pass = pass + 1;
         }
@@ -1517,9 +1524,14 @@ extern "C" int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz
   const int L = cfg->max_level;
   int kmax = 1;
   for (int l = 0; l + 1 < L; ++l) kmax *= 8;
+  // Entry-buffer capacity: soft-partition growth is data dependent (E_l/E_{l-1}
+  // ~2.5-5 on surfaces, at most 8).  Start from the largest ratio this
+  // context has seen (initially 12 x N for L >= 3) so repeated builds never
+  // take the overflow-and-retry path.
   BuildAlloc al;
   al.Kmax = std::max(1, kmax);
-  al.Emax = (int)std::min<size_t>((size_t)INT32_MAX / 16, n * (L > 1 ? 4 : 1) + 1024);
+  const double ratio = std::max(ctx->build_growth, L >= 3 ? 12.0 : (L == 2 ? 8.0 : 1.0));
+  al.Emax = (int)std::min<double>((double)INT32_MAX / 16, ratio * (double)n + 1024.0);
   al.Tmax = al.Emax / kTile + al.Kmax + 8;
   for (int attempt = 0; attempt < 4; ++attempt) {
     bool overflow = false;
@@ -1530,6 +1542,7 @@ extern "C" int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz
       return rc;
     }
     if (!overflow) return TRG_OK;
+    ctx->build_growth = std::max(ctx->build_growth, 1.25 * (double)need.Emax / (double)n);
     al.Emax = std::max(al.Emax * 2, need.Emax + 1024);
     al.Kmax = std::max(al.Kmax, need.Kmax);
     al.Tmax = al.Emax / kTile + al.Kmax + 8;

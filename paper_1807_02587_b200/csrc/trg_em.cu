@@ -77,10 +77,17 @@ __global__ void __launch_bounds__(kAssocBlock, 2) k_register(EmParams p) {
     grid_sync(p.bar, G);
     // ---- P3: CTA 0 solves and updates the transform
     if (cta == 0) {
-      if (tid < kAccStride) {
+      // fold the per-CTA normal equations: 8 lanes per value, strided over
+      // CTAs, then a fixed shuffle tree (deterministic)
+      {
+        const int v = tid >> 3, sub = tid & 7;
         double s = 0.0;
-        for (int c = 0; c < G; ++c) s += ldcg(p.cta_acc + (size_t)c * kAccStride + tid);
-        red[tid] = s;
+        if (v < kAccStride)
+          for (int c = sub; c < G; c += 8) s += ldcg(p.cta_acc + (size_t)c * kAccStride + v);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        if (v < kAccStride && sub == 0) red[v] = s;
       }
       __syncthreads();
       __shared__ SolveOut so;
@@ -292,12 +299,16 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   return TRG_OK;
 }
 
-// Bounding-box diagonal of a cloud (cloud_io.cpp:21-33).  min/max are exact,
-// so the device reduction is bit-identical to the reference.
-__global__ void k_bbox(const double* __restrict__ p, size_t n, double* out) {
+// Bounding-box diagonal of a cloud (cloud_io.cpp:21-33): per-block min/max,
+// the last block folds them.  min/max are exact, so the result is
+// bit-identical to the reference for any reduction order.
+__global__ void k_bbox(const double* __restrict__ p, size_t n, double* part, unsigned* cnt,
+                       double* out) {
   __shared__ double lo[3][256], hi[3][256];
+  __shared__ bool last;
   double l[3] = {p[0], p[1], p[2]}, h[3] = {p[0], p[1], p[2]};
-  for (size_t i = threadIdx.x; i < n; i += blockDim.x)
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
     for (int k = 0; k < 3; ++k) {
       const double v = p[3 * i + k];
       l[k] = (v < l[k]) ? v : l[k];
@@ -308,24 +319,46 @@ __global__ void k_bbox(const double* __restrict__ p, size_t n, double* out) {
     hi[k][threadIdx.x] = h[k];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int t = 1; t < blockDim.x; ++t)
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
       for (int k = 0; k < 3; ++k) {
-        l[k] = (lo[k][t] < l[k]) ? lo[k][t] : l[k];
-        h[k] = (h[k] < hi[k][t]) ? hi[k][t] : h[k];
+        lo[k][threadIdx.x] = smin(lo[k][threadIdx.x], lo[k][threadIdx.x + s]);
+        hi[k][threadIdx.x] = smax(hi[k][threadIdx.x], hi[k][threadIdx.x + s]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 3; ++k) {
+      part[6 * blockIdx.x + k] = lo[k][0];
+      part[6 * blockIdx.x + 3 + k] = hi[k][0];
+    }
+    __threadfence();
+    last = atomicAdd(cnt, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    for (int b = 0; b < (int)gridDim.x; ++b)
+      for (int k = 0; k < 3; ++k) {
+        l[k] = smin(l[k], __ldcg(&part[6 * b + k]));
+        h[k] = smax(h[k], __ldcg(&part[6 * b + 3 + k]));
       }
     double s = (h[0] - l[0]) * (h[0] - l[0]);
     s += (h[1] - l[1]) * (h[1] - l[1]);
     s += (h[2] - l[2]) * (h[2] - l[2]);
     *out = sqrt(s);
+    *cnt = 0u;
   }
 }
 
-double target_bbox_diagonal(trg_ctx* ctx, const double* dev_or_null, const double* host, size_t n) {
-  if (!dev_or_null) return trg_bbox_diagonal(host, n);
+double target_bbox_diagonal(trg_ctx* ctx, const double* dev, size_t n) {
   void* o = nullptr;
-  if (ws_get(ctx, kSlotSolve, 64, &o) != TRG_OK) return 0.0;
-  k_bbox<<<1, 256, 0, ctx->stream>>>(dev_or_null, n, static_cast<double*>(o));
+  const int nb = 64;
+  if (ws_get(ctx, kSlotBuild11, 64 + sizeof(double) * 6 * nb, &o) != TRG_OK) return 0.0;
+  double* od = static_cast<double*>(o);
+  cudaMemsetAsync(static_cast<char*>(o) + 8, 0, 8, ctx->stream);
+  k_bbox<<<nb, 256, 0, ctx->stream>>>(dev, n, od + 8, reinterpret_cast<unsigned*>(od + 1),
+                                      od);
   ctx->launches += 1;
   double d = 0.0;
   trg_memcpy(ctx, &d, o, sizeof d, cudaMemcpyDeviceToHost);
@@ -454,7 +487,9 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
   }
   TRG_CU(cudaSetDevice(ctx->device));
   const double* src = nullptr;
+  const double* tgt = nullptr;
   TRG_TRY(stage_points_public(ctx, source, n_source, on_device, kSlotPoints2, &src));
+  TRG_TRY(stage_points_public(ctx, target, n_target, on_device, kSlotPoints, &tgt));
   cudaEvent_t e0, e1;
   TRG_CU(cudaEventCreate(&e0));
   TRG_CU(cudaEventCreate(&e1));
@@ -462,10 +497,10 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
   trg_model_config mc = cfg->model_config;
   mc.max_level = cfg->variant_param;
   trg_tree_dev* tree = nullptr;
-  int rc = trg_build_tree(ctx, target, n_target, on_device, &mc, &tree, nullptr);
+  int rc = trg_build_tree(ctx, tgt, n_target, 1, &mc, &tree, nullptr);
   if (rc != TRG_OK) return rc;
   TRG_CU(cudaEventRecord(e1, ctx->stream));
-  const double diag = target_bbox_diagonal(ctx, on_device ? target : nullptr, target, n_target);
+  const double diag = target_bbox_diagonal(ctx, tgt, n_target);
   rc = run_em(ctx, tree, src, n_source, cfg, diag, out);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);

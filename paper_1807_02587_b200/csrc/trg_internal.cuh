@@ -54,6 +54,7 @@ struct trg_tree_dev {
 struct trg_ctx {
   int device = 0;
   uint64_t bytes_h2d = 0, bytes_d2h = 0;
+  double build_growth = 0.0;  // largest E_max / N a build on this context needed
   int sms = 0;
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
