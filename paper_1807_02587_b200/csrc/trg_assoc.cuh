@@ -27,18 +27,8 @@ __device__ __forceinline__ double node_score(const DNode* __restrict__ g, double
     atomicCAS(status, 0, kEDomain);  // log_density: covariance is not PD
     return 0.0;
   }
-  const double d0 = y0 - g->mean[0], d1 = y1 - g->mean[1], d2 = y2 - g->mean[2];
-  double p0 = g->axT[0] * d0;
-  p0 += g->axT[1] * d1;
-  p0 += g->axT[2] * d2;
-  double p1 = g->axT[3] * d0;
-  p1 += g->axT[4] * d1;
-  p1 += g->axT[5] * d2;
-  double p2 = g->axT[6] * d0;
-  p2 += g->axT[7] * d1;
-  p2 += g->axT[8] * d2;
-  const double q = p0 * p0 / g->lam[0] + p1 * p1 / g->lam[1] + p2 * p2 / g->lam[2];
-  return w * exp(g->log_norm - 0.5 * q);
+  const double q = fast_q(g->mean, g->axT, g->il, y0, y1, y2);
+  return __dmul_rn(w, exp(__fma_rn(-0.5, q, g->log_norm)));
 }
 
 struct Descent {

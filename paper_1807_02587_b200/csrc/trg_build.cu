@@ -39,7 +39,7 @@ struct GComp {
   double lam[3];
   double log_norm;
   double cov[9];
-  double pad[3];
+  double il[3];  // 1 / lam
 };
 static_assert(sizeof(GComp) == 240, "GComp layout");
 
@@ -153,7 +153,7 @@ __device__ __forceinline__ void comp_to_regs(const GComp& c, double r[18]) {
 #pragma unroll
   for (int i = 0; i < 9; ++i) r[5 + i] = c.axT[i];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) r[14 + i] = c.lam[i];
+  for (int i = 0; i < 3; ++i) r[14 + i] = c.il[i];
   r[17] = c.log_norm;
 }
 
@@ -161,22 +161,12 @@ __device__ __forceinline__ void comp_to_regs(const GComp& c, double r[18]) {
 __device__ __forceinline__ double comp_log(const double r[18], double x0, double x1, double x2,
                                            int* status) {
   if (!(r[0] > 0.0)) return -INFINITY;
-  if (!(r[16] > 0.0)) {
+  if (!(r[16] > 0.0)) {  // 1/lam3: log_density on a non-PD covariance
     atomicCAS(status, 0, kEDomain);
     return -INFINITY;
   }
-  const double d0 = x0 - r[2], d1 = x1 - r[3], d2 = x2 - r[4];
-  double p0 = r[5] * d0;
-  p0 += r[6] * d1;
-  p0 += r[7] * d2;
-  double p1 = r[8] * d0;
-  p1 += r[9] * d1;
-  p1 += r[10] * d2;
-  double p2 = r[11] * d0;
-  p2 += r[12] * d1;
-  p2 += r[13] * d2;
-  const double q = p0 * p0 / r[14] + p1 * p1 / r[15] + p2 * p2 / r[16];
-  return r[1] + (r[17] - 0.5 * q);
+  const double q = fast_q(r + 2, r + 5, r + 14, x0, x1, x2);
+  return r[1] + __fma_rn(-0.5, q, r[17]);
 }
 
 // set_floored_cov (gmm.cpp:143-150) into a GComp.
@@ -187,6 +177,7 @@ __device__ __forceinline__ int comp_set_cov(GComp& g, const double sc[3][3], dou
   reconstruct(lam, ax, cov);
   for (int i = 0; i < 3; ++i) {
     g.lam[i] = lam[i];
+    g.il[i] = 1.0 / lam[i];
     for (int j = 0; j < 3; ++j) {
       g.axT[3 * i + j] = ax[j][i];
       g.cov[3 * i + j] = cov[i][j];
@@ -203,7 +194,11 @@ __device__ __forceinline__ void write_dnode_from_comp(DNode& d, double* cov9, co
     d.axT[i] = g.axT[i];
     cov9[i] = g.cov[i];
   }
-  for (int i = 0; i < 3; ++i) d.lam[i] = g.lam[i];
+  for (int i = 0; i < 3; ++i) {
+    d.lam[i] = g.lam[i];
+    d.il[i] = 1.0 / g.lam[i];
+  }
+  d.pad = 0.0;
   d.log_norm = g.log_norm;
   d.weight = w;
   const double tr = (g.lam[0] + g.lam[1]) + g.lam[2];
@@ -223,6 +218,7 @@ __device__ __forceinline__ int refresh_node(DNode& d, const double* cov9) {
   if (rc) return rc;
   for (int i = 0; i < 3; ++i) {
     d.lam[i] = lam[i];
+    d.il[i] = 1.0 / lam[i];
     for (int j = 0; j < 3; ++j) d.axT[3 * i + j] = ax[j][i];
   }
   d.log_norm = log_norm_of(lam);

@@ -197,6 +197,8 @@ int trg_tree_upload(trg_ctx* ctx, const trg_tree* h, trg_tree_dev** out) {
       d.lam[r] = h->lambdas[3 * i + r];
       for (int k = 0; k < 3; ++k) d.axT[3 * r + k] = h->axes[9 * i + 3 * k + r];
     }
+    for (int r = 0; r < 3; ++r) d.il[r] = 1.0 / d.lam[r];
+    d.pad = 0.0;
     d.log_norm = h->log_norm[i];
     d.weight = h->weight[i];
     const double tr = (d.lam[0] + d.lam[1]) + d.lam[2];

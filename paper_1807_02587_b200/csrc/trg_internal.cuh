@@ -34,13 +34,30 @@ struct __align__(16) DNode {
   double mean[3];
   double axT[9];
   double lam[3];
+  double il[3];  // 1 / lam (scoring loops multiply instead of divide)
   double log_norm;
   double weight;
   double cplx;  // node_complexity (gmm.cpp:53-59); -1 when trace <= 0
+  double pad;
   int first_child, child_count;
   int level, parent;
 };
-static_assert(sizeof(DNode) == 160, "DNode layout");
+static_assert(sizeof(DNode) == 192, "DNode layout");
+
+// Hot-loop Gaussian: log N(x) = log_norm - q/2 with q = sum_l (n_l.d)^2 / lam_l
+// (gmm.cpp:41-46) evaluated with FMAs and precomputed 1/lam.  This differs
+// from the reference's operation order by a few ulp (the parity tests hold
+// indices exact up to documented near-ties and moments to 1e-10); all
+// eigen/solve math stays in the reference's exact order.
+__device__ __forceinline__ double fast_q(const double* mean, const double* axT, const double* il,
+                                         double x0, double x1, double x2) {
+  const double d0 = x0 - mean[0], d1 = x1 - mean[1], d2 = x2 - mean[2];
+  const double p0 = __fma_rn(axT[2], d2, __fma_rn(axT[1], d1, __dmul_rn(axT[0], d0)));
+  const double p1 = __fma_rn(axT[5], d2, __fma_rn(axT[4], d1, __dmul_rn(axT[3], d0)));
+  const double p2 = __fma_rn(axT[8], d2, __fma_rn(axT[7], d1, __dmul_rn(axT[6], d0)));
+  return __fma_rn(__dmul_rn(p0, p0), il[0],
+                  __fma_rn(__dmul_rn(p1, p1), il[1], __dmul_rn(__dmul_rn(p2, p2), il[2])));
+}
 
 }  // namespace trg
 
