@@ -223,6 +223,10 @@ int trg_synth_lidar_pair(uint64_t seed, double* target, double* source, double R
 int trg_debug_build_timeline(trg_ctx* ctx, uint64_t* t_ns, int* labels, int cap);
 int trg_debug_eig(trg_ctx* ctx, int n, const double* in, int count, double* evals,
                   double* evecs, int* status);
+/* Runs the device warp-level 6-DoF solve (mstep.cpp:76-98) on packed normal
+ * equations v27 = (upper-triangular ata[21], atb[6]); out16 receives
+ * omega[3], translation[3], condition estimate, degenerate flag. */
+int trg_debug_solve(trg_ctx* ctx, const double* v27, int n_virtual_points, double* out16);
 
 #ifdef __cplusplus
 }

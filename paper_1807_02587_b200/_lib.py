@@ -109,6 +109,7 @@ SIGNATURES = {
                                            dp, dp]),
     "trg_synth_lidar_pair": (C.c_int, [C.c_uint64, dp, dp, dp, dp]),
     "trg_debug_build_timeline": (C.c_int, [C.c_void_p, u64p, ip, C.c_int]),
+    "trg_debug_solve": (C.c_int, [C.c_void_p, dp, C.c_int, dp]),
     "trg_debug_eig": (C.c_int, [C.c_void_p, C.c_int, dp, C.c_int, dp, dp, ip]),
 }
 

@@ -46,13 +46,20 @@ __device__ __forceinline__ Descent descend(const DNode* __restrict__ nodes, int 
   for (int l = 0; l < depth; ++l) {
     const int first = node < 0 ? 0 : nodes[node].first_child;
     const int count = node < 0 ? root_count : nodes[node].child_count;
+    // the <= 8 sibling scores are independent: evaluate them together (ILP),
+    // then sum and arg-max in sibling order exactly like the reference
+    double sc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      sc[k] = k < count ? node_score(nodes + first + k, y0, y1, y2, status) : 0.0;
     double sum = 0.0, best_s = 0.0;
     int best = 0;
-    for (int k = 0; k < count; ++k) {
-      const double s = node_score(nodes + first + k, y0, y1, y2, status);
-      sum += s;
-      if (k == 0 || s > best_s) {  // strict '>' : lowest index wins ties
-        best_s = s;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= count) break;
+      sum += sc[k];
+      if (k == 0 || sc[k] > best_s) {  // strict '>' : lowest index wins ties
+        best_s = sc[k];
         best = k;
       }
     }

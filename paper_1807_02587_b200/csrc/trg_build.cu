@@ -850,7 +850,7 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
   BuildState* st = p.st;
   const int tid = threadIdx.x, nt = blockDim.x;
   __shared__ int wtmp[33];
-  __shared__ int sJ0, sK2, sE2, sT2, sNC, sOvf;
+  __shared__ int sOvf;
   const int K = st->Kp[par];
   const int J0 = st->J;
   const int npar = par ^ 1;
@@ -866,8 +866,6 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
   __syncthreads();
   const int NC = block_exscan(nbase, K, wtmp);
   if (tid == 0) {
-    sJ0 = J0;
-    sNC = NC;
     sOvf = (J0 + NC > p.capacity) ? 1 : 0;
   }
   __syncthreads();
@@ -907,9 +905,6 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
   const int E2 = block_exscan(ccnt, NC, wtmp);
   const int T2 = block_exscan(ctil, NC, wtmp);
   if (tid == 0) {
-    sK2 = K2;
-    sE2 = E2;
-    sT2 = T2;
     sOvf = (!last && (K2 > p.Kmax || E2 > p.Emax || T2 > p.Tmax)) ? 1 : 0;
   }
   __syncthreads();

@@ -91,10 +91,10 @@ __global__ void __launch_bounds__(kAssocBlock, 2) k_register(EmParams p) {
       }
       __syncthreads();
       __shared__ SolveOut so;
-      if (tid == 0) {
-        so.crit_before = red[kNormalEq];
-        solve_normal_eq(red, (int)red[kNormalEq + 1], &so);
-      }
+      __shared__ Eig6Smem e6;
+      if (tid == 0) so.crit_before = red[kNormalEq];
+      __syncthreads();
+      if (tid < 32) warp_solve_normal_eq(red, (int)red[kNormalEq + 1], &so, e6);
       __syncthreads();
       double c = 0.0;
       if (!so.degenerate) {

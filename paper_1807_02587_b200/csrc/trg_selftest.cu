@@ -53,3 +53,37 @@ extern "C" int trg_debug_eig(trg_ctx* ctx, int n, const double* in, int count, d
   cudaFree(dst);
   return TRG_OK;
 }
+
+#include "trg_solve.cuh"
+namespace trg {
+__global__ void k_solve_selftest(const double* v, int nvp, SolveOut* out) {
+  __shared__ SolveOut so;
+  __shared__ Eig6Smem e6;
+  __shared__ double vs[kNormalEq];
+  if (threadIdx.x < kNormalEq) vs[threadIdx.x] = v[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < 32) warp_solve_normal_eq(vs, nvp, &so, e6);
+  __syncthreads();
+  if (threadIdx.x == 0) *out = so;
+}
+}  // namespace trg
+extern "C" int trg_debug_solve(trg_ctx* ctx, const double* v27, int nvp, double* out16) {
+  double* dv;
+  trg::SolveOut* dso;
+  TRG_CU(cudaMalloc(&dv, sizeof(double) * 27));
+  TRG_CU(cudaMalloc(&dso, sizeof(trg::SolveOut)));
+  TRG_CU(cudaMemcpy(dv, v27, sizeof(double) * 27, cudaMemcpyHostToDevice));
+  trg::k_solve_selftest<<<1, 64, 0, ctx->stream>>>(dv, nvp, dso);
+  trg::SolveOut so;
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  TRG_CU(cudaMemcpy(&so, dso, sizeof so, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 3; ++i) {
+    out16[i] = so.omega[i];
+    out16[3 + i] = so.trans[i];
+  }
+  out16[6] = so.cond;
+  out16[7] = so.degenerate;
+  cudaFree(dv);
+  cudaFree(dso);
+  return TRG_OK;
+}

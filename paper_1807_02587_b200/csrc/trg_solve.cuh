@@ -170,43 +170,177 @@ struct SolveOut {
   int degenerate;  // 1: fewer than 3 VPs or cond >= 1e12 (DegenerateGeometryError)
 };
 
-// Thread-0 part of solve_mstep (mstep.cpp:76-98) from the reduced normal
-// equations.  __noinline__ keeps its 6x6 working set out of the callers'
-// register budget.
-static __device__ __noinline__ void solve_normal_eq(const double* v, int nvp, SolveOut* o) {
-  o->nvp = nvp;
-  o->degenerate = 0;
-  if (nvp < 3) {
-    o->degenerate = 1;
-    return;
-  }
-  double ata[6][6], b[6], work[6][6], ev[6], vec[6][6];
-  int k = 0;
-  for (int i = 0; i < 6; ++i)
-    for (int j = i; j < 6; ++j) {
-      ata[i][j] = v[k];
-      ata[j][i] = v[k];
-      ++k;
+// Eigenvalues of the 6x6 normal matrix (mstep.cpp:77-80, condition
+// estimate) by a WARP-parallel Jacobi: round-robin ordering, 3 disjoint
+// rotations per step (5 steps per sweep), all 36 entries updated at once.
+// Same per-rotation formulas and skip threshold as the cyclic solver; only
+// the rotation order differs (eigenvalues agree to a few ulp).
+static __constant__ int kRR6[5][3][2] = {{{0, 5}, {1, 4}, {2, 3}}, {{0, 4}, {5, 3}, {1, 2}},
+                                  {{0, 3}, {4, 2}, {5, 1}}, {{0, 2}, {3, 1}, {4, 5}},
+                                  {{0, 1}, {2, 5}, {3, 4}}};
+
+struct Eig6Smem {
+  double a[36], b[36];
+  double c[6], s[6];  // per index: rotation of the pair it belongs to
+  double tt[3];
+  int part[6];        // partner index, role (p/q) encoded by sign
+  int tidx[6];        // which of the 3 rotations index i belongs to
+  int rotated;
+};
+
+// Called by all 32 lanes of ONE warp; returns eigenvalues ascending in ev.
+static __device__ void warp_eig6(const double* in, double ev[6], Eig6Smem& w) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < 36; i += 32) w.a[i] = in[i];
+  __syncwarp();
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    if (lane == 0) w.rotated = 0;
+    __syncwarp();
+    for (int r = 0; r < 5; ++r) {
+      if (lane < 3) {
+        int p = kRR6[r][lane][0], q = kRR6[r][lane][1];
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        const double apq = w.a[6 * p + q], app = w.a[7 * p], aqq = w.a[7 * q];
+        double c = 1.0, sn = 0.0, t = 0.0;
+        bool rot = false;
+        if (apq != 0.0) {
+          const double g = 100.0 * fabs(apq);
+          if (!(fabs(app) + g == fabs(app) && fabs(aqq) + g == fabs(aqq))) {
+            rot = true;
+            const double h = aqq - app;
+            if (fabs(h) + g == fabs(h)) {
+              t = apq / h;
+            } else {
+              const double theta = 0.5 * h / apq;
+              t = 1.0 / (fabs(theta) + sqrt(1.0 + theta * theta));
+              if (theta < 0.0) t = -t;
+            }
+            c = 1.0 / sqrt(1.0 + t * t);
+            sn = t * c;
+          }
+        }
+        if (rot) w.rotated = 1;
+        w.c[p] = c;
+        w.c[q] = c;
+        w.s[p] = sn;
+        w.s[q] = sn;
+        w.tt[lane] = t;
+        w.tidx[p] = lane;
+        w.tidx[q] = lane;
+        w.part[p] = q + 1;     // p: partner q (positive)
+        w.part[q] = -(p + 1);  // q: partner p (negative)
+      }
+      __syncwarp();
+      for (int e = lane; e < 36; e += 32) {
+        const int i = e / 6, j = e % 6;
+        const int pi = w.part[i], pj = w.part[j];
+        const bool ip = pi > 0, jp = pj > 0;           // i / j is the lower index of its pair
+        const int ii = ip ? pi - 1 : -pi - 1;          // partner of i
+        const int jj = jp ? pj - 1 : -pj - 1;          // partner of j
+        double out;
+        if (j == i || j == ii) {  // same 2x2 block
+          if (i != j) {
+            out = 0.0;  // rotated (or negligible) pair entry
+          } else {
+            const int p = ip ? i : ii, q = ip ? ii : i;
+            const double apq = w.a[6 * p + q];
+            const double t = w.tt[w.tidx[p]];
+            out = ip ? w.a[7 * p] - t * apq : w.a[7 * q] + t * apq;
+          }
+        } else {
+          // rows (i, ii) rotated by their pair, columns (j, jj) by theirs:
+          // col p' = c col p - s col q, col q' = s col p + c col q (and rows alike)
+          const double cj = w.c[j], sj = w.s[j], ci = w.c[i], si = w.s[i];
+          const double xi = w.a[6 * i + j], yi = w.a[6 * i + jj];
+          const double xii = w.a[6 * ii + j], yii = w.a[6 * ii + jj];
+          const double bi = jp ? cj * xi - sj * yi : sj * yi + cj * xi;
+          const double bii = jp ? cj * xii - sj * yii : sj * yii + cj * xii;
+          out = ip ? ci * bi - si * bii : si * bii + ci * bi;
+        }
+        w.b[e] = out;
+      }
+      __syncwarp();
+      for (int e = lane; e < 36; e += 32) w.a[e] = w.b[e];
+      __syncwarp();
     }
-  for (int i = 0; i < 6; ++i) b[i] = v[21 + i];
-  for (int i = 0; i < 6; ++i)
-    for (int j = 0; j < 6; ++j) work[i][j] = ata[i][j];
-  jacobi_eig<6>(work, ev, vec);
-  const double lmin = ev[0], lmax = ev[5];
-  const double cond = lmin > 0.0 ? lmax / lmin : INFINITY;
-  o->cond = cond;
-  if (!(cond < 1e12)) {
-    o->degenerate = 1;
+    if (!w.rotated) break;
+    __syncwarp();
+  }
+  // ascending, stable
+  double d[6];
+  int order[6];
+  for (int i = 0; i < 6; ++i) {
+    d[i] = w.a[7 * i];
+    order[i] = i;
+  }
+  for (int i = 1; i < 6; ++i) {
+    const int k = order[i];
+    int j = i - 1;
+    while (j >= 0 && d[order[j]] > d[k]) {
+      order[j + 1] = order[j];
+      --j;
+    }
+    order[j + 1] = k;
+  }
+  for (int i = 0; i < 6; ++i) ev[i] = d[order[i]];
+  __syncwarp();
+}
+
+// solve_mstep (mstep.cpp:76-98) from the reduced normal equations, by one
+// warp: parallel eigenvalues for the condition estimate, then LDLT + exp map
+// on lane 0.  Result in *o (valid after the call on all lanes).
+static __device__ void warp_solve_normal_eq(const double* v, int nvp, SolveOut* o, Eig6Smem& w) {
+  const int lane = threadIdx.x & 31;
+  if (nvp < 3) {
+    if (lane == 0) {
+      o->nvp = nvp;
+      o->degenerate = 1;
+      o->cond = INFINITY;
+    }
+    __syncwarp();
     return;
   }
-  double x[6];
-  ldlt_solve6(ata, b, x);
-  for (int i = 0; i < 3; ++i) {
-    o->omega[i] = x[i];
-    o->trans[i] = x[3 + i];
-    o->dt[i] = x[3 + i];
+  __shared__ double ata_s[36];
+  for (int e = lane; e < 36; e += 32) {
+    const int i = e / 6, j = e % 6;
+    const int a = i < j ? i : j, b = i < j ? j : i;
+    ata_s[e] = v[a * 6 - a * (a - 1) / 2 + (b - a)];
   }
-  small_angle_rotation(o->omega, o->dR);
+  __syncwarp();
+  double ev[6];
+  warp_eig6(ata_s, ev, w);
+  if (lane == 0) {
+    o->nvp = nvp;
+    o->degenerate = 0;
+    const double lmin = ev[0], lmax = ev[5];
+    const double cond = lmin > 0.0 ? lmax / lmin : INFINITY;
+    o->cond = cond;
+    if (!(cond < 1e12)) {
+      o->degenerate = 1;
+    } else {
+      double ata[6][6], b[6], x[6];
+      int k = 0;
+      for (int i = 0; i < 6; ++i)
+        for (int j = i; j < 6; ++j) {
+          ata[i][j] = v[k];
+          ata[j][i] = v[k];
+          ++k;
+        }
+      for (int i = 0; i < 6; ++i) b[i] = v[21 + i];
+      ldlt_solve6(ata, b, x);
+      for (int i = 0; i < 3; ++i) {
+        o->omega[i] = x[i];
+        o->trans[i] = x[3 + i];
+        o->dt[i] = x[3 + i];
+      }
+      small_angle_rotation(o->omega, o->dR);
+    }
+  }
+  __syncwarp();
 }
 
 // Whole solve on one block from device moments (stride nm, m0 at 0, m1 at 1..3).
@@ -220,10 +354,16 @@ static __device__ void block_solve(const DNode* __restrict__ nodes, int J, const
   }
   block_reduce_acc(a, sm);
   __shared__ SolveOut so;
+  __shared__ Eig6Smem e6;
+  __shared__ double vsh[kNormalEq];
+  __shared__ int nvp_sh;
   if (threadIdx.x == 0) {
     so.crit_before = a.crit;
-    solve_normal_eq(a.v, a.nvp, &so);
+    for (int k = 0; k < kNormalEq; ++k) vsh[k] = a.v[k];
+    nvp_sh = a.nvp;
   }
+  __syncthreads();
+  if (threadIdx.x < 32) warp_solve_normal_eq(vsh, nvp_sh, &so, e6);
   __syncthreads();
   double c = 0.0;
   if (!so.degenerate) {

@@ -55,3 +55,24 @@ def test_jacobi6_matches_numpy(ctx):
     for i, m in enumerate(mats):
         ref = np.linalg.eigvalsh(m)
         assert np.allclose(ev[i], ref, rtol=1e-12, atol=1e-12 * ref.max()), (ev[i], ref)
+
+
+def test_warp_solve_matches_numpy(ctx):
+    """The warp-parallel 6x6 eigen + LDLT solve of K8 on random SPD systems
+    (guards the nvcc inlining miscompile noted in trg_math.cuh)."""
+    from paper_1807_02587_b200 import _lib
+    rng = np.random.default_rng(2)
+    for m in _spd(rng, 30, 6):
+        b = rng.standard_normal(6)
+        v = np.concatenate([m[np.triu_indices(6)], b])
+        out = np.zeros(16)
+        assert _lib.lib().trg_debug_solve(ctx.h, v.ctypes.data_as(_lib.dp), 10,
+                                          out.ctypes.data_as(_lib.dp)) == 0
+        ev = np.linalg.eigvalsh(m)
+        cond = ev[-1] / ev[0]
+        if cond >= 1e12:
+            assert out[7] == 1
+            continue
+        x = np.linalg.solve(m, b)
+        assert np.allclose(out[:6], x, rtol=1e-8, atol=1e-8 * np.abs(x).max())
+        assert abs(out[6] - cond) <= 1e-8 * cond
