@@ -110,6 +110,12 @@ typedef struct {
   int calibration_passes;
   double calibration_drift;
   uint64_t calib_density_evaluations;
+  /* node_ll_traces (gmm.hpp:45): the kept fit's EM log-likelihoods per
+   * expansion in build order, em_iterations_per_node + 1 values each.
+   * Caller-allocated [ll_trace_capacity][em_iterations_per_node + 1], or NULL. */
+  double* ll_traces;
+  int ll_trace_capacity;
+  int n_expansions;
 } trg_build_diag;
 
 /* treereg::MStepSolution, mstep.hpp:54-61 */
@@ -180,6 +186,19 @@ int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, siz
  * the reference throws DegenerateGeometryError. */
 int trg_solve_mstep(trg_ctx* ctx, const trg_tree_dev* tree, const double* m0, const double* m1,
                     uint64_t total_points, trg_mstep_solution* out);
+
+/* treereg::make_virtual_points (mstep.hpp:46-47) on the device: the ordered
+ * list of components with m0 > 1e-8 N: index[], pi* = m0/N, mu* = m1/m0
+ * (arrays sized n_components; *n_out receives the count). */
+int trg_make_virtual_points(trg_ctx* ctx, int n_components, const double* m0, const double* m1,
+                            uint64_t total_points, int* index, double* pi_star, double* mu_star,
+                            int* n_out);
+/* treereg::solve_mstep(const VirtualPointSet&) (mstep.hpp:67) on explicit
+ * virtual points and their components (mean [n*3], lambdas [n*3] descending,
+ * axes [n*9] row-major, column l = axis of lambdas[l]). */
+int trg_solve_mstep_vps(trg_ctx* ctx, int n_vps, const double* pi_star, const double* mu_star,
+                        const double* comp_mean, const double* comp_lambdas,
+                        const double* comp_axes, trg_mstep_solution* out);
 
 /* ---- driver ----------------------------------------------------------- */
 /* treereg::register_with_tree (registration.hpp:59-62). */

@@ -54,7 +54,8 @@ class MomentsC(C.Structure):
 class BuildDiagC(C.Structure):
     _fields_ = [("entries_per_round", C.c_uint64 * 8), ("expanded_per_round", C.c_int * 8),
                 ("calibration_passes", C.c_int), ("calibration_drift", C.c_double),
-                ("calib_density_evaluations", C.c_uint64)]
+                ("calib_density_evaluations", C.c_uint64), ("ll_traces", dp),
+                ("ll_trace_capacity", C.c_int), ("n_expansions", C.c_int)]
 
 
 class MStepSolutionC(C.Structure):
@@ -93,6 +94,10 @@ SIGNATURES = {
                                 C.POINTER(AssocConfigC), C.POINTER(MomentsC), ip, dp]),
     "trg_solve_mstep": (C.c_int, [C.c_void_p, C.c_void_p, dp, dp, C.c_uint64,
                                   C.POINTER(MStepSolutionC)]),
+    "trg_make_virtual_points": (C.c_int, [C.c_void_p, C.c_int, dp, dp, C.c_uint64, ip, dp, dp,
+                                          ip]),
+    "trg_solve_mstep_vps": (C.c_int, [C.c_void_p, C.c_int, dp, dp, dp, dp, dp,
+                                      C.POINTER(MStepSolutionC)]),
     "trg_register_with_tree": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int,
                                          C.POINTER(RegConfigC), C.c_double,
                                          C.POINTER(RegResultC)]),

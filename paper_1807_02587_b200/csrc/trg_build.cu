@@ -80,6 +80,8 @@ struct BuildState {
   // calibration
   int cal_pass;
   int root_count;
+  int exp_base;  // expansions done in earlier rounds
+  int n_exp;
   int lvl_start[9];
   double drift;
   unsigned long long cal_evals;
@@ -129,6 +131,8 @@ struct BuildParams {
   double* cal_moments;  // [J][10]
   double* cta_drift;    // [G]
   int* layout_scratch;  // [6 * 8 * Kmax]
+  double* ll_trace;     // [capacity][2][em_iters + 1] per expansion, both candidates
+  int* kept_exp;        // [capacity] kept candidate per expansion
   unsigned* bar;
   BuildState* st;
   int* status;
@@ -664,6 +668,13 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
     for (int i = 0; i < 3; ++i) seed[i] = nf.seeds[24 * k + 3 * lane + i];
     cand_init(p, k, 1, seed, lane);
   }
+  // ll traces (BuildDiagnostics::node_ll_traces, gmm.cpp:240, 361)
+  if (lane < 2 && ph.mode[lane] != 0) {
+    const int c = lane, I = p.em_iters;
+    const int slot = ph.mode[c] == 1 ? ph.em_it[c] - 1 : I;
+    const double ll = ph.mode[c] == 1 ? __ldcg(red + kOffEm + 81 * c + 80) : __ldcg(red + kOffFin + 9 * c);
+    p.ll_trace[((size_t)(p.st->exp_base + k) * 2 + c) * (I + 1) + slot] = ll;
+  }
   // M-steps: lanes 0-7 candidate 0, lanes 8-15 candidate 1
   if (lane < 16) {
     const int c = lane >> 3;
@@ -679,6 +690,7 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
     // candidate choice (gmm.cpp:394) and survivors (gmm.cpp:414-428)
     const int kept = (nf.final_ll[2 * k + 1] > nf.final_ll[2 * k + 0]) ? 1 : 0;
     nf.kept[k] = kept;
+    p.kept_exp[p.st->exp_base + k] = kept;
     const double* cm = nf.cmass + 16 * k + 8 * kept;
     const double thr = smax(4.0, nf.mass[k] * 1e-6);
     int ns = 0;
@@ -942,6 +954,8 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
   }
   __syncthreads();
   if (tid == 0) {
+    st->exp_base += K;
+    st->n_exp = st->exp_base;
     st->J = J0 + NC;
     if (round == 0) st->root_count = NC;
     if (round < 8) st->lvl_start[round] = J0;
@@ -1347,6 +1361,8 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
                o_md = carve(sizeof(double) * E), o_emit = carve(sizeof(double) * 8 * E),
                o_calm = carve(sizeof(double) * 10 * cap), o_bar = carve(64),
                o_lay = carve(sizeof(int) * 48 * K),
+               o_llt = carve(sizeof(double) * (size_t)cap * 2 * (cfg->em_iterations_per_node + 1)),
+               o_kex = carve(sizeof(int) * (size_t)cap),
                o_state = carve(sizeof(BuildState));
   const int G = persistent_grid(ctx, (const void*)k_build, kTile, 0);
   const size_t o_cd = carve(sizeof(double) * G);
@@ -1393,6 +1409,8 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   p.emit = (double*)(A + o_emit);
   p.cal_moments = (double*)(A + o_calm);
   p.layout_scratch = (int*)(A + o_lay);
+  p.ll_trace = (double*)(A + o_llt);
+  p.kept_exp = (int*)(A + o_kex);
   p.bar = (unsigned*)(A + o_bar);
   p.st = (BuildState*)(A + o_state);
   p.cta_drift = (double*)(A + o_cd);
@@ -1468,6 +1486,21 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
       diag->expanded_per_round[r] = r < L ? st.K_round[r] : 0;
     }
     diag->calibration_passes = st.cal_pass;
+    diag->n_expansions = st.n_exp;
+    if (diag->ll_traces && diag->ll_trace_capacity > 0) {
+      const int I1 = cfg->em_iterations_per_node + 1;
+      const int ne = std::min(st.n_exp, diag->ll_trace_capacity);
+      std::vector<double> tr((size_t)std::max(1, ne) * 2 * I1);
+      std::vector<int> kp(std::max(1, ne));
+      if (ne > 0) {
+        TRG_CU(trg_memcpy(ctx, tr.data(), p.ll_trace, sizeof(double) * tr.size(), cudaMemcpyDeviceToHost));
+        TRG_CU(trg_memcpy(ctx, kp.data(), p.kept_exp, sizeof(int) * ne, cudaMemcpyDeviceToHost));
+        TRG_CU(cudaStreamSynchronize(ctx->stream));
+      }
+      for (int e = 0; e < ne; ++e)
+        for (int i = 0; i < I1; ++i)
+          diag->ll_traces[(size_t)e * I1 + i] = tr[((size_t)e * 2 + kp[e]) * I1 + i];
+    }
     diag->calibration_drift = st.drift;
     diag->calib_density_evaluations = st.cal_evals;
   }

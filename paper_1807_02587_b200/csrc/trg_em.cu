@@ -207,6 +207,89 @@ __global__ void k_solve(const DNode* __restrict__ nodes, int J, const double* __
   block_solve(nodes, J, mom, 4, n_total, out, ss, status);
 }
 
+// solve_mstep on explicit virtual points (mstep.hpp:21-32): n VPs with their
+// components' (mean, lambdas, axes) as packed DNodes.
+__global__ void k_solve_vps(const DNode* __restrict__ comps, const double* __restrict__ pimu,
+                            int n, SolveOut* out, int* status) {
+  __shared__ SolveSmem ss;
+  __shared__ SolveOut so;
+  __shared__ Eig6Smem e6;
+  __shared__ double vsh[kNormalEq];
+  __shared__ int nvp_sh;
+  SolveAcc a;
+  acc_zero(a);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double mu[3] = {pimu[4 * j + 1], pimu[4 * j + 2], pimu[4 * j + 3]};
+    vp_rows(comps + j, pimu[4 * j], mu, a, status);
+  }
+  block_reduce_acc(a, ss);
+  if (threadIdx.x == 0) {
+    so.crit_before = a.crit;
+    for (int k = 0; k < kNormalEq; ++k) vsh[k] = a.v[k];
+    nvp_sh = a.nvp;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) warp_solve_normal_eq(vsh, nvp_sh, &so, e6);
+  __syncthreads();
+  double c = 0.0;
+  if (!so.degenerate) {
+    double dRt[12];
+    for (int i = 0; i < 9; ++i) dRt[i] = so.dR[i];
+    for (int i = 0; i < 3; ++i) dRt[9 + i] = so.dt[i];
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      // criterion term with pi, mu given: reuse crit_term via m0 = pi, N = 1
+      const double pi = pimu[4 * j];
+      c += crit_term(comps + j, pi, pi * pimu[4 * j + 1], pi * pimu[4 * j + 2],
+                     pi * pimu[4 * j + 3], 1.0, dRt);
+    }
+  }
+  c = block_sum(c, ss);
+  if (threadIdx.x == 0) {
+    so.crit_after = so.degenerate ? so.crit_before : c;
+    *out = so;
+  }
+}
+
+// make_virtual_points (mstep.cpp:8-30): order-preserving filter m0 > 1e-8 N.
+__global__ void k_make_vps(const double* __restrict__ mom, int J, double n_total, int* idx,
+                           double* pimu, int* count) {
+  __shared__ int wsum[33];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (J + nt - 1) / nt;
+  const int b = min(J, tid * per), e = min(J, b + per);
+  const double floor_mass = 1e-8 * n_total;
+  int my = 0;
+  for (int j = b; j < e; ++j) my += (mom[4 * j] <= floor_mass) ? 0 : 1;
+  int x = my;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0;
+    for (int w = 0; w < nt / 32; ++w) {
+      const int v = wsum[w];
+      wsum[w] = run;
+      run += v;
+    }
+    *count = run;
+  }
+  __syncthreads();
+  int pos = wsum[warp] + x - my;
+  for (int j = b; j < e; ++j) {
+    const double m0 = mom[4 * j];
+    if (m0 <= floor_mass) continue;
+    idx[pos] = j;
+    pimu[4 * pos] = m0 / n_total;
+    pimu[4 * pos + 1] = mom[4 * j + 1] / m0;
+    pimu[4 * pos + 2] = mom[4 * j + 2] / m0;
+    pimu[4 * pos + 3] = mom[4 * j + 3] / m0;
+    ++pos;
+  }
+}
+
 }  // namespace trg
 
 using namespace trg;
@@ -397,6 +480,107 @@ int trg_solve_mstep(trg_ctx* ctx, const trg_tree_dev* tree, const double* m0, co
   ctx->launches += 1;
   SolveOut o;
   TRG_CU(trg_memcpy(ctx, &o, so, sizeof o, cudaMemcpyDeviceToHost));
+  TRG_TRY(check_status(ctx, "solve_mstep"));
+  out->n_virtual_points = o.nvp;
+  out->condition_estimate = o.cond;
+  if (o.degenerate) {
+    set_error(o.nvp < 3 ? "solve_mstep: fewer than 3 contributing components"
+                        : "solve_mstep: normal equations condition estimate exceeds limit");
+    return TRG_EDEGENERATE;
+  }
+  for (int k = 0; k < 3; ++k) {
+    out->omega[k] = o.omega[k];
+    out->translation[k] = o.trans[k];
+    out->delta_t[k] = o.dt[k];
+  }
+  for (int k = 0; k < 9; ++k) out->delta_R[k] = o.dR[k];
+  out->criterion_before = o.crit_before;
+  out->criterion_after = o.crit_after;
+  return TRG_OK;
+}
+
+int trg_make_virtual_points(trg_ctx* ctx, int n_components, const double* m0, const double* m1,
+                            uint64_t total_points, int* index, double* pi_star, double* mu_star,
+                            int* n_out) {
+  if (total_points == 0) {
+    set_error("make_virtual_points: no points were associated");
+    return TRG_EINVAL;
+  }
+  if (n_components <= 0) {
+    *n_out = 0;
+    return TRG_OK;
+  }
+  TRG_CU(cudaSetDevice(ctx->device));
+  const int J = n_components;
+  std::vector<double> h((size_t)J * 4);
+  for (int j = 0; j < J; ++j) {
+    h[4 * j] = m0[j];
+    for (int k = 0; k < 3; ++k) h[4 * j + 1 + k] = m1[3 * j + k];
+  }
+  void* buf = nullptr;
+  const size_t bytes = sizeof(double) * 8 * (size_t)J + sizeof(int) * ((size_t)J + 1);
+  TRG_TRY(ws_get(ctx, kSlotSolve, bytes + 64, &buf));
+  double* dmom = static_cast<double*>(buf);
+  double* dpimu = dmom + 4 * J;
+  int* didx = reinterpret_cast<int*>(dpimu + 4 * J);
+  int* dcnt = didx + J;
+  TRG_CU(trg_memcpy(ctx, dmom, h.data(), sizeof(double) * 4 * J, cudaMemcpyHostToDevice));
+  k_make_vps<<<1, 256, 0, ctx->stream>>>(dmom, J, (double)total_points, didx, dpimu, dcnt);
+  ctx->launches += 1;
+  int cnt = 0;
+  TRG_CU(trg_memcpy(ctx, &cnt, dcnt, sizeof(int), cudaMemcpyDeviceToHost));
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  std::vector<double> pm((size_t)cnt * 4);
+  std::vector<int> ix(cnt);
+  if (cnt > 0) {
+    TRG_CU(trg_memcpy(ctx, pm.data(), dpimu, sizeof(double) * 4 * cnt, cudaMemcpyDeviceToHost));
+    TRG_CU(trg_memcpy(ctx, ix.data(), didx, sizeof(int) * cnt, cudaMemcpyDeviceToHost));
+  }
+  TRG_TRY(check_status(ctx, "make_virtual_points"));
+  for (int v = 0; v < cnt; ++v) {
+    index[v] = ix[v];
+    pi_star[v] = pm[4 * v];
+    for (int k = 0; k < 3; ++k) mu_star[3 * v + k] = pm[4 * v + 1 + k];
+  }
+  *n_out = cnt;
+  return TRG_OK;
+}
+
+int trg_solve_mstep_vps(trg_ctx* ctx, int n_vps, const double* pi_star, const double* mu_star,
+                        const double* comp_mean, const double* comp_lambdas,
+                        const double* comp_axes, trg_mstep_solution* out) {
+  if (n_vps < 0) {
+    set_error("solve_mstep: bad virtual point count");
+    return TRG_EINVAL;
+  }
+  TRG_CU(cudaSetDevice(ctx->device));
+  const int n = n_vps;
+  std::vector<DNode> comps(std::max(1, n));
+  std::vector<double> pimu((size_t)std::max(1, n) * 4);
+  for (int v = 0; v < n; ++v) {
+    DNode& d = comps[v];
+    for (int r = 0; r < 3; ++r) {
+      d.mean[r] = comp_mean[3 * v + r];
+      d.lam[r] = comp_lambdas[3 * v + r];
+      d.il[r] = 1.0 / d.lam[r];
+      for (int k = 0; k < 3; ++k) d.axT[3 * r + k] = comp_axes[9 * v + 3 * k + r];
+    }
+    pimu[4 * v] = pi_star[v];
+    for (int k = 0; k < 3; ++k) pimu[4 * v + 1 + k] = mu_star[3 * v + k];
+  }
+  void* buf = nullptr;
+  const size_t cb = sizeof(DNode) * comps.size(), pb = sizeof(double) * pimu.size();
+  TRG_TRY(ws_get(ctx, kSlotSolve, cb + pb + sizeof(SolveOut) + 256, &buf));
+  char* B = static_cast<char*>(buf);
+  DNode* dc = reinterpret_cast<DNode*>(B);
+  double* dp = reinterpret_cast<double*>(B + cb);
+  SolveOut* dso = reinterpret_cast<SolveOut*>(B + ((cb + pb + 15) & ~size_t(15)));
+  TRG_CU(trg_memcpy(ctx, dc, comps.data(), cb, cudaMemcpyHostToDevice));
+  TRG_CU(trg_memcpy(ctx, dp, pimu.data(), pb, cudaMemcpyHostToDevice));
+  k_solve_vps<<<1, 256, 0, ctx->stream>>>(dc, dp, n, dso, ctx->status);
+  ctx->launches += 1;
+  SolveOut o;
+  TRG_CU(trg_memcpy(ctx, &o, dso, sizeof o, cudaMemcpyDeviceToHost));
   TRG_TRY(check_status(ctx, "solve_mstep"));
   out->n_virtual_points = o.nvp;
   out->condition_estimate = o.cond;

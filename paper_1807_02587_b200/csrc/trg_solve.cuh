@@ -51,6 +51,9 @@ __device__ __forceinline__ void acc_zero(SolveAcc& a) {
 
 // Virtual point of node j (mstep.cpp:18-26) and its three weighted rows
 // (mstep.cpp:58-75) added to `a`; criterion terms at identity too.
+__device__ __forceinline__ void vp_rows(const DNode* __restrict__ g, double pi, const double mu[3],
+                                        SolveAcc& a, int* status);
+
 __device__ __forceinline__ void vp_accumulate(const DNode* __restrict__ g, double m0, double m10,
                                               double m11, double m12, double n_total,
                                               SolveAcc& a, int* status) {
@@ -58,6 +61,13 @@ __device__ __forceinline__ void vp_accumulate(const DNode* __restrict__ g, doubl
   if (m0 <= floor_mass) return;
   const double pi = m0 / n_total;
   const double mu[3] = {m10 / m0, m11 / m0, m12 / m0};
+  vp_rows(g, pi, mu, a, status);
+}
+
+// The three weighted rows of one virtual point (mstep.cpp:58-75) and its
+// criterion terms at identity.
+__device__ __forceinline__ void vp_rows(const DNode* __restrict__ g, double pi, const double mu[3],
+                                        SolveAcc& a, int* status) {
   a.nvp += 1;
   const double lf = 1e-6 * g->lam[0];
   const double e[3] = {g->mean[0] - mu[0], g->mean[1] - mu[1], g->mean[2] - mu[2]};

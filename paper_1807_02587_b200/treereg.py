@@ -315,6 +315,7 @@ class BuildDiagnostics:  # gmm.hpp:43-49 (+ device counters)
     entries_per_round: list = field(default_factory=list)
     expanded_per_round: list = field(default_factory=list)
     calib_density_evaluations: int = 0
+    node_ll_traces: list = field(default_factory=list)
 
 
 def build_tree(cloud, config: ModelConfig = ModelConfig(),
@@ -326,6 +327,12 @@ def build_tree(cloud, config: ModelConfig = ModelConfig(),
     cfg = config.c()
     h = C.c_void_p()
     d = BuildDiagC()
+    I1 = config.em_iterations_per_node + 1
+    cap = sum(8 ** l for l in range(config.max_level))  # expansions <= internal nodes + root
+    traces = np.zeros((cap, I1))
+    if diagnostics is not None:
+        d.ll_traces = _d(traces)
+        d.ll_trace_capacity = cap
     _chk(_lib.lib().trg_build_tree(ctx.h, ptr, n, on_dev, C.byref(cfg), C.byref(h), C.byref(d)))
     if diagnostics is not None:
         diagnostics.calibration_drift = d.calibration_drift
@@ -334,6 +341,7 @@ def build_tree(cloud, config: ModelConfig = ModelConfig(),
         diagnostics.entries_per_round = list(d.entries_per_round)[:L]
         diagnostics.expanded_per_round = list(d.expanded_per_round)[:L]
         diagnostics.calib_density_evaluations = int(d.calib_density_evaluations)
+        diagnostics.node_ll_traces = [traces[e].copy() for e in range(min(d.n_expansions, cap))]
     return GmmTree(h, ctx)
 
 
