@@ -235,8 +235,15 @@ __device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double
     if (i < p.n) {
       double y0, y1, y2;
       apply_rt(Rt_smem, p.pts[3 * i], p.pts[3 * i + 1], p.pts[3 * i + 2], y0, y1, y2);
-      const Descent d = descend(p.nodes, p.root_count, p.depth, p.lambda_c, p.outlier_floor, y0,
-                                y1, y2, p.status);
+      Descent d;
+      if (p.dbg_mode == 2) {
+        d.node = (int)(i % (size_t)J);
+        d.path = 0.5;
+        d.evals = 1;
+      } else {
+        d = descend(p.nodes, p.root_count, p.depth, p.lambda_c, p.outlier_floor, y0, y1, y2,
+                    p.status);
+      }
       my_ev += d.evals;
       if (d.node < 0) {
         ++my_out;
@@ -249,14 +256,19 @@ __device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double
         p.point_w[i] = d.node < 0 ? 0.0 : d.path;
       }
     }
-    tile_reduce<NM>(sm, key, v, J, kb, p.partials, p.stamps, p.epoch, G, cta);
+    if (p.dbg_mode != 1) tile_reduce<NM>(sm, key, v, J, kb, p.partials, p.stamps, p.epoch, G, cta);
+    else if (key < (unsigned)J) p.partials[key] += v[0] * 0.0;
   }
-  atomicAdd(&sm.outliers, my_out);
-  atomicAdd(&sm.evals, my_ev);
-  __syncthreads();
-  if (tid == 0) {
-    atomicAdd(&p.counters[0], sm.outliers);
-    atomicAdd(&p.counters[1], sm.evals);
+  // integer counters: warp shuffle sums, then one add per warp (no 64-bit
+  // shared-memory CAS loops)
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    my_out += __shfl_xor_sync(0xffffffffu, my_out, off);
+    my_ev += __shfl_xor_sync(0xffffffffu, my_ev, off);
+  }
+  if ((tid & 31) == 0 && (my_out | my_ev)) {
+    atomicAdd(&p.counters[0], my_out);
+    atomicAdd(&p.counters[1], my_ev);
   }
 }
 

@@ -130,6 +130,8 @@ struct BuildParams {
   AssocParams a;
   double* cal_moments;  // [J][10]
   double* cta_drift;    // [G]
+  unsigned* cal_arrive;  // [capacity + 1] last-arriver counters (+ virtual root)
+  unsigned long long* drift_bits;  // [2] per-pass max drift (bits of a double >= 0)
   int* layout_scratch;  // [6 * 8 * Kmax]
   double* ll_trace;     // [capacity][2][em_iters + 1] per expansion, both candidates
   int* kept_exp;        // [capacity] kept candidate per expansion
@@ -1072,7 +1074,7 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
 constexpr size_t kBuildSmemBytes =
     sizeof(BuildSmem) > sizeof(AssocSmem<10>) ? sizeof(BuildSmem) : sizeof(AssocSmem<10>);
 
-__global__ void __launch_bounds__(kTile, 2) k_build(BuildParams p) {
+__global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
   __shared__ __align__(16) unsigned char smem_raw[kBuildSmemBytes];
   BuildSmem& sm = *reinterpret_cast<BuildSmem*>(smem_raw);
   AssocSmem<10>& asm_ = *reinterpret_cast<AssocSmem<10>*>(smem_raw);
@@ -1153,9 +1155,20 @@ __global__ void __launch_bounds__(kTile, 2) k_build(BuildParams p) {
   grid_sync(p.bar, G);
   tl_mark(st, 902);
   // ------------------------------------------------ leaf calibration
+  // calibrate_pass (gmm.cpp:523-580) per pass: association at identity with
+  // m2 (stage 1); then leaf refits and the whole bottom-up tree update
+  // (branch masses, octet reweights, parent moment match, refresh_eig) run as
+  // a last-arriver climb: each leaf's warp refits it and arrives at its
+  // parent; the parent's last-arriving child processes the parent and climbs
+  // on.  Every node is updated from the same inputs, in the same order, as
+  // the reference's level loops.  2 grid barriers per pass.
   const int root_count = lvl[1] - lvl[0];
   for (int pass = 0; pass < 40; ++pass) {
-    if (!(__ldcg(&st->drift) > 1e-13)) break;  // gmm.cpp:652
+    if (pass > 0) {
+      const double dprev = __longlong_as_double((long long)__ldcg(&p.drift_bits[(pass - 1) & 1]));
+      if (!(dprev > 1e-13)) break;  // gmm.cpp:652
+    }
+    if (cta == 0 && tid == 0) p.drift_bits[pass & 1] = 0ull;
     AssocParams a = p.a;
     a.n_nodes = J;
     a.root_count = root_count;
@@ -1163,119 +1176,101 @@ __global__ void __launch_bounds__(kTile, 2) k_build(BuildParams p) {
     assoc_pass<10>(asm_, a, nullptr, G, cta);
     grid_sync(p.bar, G);
     tl_mark(st, 1000 + pass * 10 + 1);
-    // combine + leaf refit (calibrate_pass gmm.cpp:532-545)
     double drift = 0.0;
     for (int j = cta * (kTile / 32) + warp; j < J; j += G * (kTile / 32)) {
+      if (__ldcg(&p.nodes[j].child_count) != 0) continue;  // leaves only
       double m[10];
       combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
-      if (lane == 0) {
-        p.cal_moments[(size_t)j * 10] = m[0];  // branch mass seed (leaves)
-        DNode& nd = p.nodes[j];
-        if (nd.child_count == 0 && m[0] > 0.0) {
-          const double mu[3] = {m[1] / m[0], m[2] / m[0], m[3] / m[0]};
-          const double M[3][3] = {{m[4], m[5], m[6]}, {m[5], m[7], m[8]}, {m[6], m[8], m[9]}};
-          double S[3][3], S2[3][3];
-          for (int r = 0; r < 3; ++r)
-            for (int s = 0; s < 3; ++s) S[r][s] = M[r][s] / m[0] - mu[r] * mu[s];
-          for (int r = 0; r < 3; ++r)
-            for (int s = 0; s < 3; ++s) S2[r][s] = 0.5 * (S[r][s] + S[s][r]);
-          double dm = (nd.mean[0] - mu[0]) * (nd.mean[0] - mu[0]);
-          dm += (nd.mean[1] - mu[1]) * (nd.mean[1] - mu[1]);
-          dm += (nd.mean[2] - mu[2]) * (nd.mean[2] - mu[2]);
-          drift = smax(drift, sqrt(dm));
-          double before[3][3];
-          for (int r = 0; r < 3; ++r)
-            for (int s = 0; s < 3; ++s) before[r][s] = p.cov[9 * (size_t)j + 3 * r + s];
-          GComp g;
-          g.w = nd.weight;
-          for (int q = 0; q < 3; ++q) g.mean[q] = mu[q];
-          if (comp_set_cov(g, S2, cov_floor(S2, p.eps, p.abs_floor))) atomicCAS(p.status, 0, kEInval);
-          double dc[3][3];
-          for (int r = 0; r < 3; ++r)
-            for (int s = 0; s < 3; ++s) dc[r][s] = g.cov[3 * r + s] - before[r][s];
-          drift = smax(drift, norm33(dc));
-          write_dnode_from_comp(nd, p.cov + 9 * (size_t)j, g, nd.weight, nd.level, nd.parent);
+      if (lane != 0) continue;
+      double* branch = p.cal_moments;  // slot 0 of each node
+      branch[(size_t)j * 10] = m[0];
+      DNode& nd = p.nodes[j];
+      if (m[0] > 0.0) {  // leaf refit (gmm.cpp:532-545)
+        const double mu[3] = {m[1] / m[0], m[2] / m[0], m[3] / m[0]};
+        const double M[3][3] = {{m[4], m[5], m[6]}, {m[5], m[7], m[8]}, {m[6], m[8], m[9]}};
+        double S[3][3], S2[3][3];
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) S[r][c] = M[r][c] / m[0] - mu[r] * mu[c];
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) S2[r][c] = 0.5 * (S[r][c] + S[c][r]);
+        double dm = (nd.mean[0] - mu[0]) * (nd.mean[0] - mu[0]);
+        dm += (nd.mean[1] - mu[1]) * (nd.mean[1] - mu[1]);
+        dm += (nd.mean[2] - mu[2]) * (nd.mean[2] - mu[2]);
+        drift = smax(drift, sqrt(dm));
+        double before[3][3];
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) before[r][c] = p.cov[9 * (size_t)j + 3 * r + c];
+        GComp g;
+        g.w = nd.weight;
+        for (int q = 0; q < 3; ++q) g.mean[q] = mu[q];
+        if (comp_set_cov(g, S2, cov_floor(S2, p.eps, p.abs_floor))) atomicCAS(p.status, 0, kEInval);
+        double dc[3][3];
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) dc[r][c] = g.cov[3 * r + c] - before[r][c];
+        drift = smax(drift, norm33(dc));
+        write_dnode_from_comp(nd, p.cov + 9 * (size_t)j, g, nd.weight, nd.level, nd.parent);
+      }
+      // climb: arrive at the parent; the last child processes it
+      int node = j;
+      for (;;) {
+        const int par = __ldcg(&p.nodes[node].parent);
+        unsigned* ctr = par >= 0 ? &p.cal_arrive[par] : &p.cal_arrive[p.capacity];
+        const unsigned need = par >= 0 ? (unsigned)__ldcg(&p.nodes[par].child_count)
+                                       : (unsigned)root_count;
+        __threadfence();
+        if (atomicAdd(ctr, 1u) != need - 1) break;
+        *ctr = 0u;
+        __threadfence();
+        const int first = par >= 0 ? __ldcg(&p.nodes[par].first_child) : 0;
+        const int count = (int)need;
+        // branch mass (gmm.cpp:547-556) and sibling reweight (gmm.cpp:557-566)
+        double sb = 0.0;
+        for (int c = 0; c < count; ++c) sb += __ldcg(&branch[(size_t)(first + c) * 10]);
+        if (par >= 0) branch[(size_t)par * 10] = sb;
+        if (sb > 0.0)
+          for (int c = 0; c < count; ++c) {
+            const double w = __ldcg(&branch[(size_t)(first + c) * 10]) / sb;
+            drift = smax(drift, fabs(__ldcg(&p.nodes[first + c].weight) - w));
+            p.nodes[first + c].weight = w;
+          }
+        if (par < 0) break;  // top octet done
+        // parent moment match (gmm.cpp:489-513) + refresh_eig (gmm.cpp:576-578)
+        DNode& pn = p.nodes[par];
+        double w = 0.0, mu[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c < count; ++c) {
+          const DNode& ch = p.nodes[first + c];
+          const double cw = __ldcg(&ch.weight);
+          w += cw;
+          for (int k = 0; k < 3; ++k) mu[k] = mu[k] + cw * __ldcg(&ch.mean[k]);
         }
+        if (w > 0.0) {
+          for (int k = 0; k < 3; ++k) mu[k] = mu[k] / w;
+          double cv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+          for (int c = 0; c < count; ++c) {
+            const int ci = first + c;
+            const DNode& ch = p.nodes[ci];
+            const double cw = __ldcg(&ch.weight);
+            const double d[3] = {__ldcg(&ch.mean[0]) - mu[0], __ldcg(&ch.mean[1]) - mu[1],
+                                 __ldcg(&ch.mean[2]) - mu[2]};
+            for (int r = 0; r < 3; ++r)
+              for (int q = 0; q < 3; ++q)
+                cv[3 * r + q] = cv[3 * r + q] + cw * (__ldcg(&p.cov[9 * (size_t)ci + 3 * r + q]) + d[r] * d[q]);
+          }
+          for (int k = 0; k < 9; ++k) p.cov[9 * (size_t)par + k] = cv[k] / w;
+          for (int k = 0; k < 3; ++k) pn.mean[k] = mu[k];
+        }
+        if (refresh_node(pn, p.cov + 9 * (size_t)par)) atomicCAS(p.status, 0, kEInval);
+        node = par;
       }
     }
-    {  // CTA max of drift (order-free)
-      __shared__ double dmax[kTile / 32];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) drift = smax(drift, __shfl_xor_sync(0xffffffffu, drift, off));
-      if (lane == 0) dmax[warp] = drift;
-      __syncthreads();
-      if (tid == 0) {
-        double d = dmax[0];
-        for (int w = 1; w < kTile / 32; ++w) d = smax(d, dmax[w]);
-        p.cta_drift[cta] = d;
-      }
-    }
+    if (lane == 0 && drift > 0.0)
+      atomicMax(&p.drift_bits[pass & 1], (unsigned long long)__double_as_longlong(drift));
     grid_sync(p.bar, G);
     tl_mark(st, 1000 + pass * 10 + 2);
-    if (cta == 0) {
-      // branch masses bottom-up (gmm.cpp:547-556), level-parallel
-      double* branch = p.cal_moments;  // slot 0 of each node
-      for (int l = p.L - 2; l >= 0; --l) {
-        for (int j = lvl[l] + tid; j < lvl[l + 1]; j += blockDim.x) {
-          const DNode& nd = p.nodes[j];
-          if (nd.child_count == 0) continue;
-          double sb = 0.0;
-          for (int c = 0; c < nd.child_count; ++c) sb += branch[(size_t)(nd.first_child + c) * 10];
-          branch[(size_t)j * 10] = sb;
-        }
-        __syncthreads();
-      }
-      // sibling reweight per octet (gmm.cpp:557-574), octets in parallel
-      double drift2 = 0.0;
-      for (int j = tid - 1; j < J; j += blockDim.x) {
-        int first, count;
-        if (j < 0) {
-          first = 0;
-          count = root_count;
-        } else {
-          if (p.nodes[j].child_count == 0) continue;
-          first = p.nodes[j].first_child;
-          count = p.nodes[j].child_count;
-        }
-        double sb = 0.0;
-        for (int c = 0; c < count; ++c) sb += branch[(size_t)(first + c) * 10];
-        if (!(sb > 0.0)) continue;  // shadowed octet keeps the fitted shares
-        for (int c = 0; c < count; ++c) {
-          const double w = branch[(size_t)(first + c) * 10] / sb;
-          drift2 = smax(drift2, fabs(p.nodes[first + c].weight - w));
-          p.nodes[first + c].weight = w;
-        }
-      }
-      {
-        __shared__ double dmx[kTile / 32];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) drift2 = smax(drift2, __shfl_xor_sync(0xffffffffu, drift2, off));
-        if (lane == 0) dmx[warp] = drift2;
-        __syncthreads();
-        double dc = 0.0;
-        for (int c = tid; c < G; c += blockDim.x) dc = smax(dc, __ldcg(&p.cta_drift[c]));
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) dc = smax(dc, __shfl_xor_sync(0xffffffffu, dc, off));
-        __shared__ double dcw[kTile / 32];
-        if (lane == 0) dcw[warp] = dc;
-        __syncthreads();
-        if (tid == 0) {
-          double d = 0.0;
-          for (int w = 0; w < kTile / 32; ++w) d = smax(d, smax(dmx[w], dcw[w]));
-          st->drift = d;
-          st->cal_pass = pass + 1;
-        }
-        __syncthreads();
-      }
-      reset_parents(p, lvl);
-      // refresh_eig of internal nodes (gmm.cpp:576-578)
-      for (int j = tid; j < J; j += blockDim.x)
-        if (p.nodes[j].child_count != 0)
-          if (refresh_node(p.nodes[j], p.cov + 9 * (size_t)j)) atomicCAS(p.status, 0, kEInval);
-      __threadfence();
+    if (cta == 0 && tid == 0) {
+      st->drift = __longlong_as_double((long long)__ldcg(&p.drift_bits[pass & 1]));
+      st->cal_pass = pass + 1;
     }
-    grid_sync(p.bar, G);
-    tl_mark(st, 1000 + pass * 10 + 3);
   }
   if (cta == 0 && tid == 0) st->cal_evals = __ldcg(&p.a.counters[1]);
 }
@@ -1363,6 +1358,7 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
                o_lay = carve(sizeof(int) * 48 * K),
                o_llt = carve(sizeof(double) * (size_t)cap * 2 * (cfg->em_iterations_per_node + 1)),
                o_kex = carve(sizeof(int) * (size_t)cap),
+               o_car = carve(sizeof(unsigned) * ((size_t)cap + 1)), o_dbits = carve(16),
                o_state = carve(sizeof(BuildState));
   const int G = persistent_grid(ctx, (const void*)k_build, kTile, 0);
   const size_t o_cd = carve(sizeof(double) * G);
@@ -1411,6 +1407,8 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   p.layout_scratch = (int*)(A + o_lay);
   p.ll_trace = (double*)(A + o_llt);
   p.kept_exp = (int*)(A + o_kex);
+  p.cal_arrive = (unsigned*)(A + o_car);
+  p.drift_bits = (unsigned long long*)(A + o_dbits);
   p.bar = (unsigned*)(A + o_bar);
   p.st = (BuildState*)(A + o_state);
   p.cta_drift = (double*)(A + o_cd);
@@ -1451,6 +1449,7 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   TRG_CU(cudaMemsetAsync(A + o_bar, 0, 64, ctx->stream));
   TRG_CU(cudaMemsetAsync(A + o_arr, 0, sizeof(unsigned) * K, ctx->stream));
   TRG_CU(cudaMemsetAsync(A + o_fd, 0, sizeof(unsigned) * K, ctx->stream));
+  TRG_CU(cudaMemsetAsync(A + o_car, 0, sizeof(unsigned) * ((size_t)cap + 1), ctx->stream));
   TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
   TRG_CU(trg_memcpy(ctx, p.st, &st, sizeof st, cudaMemcpyHostToDevice));
   const int h_rn[5] = {-1, 0, (int)n, 0, st.Tp[0]};

@@ -2,6 +2,7 @@
 // upload/download and the E-step.  Host code here only validates, stages
 // and launches; all arithmetic on the hot path runs in the kernels.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -300,6 +301,10 @@ int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, siz
   p.n = n;
   p.epoch = ++ctx->epoch;
   p.status = ctx->status;
+  {
+    const char* dm = getenv("TRG_ASSOC_DBG");
+    p.dbg_mode = dm ? atoi(dm) : 0;
+  }
   TRG_TRY(stage_points_public(ctx, xyz, n, xyz_on_device, kSlotPoints, &p.pts));
   void *part, *stamps, *mom, *cnt, *rt;
   TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * nm * (size_t)J * G, &part));

@@ -34,7 +34,7 @@ struct EmParams {
 
 constexpr int kAccStride = kNormalEq + 2;
 
-__global__ void __launch_bounds__(kAssocBlock, 2) k_register(EmParams p) {
+__global__ void __launch_bounds__(kAssocBlock, 4) k_register(EmParams p) {
   __shared__ AssocSmem<4> sm;
   __shared__ SolveSmem ss;
   __shared__ double rt[12];

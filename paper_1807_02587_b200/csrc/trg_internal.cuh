@@ -147,6 +147,7 @@ struct AssocParams {
   int* point_node;               // nullable
   double* point_w;               // nullable
   int* status;
+  int dbg_mode;                  // 0 normal; experiments: 1 skip reduction, 2 skip descent
 };
 int launch_associate(trg_ctx* ctx, const AssocParams& p, int nm, double* moments /*[J][nm]*/,
                      int grid);
