@@ -454,8 +454,10 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) s += __shfl_sync(0xffffffffu, ek, gbase + k);
+    // gamma_k = exp(log_k - log_total) = e_k / s (gmm.cpp:189, 354): one
+    // reciprocal per entry instead of a second exp per component (ulp-level)
     const double lt = fin ? m + log(s) : 0.0;
-    const double gam = fin ? exp(lg - lt) : 0.0;
+    const double gam = fin ? __dmul_rn(ek, __drcp_rn(s)) : 0.0;
     double denom = 0.0;
     if (mode == 3)
       for (int s2 = 0; s2 < sm.ns; ++s2) denom += __shfl_sync(0xffffffffu, gam, gbase + sm.surv[s2]);
