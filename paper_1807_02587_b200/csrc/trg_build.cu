@@ -141,15 +141,15 @@ struct BuildParams {
 };
 
 // ----------------------------------------------------------------- helpers
-__device__ __forceinline__ void tl_mark(BuildState* st, int label) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const int i = st->tl_n;
-    if (i < 1024) {
-      st->tl_lab[i] = label;
-      st->tl_t[i] = gtimer();
-      st->tl_n = i + 1;
-    }
+__device__ __forceinline__ void tl_mark_any(BuildState* st, int label) {
+  const int i = atomicAdd(&st->tl_n, 1);
+  if (i < 1024) {
+    st->tl_lab[i] = label;
+    st->tl_t[i] = gtimer();
   }
+}
+__device__ __forceinline__ void tl_mark(BuildState* st, int label) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) tl_mark_any(st, label);
 }
 __device__ __forceinline__ void comp_to_regs(const GComp& c, double r[18]) {
   r[0] = c.w;
@@ -1122,6 +1122,7 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
       __syncthreads();
       const int NI = sm.nitems;
       const int K = __ldcg(&st->Kp[par]);
+      if (round == 2 && ph_i == 2) tl_mark(st, 4999);
       for (int it = cta * (kTile / 32) + warp; it < K * NI; it += G * (kTile / 32)) {
         const int k = it / NI, f = it % NI;
         reduce_item(p, par, k, sm.item_off[f], sm.item_kind[f]);
@@ -1135,7 +1136,10 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
           }
         }
         last = __shfl_sync(0xffffffffu, last, 0);
+        const bool dbg = (round == 2 && ph_i == 2 && lane == 0);
+        if (dbg && last) tl_mark_any(st, 5000 + k);
         if (last) node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
+        if (dbg && last) tl_mark_any(st, 6000 + k);
       }
       grid_sync(p.bar, G);
       tl_mark(st, round * 100 + 50 + ph_i);
