@@ -34,68 +34,82 @@ struct EmParams {
 
 constexpr int kAccStride = kNormalEq + 2;
 
+// One EM iteration = E-step (all CTAs) | grid barrier | per-node combine +
+// virtual-point rows (the first ceil(J/8) CTAs, one warp per node) | grid
+// barrier | EVERY CTA folds those per-CTA normal equations in the same fixed
+// order and solves redundantly (identical bits everywhere), so the running
+// transform and the stop decision need no third barrier.  CTA 0 alone adds
+// the criterion-after trace and publishes the state for the host.
 __global__ void __launch_bounds__(kAssocBlock, 4) k_register(EmParams p) {
   __shared__ AssocSmem<4> sm;
   __shared__ SolveSmem ss;
+  __shared__ Eig6Smem e6;
+  __shared__ SolveOut so;
   __shared__ double rt[12];
-  __shared__ int done;
   __shared__ double red[kAccStride];
+  __shared__ int s_done, s_fails, s_conv, s_iters;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int J = p.a.n_nodes;
+  const int P2 = (J + (kAssocBlock / 32) - 1) / (kAssocBlock / 32);  // producer CTAs
   const double n_total = (double)p.a.n;
+  if (tid < 12) rt[tid] = ldcg(&p.st->Rt[tid]);
+  if (tid == 0) {
+    s_done = 0;
+    s_fails = 0;
+    s_conv = 0;
+    s_iters = 0;
+  }
+  __syncthreads();
+  const double trans_limit = ldcg(&p.st->trans_limit);
   for (int it = 0; it < p.max_iters; ++it) {
-    if (tid < 12) rt[tid] = ldcg(&p.st->Rt[tid]);
-    if (tid == 0) done = __ldcg(&p.st->done);
-    __syncthreads();
-    if (done) break;
     // ---- P1: E-step over this CTA's point tiles
     AssocParams a = p.a;
     a.epoch = p.epoch0 + (uint32_t)it;
     assoc_pass<4>(sm, a, rt, G, cta);
     grid_sync(p.bar, G);
     // ---- P2: per-node combine over CTAs + virtual-point rows
-    SolveAcc acc;
-    acc_zero(acc);
-    for (int j = cta * (kAssocBlock / 32) + warp; j < J; j += G * (kAssocBlock / 32)) {
-      double m[4];
-      combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
-      if (lane == 0) {
+    if (cta < P2) {
+      SolveAcc acc;
+      acc_zero(acc);
+      const int j = cta * (kAssocBlock / 32) + warp;
+      if (j < J) {
+        double m[4];
+        combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
+        if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) p.moments[(size_t)j * 4 + k] = m[k];
-        vp_accumulate(a.nodes + j, m[0], m[1], m[2], m[3], n_total, acc, a.status);
+          for (int k = 0; k < 4; ++k) p.moments[(size_t)j * 4 + k] = m[k];
+          vp_accumulate(a.nodes + j, m[0], m[1], m[2], m[3], n_total, acc, a.status);
+        }
       }
-    }
-    block_reduce_acc(acc, ss);
-    if (tid == 0) {
-      double* o = p.cta_acc + (size_t)cta * kAccStride;
+      block_reduce_acc(acc, ss);
+      if (tid == 0) {
+        double* o = p.cta_acc + (size_t)cta * kAccStride;
 #pragma unroll
-      for (int k = 0; k < kNormalEq; ++k) o[k] = acc.v[k];
-      o[kNormalEq] = acc.crit;
-      o[kNormalEq + 1] = (double)acc.nvp;
+        for (int k = 0; k < kNormalEq; ++k) o[k] = acc.v[k];
+        o[kNormalEq] = acc.crit;
+        o[kNormalEq + 1] = (double)acc.nvp;
+      }
     }
     grid_sync(p.bar, G);
-    // ---- P3: CTA 0 solves and updates the transform
-    if (cta == 0) {
-      // fold the per-CTA normal equations: 8 lanes per value, strided over
-      // CTAs, then a fixed shuffle tree (deterministic)
-      {
-        const int v = tid >> 3, sub = tid & 7;
-        double s = 0.0;
-        if (v < kAccStride)
-          for (int c = sub; c < G; c += 8) s += ldcg(p.cta_acc + (size_t)c * kAccStride + v);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        s += __shfl_xor_sync(0xffffffffu, s, 4);
-        if (v < kAccStride && sub == 0) red[v] = s;
-      }
-      __syncthreads();
-      __shared__ SolveOut so;
-      __shared__ Eig6Smem e6;
-      if (tid == 0) so.crit_before = red[kNormalEq];
-      __syncthreads();
-      if (tid < 32) warp_solve_normal_eq(red, (int)red[kNormalEq + 1], &so, e6);
-      __syncthreads();
+    // ---- P3 (every CTA): fold the P2 partials (8 lanes per value, strided,
+    // fixed shuffle tree), solve, update T
+    {
+      const int v = tid >> 3, sub = tid & 7;
+      double s = 0.0;
+      if (v < kAccStride)
+        for (int c = sub; c < P2; c += 8) s += ldcg(p.cta_acc + (size_t)c * kAccStride + v);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      if (v < kAccStride && sub == 0) red[v] = s;
+    }
+    __syncthreads();
+    if (tid == 0) so.crit_before = red[kNormalEq];
+    __syncthreads();
+    if (tid < 32) warp_solve_normal_eq(red, (int)red[kNormalEq + 1], &so, e6);
+    __syncthreads();
+    if (cta == 0) {  // criterion after the update (trace only)
       double c = 0.0;
       if (!so.degenerate) {
         double dRt[12];
@@ -109,50 +123,56 @@ __global__ void __launch_bounds__(kAssocBlock, 4) k_register(EmParams p) {
       }
       c = block_sum(c, ss);
       if (tid == 0) {
-        EmState* st = p.st;
-        const unsigned long long ev = atomicExch(&a.counters[1], 0ull);
-        p.evals[it] = ev;
-        st->iterations = it + 1;
+        p.evals[it] = atomicExch(&a.counters[1], 0ull);
         p.crit_before[it] = so.crit_before;
-        if (!so.degenerate) {
-          p.crit_after[it] = c;
-          // T = delta * T (geometry.hpp:42-47)
-          double nR[9], nt[3];
-          for (int i = 0; i < 3; ++i)
-            for (int jj = 0; jj < 3; ++jj) {
-              double s = so.dR[3 * i] * rt[jj];
-              s += so.dR[3 * i + 1] * rt[3 + jj];
-              s += so.dR[3 * i + 2] * rt[6 + jj];
-              nR[3 * i + jj] = s;
-            }
-          for (int i = 0; i < 3; ++i) {
-            double s = so.dR[3 * i] * rt[9];
-            s += so.dR[3 * i + 1] * rt[10];
-            s += so.dR[3 * i + 2] * rt[11];
-            nt[i] = s + so.dt[i];
-          }
-          for (int k = 0; k < 9; ++k) st->Rt[k] = nR[k];
-          for (int k = 0; k < 3; ++k) st->Rt[9 + k] = nt[k];
-          st->fails = 0;
-          // rotation_angle (geometry.cpp:17-20) and |t| (registration.cpp:68-69)
-          double cth = ((so.dR[0] + so.dR[4]) + so.dR[8] - 1.0) * 0.5;
-          cth = cth < -1.0 ? -1.0 : (cth > 1.0 ? 1.0 : cth);
-          double tn = so.trans[0] * so.trans[0];
-          tn += so.trans[1] * so.trans[1];
-          tn += so.trans[2] * so.trans[2];
-          if (acos(cth) < p.rot_tol && sqrt(tn) < st->trans_limit) {
-            st->converged = 1;
-            st->done = 1;
-          }
-        } else {
-          p.crit_after[it] = so.crit_before;
-          if (++st->fails >= 3) st->done = 1;
-        }
-        __threadfence();
+        p.crit_after[it] = so.degenerate ? so.crit_before : c;
       }
-      __syncthreads();
     }
-    grid_sync(p.bar, G);
+    if (tid == 0) {
+      s_iters = it + 1;
+      if (!so.degenerate) {
+        // T = delta * T (geometry.hpp:42-47)
+        double nR[9], nt[3];
+        for (int i = 0; i < 3; ++i)
+          for (int jj = 0; jj < 3; ++jj) {
+            double q = so.dR[3 * i] * rt[jj];
+            q += so.dR[3 * i + 1] * rt[3 + jj];
+            q += so.dR[3 * i + 2] * rt[6 + jj];
+            nR[3 * i + jj] = q;
+          }
+        for (int i = 0; i < 3; ++i) {
+          double q = so.dR[3 * i] * rt[9];
+          q += so.dR[3 * i + 1] * rt[10];
+          q += so.dR[3 * i + 2] * rt[11];
+          nt[i] = q + so.dt[i];
+        }
+        for (int k = 0; k < 9; ++k) rt[k] = nR[k];
+        for (int k = 0; k < 3; ++k) rt[9 + k] = nt[k];
+        s_fails = 0;
+        // rotation_angle (geometry.cpp:17-20) and |t| (registration.cpp:68-69)
+        double cth = ((so.dR[0] + so.dR[4]) + so.dR[8] - 1.0) * 0.5;
+        cth = cth < -1.0 ? -1.0 : (cth > 1.0 ? 1.0 : cth);
+        double tn = so.trans[0] * so.trans[0];
+        tn += so.trans[1] * so.trans[1];
+        tn += so.trans[2] * so.trans[2];
+        if (acos(cth) < p.rot_tol && sqrt(tn) < trans_limit) {
+          s_conv = 1;
+          s_done = 1;
+        }
+      } else if (++s_fails >= 3) {
+        s_done = 1;
+      }
+    }
+    __syncthreads();
+    if (s_done) break;
+  }
+  if (cta == 0 && tid == 0) {
+    EmState* st = p.st;
+    for (int k = 0; k < 12; ++k) st->Rt[k] = rt[k];
+    st->iterations = s_iters;
+    st->converged = s_conv;
+    st->fails = s_fails;
+    st->done = 1;
   }
 }
 
