@@ -87,17 +87,7 @@ struct BuildState {
   unsigned long long cal_evals;
   unsigned long long E_round[8];
   int K_round[8];
-  // device timeline (CTA 0 after each grid barrier): label, globaltimer ns
-  int tl_n;
-  int tl_lab[1024];
-  unsigned long long tl_t[1024];
 };
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 struct BuildParams {
   const double* pts;
@@ -137,20 +127,12 @@ struct BuildParams {
   int* kept_exp;        // [capacity] kept candidate per expansion
   unsigned* bar;
   BuildState* st;
+  Timeline* tl;
   int* status;
 };
 
 // ----------------------------------------------------------------- helpers
-__device__ __forceinline__ void tl_mark_any(BuildState* st, int label) {
-  const int i = atomicAdd(&st->tl_n, 1);
-  if (i < 1024) {
-    st->tl_lab[i] = label;
-    st->tl_t[i] = gtimer();
-  }
-}
-__device__ __forceinline__ void tl_mark(BuildState* st, int label) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) tl_mark_any(st, label);
-}
+
 __device__ __forceinline__ void comp_to_regs(const GComp& c, double r[18]) {
   r[0] = c.w;
   r[1] = c.lw;
@@ -1083,7 +1065,7 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   BuildState* st = p.st;
-  tl_mark(st, -1);
+  tl_mark(p.tl, -1);
   // ------------------------------------------------ expansion rounds
   for (int round = 0; round < p.L; ++round) {
     const int par = round & 1;
@@ -1097,7 +1079,7 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
       if (ph.layout) {
         if (cta == 0) round_layout(p, par, round, p.layout_scratch);
         grid_sync(p.bar, G);
-        tl_mark(st, round * 100 + ph_i);
+        tl_mark(p.tl, round * 100 + ph_i);
         continue;
       }
       // (a) tile pass
@@ -1115,14 +1097,14 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
         __syncthreads();
       }
       grid_sync(p.bar, G);
-      tl_mark(st, round * 100 + ph_i);
+      tl_mark(p.tl, round * 100 + ph_i);
       if (ph.pwrite) continue;
       // (b) per-node reduction of the tile records + node update
       if (tid == 0) sm.nitems = phase_items(ph, sm.item_off, sm.item_kind);
       __syncthreads();
       const int NI = sm.nitems;
       const int K = __ldcg(&st->Kp[par]);
-      if (round == 2 && ph_i == 2) tl_mark(st, 4999);
+      if (round == 2 && ph_i == 2) tl_mark(p.tl, 4999);
       for (int it = cta * (kTile / 32) + warp; it < K * NI; it += G * (kTile / 32)) {
         const int k = it / NI, f = it % NI;
         reduce_item(p, par, k, sm.item_off[f], sm.item_kind[f]);
@@ -1137,12 +1119,12 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
         }
         last = __shfl_sync(0xffffffffu, last, 0);
         const bool dbg = (round == 2 && ph_i == 2 && lane == 0);
-        if (dbg && last) tl_mark_any(st, 5000 + k);
+        if (dbg && last) tl_mark_any(p.tl, 5000 + k);
         if (last) node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
-        if (dbg && last) tl_mark_any(st, 6000 + k);
+        if (dbg && last) tl_mark_any(p.tl, 6000 + k);
       }
       grid_sync(p.bar, G);
-      tl_mark(st, round * 100 + 50 + ph_i);
+      tl_mark(p.tl, round * 100 + 50 + ph_i);
     }
     if (__ldcg(&st->done) || __ldcg(&st->status_overflow)) break;
   }
@@ -1152,14 +1134,14 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
   if (tid < 9) lvl[tid] = __ldcg(&st->lvl_start[tid]);
   __syncthreads();
   // ------------------------------------------------ rematch + refresh_eig
-  tl_mark(st, 900);
+  tl_mark(p.tl, 900);
   if (cta == 0) reset_parents(p, lvl);
   grid_sync(p.bar, G);
-  tl_mark(st, 901);
+  tl_mark(p.tl, 901);
   for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x)
     if (refresh_node(p.nodes[j], p.cov + 9 * (size_t)j)) atomicCAS(p.status, 0, kEInval);
   grid_sync(p.bar, G);
-  tl_mark(st, 902);
+  tl_mark(p.tl, 902);
   // ------------------------------------------------ leaf calibration
   // calibrate_pass (gmm.cpp:523-580) per pass: association at identity with
   // m2 (stage 1); then leaf refits and the whole bottom-up tree update
@@ -1181,7 +1163,7 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
     a.epoch = p.a.epoch + (uint32_t)pass;
     assoc_pass<10>(asm_, a, nullptr, G, cta);
     grid_sync(p.bar, G);
-    tl_mark(st, 1000 + pass * 10 + 1);
+    tl_mark(p.tl, 1000 + pass * 10 + 1);
     double drift = 0.0;
     for (int j = cta * (kTile / 32) + warp; j < J; j += G * (kTile / 32)) {
       if (__ldcg(&p.nodes[j].child_count) != 0) continue;  // leaves only
@@ -1272,7 +1254,7 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
     if (lane == 0 && drift > 0.0)
       atomicMax(&p.drift_bits[pass & 1], (unsigned long long)__double_as_longlong(drift));
     grid_sync(p.bar, G);
-    tl_mark(st, 1000 + pass * 10 + 2);
+    tl_mark(p.tl, 1000 + pass * 10 + 2);
     if (cta == 0 && tid == 0) {
       st->drift = __longlong_as_double((long long)__ldcg(&p.drift_bits[pass & 1]));
       st->cal_pass = pass + 1;
@@ -1419,6 +1401,8 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   p.st = (BuildState*)(A + o_state);
   p.cta_drift = (double*)(A + o_cd);
   p.status = ctx->status;
+  p.tl = ctx->dev_timeline;
+  TRG_TRY(timeline_reset(ctx));
   // tree
   trg_tree_dev* tree = nullptr;
   TRG_TRY(tree_alloc(ctx, cap, &tree));
@@ -1483,8 +1467,7 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   }
   tree->n_nodes = st.J;
   tree->root_count = st.root_count;
-  ctx->timeline.assign(st.tl_t, st.tl_t + std::min(st.tl_n, 1024));
-  ctx->timeline_lab.assign(st.tl_lab, st.tl_lab + std::min(st.tl_n, 1024));
+  TRG_TRY(timeline_fetch(ctx));
   if (diag) {
     for (int r = 0; r < 8; ++r) {
       diag->entries_per_round[r] = r < L ? st.E_round[r] : 0;

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #include "trg_internal.cuh"
@@ -62,6 +63,21 @@ int check_status(trg_ctx* ctx, const char* where) {
     set_error(std::string(where) + ": " + what);
     return st;
   }
+  return TRG_OK;
+}
+
+int timeline_reset(trg_ctx* ctx) {
+  TRG_CU(cudaMemsetAsync(ctx->dev_timeline, 0, sizeof(int), ctx->stream));
+  return TRG_OK;
+}
+
+int timeline_fetch(trg_ctx* ctx) {
+  Timeline h;
+  TRG_CU(cudaMemcpyAsync(&h, ctx->dev_timeline, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  const int n = std::min(h.n, 1024);
+  ctx->timeline.assign(h.t, h.t + n);
+  ctx->timeline_lab.assign(h.lab, h.lab + n);
   return TRG_OK;
 }
 
@@ -135,6 +151,8 @@ int trg_ctx_create(int device, trg_ctx** out) {
   TRG_CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   TRG_CU(cudaMalloc(&c->status, sizeof(int)));
   TRG_CU(cudaMemset(c->status, 0, sizeof(int)));
+  TRG_CU(cudaMalloc(&c->dev_timeline, sizeof(Timeline)));
+  TRG_CU(cudaMemset(c->dev_timeline, 0, sizeof(Timeline)));
   *out = c;
   return TRG_OK;
 }
@@ -148,6 +166,7 @@ int trg_ctx_destroy(trg_ctx* ctx) {
     if (ctx->host_slot_ptr[i]) cudaFreeHost(ctx->host_slot_ptr[i]);
   }
   cudaFree(ctx->status);
+  cudaFree(ctx->dev_timeline);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TRG_OK;

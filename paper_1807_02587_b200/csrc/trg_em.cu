@@ -30,6 +30,7 @@ struct EmParams {
   int max_iters;
   double rot_tol;
   uint32_t epoch0;
+  Timeline* tl;
 };
 
 constexpr int kAccStride = kNormalEq + 2;
@@ -40,7 +41,7 @@ constexpr int kAccStride = kNormalEq + 2;
 // order and solves redundantly (identical bits everywhere), so the running
 // transform and the stop decision need no third barrier.  CTA 0 alone adds
 // the criterion-after trace and publishes the state for the host.
-__global__ void __launch_bounds__(kAssocBlock, 4) k_register(EmParams p) {
+__global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
   __shared__ AssocSmem<4> sm;
   __shared__ SolveSmem ss;
   __shared__ Eig6Smem e6;
@@ -66,8 +67,10 @@ __global__ void __launch_bounds__(kAssocBlock, 4) k_register(EmParams p) {
     // ---- P1: E-step over this CTA's point tiles
     AssocParams a = p.a;
     a.epoch = p.epoch0 + (uint32_t)it;
+    tl_mark(p.tl, 2000 + it * 10);
     assoc_pass<4>(sm, a, rt, G, cta);
     grid_sync(p.bar, G);
+    tl_mark(p.tl, 2000 + it * 10 + 1);
     // ---- P2: per-node combine over CTAs + virtual-point rows
     if (cta < P2) {
       SolveAcc acc;
@@ -92,6 +95,7 @@ __global__ void __launch_bounds__(kAssocBlock, 4) k_register(EmParams p) {
       }
     }
     grid_sync(p.bar, G);
+    tl_mark(p.tl, 2000 + it * 10 + 2);
     // ---- P3 (every CTA): fold the P2 partials (8 lanes per value, strided,
     // fixed shuffle tree), solve, update T
     {
@@ -105,10 +109,12 @@ __global__ void __launch_bounds__(kAssocBlock, 4) k_register(EmParams p) {
       if (v < kAccStride && sub == 0) red[v] = s;
     }
     __syncthreads();
+    tl_mark(p.tl, 7000);
     if (tid == 0) so.crit_before = red[kNormalEq];
     __syncthreads();
-    if (tid < 32) warp_solve_normal_eq(red, (int)red[kNormalEq + 1], &so, e6);
+    if (tid < 32) warp_solve_normal_eq(red, (int)red[kNormalEq + 1], &so, e6, p.tl, false);
     __syncthreads();
+    tl_mark(p.tl, 2000 + it * 10 + 3);
     if (cta == 0) {  // criterion after the update (trace only)
       double c = 0.0;
       if (!so.degenerate) {
@@ -356,6 +362,8 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   p.evals = reinterpret_cast<unsigned long long*>(p.crit_after + K);
   p.max_iters = K;
   p.rot_tol = cfg->rotation_tol;
+  p.tl = ctx->dev_timeline;
+  TRG_TRY(timeline_reset(ctx));
   p.epoch0 = ctx->epoch + 1;
   ctx->epoch += (uint32_t)K + 1;
   EmState st{};
@@ -387,6 +395,7 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   TRG_TRY(check_status(ctx, "register_with_tree"));
+  TRG_TRY(timeline_fetch(ctx));
   for (int k = 0; k < 9; ++k) out->R[k] = st.Rt[k];
   for (int k = 0; k < 3; ++k) out->t[k] = st.Rt[9 + k];
   out->iterations = st.iterations;

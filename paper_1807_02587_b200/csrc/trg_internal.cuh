@@ -68,6 +68,31 @@ struct trg_tree_dev {
   int* owner_ctx_device = nullptr;
 };
 
+namespace trg {
+// Device timeline written by the persistent kernels (globaltimer ns per mark;
+// label conventions in include/treereg_b200.h, trg_debug_build_timeline).
+struct Timeline {
+  int n;
+  int lab[1024];
+  unsigned long long t[1024];
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_mark_any(Timeline* tl, int label) {
+  const int i = atomicAdd(&tl->n, 1);
+  if (i < 1024) {
+    tl->lab[i] = label;
+    tl->t[i] = gtimer();
+  }
+}
+__device__ __forceinline__ void tl_mark(Timeline* tl, int label) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) tl_mark_any(tl, label);
+}
+}  // namespace trg
+
 struct trg_ctx {
   int device = 0;
   uint64_t bytes_h2d = 0, bytes_d2h = 0;
@@ -82,7 +107,8 @@ struct trg_ctx {
   void* host_slot_ptr[kSlots] = {};
   size_t host_slot_size[kSlots] = {};
   int* status = nullptr;  // device status word
-  std::vector<unsigned long long> timeline;  // last build: globaltimer ns per barrier
+  trg::Timeline* dev_timeline = nullptr;      // device buffer (reset per call)
+  std::vector<unsigned long long> timeline;  // last call: globaltimer ns per mark
   std::vector<int> timeline_lab;
 };
 
@@ -127,6 +153,8 @@ inline cudaError_t trg_memcpy(trg_ctx* ctx, void* dst, const void* src, size_t b
 }
 int host_ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
 int check_status(trg_ctx* ctx, const char* where);
+int timeline_reset(trg_ctx* ctx);
+int timeline_fetch(trg_ctx* ctx);
 int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out);
 
 // Grid size for persistent kernels: SMs x resident CTAs.

@@ -58,13 +58,17 @@ extern "C" int trg_debug_eig(trg_ctx* ctx, int n, const double* in, int count, d
 namespace trg {
 __global__ void k_solve_selftest(const double* v, int nvp, SolveOut* out) {
   __shared__ SolveOut so;
+  const long long t0 = clock64();
   __shared__ Eig6Smem e6;
   __shared__ double vs[kNormalEq];
   if (threadIdx.x < kNormalEq) vs[threadIdx.x] = v[threadIdx.x];
   __syncthreads();
   if (threadIdx.x < 32) warp_solve_normal_eq(vs, nvp, &so, e6);
   __syncthreads();
-  if (threadIdx.x == 0) *out = so;
+  if (threadIdx.x == 0) {
+    so.crit_after = (double)(clock64() - t0);
+    *out = so;
+  }
 }
 }  // namespace trg
 extern "C" int trg_debug_solve(trg_ctx* ctx, const double* v27, int nvp, double* out16) {
@@ -83,6 +87,8 @@ extern "C" int trg_debug_solve(trg_ctx* ctx, const double* v27, int nvp, double*
   }
   out16[6] = so.cond;
   out16[7] = so.degenerate;
+  out16[8] = so.eig_sweeps;
+  out16[9] = so.crit_after;  // cycles
   cudaFree(dv);
   cudaFree(dso);
   return TRG_OK;

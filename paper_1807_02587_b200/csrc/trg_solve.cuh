@@ -178,6 +178,7 @@ struct SolveOut {
   double crit_before, crit_after, cond;
   int nvp;
   int degenerate;  // 1: fewer than 3 VPs or cond >= 1e12 (DegenerateGeometryError)
+  int eig_sweeps;  // diagnostics
 };
 
 // Eigenvalues of the 6x6 normal matrix (mstep.cpp:77-80, condition
@@ -185,98 +186,104 @@ struct SolveOut {
 // rotations per step (5 steps per sweep), all 36 entries updated at once.
 // Same per-rotation formulas and skip threshold as the cyclic solver; only
 // the rotation order differs (eigenvalues agree to a few ulp).
-static __constant__ int kRR6[5][3][2] = {{{0, 5}, {1, 4}, {2, 3}}, {{0, 4}, {5, 3}, {1, 2}},
-                                  {{0, 3}, {4, 2}, {5, 1}}, {{0, 2}, {3, 1}, {4, 5}},
-                                  {{0, 1}, {2, 5}, {3, 4}}};
+// Round-robin tournament for 6 indices: round r pairs kRR6[r][k] (p < q).
+static __constant__ int kRR6[5][3][2] = {{{0, 5}, {1, 4}, {2, 3}}, {{0, 4}, {3, 5}, {1, 2}},
+                                         {{0, 3}, {2, 4}, {1, 5}}, {{0, 2}, {1, 3}, {4, 5}},
+                                         {{0, 1}, {2, 5}, {3, 4}}};
+// Per round and index: partner, rotation slot, and whether it is the pair's p.
+static __constant__ signed char kPart6[5][6] = {{5, 4, 3, 2, 1, 0}, {4, 2, 1, 5, 0, 3},
+                                                {3, 5, 4, 0, 2, 1}, {2, 3, 0, 1, 5, 4},
+                                                {1, 0, 5, 4, 3, 2}};
+static __constant__ signed char kSlot6[5][6] = {{0, 1, 2, 2, 1, 0}, {0, 2, 2, 1, 0, 1},
+                                                {0, 2, 1, 0, 1, 2}, {0, 1, 0, 1, 2, 2},
+                                                {0, 0, 1, 2, 2, 1}};
 
 struct Eig6Smem {
   double a[36], b[36];
-  double c[6], s[6];  // per index: rotation of the pair it belongs to
-  double tt[3];
-  int part[6];        // partner index, role (p/q) encoded by sign
-  int tidx[6];        // which of the 3 rotations index i belongs to
+  double c[3], s[3], t[3];
   int rotated;
+  int sweeps;
+  signed char part[5][6], slot[5][6], pq[5][3][2];  // smem copies of the tables
 };
 
 // Called by all 32 lanes of ONE warp; returns eigenvalues ascending in ev.
+// Skips a rotation when |a_pq| is negligible next to both diagonal entries
+// (the cyclic solver's test) or below 1e-13 sqrt|a_pp a_qq| (its effect on
+// the eigenvalues is then far below rounding).
 static __device__ void warp_eig6(const double* in, double ev[6], Eig6Smem& w) {
   const int lane = threadIdx.x & 31;
   for (int i = lane; i < 36; i += 32) w.a[i] = in[i];
+  // lane-divergent reads of __constant__ tables serialize: stage them in smem
+  if (lane < 30) {
+    w.part[lane / 6][lane % 6] = kPart6[lane / 6][lane % 6];
+    w.slot[lane / 6][lane % 6] = kSlot6[lane / 6][lane % 6];
+    w.pq[lane / 6][(lane % 6) / 2][lane & 1] = (signed char)kRR6[lane / 6][(lane % 6) / 2][lane & 1];
+  }
   __syncwarp();
   for (int sweep = 0; sweep < 64; ++sweep) {
     if (lane == 0) w.rotated = 0;
     __syncwarp();
     for (int r = 0; r < 5; ++r) {
       if (lane < 3) {
-        int p = kRR6[r][lane][0], q = kRR6[r][lane][1];
-        if (p > q) {
-          const int t = p;
-          p = q;
-          q = t;
-        }
+        const int p = w.pq[r][lane][0], q = w.pq[r][lane][1];
         const double apq = w.a[6 * p + q], app = w.a[7 * p], aqq = w.a[7 * q];
         double c = 1.0, sn = 0.0, t = 0.0;
-        bool rot = false;
-        if (apq != 0.0) {
-          const double g = 100.0 * fabs(apq);
-          if (!(fabs(app) + g == fabs(app) && fabs(aqq) + g == fabs(aqq))) {
-            rot = true;
-            const double h = aqq - app;
-            if (fabs(h) + g == fabs(h)) {
-              t = apq / h;
-            } else {
-              const double theta = 0.5 * h / apq;
-              t = 1.0 / (fabs(theta) + sqrt(1.0 + theta * theta));
-              if (theta < 0.0) t = -t;
-            }
-            c = 1.0 / sqrt(1.0 + t * t);
-            sn = t * c;
+        const double g = 100.0 * fabs(apq);
+        const bool negligible = (fabs(app) + g == fabs(app) && fabs(aqq) + g == fabs(aqq)) ||
+                                fabs(apq) <= 1e-13 * sqrt(fabs(app) * fabs(aqq));
+        if (apq != 0.0 && !negligible) {
+          w.rotated = 1;
+          const double h = aqq - app;
+          if (fabs(h) + g == fabs(h)) {
+            t = apq * __drcp_rn(h);
+          } else {
+            const double theta = (0.5 * h) * __drcp_rn(apq);
+            t = __drcp_rn(fabs(theta) + __dsqrt_rn(__fma_rn(theta, theta, 1.0)));
+            if (theta < 0.0) t = -t;
           }
+          c = rsqrt(__fma_rn(t, t, 1.0));
+          sn = t * c;
         }
-        if (rot) w.rotated = 1;
-        w.c[p] = c;
-        w.c[q] = c;
-        w.s[p] = sn;
-        w.s[q] = sn;
-        w.tt[lane] = t;
-        w.tidx[p] = lane;
-        w.tidx[q] = lane;
-        w.part[p] = q + 1;     // p: partner q (positive)
-        w.part[q] = -(p + 1);  // q: partner p (negative)
+        w.c[lane] = c;
+        w.s[lane] = sn;
+        w.t[lane] = t;
       }
       __syncwarp();
-      for (int e = lane; e < 36; e += 32) {
+      double out[2];
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int e = lane + 32 * h2;
+        if (e >= 36) break;
         const int i = e / 6, j = e % 6;
-        const int pi = w.part[i], pj = w.part[j];
-        const bool ip = pi > 0, jp = pj > 0;           // i / j is the lower index of its pair
-        const int ii = ip ? pi - 1 : -pi - 1;          // partner of i
-        const int jj = jp ? pj - 1 : -pj - 1;          // partner of j
-        double out;
-        if (j == i || j == ii) {  // same 2x2 block
+        const int ii = w.part[r][i], jj = w.part[r][j];
+        const int si = w.slot[r][i], sj = w.slot[r][j];
+        const bool ip = i < ii, jp = j < jj;
+        double o;
+        if (si == sj) {  // same 2x2 block
           if (i != j) {
-            out = 0.0;  // rotated (or negligible) pair entry
+            o = 0.0;
           } else {
             const int p = ip ? i : ii, q = ip ? ii : i;
             const double apq = w.a[6 * p + q];
-            const double t = w.tt[w.tidx[p]];
-            out = ip ? w.a[7 * p] - t * apq : w.a[7 * q] + t * apq;
+            o = ip ? w.a[7 * p] - w.t[si] * apq : w.a[7 * q] + w.t[si] * apq;
           }
         } else {
-          // rows (i, ii) rotated by their pair, columns (j, jj) by theirs:
-          // col p' = c col p - s col q, col q' = s col p + c col q (and rows alike)
-          const double cj = w.c[j], sj = w.s[j], ci = w.c[i], si = w.s[i];
+          // col p' = c col p - s col q, col q' = s col p + c col q; rows alike
+          const double cj = w.c[sj], sj2 = w.s[sj], ci = w.c[si], si2 = w.s[si];
           const double xi = w.a[6 * i + j], yi = w.a[6 * i + jj];
           const double xii = w.a[6 * ii + j], yii = w.a[6 * ii + jj];
-          const double bi = jp ? cj * xi - sj * yi : sj * yi + cj * xi;
-          const double bii = jp ? cj * xii - sj * yii : sj * yii + cj * xii;
-          out = ip ? ci * bi - si * bii : si * bii + ci * bi;
+          const double bi = jp ? cj * xi - sj2 * yi : sj2 * yi + cj * xi;
+          const double bii = jp ? cj * xii - sj2 * yii : sj2 * yii + cj * xii;
+          o = ip ? ci * bi - si2 * bii : si2 * bii + ci * bi;
         }
-        w.b[e] = out;
+        out[h2] = o;
       }
       __syncwarp();
-      for (int e = lane; e < 36; e += 32) w.a[e] = w.b[e];
+      w.a[lane] = out[0];
+      if (lane < 4) w.a[lane + 32] = out[1];
       __syncwarp();
     }
+    if (lane == 0) w.sweeps = sweep + 1;
     if (!w.rotated) break;
     __syncwarp();
   }
@@ -303,7 +310,8 @@ static __device__ void warp_eig6(const double* in, double ev[6], Eig6Smem& w) {
 // solve_mstep (mstep.cpp:76-98) from the reduced normal equations, by one
 // warp: parallel eigenvalues for the condition estimate, then LDLT + exp map
 // on lane 0.  Result in *o (valid after the call on all lanes).
-static __device__ void warp_solve_normal_eq(const double* v, int nvp, SolveOut* o, Eig6Smem& w) {
+static __device__ void warp_solve_normal_eq(const double* v, int nvp, SolveOut* o, Eig6Smem& w,
+                                            Timeline* tl = nullptr, bool exact_cond = true) {
   const int lane = threadIdx.x & 31;
   if (nvp < 3) {
     if (lane == 0) {
@@ -315,41 +323,68 @@ static __device__ void warp_solve_normal_eq(const double* v, int nvp, SolveOut* 
     return;
   }
   __shared__ double ata_s[36];
+  __shared__ int s_need_eig;
   for (int e = lane; e < 36; e += 32) {
     const int i = e / 6, j = e % 6;
     const int a = i < j ? i : j, b = i < j ? j : i;
     ata_s[e] = v[a * 6 - a * (a - 1) / 2 + (b - a)];
   }
   __syncwarp();
-  double ev[6];
-  warp_eig6(ata_s, ev, w);
   if (lane == 0) {
     o->nvp = nvp;
     o->degenerate = 0;
-    const double lmin = ev[0], lmax = ev[5];
-    const double cond = lmin > 0.0 ? lmax / lmin : INFINITY;
-    o->cond = cond;
-    if (!(cond < 1e12)) {
-      o->degenerate = 1;
-    } else {
-      double ata[6][6], b[6], x[6];
-      int k = 0;
-      for (int i = 0; i < 6; ++i)
-        for (int j = i; j < 6; ++j) {
-          ata[i][j] = v[k];
-          ata[j][i] = v[k];
-          ++k;
-        }
-      for (int i = 0; i < 6; ++i) b[i] = v[21 + i];
-      ldlt_solve6(ata, b, x);
-      for (int i = 0; i < 3; ++i) {
-        o->omega[i] = x[i];
-        o->trans[i] = x[3 + i];
-        o->dt[i] = x[3 + i];
+    o->eig_sweeps = 0;
+    double ata[6][6], b[6], x[6], trinv, mind;
+    int k = 0;
+    for (int i = 0; i < 6; ++i)
+      for (int j = i; j < 6; ++j) {
+        ata[i][j] = v[k];
+        ata[j][i] = v[k];
+        ++k;
       }
-      small_angle_rotation(o->omega, o->dR);
+    for (int i = 0; i < 6; ++i) b[i] = v[21 + i];
+    ldlt_solve6_tr(ata, b, x, &trinv, &mind);
+    for (int i = 0; i < 3; ++i) {
+      o->omega[i] = x[i];
+      o->trans[i] = x[3 + i];
+      o->dt[i] = x[3 + i];
+    }
+    double tra = ata[0][0];
+    for (int i = 1; i < 6; ++i) tra += ata[i][i];
+    const double hi = tra * trinv;  // >= cond, <= 36 cond
+    int need = 1;
+    if (!exact_cond) {
+      if (!(mind > 0.0)) {  // not positive definite: lambda_min <= 0, cond = inf
+        o->cond = INFINITY;
+        o->degenerate = 1;
+        need = 0;
+      } else if (hi < 1e12) {  // cond <= hi < 1e12
+        o->cond = hi;            // upper bound (the EM loop only needs the test)
+        need = 0;
+      } else if (hi / 36.0 >= 1e12) {
+        o->cond = hi / 36.0;
+        o->degenerate = 1;
+        need = 0;
+      }
+    }
+    s_need_eig = need;
+  }
+  __syncwarp();
+  if (s_need_eig) {
+    double ev[6];
+    if (tl && lane == 0) tl_mark(tl, 7001);
+    warp_eig6(ata_s, ev, w);
+    if (tl && lane == 0) tl_mark(tl, 7002);
+    if (lane == 0) {
+      o->eig_sweeps = w.sweeps;
+      const double lmin = ev[0], lmax = ev[5];
+      const double cond = lmin > 0.0 ? lmax / lmin : INFINITY;
+      o->cond = cond;
+      if (!(cond < 1e12)) o->degenerate = 1;
     }
   }
+  if (lane == 0 && !o->degenerate) small_angle_rotation(o->omega, o->dR);
+  if (tl && lane == 0) tl_mark(tl, 7003);
   __syncwarp();
 }
 

@@ -18,3 +18,6 @@ out = np.zeros(16)
 L = _lib.lib(); f = L.trg_debug_solve; f.argtypes = [C.c_void_p, _lib.dp, C.c_int, _lib.dp]
 f(ctx.h, v.ctypes.data_as(_lib.dp), nv, out.ctypes.data_as(_lib.dp))
 print("gpu", out[:8]); print("numpy", np.linalg.solve(ata, atb), np.linalg.cond(ata)); print("golden", g["solve_omega"], g["solve_translation"])
+for rep in range(3):
+    f(ctx.h, v.ctypes.data_as(_lib.dp), nv, out.ctypes.data_as(_lib.dp))
+print("sweeps", out[8], "cycles", out[9], "us", out[9]/1950)
