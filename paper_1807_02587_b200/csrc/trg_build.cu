@@ -16,6 +16,7 @@
 //   p = I+10       layout: create tree nodes, next round's segments (CTA 0)
 //   p = I+11       partition write pass (skipped in the last round)
 #include <cub/block/block_scan.cuh>
+#include <cstdlib>
 #include <vector>
 
 #include "trg_solve.cuh"
@@ -129,6 +130,7 @@ struct BuildParams {
   BuildState* st;
   Timeline* tl;
   int* status;
+  int dbg;  // experiments only (TRG_BUILD_DBG): 1 = calibration combine only, 2 = + leaf refit
 };
 
 // ----------------------------------------------------------------- helpers
@@ -666,6 +668,7 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
     const int c = lane >> 3;
     if (ph.mode[c] == 1) node_mstep(p, k, c, red, lane & 7);
   }
+  __syncwarp();
   if (lane < 2 && ph.mode[lane] == 2) {
     const int c = lane;
     nf.final_ll[2 * k + c] = __ldcg(red + kOffFin + 9 * c);
@@ -1055,13 +1058,9 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
   }
 }
 
-constexpr size_t kBuildSmemBytes =
-    sizeof(BuildSmem) > sizeof(AssocSmem<10>) ? sizeof(BuildSmem) : sizeof(AssocSmem<10>);
 
 __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
-  __shared__ __align__(16) unsigned char smem_raw[kBuildSmemBytes];
-  BuildSmem& sm = *reinterpret_cast<BuildSmem*>(smem_raw);
-  AssocSmem<10>& asm_ = *reinterpret_cast<AssocSmem<10>*>(smem_raw);
+  __shared__ BuildSmem sm;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   BuildState* st = p.st;
@@ -1104,7 +1103,6 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
       __syncthreads();
       const int NI = sm.nitems;
       const int K = __ldcg(&st->Kp[par]);
-      if (round == 2 && ph_i == 2) tl_mark(p.tl, 4999);
       for (int it = cta * (kTile / 32) + warp; it < K * NI; it += G * (kTile / 32)) {
         const int k = it / NI, f = it % NI;
         reduce_item(p, par, k, sm.item_off[f], sm.item_kind[f]);
@@ -1118,16 +1116,24 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
           }
         }
         last = __shfl_sync(0xffffffffu, last, 0);
-        const bool dbg = (round == 2 && ph_i == 2 && lane == 0);
-        if (dbg && last) tl_mark_any(p.tl, 5000 + k);
         if (last) node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
-        if (dbg && last) tl_mark_any(p.tl, 6000 + k);
       }
       grid_sync(p.bar, G);
       tl_mark(p.tl, round * 100 + 50 + ph_i);
     }
     if (__ldcg(&st->done) || __ldcg(&st->status_overflow)) break;
   }
+}
+
+// Second persistent kernel of the build (launched right behind k_build on
+// the same stream): parent moment match + refresh_eig, then the leaf
+// calibration passes.  Separate so its 3x3 eigen chains get a full register
+// budget while k_build's E-step passes keep 3 CTAs per SM.
+__global__ void __launch_bounds__(kTile, 3) k_calibrate(BuildParams p) {
+  __shared__ AssocSmem<10> asm_;
+  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  BuildState* st = p.st;
   if (__ldcg(&st->status_overflow)) return;
   const int J = __ldcg(&st->J);
   __shared__ int lvl[9];
@@ -1169,88 +1175,113 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
       if (__ldcg(&p.nodes[j].child_count) != 0) continue;  // leaves only
       double m[10];
       combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
-      if (lane != 0) continue;
+      if (p.dbg == 1) continue;
       double* branch = p.cal_moments;  // slot 0 of each node
-      branch[(size_t)j * 10] = m[0];
-      DNode& nd = p.nodes[j];
-      if (m[0] > 0.0) {  // leaf refit (gmm.cpp:532-545)
-        const double mu[3] = {m[1] / m[0], m[2] / m[0], m[3] / m[0]};
-        const double M[3][3] = {{m[4], m[5], m[6]}, {m[5], m[7], m[8]}, {m[6], m[8], m[9]}};
-        double S[3][3], S2[3][3];
-        for (int r = 0; r < 3; ++r)
-          for (int c = 0; c < 3; ++c) S[r][c] = M[r][c] / m[0] - mu[r] * mu[c];
-        for (int r = 0; r < 3; ++r)
-          for (int c = 0; c < 3; ++c) S2[r][c] = 0.5 * (S[r][c] + S[c][r]);
-        double dm = (nd.mean[0] - mu[0]) * (nd.mean[0] - mu[0]);
-        dm += (nd.mean[1] - mu[1]) * (nd.mean[1] - mu[1]);
-        dm += (nd.mean[2] - mu[2]) * (nd.mean[2] - mu[2]);
-        drift = smax(drift, sqrt(dm));
-        double before[3][3];
-        for (int r = 0; r < 3; ++r)
-          for (int c = 0; c < 3; ++c) before[r][c] = p.cov[9 * (size_t)j + 3 * r + c];
-        GComp g;
-        g.w = nd.weight;
-        for (int q = 0; q < 3; ++q) g.mean[q] = mu[q];
-        if (comp_set_cov(g, S2, cov_floor(S2, p.eps, p.abs_floor))) atomicCAS(p.status, 0, kEInval);
-        double dc[3][3];
-        for (int r = 0; r < 3; ++r)
-          for (int c = 0; c < 3; ++c) dc[r][c] = g.cov[3 * r + c] - before[r][c];
-        drift = smax(drift, norm33(dc));
-        write_dnode_from_comp(nd, p.cov + 9 * (size_t)j, g, nd.weight, nd.level, nd.parent);
+      if (lane == 0) {
+        branch[(size_t)j * 10] = m[0];
+        DNode& nd = p.nodes[j];
+        if (m[0] > 0.0) {  // leaf refit (gmm.cpp:532-545)
+          const double mu[3] = {m[1] / m[0], m[2] / m[0], m[3] / m[0]};
+          const double M[3][3] = {{m[4], m[5], m[6]}, {m[5], m[7], m[8]}, {m[6], m[8], m[9]}};
+          double S[3][3], S2[3][3];
+          for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) S[r][c] = M[r][c] / m[0] - mu[r] * mu[c];
+          for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) S2[r][c] = 0.5 * (S[r][c] + S[c][r]);
+          double dm = (nd.mean[0] - mu[0]) * (nd.mean[0] - mu[0]);
+          dm += (nd.mean[1] - mu[1]) * (nd.mean[1] - mu[1]);
+          dm += (nd.mean[2] - mu[2]) * (nd.mean[2] - mu[2]);
+          drift = smax(drift, sqrt(dm));
+          double before[3][3];
+          for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) before[r][c] = p.cov[9 * (size_t)j + 3 * r + c];
+          GComp g;
+          g.w = nd.weight;
+          for (int q = 0; q < 3; ++q) g.mean[q] = mu[q];
+          if (comp_set_cov(g, S2, cov_floor(S2, p.eps, p.abs_floor))) atomicCAS(p.status, 0, kEInval);
+          double dc[3][3];
+          for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) dc[r][c] = g.cov[3 * r + c] - before[r][c];
+          drift = smax(drift, norm33(dc));
+          write_dnode_from_comp(nd, p.cov + 9 * (size_t)j, g, nd.weight, nd.level, nd.parent);
+        }
       }
-      // climb: arrive at the parent; the last child processes it
+      __syncwarp();
+      if (p.dbg == 2) continue;
+      // climb: arrive at the parent; the parent's last-arriving child's warp
+      // processes it (lanes load one child each; sums run in child order on
+      // every lane, so the arithmetic is the reference's), then climbs on
       int node = j;
       for (;;) {
-        const int par = __ldcg(&p.nodes[node].parent);
-        unsigned* ctr = par >= 0 ? &p.cal_arrive[par] : &p.cal_arrive[p.capacity];
-        const unsigned need = par >= 0 ? (unsigned)__ldcg(&p.nodes[par].child_count)
-                                       : (unsigned)root_count;
-        __threadfence();
-        if (atomicAdd(ctr, 1u) != need - 1) break;
-        *ctr = 0u;
-        __threadfence();
-        const int first = par >= 0 ? __ldcg(&p.nodes[par].first_child) : 0;
-        const int count = (int)need;
-        // branch mass (gmm.cpp:547-556) and sibling reweight (gmm.cpp:557-566)
-        double sb = 0.0;
-        for (int c = 0; c < count; ++c) sb += __ldcg(&branch[(size_t)(first + c) * 10]);
-        if (par >= 0) branch[(size_t)par * 10] = sb;
-        if (sb > 0.0)
-          for (int c = 0; c < count; ++c) {
-            const double w = __ldcg(&branch[(size_t)(first + c) * 10]) / sb;
-            drift = smax(drift, fabs(__ldcg(&p.nodes[first + c].weight) - w));
-            p.nodes[first + c].weight = w;
+        int par = 0, last = 0, need = 0;
+        if (lane == 0) {
+          par = __ldcg(&p.nodes[node].parent);
+          unsigned* ctr = par >= 0 ? &p.cal_arrive[par] : &p.cal_arrive[p.capacity];
+          need = par >= 0 ? __ldcg(&p.nodes[par].child_count) : root_count;
+          __threadfence();
+          last = atomicAdd(ctr, 1u) == (unsigned)need - 1;
+          if (last) {
+            *ctr = 0u;
+            __threadfence();
           }
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) break;
+        par = __shfl_sync(0xffffffffu, par, 0);
+        need = __shfl_sync(0xffffffffu, need, 0);
+        const int first = par >= 0 ? __ldcg(&p.nodes[par].first_child) : 0;
+        const int count = need;
+        // lane c < count holds child c: branch mass, weight, mean, cov
+        const int ci = first + (lane < count ? lane : 0);
+        const double cb = lane < count ? __ldcg(&branch[(size_t)ci * 10]) : 0.0;
+        double cwt = __ldcg(&p.nodes[ci].weight);
+        double cm[3], cc[9];
+        for (int k = 0; k < 3; ++k) cm[k] = __ldcg(&p.nodes[ci].mean[k]);
+        for (int k = 0; k < 9; ++k) cc[k] = __ldcg(&p.cov[9 * (size_t)ci + k]);
+        // branch mass and sibling reweight (gmm.cpp:547-566): sequential sum
+        double sb = 0.0;
+        for (int c = 0; c < count; ++c) sb += __shfl_sync(0xffffffffu, cb, c);
+        if (par >= 0 && lane == 0) branch[(size_t)par * 10] = sb;
+        if (sb > 0.0 && lane < count) {
+          const double w = cb / sb;
+          drift = smax(drift, fabs(cwt - w));
+          cwt = w;
+          p.nodes[ci].weight = w;
+        }
         if (par < 0) break;  // top octet done
-        // parent moment match (gmm.cpp:489-513) + refresh_eig (gmm.cpp:576-578)
-        DNode& pn = p.nodes[par];
+        // parent moment match (gmm.cpp:489-513), sums in child order
         double w = 0.0, mu[3] = {0.0, 0.0, 0.0};
         for (int c = 0; c < count; ++c) {
-          const DNode& ch = p.nodes[first + c];
-          const double cw = __ldcg(&ch.weight);
-          w += cw;
-          for (int k = 0; k < 3; ++k) mu[k] = mu[k] + cw * __ldcg(&ch.mean[k]);
+          const double wc = __shfl_sync(0xffffffffu, cwt, c);
+          w += wc;
+          for (int k = 0; k < 3; ++k) mu[k] = mu[k] + wc * __shfl_sync(0xffffffffu, cm[k], c);
         }
         if (w > 0.0) {
           for (int k = 0; k < 3; ++k) mu[k] = mu[k] / w;
           double cv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
           for (int c = 0; c < count; ++c) {
-            const int ci = first + c;
-            const DNode& ch = p.nodes[ci];
-            const double cw = __ldcg(&ch.weight);
-            const double d[3] = {__ldcg(&ch.mean[0]) - mu[0], __ldcg(&ch.mean[1]) - mu[1],
-                                 __ldcg(&ch.mean[2]) - mu[2]};
+            const double wc = __shfl_sync(0xffffffffu, cwt, c);
+            double d[3], cov9[9];
+            for (int k = 0; k < 3; ++k) d[k] = __shfl_sync(0xffffffffu, cm[k], c) - mu[k];
+            for (int k = 0; k < 9; ++k) cov9[k] = __shfl_sync(0xffffffffu, cc[k], c);
             for (int r = 0; r < 3; ++r)
               for (int q = 0; q < 3; ++q)
-                cv[3 * r + q] = cv[3 * r + q] + cw * (__ldcg(&p.cov[9 * (size_t)ci + 3 * r + q]) + d[r] * d[q]);
+                cv[3 * r + q] = cv[3 * r + q] + wc * (cov9[3 * r + q] + d[r] * d[q]);
           }
-          for (int k = 0; k < 9; ++k) p.cov[9 * (size_t)par + k] = cv[k] / w;
-          for (int k = 0; k < 3; ++k) pn.mean[k] = mu[k];
+          if (lane == 0) {
+            for (int k = 0; k < 9; ++k) p.cov[9 * (size_t)par + k] = cv[k] / w;
+            for (int k = 0; k < 3; ++k) p.nodes[par].mean[k] = mu[k];
+          }
         }
-        if (refresh_node(pn, p.cov + 9 * (size_t)par)) atomicCAS(p.status, 0, kEInval);
+        __syncwarp();
+        if (lane == 0 && refresh_node(p.nodes[par], p.cov + 9 * (size_t)par))  // gmm.cpp:576-578
+          atomicCAS(p.status, 0, kEInval);
+        __syncwarp();
         node = par;
       }
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) drift = smax(drift, __shfl_xor_sync(0xffffffffu, drift, off));
     if (lane == 0 && drift > 0.0)
       atomicMax(&p.drift_bits[pass & 1], (unsigned long long)__double_as_longlong(drift));
     grid_sync(p.bar, G);
@@ -1349,7 +1380,8 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
                o_car = carve(sizeof(unsigned) * ((size_t)cap + 1)), o_dbits = carve(16),
                o_state = carve(sizeof(BuildState));
   const int G = persistent_grid(ctx, (const void*)k_build, kTile, 0);
-  const size_t o_cd = carve(sizeof(double) * G);
+  const int Gc = persistent_grid(ctx, (const void*)k_calibrate, kTile, 0);
+  const size_t o_cd = carve(sizeof(double) * std::max(G, Gc));
   void* arena = nullptr;
   TRG_TRY(ws_get(ctx, kSlotBuild0, off, &arena));
   char* A = static_cast<char*>(arena);
@@ -1402,6 +1434,10 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   p.cta_drift = (double*)(A + o_cd);
   p.status = ctx->status;
   p.tl = ctx->dev_timeline;
+  {
+    const char* dbg = getenv("TRG_BUILD_DBG");
+    p.dbg = dbg ? atoi(dbg) : 0;
+  }
   TRG_TRY(timeline_reset(ctx));
   // tree
   trg_tree_dev* tree = nullptr;
@@ -1411,8 +1447,8 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   p.cov = tree->cov;
   // calibration association (NM = 10, identity, lambda_c = 0, full depth)
   void *part, *stamps, *cnt;
-  TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * 10 * (size_t)cap * G, &part));
-  TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)cap * G, &stamps));
+  TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * 10 * (size_t)cap * Gc, &part));
+  TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)cap * Gc, &stamps));
   TRG_TRY(ws_get(ctx, kSlotCounters, 64, &cnt));
   p.a.nodes = tree->nodes;
   p.a.depth = L;
@@ -1450,7 +1486,13 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
                                                ctx->status);
   void* args[] = {&p};
   TRG_CU(cudaLaunchCooperativeKernel((const void*)k_build, G, kTile, args, 0, ctx->stream));
-  ctx->launches += 2;
+  {
+    BuildParams pc = p;  // same buffers; calibration grid sized for k_calibrate
+    pc.a.partials = p.a.partials;
+    void* cargs[] = {&pc};
+    TRG_CU(cudaLaunchCooperativeKernel((const void*)k_calibrate, Gc, kTile, cargs, 0, ctx->stream));
+  }
+  ctx->launches += 3;
   TRG_CU(trg_memcpy(ctx, &st, p.st, sizeof st, cudaMemcpyDeviceToHost));
   int rc = check_status(ctx, "build_tree");
   if (rc == TRG_OK && st.status_overflow) {

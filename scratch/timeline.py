@@ -11,6 +11,7 @@ for _ in range(2):
 t = np.zeros(1024, np.uint64); lab = np.zeros(1024, np.int32)
 n = _lib.lib().trg_debug_build_timeline(ctx.h, t.ctypes.data_as(_lib.u64p), lab.ctypes.data_as(_lib.ip), 1024)
 t = t[:n].astype(np.float64) / 1e3; lab = lab[:n]
+o = np.argsort(t, kind="stable"); t = t[o]; lab = lab[o]
 dt = np.diff(t)
 groups = collections.OrderedDict()
 for i in range(1, n):

@@ -18,3 +18,8 @@ d = [(starts[k]-t0, ends[k]-starts[k]) for k in sorted(starts)]
 st = np.array([x[0] for x in d]); du = np.array([x[1] for x in d])
 print("node update start (us after phase start): min %.1f med %.1f max %.1f" % (st.min(), np.median(st), st.max()))
 print("node update duration (us): min %.1f med %.1f max %.1f" % (du.min(), np.median(du), du.max()))
+ms = {l-8000: v for l, v in zip(lab, t) if 8000 <= l < 8100}
+me = {l-8100: v for l, v in zip(lab, t) if 8100 <= l < 8200}
+du2 = np.array([me[k]-ms[k] for k in ms if k in me])
+pre = np.array([ms[k]-starts[k] for k in ms if k in starts])
+print("M-step part (us): min %.1f med %.1f max %.1f; before M-step: med %.1f" % (du2.min(), np.median(du2), du2.max(), np.median(pre)))
