@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int J = p.a.n_nodes;
-  const int P2 = (J + (kAssocBlock / 32) - 1) / (kAssocBlock / 32);  // producer CTAs
+  const int P2 = min(G, (J + (kAssocBlock / 32) - 1) / (kAssocBlock / 32));  // producer CTAs
   const double n_total = (double)p.a.n;
   if (tid < 12) rt[tid] = ldcg(&p.st->Rt[tid]);
   if (tid == 0) {
@@ -75,8 +75,7 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
     if (cta < P2) {
       SolveAcc acc;
       acc_zero(acc);
-      const int j = cta * (kAssocBlock / 32) + warp;
-      if (j < J) {
+      for (int j = cta * (kAssocBlock / 32) + warp; j < J; j += P2 * (kAssocBlock / 32)) {
         double m[4];
         combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
         if (lane == 0) {
