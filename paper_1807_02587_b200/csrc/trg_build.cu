@@ -131,6 +131,7 @@ struct BuildParams {
   Timeline* tl;
   int* status;
   int dbg;  // experiments only (TRG_BUILD_DBG): 1 = calibration combine only, 2 = + leaf refit
+  int want_traces;  // per-iteration log-likelihoods only feed BuildDiagnostics (gmm.cpp:240)
 };
 
 // ----------------------------------------------------------------- helpers
@@ -440,7 +441,10 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     for (int k = 0; k < 8; ++k) s += __shfl_sync(0xffffffffu, ek, gbase + k);
     // gamma_k = exp(log_k - log_total) = e_k / s (gmm.cpp:189, 354): one
     // reciprocal per entry instead of a second exp per component (ulp-level)
-    const double lt = fin ? m + log(s) : 0.0;
+    // the per-iteration log-likelihood only feeds the diagnostics trace
+    // (gmm.cpp:240); the final pass (mode 2) always needs it (gmm.cpp:394)
+    const bool want_ll = mode == 2 || (mode == 1 && p.want_traces);
+    const double lt = (fin && want_ll) ? m + log(s) : 0.0;
     const double gam = fin ? __dmul_rn(ek, __drcp_rn(s)) : 0.0;
     double denom = 0.0;
     if (mode == 3)
@@ -1437,6 +1441,7 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   {
     const char* dbg = getenv("TRG_BUILD_DBG");
     p.dbg = dbg ? atoi(dbg) : 0;
+    p.want_traces = (diag && diag->ll_traces && diag->ll_trace_capacity > 0) ? 1 : 0;
   }
   TRG_TRY(timeline_reset(ctx));
   // tree
