@@ -151,6 +151,11 @@ int trg_ctx_create(int device, trg_ctx** out);
 int trg_ctx_destroy(trg_ctx* ctx);
 const char* trg_last_error(void);
 int trg_device_sms(trg_ctx* ctx);
+/* Limits this context's persistent grids to `sms` SMs' worth of CTAs (0 =
+ * the whole device).  Several contexts on one device, each on its own
+ * stream and host thread, then run independent registrations concurrently
+ * (batched frame pairs, BASELINE config C5).  No reference counterpart. */
+int trg_ctx_set_sm_budget(trg_ctx* ctx, int sms);
 /* Launch count of this library's kernels since ctx creation (bench evidence). */
 uint64_t trg_kernel_launches(trg_ctx* ctx);
 /* Bytes copied host->device / device->host by this context so far. */

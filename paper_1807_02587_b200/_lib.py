@@ -79,6 +79,7 @@ SIGNATURES = {
     "trg_ctx_destroy": (C.c_int, [C.c_void_p]),
     "trg_last_error": (C.c_char_p, []),
     "trg_device_sms": (C.c_int, [C.c_void_p]),
+    "trg_ctx_set_sm_budget": (C.c_int, [C.c_void_p, C.c_int]),
     "trg_kernel_launches": (C.c_uint64, [C.c_void_p]),
     "trg_ctx_stream": (C.c_void_p, [C.c_void_p]),
     "trg_ctx_transfer_bytes": (None, [C.c_void_p, u64p, u64p]),

@@ -1490,12 +1490,12 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
                                                p.tile_node[0], p.tile_start[0], p.tile_len[0],
                                                ctx->status);
   void* args[] = {&p};
-  TRG_CU(cudaLaunchCooperativeKernel((const void*)k_build, G, kTile, args, 0, ctx->stream));
+  TRG_CU(launch_persistent(ctx, (const void*)k_build, G, kTile, args));
   {
     BuildParams pc = p;  // same buffers; calibration grid sized for k_calibrate
     pc.a.partials = p.a.partials;
     void* cargs[] = {&pc};
-    TRG_CU(cudaLaunchCooperativeKernel((const void*)k_calibrate, Gc, kTile, cargs, 0, ctx->stream));
+    TRG_CU(launch_persistent(ctx, (const void*)k_calibrate, Gc, kTile, cargs));
   }
   ctx->launches += 3;
   TRG_CU(trg_memcpy(ctx, &st, p.st, sizeof st, cudaMemcpyDeviceToHost));

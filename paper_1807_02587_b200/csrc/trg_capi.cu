@@ -50,6 +50,37 @@ int host_ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out) {
   return TRG_OK;
 }
 
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+cudaError_t trg_memcpy(trg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  if (bytes == 0) return cudaSuccess;
+  if (kind == cudaMemcpyHostToDevice) ctx->bytes_h2d += bytes;
+  if (kind == cudaMemcpyDeviceToHost) ctx->bytes_d2h += bytes;
+  const bool h2d = kind == cudaMemcpyHostToDevice, d2h = kind == cudaMemcpyDeviceToHost;
+  if ((!h2d && !d2h) || is_pinned(h2d ? src : dst))
+    return cudaMemcpyAsync(dst, src, bytes, kind, ctx->stream);
+  void* stage = nullptr;
+  if (host_ws_get(ctx, kSlotHostStage, bytes, &stage) != TRG_OK) return cudaErrorMemoryAllocation;
+  cudaError_t e;
+  if (h2d) {
+    // the staging buffer may still feed an earlier copy on this stream
+    if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) return e;
+    std::memcpy(stage, src, bytes);
+    return cudaMemcpyAsync(dst, stage, bytes, kind, ctx->stream);
+  }
+  if ((e = cudaMemcpyAsync(stage, src, bytes, kind, ctx->stream)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) return e;
+  std::memcpy(dst, stage, bytes);
+  return cudaSuccess;
+}
+
 int check_status(trg_ctx* ctx, const char* where) {
   int st = 0;
   TRG_CU(trg_memcpy(ctx, &st, ctx->status, sizeof(int), cudaMemcpyDeviceToHost));
@@ -71,13 +102,13 @@ int timeline_reset(trg_ctx* ctx) {
   return TRG_OK;
 }
 
+// Stream-ordered copy into a pinned buffer; parsed only when asked for
+// (trg_debug_build_timeline), so the hot path never waits on it.
 int timeline_fetch(trg_ctx* ctx) {
-  Timeline h;
-  TRG_CU(cudaMemcpyAsync(&h, ctx->dev_timeline, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
-  TRG_CU(cudaStreamSynchronize(ctx->stream));
-  const int n = std::min(h.n, 1024);
-  ctx->timeline.assign(h.t, h.t + n);
-  ctx->timeline_lab.assign(h.lab, h.lab + n);
+  void* h = nullptr;
+  TRG_TRY(host_ws_get(ctx, kSlotTimelineHost, sizeof(Timeline), &h));
+  TRG_CU(cudaMemcpyAsync(h, ctx->dev_timeline, sizeof(Timeline), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->timeline_pending = true;
   return TRG_OK;
 }
 
@@ -88,8 +119,28 @@ int persistent_grid(trg_ctx* ctx, const void* kernel, int block, size_t smem) {
   return ctx->sms * per_sm;
 }
 
+cudaError_t launch_persistent(trg_ctx* ctx, const void* kernel, int G, int block, void** args) {
+  if (ctx->sms < ctx->device_sms)
+    return cudaLaunchKernel(kernel, dim3(G), dim3(block), args, 0, ctx->stream);
+  return cudaLaunchCooperativeKernel(kernel, dim3(G), dim3(block), args, 0, ctx->stream);
+}
+
 int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out) {
-  (void)ctx;
+  if (ctx->build_into_scratch) {
+    // register_clouds' internal model: reuse the context's tree so repeated
+    // registrations never call cudaMalloc/cudaFree (both synchronise the
+    // device and would serialise concurrent contexts)
+    if (ctx->scratch_tree && ctx->scratch_tree->capacity >= capacity) {
+      *out = ctx->scratch_tree;
+      return TRG_OK;
+    }
+    if (ctx->scratch_tree) {
+      TRG_CU(cudaStreamSynchronize(ctx->stream));
+      ctx->scratch_tree->ctx_scratch = false;
+      trg_tree_free(ctx, ctx->scratch_tree);
+      ctx->scratch_tree = nullptr;
+    }
+  }
   auto* t = new trg_tree_dev;
   t->capacity = capacity;
   if (cudaMalloc(&t->nodes, sizeof(DNode) * capacity) != cudaSuccess ||
@@ -99,6 +150,10 @@ int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out) {
     delete t;
     set_error("tree_alloc: cudaMalloc failed");
     return TRG_ECUDA;
+  }
+  if (ctx->build_into_scratch) {
+    t->ctx_scratch = true;
+    ctx->scratch_tree = t;
   }
   *out = t;
   return TRG_OK;
@@ -148,6 +203,7 @@ int trg_ctx_create(int device, trg_ctx** out) {
     return TRG_ECUDA;
   }
   c->sms = prop.multiProcessorCount;
+  c->device_sms = c->sms;
   TRG_CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   TRG_CU(cudaMalloc(&c->status, sizeof(int)));
   TRG_CU(cudaMemset(c->status, 0, sizeof(int)));
@@ -165,6 +221,10 @@ int trg_ctx_destroy(trg_ctx* ctx) {
     if (ctx->slot_ptr[i]) cudaFree(ctx->slot_ptr[i]);
     if (ctx->host_slot_ptr[i]) cudaFreeHost(ctx->host_slot_ptr[i]);
   }
+  if (ctx->scratch_tree) {
+    ctx->scratch_tree->ctx_scratch = false;
+    trg_tree_free(ctx, ctx->scratch_tree);
+  }
   cudaFree(ctx->status);
   cudaFree(ctx->dev_timeline);
   cudaStreamDestroy(ctx->stream);
@@ -173,7 +233,23 @@ int trg_ctx_destroy(trg_ctx* ctx) {
 }
 
 int trg_device_sms(trg_ctx* ctx) { return ctx->sms; }
+int trg_ctx_set_sm_budget(trg_ctx* ctx, int sms) {
+  if (!ctx || sms < 0) {
+    set_error("trg_ctx_set_sm_budget: bad argument");
+    return TRG_EINVAL;
+  }
+  ctx->sms = (sms == 0 || sms > ctx->device_sms) ? ctx->device_sms : sms;
+  return TRG_OK;
+}
 int trg_debug_build_timeline(trg_ctx* ctx, uint64_t* t_ns, int* labels, int cap) {
+  if (ctx->timeline_pending) {
+    TRG_CU(cudaStreamSynchronize(ctx->stream));
+    const Timeline* h = (const Timeline*)ctx->host_slot_ptr[kSlotTimelineHost];
+    const int m = std::min(h->n, 1024);
+    ctx->timeline.assign(h->t, h->t + m);
+    ctx->timeline_lab.assign(h->lab, h->lab + m);
+    ctx->timeline_pending = false;
+  }
   const int n = (int)ctx->timeline.size();
   for (int i = 0; i < n && i < cap; ++i) {
     t_ns[i] = ctx->timeline[i];
@@ -275,7 +351,7 @@ int trg_tree_download(trg_ctx* ctx, const trg_tree_dev* t, trg_tree* h) {
 }
 
 int trg_tree_free(trg_ctx* ctx, trg_tree_dev* t) {
-  if (!t) return TRG_OK;
+  if (!t || t->ctx_scratch) return TRG_OK;
   if (ctx) cudaSetDevice(ctx->device);
   cudaFree(t->nodes);
   cudaFree(t->cov);

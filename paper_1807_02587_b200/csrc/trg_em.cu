@@ -378,8 +378,7 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   TRG_CU(cudaEventCreate(&e1));
   TRG_CU(cudaEventRecord(e0, ctx->stream));
   void* args[] = {&p};
-  TRG_CU(cudaLaunchCooperativeKernel((const void*)k_register, G, kAssocBlock, args, 0,
-                                     ctx->stream));
+  TRG_CU(launch_persistent(ctx, (const void*)k_register, G, kAssocBlock, args));
   TRG_CU(cudaEventRecord(e1, ctx->stream));
   ctx->launches += 3;
   TRG_CU(trg_memcpy(ctx, &st, p.st, sizeof st, cudaMemcpyDeviceToHost));
@@ -709,7 +708,9 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
   trg_model_config mc = cfg->model_config;
   mc.max_level = cfg->variant_param;
   trg_tree_dev* tree = nullptr;
+  ctx->build_into_scratch = true;
   int rc = trg_build_tree(ctx, tgt, n_target, 1, &mc, &tree, nullptr);
+  ctx->build_into_scratch = false;
   if (rc != TRG_OK) return rc;
   TRG_CU(cudaEventRecord(e1, ctx->stream));
   const double diag = target_bbox_diagonal(ctx, tgt, n_target);

@@ -66,6 +66,7 @@ struct trg_tree_dev {
   trg::DNode* nodes = nullptr;  // [capacity]
   double* cov = nullptr;        // [capacity*9] row-major
   int* owner_ctx_device = nullptr;
+  bool ctx_scratch = false;  // owned by a context (register_clouds' model); free is a no-op
 };
 
 namespace trg {
@@ -97,10 +98,14 @@ struct trg_ctx {
   int device = 0;
   uint64_t bytes_h2d = 0, bytes_d2h = 0;
   double build_growth = 0.0;  // largest E_max / N a build on this context needed
-  int sms = 0;
+  int sms = 0;         // SMs this context's persistent grids may use (trg_ctx_set_sm_budget)
+  int device_sms = 0;
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
   uint32_t epoch = 1;
+  trg_tree_dev* scratch_tree = nullptr;  // reused by register_clouds (no cudaMalloc/cudaFree per call)
+  bool build_into_scratch = false;
+  bool timeline_pending = false;
   static constexpr int kSlots = 32;
   void* slot_ptr[kSlots] = {};
   size_t slot_size[kSlots] = {};
@@ -139,18 +144,19 @@ enum Slot : int {
   kSlotBuild10,
   kSlotBuild11,
   kSlotPoints2,
+  kSlotHostStage,     // host slots only: pinned staging for pageable copies
+  kSlotTimelineHost,  // host slots only: last device timeline
 };
 
 int ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
 
 // Every host<->device copy of the library goes through here (byte counters
-// back the e2e h2d/d2h figures of bench.py).
-inline cudaError_t trg_memcpy(trg_ctx* ctx, void* dst, const void* src, size_t bytes,
-                              cudaMemcpyKind kind) {
-  if (kind == cudaMemcpyHostToDevice) ctx->bytes_h2d += bytes;
-  if (kind == cudaMemcpyDeviceToHost) ctx->bytes_d2h += bytes;
-  return cudaMemcpyAsync(dst, src, bytes, kind, ctx->stream);
-}
+// back the e2e h2d/d2h figures of bench.py).  Pinned host buffers are copied
+// asynchronously on the context's stream; pageable ones are staged through
+// the context's pinned buffer (a pageable cudaMemcpyAsync holds driver locks
+// that serialise every other context's launches), which makes those copies
+// complete before the call returns.
+cudaError_t trg_memcpy(trg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind);
 int host_ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
 int check_status(trg_ctx* ctx, const char* where);
 int timeline_reset(trg_ctx* ctx);
@@ -159,6 +165,12 @@ int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out);
 
 // Grid size for persistent kernels: SMs x resident CTAs.
 int persistent_grid(trg_ctx* ctx, const void* kernel, int block, size_t smem);
+// Launches a persistent (grid-barrier) kernel of G = persistent_grid() CTAs.
+// Whole-device contexts use a cooperative launch (co-residency checked by
+// the driver).  SM-budgeted contexts (trg_ctx_set_sm_budget) use a plain
+// launch so several contexts' persistent kernels run concurrently: their
+// budgets sum to at most the device's SMs, so every grid stays co-resident.
+cudaError_t launch_persistent(trg_ctx* ctx, const void* kernel, int G, int block, void** args);
 
 // ---- association (trg_assoc.cu)
 struct AssocParams {

@@ -93,6 +93,10 @@ class Context:
     def sms(self) -> int:
         return _lib.lib().trg_device_sms(self.h)
 
+    def set_sm_budget(self, sms: int) -> None:
+        """Limit this context's persistent grids to `sms` SMs (0 = all)."""
+        _chk(_lib.lib().trg_ctx_set_sm_budget(self.h, int(sms)))
+
     @property
     def kernel_launches(self) -> int:
         return int(_lib.lib().trg_kernel_launches(self.h))
