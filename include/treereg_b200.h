@@ -214,6 +214,20 @@ int trg_register_with_tree(trg_ctx* ctx, const trg_tree_dev* tree, const double*
 int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target, const double* source,
                         size_t n_source, int on_device, const trg_reg_config* cfg,
                         trg_reg_result* out);
+/* Batch of independent frame pairs (BASELINE config C5).  No reference
+ * counterpart: the reference registers one pair per register_clouds call
+ * (registration.hpp:53-55) and a caller loops; this entry point is that
+ * loop.  Pair i registers sources[i] (n_sources[i] points) to targets[i]
+ * with `cfg` and fills out[i] (trace pointers as in trg_reg_result, may be
+ * NULL).  `streams` pairs (1..16; 0 = 4) run concurrently, each on its own
+ * worker thread, CUDA stream and 1/streams of the SMs; results equal
+ * trg_register_clouds on each pair up to rounding (the per-CTA reduction
+ * tree follows the grid size).  Returns TRG_OK or the
+ * status of the lowest-index failing pair (out[] of the others is filled). */
+int trg_register_batch(trg_ctx* ctx, int n_pairs, const double* const* targets,
+                       const size_t* n_targets, const double* const* sources,
+                       const size_t* n_sources, int on_device, const trg_reg_config* cfg,
+                       int streams, trg_reg_result* out);
 
 /* ---- host-side data (synthetic inputs; the reference's generators,
  *      synthetic.cpp / cloud_io.cpp, restated + the new Kinect / LiDAR

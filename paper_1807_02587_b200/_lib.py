@@ -102,6 +102,9 @@ SIGNATURES = {
     "trg_register_with_tree": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int,
                                          C.POINTER(RegConfigC), C.c_double,
                                          C.POINTER(RegResultC)]),
+    "trg_register_batch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                                     C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int,
+                                     C.c_void_p, C.c_int, C.c_void_p]),
     "trg_register_clouds": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                       C.c_size_t, C.c_int, C.POINTER(RegConfigC),
                                       C.POINTER(RegResultC)]),

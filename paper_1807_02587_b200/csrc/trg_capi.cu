@@ -215,6 +215,8 @@ int trg_ctx_create(int device, trg_ctx** out) {
 
 int trg_ctx_destroy(trg_ctx* ctx) {
   if (!ctx) return TRG_OK;
+  for (trg_ctx* w : ctx->workers) trg_ctx_destroy(w);
+  ctx->workers.clear();
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (int i = 0; i < trg_ctx::kSlots; ++i) {

@@ -106,6 +106,7 @@ struct trg_ctx {
   trg_tree_dev* scratch_tree = nullptr;  // reused by register_clouds (no cudaMalloc/cudaFree per call)
   bool build_into_scratch = false;
   bool timeline_pending = false;
+  std::vector<trg_ctx*> workers;  // trg_register_batch: SM-budgeted sub-contexts
   static constexpr int kSlots = 32;
   void* slot_ptr[kSlots] = {};
   size_t slot_size[kSlots] = {};

@@ -489,6 +489,37 @@ def register_clouds(target, source, config: RegistrationConfig = RegistrationCon
     return _result(r, cb, ca, ev)
 
 
+def register_batch(targets, sources, config: RegistrationConfig = RegistrationConfig(),
+                   ctx: Context | None = None, streams: int = 0) -> list:
+    """Independent frame pairs (BASELINE config C5): pair i registers
+    sources[i] to targets[i] exactly as register_clouds would; `streams`
+    pairs run concurrently (0 = library default).  No reference counterpart
+    (the reference loops over register_clouds)."""
+    ctx = ctx or default_context()
+    if len(targets) != len(sources):
+        raise InvalidArgument("register_batch: targets and sources differ in length")
+    n = len(targets)
+    keep, sides = [], set()
+    tp, tn = (C.c_void_p * max(1, n))(), (C.c_size_t * max(1, n))()
+    sp, sn = (C.c_void_p * max(1, n))(), (C.c_size_t * max(1, n))()
+    for i in range(n):
+        pt, nt, dt, k1 = _cloud_ptr(targets[i])
+        ps, ns, ds, k2 = _cloud_ptr(sources[i])
+        keep += [k1, k2]
+        sides |= {dt, ds}
+        tp[i], tn[i], sp[i], sn[i] = pt.value, nt, ps.value, ns
+    if len(sides) > 1:
+        raise InvalidArgument("register_batch: all clouds must live on the same side")
+    bufs = [_result_buffers(config) for _ in range(n)]
+    arr = (RegResultC * max(1, n))()
+    for i, (r, _, _, _) in enumerate(bufs):
+        arr[i] = r
+    cfg = config.c()
+    _chk(_lib.lib().trg_register_batch(ctx.h, n, tp, tn, sp, sn, sides.pop() if sides else 0,
+                                       C.byref(cfg), int(streams), arr))
+    return [_result(arr[i], cb, ca, ev) for i, (_, cb, ca, ev) in enumerate(bufs)]
+
+
 # ------------------------------------------------------------------ inputs
 def synthetic(kind: str, n: int, seed: int) -> np.ndarray:
     """synthetic.cpp generators (bit-identical restatement)."""

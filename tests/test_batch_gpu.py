@@ -1,0 +1,62 @@
+"""trg_register_batch (BASELINE config C5: independent frame pairs run as
+concurrent SM-budgeted registrations) against the reference's own
+register_clouds results (golden fixtures) and against one-pair calls.
+Tolerances as north_star: 1e-4 rad rotation, 1e-4 x extent translation."""
+import numpy as np
+import pytest
+
+from tests.helpers import load_golden, rotation_angle_between
+
+pytestmark = pytest.mark.gpu
+
+L3 = ["scene3k_L3", "kinect4k_L3"]
+
+
+def _tr():
+    from paper_1807_02587_b200 import treereg
+    return treereg
+
+
+@pytest.mark.parametrize("streams", [1, 2, 3])
+def test_batch_matches_reference(ctx, streams):
+    tr = _tr()
+    gs = [load_golden(n) for n in L3] * 2  # 4 pairs, each fixture twice
+    cfg = tr.RegistrationConfig(variant=tr.Variant("adaptive", 3))
+    res = tr.register_batch([g["points"] for g in gs], [g["src"] for g in gs], cfg, ctx, streams)
+    assert len(res) == len(gs)
+    for g, r in zip(gs, res):
+        diag = float(g["reg_meta"][2])
+        assert rotation_angle_between(r.transform.rotation, g["rc_R"]) <= 1e-4
+        assert np.linalg.norm(r.transform.translation - g["rc_t"]) <= 1e-4 * diag
+        assert r.converged == bool(g["rc_meta"][1])
+    # the same pair twice in one batch: same answer to rounding
+    for a, b in zip(res[:2], res[2:]):
+        assert rotation_angle_between(a.transform.rotation, b.transform.rotation) <= 1e-9
+
+
+def test_batch_device_resident_kinect_pairs(ctx):
+    torch = pytest.importorskip("torch")
+    tr = _tr()
+    pairs = [tr.kinect_pair(k) for k in (3, 4, 5)]
+    cfg = tr.RegistrationConfig(variant=tr.Variant("adaptive", 3))
+    tg = [torch.from_numpy(p[0]).cuda() for p in pairs]
+    sr = [torch.from_numpy(p[1]).cuda() for p in pairs]
+    res = tr.register_batch(tg, sr, cfg, ctx, 3)
+    for (t, s, gt), r in zip(pairs, res):
+        one = tr.register_clouds(t, s, cfg, ctx)
+        assert rotation_angle_between(r.transform.rotation, one.transform.rotation) <= 1e-6
+        assert np.abs(r.transform.translation - one.transform.translation).max() <= 1e-7
+        assert r.converged == one.converged and r.iterations == one.iterations
+
+
+def test_batch_errors(ctx):
+    tr = _tr()
+    g = load_golden("scene3k_L3")
+    bad = g["src"].copy()
+    bad[7, 1] = np.nan
+    cfg = tr.RegistrationConfig(variant=tr.Variant("adaptive", 3))
+    with pytest.raises(tr.InvalidArgument, match="pair 1"):
+        tr.register_batch([g["points"]] * 3, [g["src"], bad, g["src"]], cfg, ctx, 2)
+    with pytest.raises(tr.InvalidArgument):
+        tr.register_batch([g["points"]], [g["src"]], cfg, ctx, 17)
+    assert tr.register_batch([], [], cfg, ctx) == []
