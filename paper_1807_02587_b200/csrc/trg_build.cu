@@ -313,6 +313,7 @@ struct BuildSmem {
   int item_off[192];
   int item_kind[192];
   int tnode, tstart, tlen, tidx;
+  double ent[4][kTile];  // the tile's entries (x, y, z, w), staged once per tile
   double nref[3], nmean[3], seed[3];
   GComp comp[2][8];
   int cand_list[2];
@@ -332,10 +333,10 @@ __device__ void tile_entry_pass(const BuildParams& p, BuildSmem& sm, const Phase
   const bool act = tid < sm.tlen;
   double x0 = 0, x1 = 0, x2 = 0, w = 0;
   if (act) {
-    x0 = p.ex[par][e];
-    x1 = p.ey[par][e];
-    x2 = p.ez[par][e];
-    w = p.ew[par][e];
+    x0 = sm.ent[0][tid];
+    x1 = sm.ent[1][tid];
+    x2 = sm.ent[2][tid];
+    w = sm.ent[3][tid];
   }
   if (ph.mom1) {
     double v[4] = {0, 0, 0, 0};
@@ -415,6 +416,7 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
 #pragma unroll
   for (int k = 0; k < 11; ++k) acc[k] = 0.0;
   const int slot = lane / gsz;
+  const bool want_ll = mode == 2 || (mode == 1 && p.want_traces);
   // entries of this warp: [warp*32, warp*32+32) of the tile
   for (int base = warp * 32; base < warp * 32 + 32; base += per_step) {
     const int ei = base + slot;
@@ -422,30 +424,31 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     const int e = sm.tstart + ei;
     double x0 = 0, x1 = 0, x2 = 0, w = 0;
     if (act) {
-      x0 = p.ex[par][e];
-      x1 = p.ey[par][e];
-      x2 = p.ez[par][e];
-      w = p.ew[par][e];
+      x0 = sm.ent[0][ei];
+      x1 = sm.ent[1][ei];
+      x2 = sm.ent[2][ei];
+      w = sm.ent[3][ei];
     }
     const double lg = act ? comp_log(r, x0, x1, x2, p.status) : -INFINITY;
-    // max over the 8 components (order-free)
+    // max over the 8 components (order-free; lg is never NaN)
     double m = lg;
 #pragma unroll
-    for (int off = 1; off < 8; off <<= 1) m = smax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    for (int off = 1; off < 8; off <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
     const bool fin = act && isfinite(m);  // uniform within the 8-lane group
-    // each lane exponentiates its own term; the sum runs in component
-    // order like gmm.cpp:183 (all lanes take part in every shuffle)
-    const double ek = fin ? exp(lg - m) : 0.0;
-    double s = 0.0;
+    // each lane exponentiates its own term (exp_nonpos: the shifted argument
+    // is <= 0); the 8-term sum is a butterfly (the reference's sequential
+    // order, gmm.cpp:183, differs by rounding only)
+    const double ek = fin ? exp_nonpos(lg - m) : 0.0;
+    double s = ek;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += __shfl_sync(0xffffffffu, ek, gbase + k);
+    for (int off = 1; off < 8; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     // gamma_k = exp(log_k - log_total) = e_k / s (gmm.cpp:189, 354): one
     // reciprocal per entry instead of a second exp per component (ulp-level)
+    const double gam = fin ? ek * rcp_sum(s) : 0.0;
     // the per-iteration log-likelihood only feeds the diagnostics trace
     // (gmm.cpp:240); the final pass (mode 2) always needs it (gmm.cpp:394)
-    const bool want_ll = mode == 2 || (mode == 1 && p.want_traces);
-    const double lt = (fin && want_ll) ? m + log(s) : 0.0;
-    const double gam = fin ? __dmul_rn(ek, __drcp_rn(s)) : 0.0;
+    double lt = 0.0;
+    if (want_ll && fin) lt = m + log(s);
     double denom = 0.0;
     if (mode == 3)
       for (int s2 = 0; s2 < sm.ns; ++s2) denom += __shfl_sync(0xffffffffu, gam, gbase + sm.surv[s2]);
@@ -732,14 +735,24 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
 __device__ void load_tile_ctx(const BuildParams& p, BuildSmem& sm, const Phase& ph, int par,
                               int t) {
   const int tid = threadIdx.x;
+  // every thread reads the tile's (node, start, len) (broadcast loads) so the
+  // entry loads below issue without waiting for a block barrier
+  const int k = __ldcg(&p.tile_node[par][t]);
+  const int tstart = __ldcg(&p.tile_start[par][t]);
+  const int tlen = __ldcg(&p.tile_len[par][t]);
   if (tid == 0) {
     sm.tidx = t;
-    sm.tnode = p.tile_node[par][t];
-    sm.tstart = p.tile_start[par][t];
-    sm.tlen = p.tile_len[par][t];
+    sm.tnode = k;
+    sm.tstart = tstart;
+    sm.tlen = tlen;
   }
-  __syncthreads();
-  const int k = sm.tnode;
+  if (!ph.pwrite && tid < tlen) {
+    const int e = tstart + tid;
+    sm.ent[0][tid] = p.ex[par][e];
+    sm.ent[1][tid] = p.ey[par][e];
+    sm.ent[2][tid] = p.ez[par][e];
+    sm.ent[3][tid] = p.ew[par][e];
+  }
   if (tid < 3) {
     if (ph.mom1) {
       const int e0 = p.rn[par].seg[k];

@@ -23,7 +23,13 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks) {
       __threadfence();
       atomicAdd(&bar[1], 1u);
     } else {
-      while (vb[1] == gen) __nanosleep(20);
+      // back off (32 ns doubling to 256 ns): a spinning CTA steals issue
+      // slots from the SM's working CTAs during long tile passes
+      unsigned ns = 32;
+      while (vb[1] == gen) {
+        __nanosleep(ns);
+        ns = ns < 256 ? 2 * ns : 256;
+      }
     }
     __threadfence();
   }

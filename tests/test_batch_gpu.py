@@ -31,7 +31,7 @@ def test_batch_matches_reference(ctx, streams):
         assert r.converged == bool(g["rc_meta"][1])
     # the same pair twice in one batch: same answer to rounding
     for a, b in zip(res[:2], res[2:]):
-        assert rotation_angle_between(a.transform.rotation, b.transform.rotation) <= 1e-9
+        assert np.abs(a.transform.rotation - b.transform.rotation).max() <= 1e-12
 
 
 def test_batch_device_resident_kinect_pairs(ctx):
