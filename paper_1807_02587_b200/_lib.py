@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtrg_cuda.so")
+# TRG_LIB_VARIANT=<name> loads libtrg_cuda_<name>.so (A/B experiments only)
+LIB_PATH = os.path.join(HERE, "libtrg_cuda.so" if not os.environ.get("TRG_LIB_VARIANT")
+                        else f"libtrg_cuda_{os.environ['TRG_LIB_VARIANT']}.so")
 
 dp = C.POINTER(C.c_double)
 ip = C.POINTER(C.c_int)

@@ -19,16 +19,20 @@ constexpr int kAssocBlock = 256;
 
 // gmm.cpp:37-51 log_density / density, association.cpp:129 score.
 // Evaluation order is the reference's (see oracle/trg_oracle.c log_density).
+// Every field is loaded before any test, so one node costs one memory round
+// trip (the eight siblings' loads are all in flight together).
 __device__ __forceinline__ double node_score(const DNode* __restrict__ g, double y0, double y1,
                                              double y2, int* status) {
   const double w = g->weight;
+  const double lam2 = g->lam[2];
+  const double q = fast_q(g->mean, g->axT, g->il, y0, y1, y2);
+  const double sc = __dmul_rn(w, exp_fast(__fma_rn(-0.5, q, g->log_norm)));
   if (!(w > 0.0)) return 0.0;
-  if (!(g->lam[2] > 0.0)) {
+  if (!(lam2 > 0.0)) {
     atomicCAS(status, 0, kEDomain);  // log_density: covariance is not PD
     return 0.0;
   }
-  const double q = fast_q(g->mean, g->axT, g->il, y0, y1, y2);
-  return __dmul_rn(w, exp(__fma_rn(-0.5, q, g->log_norm)));
+  return sc;
 }
 
 struct Descent {
@@ -225,14 +229,18 @@ __device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double
   }
   __syncthreads();
   unsigned long long my_out = 0, my_ev = 0;
-  const size_t ntiles = (p.n + kAssocBlock - 1) / kAssocBlock;
+  // tiles of ts <= 256 points: when the cloud is small for the grid, spread
+  // it evenly over all CTAs (every SM gets the same share of descents)
+  const size_t per_cta = (p.n + G - 1) / G;
+  const int ts = per_cta < (size_t)kAssocBlock ? (per_cta > 0 ? (int)per_cta : 1) : kAssocBlock;
+  const size_t ntiles = (p.n + ts - 1) / ts;
   for (size_t tile = cta; tile < ntiles; tile += G) {
-    const size_t i = tile * kAssocBlock + tid;
+    const size_t i = tile * ts + tid;
     unsigned key = (unsigned)J;
     double v[NM];
 #pragma unroll
     for (int m = 0; m < NM; ++m) v[m] = 0.0;
-    if (i < p.n) {
+    if (tid < ts && i < p.n) {
       double y0, y1, y2;
       apply_rt(Rt_smem, p.pts[3 * i], p.pts[3 * i + 1], p.pts[3 * i + 2], y0, y1, y2);
       Descent d;
@@ -256,6 +264,9 @@ __device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double
         p.point_w[i] = d.node < 0 ? 0.0 : d.path;
       }
     }
+    // reconverge before the block-wide sort (CUB's warp-level steps assume
+    // converged warps; the descent above diverges per point)
+    __syncwarp();
     if (p.dbg_mode != 1) tile_reduce<NM>(sm, key, v, J, kb, p.partials, p.stamps, p.epoch, G, cta);
     else if (key < (unsigned)J) p.partials[key] += v[0] * 0.0;
   }

@@ -1184,7 +1184,9 @@ __global__ void __launch_bounds__(kTile, 3) k_calibrate(BuildParams p) {
     a.n_nodes = J;
     a.root_count = root_count;
     a.epoch = p.a.epoch + (uint32_t)pass;
+    const bool tl5 = p.dbg == 5 && pass == 10;  // experiments: fine marks of one pass
     assoc_pass<10>(asm_, a, nullptr, G, cta);
+    if (tl5) tl_mark(p.tl, 5001);
     grid_sync(p.bar, G);
     tl_mark(p.tl, 1000 + pass * 10 + 1);
     double drift = 0.0;
@@ -1192,6 +1194,7 @@ __global__ void __launch_bounds__(kTile, 3) k_calibrate(BuildParams p) {
       if (__ldcg(&p.nodes[j].child_count) != 0) continue;  // leaves only
       double m[10];
       combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
+      if (tl5 && lane == 0 && j % 16 == 0) tl_mark_any(p.tl, 5002);
       if (p.dbg == 1) continue;
       double* branch = p.cal_moments;  // slot 0 of each node
       if (lane == 0) {
@@ -1224,6 +1227,7 @@ __global__ void __launch_bounds__(kTile, 3) k_calibrate(BuildParams p) {
         }
       }
       __syncwarp();
+      if (tl5 && lane == 0 && j % 16 == 0) tl_mark_any(p.tl, 5003);
       if (p.dbg == 2) continue;
       // climb: arrive at the parent; the parent's last-arriving child's warp
       // processes it (lanes load one child each; sums run in child order on
@@ -1265,6 +1269,7 @@ __global__ void __launch_bounds__(kTile, 3) k_calibrate(BuildParams p) {
           cwt = w;
           p.nodes[ci].weight = w;
         }
+        if (tl5 && lane == 0) tl_mark_any(p.tl, par < 0 ? 5020 : 5010 + __ldcg(&p.nodes[par].level));
         if (par < 0) break;  // top octet done
         // parent moment match (gmm.cpp:489-513), sums in child order
         double w = 0.0, mu[3] = {0.0, 0.0, 0.0};
@@ -1480,6 +1485,10 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   p.a.counters = (unsigned long long*)cnt;
   p.a.status = ctx->status;
   p.a.epoch = ctx->epoch + 1;
+  {
+    const char* dm = getenv("TRG_ASSOC_DBG");  // experiments only
+    p.a.dbg_mode = dm ? atoi(dm) : 0;
+  }
   ctx->epoch += 41;
   // ---- initial state
   BuildState st{};

@@ -17,7 +17,8 @@ int main() {
     double x = -std::ldexp(std::uniform_real_distribution<double>(0, 1)(g), (int)(g() % 12) - 2);
     if (i % 7 == 0) x = -std::uniform_real_distribution<double>(0, 708)(g);
     if (i % 11 == 0) x = -std::uniform_real_distribution<double>(700, 746)(g);
-    const double u = ulps(trg::exp_nonpos(x), std::exp(x));
+    if (i % 13 == 0) x = std::uniform_real_distribution<double>(0, 700)(g);
+    const double u = ulps(trg::exp_fast(x), std::exp(x));
     if (u > worst) { worst = u; wx = x; }
   }
   printf("max ulp %.0f at x=%.17g; exp(0)=%.17g exp(-708)=%g exp(-709)=%g exp(-745)=%g exp(-746)=%g exp(-inf)=%g\n", worst, wx,
