@@ -264,7 +264,7 @@ def run_b200(args):
     prof = os.path.join(ROOT, "profiles", "k_build_dram_bytes.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")  # ncu, same command
         except Exception:
             traffic = None
     out = {
@@ -280,7 +280,7 @@ def run_b200(args):
         "rot_err_deg_vs_gt": rot_err,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_build (tree build + leaf calibration)",
+                     "kernel": "tree build: k_build + k_calibrate (one launch each per step)",
                      "algorithmic_bytes": b_build, "peak_kind": peak_kind,
                      "E_per_round": list(diag.entries_per_round),
                      "calibration_passes": diag.calibration_passes},
