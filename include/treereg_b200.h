@@ -229,6 +229,44 @@ int trg_register_batch(trg_ctx* ctx, int n_pairs, const double* const* targets,
                        const size_t* n_sources, int on_device, const trg_reg_config* cfg,
                        int streams, trg_reg_result* out);
 
+/* ---- point-sharded execution (no reference counterpart:
+ *      the reference is single-process).  A large cloud is split into
+ *      contiguous blocks, one per shard; entries never move between shards.
+ *      Every per-node reduction of the build (phase records), of the leaf
+ *      calibration (leaf moments) and of the EM loop (per-node m0/m1) is
+ *      all-reduced between kernel segments; argmax seeds (heaviest entry,
+ *      farthest points) are all-gathered and resolved to the lowest global
+ *      position.  Every shard then computes the same node updates, so the
+ *      tree and the transform agree across shards without a broadcast.
+ *      Results match the single-GPU path within the north_star tolerances
+ *      (sums regroup across shards). ------------------------------------- */
+typedef struct trg_comm trg_comm;
+/* NCCL unique id (128 bytes) for rank 0 to share with the other ranks. */
+int trg_comm_unique_id(unsigned char id[128]);
+/* One shard per process over NCCL (libnccl.so.2 bound at run time). */
+int trg_comm_create_nccl(trg_ctx* ctx, const unsigned char id[128], int rank, int world,
+                         trg_comm** out);
+/* `shards` (1..16) shards driven by this process on ctx's device, exchanged
+ * by a fixed-order device reduction: the sharded algorithm on one GPU. */
+int trg_comm_create_local(trg_ctx* ctx, int shards, trg_comm** out);
+int trg_comm_destroy(trg_comm* comm);
+int trg_comm_rank(trg_comm* comm);
+int trg_comm_world(trg_comm* comm);
+int trg_comm_local_shards(trg_comm* comm);
+/* build_tree over the union of the shards' clouds: xyz[i] / n[i] for each of
+ * the comm's local shards (one entry in NCCL mode).  Every shard gets the
+ * same tree; *out is the first local shard's (on ctx's device).  diag:
+ * entries_per_round summed over all shards. */
+int trg_build_tree_sharded(trg_comm* comm, const double* const* xyz, const size_t* n,
+                           int on_device, const trg_model_config* cfg, trg_tree_dev** out,
+                           trg_build_diag* diag);
+/* register_clouds over sharded target and source clouds (adaptive:L /
+ * tree:L): sharded build, global bounding-box diagonal, sharded EM. */
+int trg_register_clouds_sharded(trg_comm* comm, const double* const* target,
+                                const size_t* n_target, const double* const* source,
+                                const size_t* n_source, int on_device, const trg_reg_config* cfg,
+                                trg_reg_result* out);
+
 /* ---- host-side data (synthetic inputs; the reference's generators,
  *      synthetic.cpp / cloud_io.cpp, restated + the new Kinect / LiDAR
  *      frame-pair generators of SURVEY.md §8d) -------------------------- */

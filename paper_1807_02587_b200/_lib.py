@@ -104,6 +104,18 @@ SIGNATURES = {
     "trg_register_with_tree": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int,
                                          C.POINTER(RegConfigC), C.c_double,
                                          C.POINTER(RegResultC)]),
+    "trg_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "trg_comm_create_nccl": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "trg_comm_create_local": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "trg_comm_destroy": (C.c_int, [C.c_void_p]),
+    "trg_comm_rank": (C.c_int, [C.c_void_p]),
+    "trg_comm_world": (C.c_int, [C.c_void_p]),
+    "trg_comm_local_shards": (C.c_int, [C.c_void_p]),
+    "trg_build_tree_sharded": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int,
+                                         C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p]),
+    "trg_register_clouds_sharded": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                                              C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int,
+                                              C.c_void_p, C.c_void_p]),
     "trg_register_batch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
                                      C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int,
                                      C.c_void_p, C.c_int, C.c_void_p]),

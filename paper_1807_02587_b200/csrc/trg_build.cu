@@ -85,6 +85,7 @@ struct BuildState {
   int n_exp;
   int lvl_start[9];
   double drift;
+  int cal_done;  // sharded calibration: drift reached the stop test
   unsigned long long cal_evals;
   unsigned long long E_round[8];
   int K_round[8];
@@ -132,6 +133,15 @@ struct BuildParams {
   int* status;
   int dbg;  // experiments only (TRG_BUILD_DBG): 1 = calibration combine only, 2 = + leaf refit
   int want_traces;  // per-iteration log-likelihoods only feed BuildDiagnostics (gmm.cpp:240)
+  // Point-sharded mode (trg_build_tree_sharded): seg >= 0 runs
+  // one segment between two exchange points (k_build: the per-node phase
+  // records; k_calibrate: the leaf moments) and exits; the host all-reduces
+  // nodered (sums) and all-gathers xarg (argmax candidates) between launches.
+  int seg;            // -1: whole build in one launch (single GPU)
+  int n_ranks;        // shards contributing to the exchange
+  double* xarg;       // [Kmax][8] this shard's (score, x, y, z) for wmax and FPS argmax
+  double* xarg_all;   // [n_ranks][Kmax][8] gathered
+  double* xcal;       // [capacity][10] calibration leaf moments (exchanged)
 };
 
 // ----------------------------------------------------------------- helpers
@@ -594,6 +604,35 @@ __device__ void cand_init(const BuildParams& p, int k, int c, const double seed[
   if (comp_set_cov(g, cs, p.nf.floorv[k])) atomicCAS(p.status, 0, kEInval);
 }
 
+// Winner of an argmax field (score, entry index) of node k: its score, and
+// the entry's point in xyz.  Single GPU: straight from the reduced record.
+// Sharded: every shard's candidate (score, x, y, z) was all-gathered into
+// xarg_all; the highest score wins, ties to the lowest shard (shards hold
+// contiguous blocks of the cloud, so this is the lowest global position,
+// like the reference's first-maximum scan).
+__device__ double argmax_point(const BuildParams& p, int par, int k, const double* red, int off,
+                               int slot, double xyz[3]) {
+  if (p.seg < 0) {
+    const int e = (int)__ldcg(red + off + 1);
+    xyz[0] = p.ex[par][e];
+    xyz[1] = p.ey[par][e];
+    xyz[2] = p.ez[par][e];
+    return __ldcg(red + off);
+  }
+  double best = -INFINITY;
+  int br = 0;
+  for (int r = 0; r < p.n_ranks; ++r) {
+    const double sc = __ldcg(p.xarg_all + ((size_t)r * p.Kmax + k) * 8 + 4 * slot);
+    if (sc > best) {
+      best = sc;
+      br = r;
+    }
+  }
+  const double* c = p.xarg_all + ((size_t)br * p.Kmax + k) * 8 + 4 * slot;
+  for (int i = 0; i < 3; ++i) xyz[i] = __ldcg(c + 1 + i);
+  return best;
+}
+
 // Node work after phase ph, done by ONE warp (the warp that reduced the
 // node's last field); `red` is the node's reduced record (global, L2).
 __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, int par,
@@ -604,13 +643,19 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
     const double mass = __ldcg(red + kOffMom1);
     nf.mass[k] = mass;
     if (!(mass > 0.0)) atomicCAS(p.status, 0, kEInval);  // list_moments: no mass
-    for (int i = 0; i < 3; ++i)
-      nf.mean[3 * k + i] = nf.ref[3 * k + i] + __ldcg(red + kOffMom1 + 1 + i) / mass;
-    const int e0 = (int)__ldcg(red + kOffMom1 + 5);
-    nf.wmax_idx[k] = e0;
-    nf.seeds[24 * k + 0] = p.ex[par][e0];
-    nf.seeds[24 * k + 1] = p.ey[par][e0];
-    nf.seeds[24 * k + 2] = p.ez[par][e0];
+    // sharded: a shard without entries in node k never staged its shift
+    // point, so every shard recomputes it (same value everywhere)
+    for (int i = 0; i < 3; ++i) {
+      double r = nf.ref[3 * k + i];
+      if (p.seg >= 0) {
+        const int id = p.rn[par].tree_id[k];
+        r = id >= 0 ? p.nodes[id].mean[i] : 0.0;
+      }
+      nf.mean[3 * k + i] = r + __ldcg(red + kOffMom1 + 1 + i) / mass;
+    }
+    double xyz[3];
+    argmax_point(p, par, k, red, kOffMom1 + 4, 0, xyz);
+    for (int i = 0; i < 3; ++i) nf.seeds[24 * k + i] = xyz[i];
   }
   if (ph.mom2) {
     if (lane == 0) {
@@ -646,15 +691,13 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
     __syncwarp();
   }
   if (ph.fps && lane == 0) {
-    const double bs = __ldcg(red + kOffFps);
+    double xyz[3];
+    const double bs = argmax_point(p, par, k, red, kOffFps, 1, xyz);
     double* sd = nf.seeds + 24 * k;
     if (!(bs > 0.0)) {  // degenerate support: duplicate seed 0 (gmm.cpp:291-294)
       for (int i = 0; i < 3; ++i) sd[3 * ph.fps + i] = sd[i];
     } else {
-      const int e = (int)__ldcg(red + kOffFps + 1);
-      sd[3 * ph.fps + 0] = p.ex[par][e];
-      sd[3 * ph.fps + 1] = p.ey[par][e];
-      sd[3 * ph.fps + 2] = p.ez[par][e];
+      for (int i = 0; i < 3; ++i) sd[3 * ph.fps + i] = xyz[i];
     }
   }
   __syncwarp();
@@ -755,8 +798,16 @@ __device__ void load_tile_ctx(const BuildParams& p, BuildSmem& sm, const Phase& 
   }
   if (tid < 3) {
     if (ph.mom1) {
-      const int e0 = p.rn[par].seg[k];
-      const double v = tid == 0 ? p.ex[par][e0] : (tid == 1 ? p.ey[par][e0] : p.ez[par][e0]);
+      // list_moments' shift point: the node's first entry (gmm.cpp); sharded,
+      // a point every shard knows: the node's fitted mean (0 for the root)
+      double v;
+      if (p.seg < 0) {
+        const int e0 = p.rn[par].seg[k];
+        v = tid == 0 ? p.ex[par][e0] : (tid == 1 ? p.ey[par][e0] : p.ez[par][e0]);
+      } else {
+        const int id = p.rn[par].tree_id[k];
+        v = id >= 0 ? p.nodes[id].mean[tid] : 0.0;
+      }
       sm.nref[tid] = v;
       p.nf.ref[3 * k + tid] = v;
     }
@@ -1076,12 +1127,40 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
 }
 
 
+// Writes this shard's argmax candidates of the phase (score + the entry's
+// point) for the all-gather (sharded mode).
+__device__ void write_xarg(const BuildParams& p, const Phase& ph, int par, int K) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int k = gt; k < K; k += nt) {
+    const double* red = p.nodered + (size_t)k * kRec;
+    double* o = p.xarg + (size_t)k * 8;
+    for (int slot = 0; slot < 2; ++slot) {
+      const bool on = slot == 0 ? ph.mom1 : ph.fps != 0;
+      if (!on) continue;
+      const int off = slot == 0 ? kOffMom1 + 4 : kOffFps;
+      const double sc = __ldcg(red + off), ix = __ldcg(red + off + 1);
+      const bool valid = sc > -INFINITY && ix < 1e299;
+      const int e = valid ? (int)ix : 0;
+      o[4 * slot] = valid ? sc : -INFINITY;
+      o[4 * slot + 1] = valid ? p.ex[par][e] : 0.0;
+      o[4 * slot + 2] = valid ? p.ey[par][e] : 0.0;
+      o[4 * slot + 3] = valid ? p.ez[par][e] : 0.0;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
   __shared__ BuildSmem sm;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   BuildState* st = p.st;
+  const bool sharded = p.seg >= 0;
+  if (sharded && (__ldcg(&st->done) || __ldcg(&st->status_overflow))) return;
   tl_mark(p.tl, -1);
+  // Sharded segments: exchange point xp = the per-node reduction of a phase.
+  // Segment q finishes exchange point q-1 (node updates from the all-reduced
+  // record) and runs up to and including the reduction of exchange point q.
+  int xp = 0;
   // ------------------------------------------------ expansion rounds
   for (int round = 0; round < p.L; ++round) {
     const int par = round & 1;
@@ -1092,54 +1171,95 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
       if (!(ph.mom1 || ph.mom2 || ph.fps || ph.mode[0] || ph.mode[1] || ph.pcount || ph.layout ||
             ph.pwrite))
         continue;
+      const bool mine = !sharded || xp == p.seg;  // this launch runs the phase's work
       if (ph.layout) {
-        if (cta == 0) round_layout(p, par, round, p.layout_scratch);
-        grid_sync(p.bar, G);
-        tl_mark(p.tl, round * 100 + ph_i);
+        if (mine) {
+          if (cta == 0) round_layout(p, par, round, p.layout_scratch);
+          grid_sync(p.bar, G);
+          tl_mark(p.tl, round * 100 + ph_i);
+        }
         continue;
       }
-      // (a) tile pass
-      const int T = __ldcg(&st->Tp[par]);
-      for (int t = cta; t < T; t += G) {
-        load_tile_ctx(p, sm, ph, par, t);
-        if (ph.pwrite) {
-          tile_pwrite(p, sm, par, t);
-        } else {
+      if (ph.pwrite) {
+        if (mine) {
+          const int T = __ldcg(&st->Tp[par]);
+          for (int t = cta; t < T; t += G) {
+            load_tile_ctx(p, sm, ph, par, t);
+            tile_pwrite(p, sm, par, t);
+            __syncthreads();
+          }
+          grid_sync(p.bar, G);
+          tl_mark(p.tl, round * 100 + ph_i);
+        }
+        continue;
+      }
+      if (mine) {
+        // (a) tile pass
+        const int T = __ldcg(&st->Tp[par]);
+        for (int t = cta; t < T; t += G) {
+          load_tile_ctx(p, sm, ph, par, t);
           double* rec = p.partial + (size_t)t * kRec;
           tile_entry_pass(p, sm, ph, par, rec);
           if (ph.mode[0] || ph.mode[1]) tile_comp_pass(p, sm, ph, par, rec, false);
           if (ph.pcount) tile_comp_pass(p, sm, ph, par, rec, true);
+          __syncthreads();
         }
+        grid_sync(p.bar, G);
+        tl_mark(p.tl, round * 100 + ph_i);
+        // (b) per-node reduction of the tile records (+ node update when the
+        // whole cloud is here)
+        if (tid == 0) sm.nitems = phase_items(ph, sm.item_off, sm.item_kind);
         __syncthreads();
-      }
-      grid_sync(p.bar, G);
-      tl_mark(p.tl, round * 100 + ph_i);
-      if (ph.pwrite) continue;
-      // (b) per-node reduction of the tile records + node update
-      if (tid == 0) sm.nitems = phase_items(ph, sm.item_off, sm.item_kind);
-      __syncthreads();
-      const int NI = sm.nitems;
-      const int K = __ldcg(&st->Kp[par]);
-      for (int it = cta * (kTile / 32) + warp; it < K * NI; it += G * (kTile / 32)) {
-        const int k = it / NI, f = it % NI;
-        reduce_item(p, par, k, sm.item_off[f], sm.item_kind[f]);
-        unsigned last = 0;
-        if (lane == 0) {
-          __threadfence();
-          last = (atomicAdd(&p.fdone[k], 1u) == (unsigned)NI - 1) ? 1u : 0u;
-          if (last) {
-            p.fdone[k] = 0u;
+        const int NI = sm.nitems;
+        const int K = __ldcg(&st->Kp[par]);
+        for (int it = cta * (kTile / 32) + warp; it < K * NI; it += G * (kTile / 32)) {
+          const int k = it / NI, f = it % NI;
+          reduce_item(p, par, k, sm.item_off[f], sm.item_kind[f]);
+          if (sharded) continue;
+          unsigned last = 0;
+          if (lane == 0) {
             __threadfence();
+            last = (atomicAdd(&p.fdone[k], 1u) == (unsigned)NI - 1) ? 1u : 0u;
+            if (last) {
+              p.fdone[k] = 0u;
+              __threadfence();
+            }
           }
+          last = __shfl_sync(0xffffffffu, last, 0);
+          if (last) node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
         }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
+        if (sharded) {
+          grid_sync(p.bar, G);
+          if (ph.mom1 || ph.fps) write_xarg(p, ph, par, K);
+          return;  // exchange point: the host all-reduces nodered / gathers xarg
+        }
+        grid_sync(p.bar, G);
+        tl_mark(p.tl, round * 100 + 50 + ph_i);
+      } else if (xp == p.seg - 1) {
+        // node updates of the previous segment's exchange point, from the
+        // all-reduced records (every shard computes the same)
+        const int K = __ldcg(&st->Kp[par]);
+        for (int k = cta * (kTile / 32) + warp; k < K; k += G * (kTile / 32))
+          node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
+        grid_sync(p.bar, G);
       }
-      grid_sync(p.bar, G);
-      tl_mark(p.tl, round * 100 + 50 + ph_i);
+      ++xp;
     }
     if (__ldcg(&st->done) || __ldcg(&st->status_overflow)) break;
   }
+}
+
+// Number of exchange points of a sharded build of depth L (k_build runs
+// L * this + 1 segments).
+inline int build_exchange_points_per_round(int em_iters) {
+  int n = 0;
+  for (int ph_i = 0; ph_i < em_iters + 12; ++ph_i) {
+    // mirrors phase_of: every phase but layout and partition write reduces
+    const int I = em_iters;
+    const bool layout = ph_i == I + 10, pwrite = ph_i == I + 11;
+    if (!layout && !pwrite) ++n;
+  }
+  return n;
 }
 
 // Second persistent kernel of the build (launched right behind k_build on
@@ -1151,20 +1271,24 @@ __global__ void __launch_bounds__(kTile, 3) k_calibrate(BuildParams p) {
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   BuildState* st = p.st;
+  const bool sharded = p.seg >= 0;
   if (__ldcg(&st->status_overflow)) return;
+  if (sharded && __ldcg(&st->cal_done)) return;
   const int J = __ldcg(&st->J);
   __shared__ int lvl[9];
   if (tid < 9) lvl[tid] = __ldcg(&st->lvl_start[tid]);
   __syncthreads();
   // ------------------------------------------------ rematch + refresh_eig
-  tl_mark(p.tl, 900);
-  if (cta == 0) reset_parents(p, lvl);
-  grid_sync(p.bar, G);
-  tl_mark(p.tl, 901);
-  for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x)
-    if (refresh_node(p.nodes[j], p.cov + 9 * (size_t)j)) atomicCAS(p.status, 0, kEInval);
-  grid_sync(p.bar, G);
-  tl_mark(p.tl, 902);
+  if (!sharded || p.seg == 0) {
+    tl_mark(p.tl, 900);
+    if (cta == 0) reset_parents(p, lvl);
+    grid_sync(p.bar, G);
+    tl_mark(p.tl, 901);
+    for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x)
+      if (refresh_node(p.nodes[j], p.cov + 9 * (size_t)j)) atomicCAS(p.status, 0, kEInval);
+    grid_sync(p.bar, G);
+    tl_mark(p.tl, 902);
+  }
   // ------------------------------------------------ leaf calibration
   // calibrate_pass (gmm.cpp:523-580) per pass: association at identity with
   // m2 (stage 1); then leaf refits and the whole bottom-up tree update
@@ -1173,27 +1297,53 @@ __global__ void __launch_bounds__(kTile, 3) k_calibrate(BuildParams p) {
   // parent; the parent's last-arriving child processes the parent and climbs
   // on.  Every node is updated from the same inputs, in the same order, as
   // the reference's level loops.  2 grid barriers per pass.
+  // Sharded (p.seg >= 0): segment s runs stage 2 of pass s-1 (from the
+  // all-reduced leaf moments in xcal) and stage 1 of pass s up to the local
+  // leaf combine, then exits for the exchange.
   const int root_count = lvl[1] - lvl[0];
   for (int pass = 0; pass < 40; ++pass) {
-    if (pass > 0) {
-      const double dprev = __longlong_as_double((long long)__ldcg(&p.drift_bits[(pass - 1) & 1]));
-      if (!(dprev > 1e-13)) break;  // gmm.cpp:652
-    }
-    if (cta == 0 && tid == 0) p.drift_bits[pass & 1] = 0ull;
+    const bool run_s1 = !sharded || p.seg == pass;
+    const bool run_s2 = !sharded || p.seg == pass + 1;
+    if (!run_s1 && !run_s2) continue;
     AssocParams a = p.a;
     a.n_nodes = J;
     a.root_count = root_count;
     a.epoch = p.a.epoch + (uint32_t)pass;
     const bool tl5 = p.dbg == 5 && pass == 10;  // experiments: fine marks of one pass
-    assoc_pass<10>(asm_, a, nullptr, G, cta);
-    if (tl5) tl_mark(p.tl, 5001);
-    grid_sync(p.bar, G);
-    tl_mark(p.tl, 1000 + pass * 10 + 1);
+    if (run_s1) {
+      if (pass > 0) {
+        const double dprev = __longlong_as_double((long long)__ldcg(&p.drift_bits[(pass - 1) & 1]));
+        if (!(dprev > 1e-13)) {  // gmm.cpp:652
+          if (sharded && cta == 0 && tid == 0) st->cal_done = 1;
+          break;
+        }
+      }
+      if (cta == 0 && tid == 0) p.drift_bits[pass & 1] = 0ull;
+      assoc_pass<10>(asm_, a, nullptr, G, cta);
+      if (tl5) tl_mark(p.tl, 5001);
+      grid_sync(p.bar, G);
+      tl_mark(p.tl, 1000 + pass * 10 + 1);
+      if (sharded) {
+        // this shard's leaf moments, for the all-reduce
+        for (int j = cta * (kTile / 32) + warp; j < J; j += G * (kTile / 32)) {
+          if (__ldcg(&p.nodes[j].child_count) != 0) continue;
+          double m[10];
+          combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
+          if (lane == 0)
+            for (int q = 0; q < 10; ++q) p.xcal[(size_t)j * 10 + q] = m[q];
+        }
+        return;
+      }
+    }
     double drift = 0.0;
     for (int j = cta * (kTile / 32) + warp; j < J; j += G * (kTile / 32)) {
       if (__ldcg(&p.nodes[j].child_count) != 0) continue;  // leaves only
       double m[10];
-      combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
+      if (sharded) {
+        for (int q = 0; q < 10; ++q) m[q] = __ldcg(p.xcal + (size_t)j * 10 + q);
+      } else {
+        combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
+      }
       if (tl5 && lane == 0 && j % 16 == 0) tl_mark_any(p.tl, 5002);
       if (p.dbg == 1) continue;
       double* branch = p.cal_moments;  // slot 0 of each node
@@ -1351,9 +1501,18 @@ struct BuildAlloc {
   int Kmax, Tmax, Emax;
 };
 
-int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config* cfg,
-              BuildAlloc al, trg_tree_dev** out, trg_build_diag* diag, bool* overflow,
-              BuildAlloc* need) {
+struct BuildJob {
+  BuildParams p;
+  trg_tree_dev* tree = nullptr;
+  int G = 0, Gc = 0;
+  BuildAlloc al;
+};
+
+// Everything up to the persistent launches: arena, parameters, initial
+// state, entry buffer (k_init_entries).  `world` > 0 adds the sharded
+// exchange buffers (seg mode) for that many shards.
+int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config* cfg,
+                  BuildAlloc al, trg_build_diag* diag, int world, BuildJob* job) {
   const int L = cfg->max_level;
   const int cap = trg_tree_capacity(L);
   BuildParams p{};
@@ -1404,6 +1563,9 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   const int G = persistent_grid(ctx, (const void*)k_build, kTile, 0);
   const int Gc = persistent_grid(ctx, (const void*)k_calibrate, kTile, 0);
   const size_t o_cd = carve(sizeof(double) * std::max(G, Gc));
+  const int W = std::max(world, 1);
+  const size_t o_xa = carve(sizeof(double) * 8 * K), o_xaa = carve(sizeof(double) * 8 * K * W),
+               o_xc = carve(sizeof(double) * 10 * (size_t)cap);
   void* arena = nullptr;
   TRG_TRY(ws_get(ctx, kSlotBuild0, off, &arena));
   char* A = static_cast<char*>(arena);
@@ -1456,6 +1618,11 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   p.cta_drift = (double*)(A + o_cd);
   p.status = ctx->status;
   p.tl = ctx->dev_timeline;
+  p.seg = world > 0 ? 0 : -1;
+  p.n_ranks = W;
+  p.xarg = (double*)(A + o_xa);
+  p.xarg_all = (double*)(A + o_xaa);
+  p.xcal = (double*)(A + o_xc);
   {
     const char* dbg = getenv("TRG_BUILD_DBG");
     p.dbg = dbg ? atoi(dbg) : 0;
@@ -1511,15 +1678,40 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   k_init_entries<<<256, 256, 0, ctx->stream>>>(pts, n, p.ex[0], p.ey[0], p.ez[0], p.ew[0],
                                                p.tile_node[0], p.tile_start[0], p.tile_len[0],
                                                ctx->status);
-  void* args[] = {&p};
-  TRG_CU(launch_persistent(ctx, (const void*)k_build, G, kTile, args));
-  {
-    BuildParams pc = p;  // same buffers; calibration grid sized for k_calibrate
-    pc.a.partials = p.a.partials;
-    void* cargs[] = {&pc};
-    TRG_CU(launch_persistent(ctx, (const void*)k_calibrate, Gc, kTile, cargs));
-  }
-  ctx->launches += 3;
+  ctx->launches += 1;
+  job->p = p;
+  job->tree = tree;
+  job->G = G;
+  job->Gc = Gc;
+  job->al = al;
+  return TRG_OK;
+}
+
+// One k_build launch (seg = -1: the whole build; else one sharded segment).
+int build_launch(trg_ctx* ctx, BuildJob* job, int seg) {
+  job->p.seg = seg;
+  void* args[] = {&job->p};
+  TRG_CU(launch_persistent(ctx, (const void*)k_build, job->G, kTile, args));
+  ctx->launches += 1;
+  return TRG_OK;
+}
+
+int calibrate_launch(trg_ctx* ctx, BuildJob* job, int seg) {
+  job->p.seg = seg;
+  void* args[] = {&job->p};
+  TRG_CU(launch_persistent(ctx, (const void*)k_calibrate, job->Gc, kTile, args));
+  ctx->launches += 1;
+  return TRG_OK;
+}
+
+// Reads the build state back, checks status / overflow, fills diagnostics.
+int build_collect(trg_ctx* ctx, BuildJob* job, const trg_model_config* cfg, trg_tree_dev** out,
+                  trg_build_diag* diag, bool* overflow, BuildAlloc* need) {
+  BuildParams& p = job->p;
+  trg_tree_dev* tree = job->tree;
+  const BuildAlloc al = job->al;
+  const int L = cfg->max_level;
+  BuildState st{};
   TRG_CU(trg_memcpy(ctx, &st, p.st, sizeof st, cudaMemcpyDeviceToHost));
   int rc = check_status(ctx, "build_tree");
   if (rc == TRG_OK && st.status_overflow) {
@@ -1565,12 +1757,22 @@ int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config*
   return TRG_OK;
 }
 
-}  // namespace
+int run_build(trg_ctx* ctx, const double* pts, size_t n, const trg_model_config* cfg,
+              BuildAlloc al, trg_tree_dev** out, trg_build_diag* diag, bool* overflow,
+              BuildAlloc* need) {
+  BuildJob job;
+  TRG_TRY(build_prepare(ctx, pts, n, cfg, al, diag, 0, &job));
+  TRG_TRY(build_launch(ctx, &job, -1));
+  TRG_TRY(calibrate_launch(ctx, &job, -1));
+  return build_collect(ctx, &job, cfg, out, diag, overflow, need);
+}
 
-extern "C" int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz_on_device,
-                              const trg_model_config* cfg, trg_tree_dev** out,
-                              trg_build_diag* diag) {
-  // validate_config gmm.cpp:465-477, validate_cloud :479-484
+// validate_config gmm.cpp:465-477
+int validate_model_config(const trg_model_config* cfg) {
+  if (!cfg) {
+    set_error("model config is null");
+    return TRG_EINVAL;
+  }
   if (cfg->max_level < 1) {
     set_error("max_level must be >= 1");
     return TRG_EINVAL;
@@ -1591,6 +1793,35 @@ extern "C" int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz
     set_error("covariance regularization must be positive");
     return TRG_EINVAL;
   }
+  return TRG_OK;
+}
+
+// Initial entry-buffer capacity: soft-partition growth is data dependent
+// (E_l/E_{l-1} ~2.5-5 on surfaces, at most 8).  Start from the largest ratio
+// this context has seen (initially 12 x N for L >= 3) so repeated builds never
+// take the overflow-and-retry path.
+BuildAlloc initial_alloc(trg_ctx* ctx, size_t n, int L) {
+  int kmax = 1;
+  for (int l = 0; l + 1 < L; ++l) kmax *= 8;
+  BuildAlloc al;
+  al.Kmax = std::max(1, kmax);
+  const double ratio = std::max(ctx->build_growth, L >= 3 ? 12.0 : (L == 2 ? 8.0 : 1.0));
+  al.Emax = (int)std::min<double>((double)INT32_MAX / 16, ratio * (double)n + 1024.0);
+  al.Tmax = al.Emax / kTile + al.Kmax + 8;
+  return al;
+}
+
+}  // namespace
+
+namespace trg {
+int check_model_config(const trg_model_config* cfg) { return validate_model_config(cfg); }
+}  // namespace trg
+
+extern "C" int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz_on_device,
+                              const trg_model_config* cfg, trg_tree_dev** out,
+                              trg_build_diag* diag) {
+  // validate_config gmm.cpp:465-477, validate_cloud :479-484
+  TRG_TRY(validate_model_config(cfg));
   if (n == 0 || !xyz) {
     set_error("point cloud is empty");
     return TRG_EINVAL;
@@ -1602,18 +1833,7 @@ extern "C" int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz
   TRG_CU(cudaSetDevice(ctx->device));
   const double* dev = nullptr;
   TRG_TRY(stage_points_public(ctx, xyz, n, xyz_on_device, kSlotPoints, &dev));
-  const int L = cfg->max_level;
-  int kmax = 1;
-  for (int l = 0; l + 1 < L; ++l) kmax *= 8;
-  // Entry-buffer capacity: soft-partition growth is data dependent (E_l/E_{l-1}
-  // ~2.5-5 on surfaces, at most 8).  Start from the largest ratio this
-  // context has seen (initially 12 x N for L >= 3) so repeated builds never
-  // take the overflow-and-retry path.
-  BuildAlloc al;
-  al.Kmax = std::max(1, kmax);
-  const double ratio = std::max(ctx->build_growth, L >= 3 ? 12.0 : (L == 2 ? 8.0 : 1.0));
-  al.Emax = (int)std::min<double>((double)INT32_MAX / 16, ratio * (double)n + 1024.0);
-  al.Tmax = al.Emax / kTile + al.Kmax + 8;
+  BuildAlloc al = initial_alloc(ctx, n, cfg->max_level);
   for (int attempt = 0; attempt < 4; ++attempt) {
     bool overflow = false;
     BuildAlloc need = al;
@@ -1630,4 +1850,136 @@ extern "C" int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz
   }
   set_error("build_tree: entry buffer growth did not converge");
   return TRG_ERUNTIME;
+}
+
+// ------------------------------------------------------------ sharded build
+namespace trg {
+
+// The segmented build over a comm's shards (device-resident clouds, one per
+// local shard).  trees[i] receives shard i's (identical) tree.
+int build_sharded_dev(trg_comm* c, const double* const* dev, const size_t* n,
+                      const trg_model_config* cfg, trg_tree_dev** trees, trg_build_diag* diag) {
+  const int S = c->local;
+  const int L = cfg->max_level;
+  std::vector<BuildAlloc> al(S);
+  for (int i = 0; i < S; ++i) al[i] = initial_alloc(c->shard_ctx[i], std::max<size_t>(n[i], 1), L);
+  const int XP = cfg->em_iterations_per_node + 10;  // exchange points per round
+  const int nseg = L * XP + 1;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    std::vector<BuildJob> job(S);
+    for (int i = 0; i < S; ++i)
+      TRG_TRY(build_prepare(c->shard_ctx[i], dev[i], n[i], cfg, al[i], i == 0 ? diag : nullptr,
+                            c->world, &job[i]));
+    std::vector<double*> red(S), xa(S), xaa(S), xc(S);
+    for (int i = 0; i < S; ++i) {
+      red[i] = job[i].p.nodered;
+      xa[i] = job[i].p.xarg;
+      xaa[i] = job[i].p.xarg_all;
+      xc[i] = job[i].p.xcal;
+    }
+    const size_t kmax = (size_t)job[0].p.Kmax;
+    for (int q = 0; q < nseg; ++q) {
+      for (int i = 0; i < S; ++i) TRG_TRY(build_launch(c->shard_ctx[i], &job[i], q));
+      if (q + 1 == nseg) break;
+      TRG_TRY(comm_allreduce_sum(c, red.data(), kmax * kRec));
+      if (q % XP <= 7) TRG_TRY(comm_allgather(c, xa.data(), xaa.data(), kmax * 8));  // mom1 / FPS
+    }
+    const size_t cap = (size_t)job[0].p.capacity;
+    for (int s = 0; s <= 40; ++s) {
+      for (int i = 0; i < S; ++i) TRG_TRY(calibrate_launch(c->shard_ctx[i], &job[i], s));
+      if (s < 40) TRG_TRY(comm_allreduce_sum(c, xc.data(), cap * 10));
+    }
+    // consensus on errors / overflow (a shard that overflowed stopped early,
+    // so the others' results are void too)
+    std::vector<double> v((size_t)S * 6, 0.0);
+    std::vector<int> rc(S);
+    std::vector<bool> ovf(S);
+    std::vector<BuildAlloc> need(S);
+    std::vector<unsigned long long> eround((size_t)S * 8, 0);
+    for (int i = 0; i < S; ++i) {
+      bool o = false;
+      need[i] = al[i];
+      trg_build_diag d{};
+      rc[i] = build_collect(c->shard_ctx[i], &job[i], cfg, &trees[i], i == 0 ? diag : &d, &o,
+                            &need[i]);
+      const trg_build_diag& di = i == 0 && diag ? *diag : d;
+      for (int r = 0; r < 8; ++r) eround[(size_t)i * 8 + r] = di.entries_per_round[r];
+      ovf[i] = o;
+      v[(size_t)i * 6 + 0] = o ? 1.0 : 0.0;
+      v[(size_t)i * 6 + 1] = rc[i] != TRG_OK ? (double)rc[i] : 0.0;
+      v[(size_t)i * 6 + 2] = (double)need[i].Emax / (double)std::max<size_t>(n[i], 1);
+      v[(size_t)i * 6 + 3] = (double)need[i].Kmax;
+    }
+    TRG_TRY(comm_host_reduce(c, v.data(), 6, 1));
+    const bool any_ovf = v[0] > 0.0;
+    if (!any_ovf && v[1] > 0.0) {
+      int mine = TRG_OK;
+      for (int i = 0; i < S; ++i)
+        if (rc[i] != TRG_OK) mine = rc[i];
+      for (int i = 0; i < S; ++i)
+        if (rc[i] == TRG_OK && trees[i]) trg_tree_free(c->shard_ctx[i], trees[i]);
+      if (mine == TRG_OK) {
+        set_error("build_tree (sharded): another shard failed");
+        return (int)v[1];
+      }
+      return mine;
+    }
+    if (!any_ovf) {
+      if (diag) {
+        std::vector<double> e((size_t)S * 8);
+        for (size_t k = 0; k < e.size(); ++k) e[k] = (double)eround[k];
+        TRG_TRY(comm_host_reduce(c, e.data(), 8, 0));
+        for (int r = 0; r < 8; ++r) diag->entries_per_round[r] = (unsigned long long)e[r];
+      }
+      return TRG_OK;
+    }
+    for (int i = 0; i < S; ++i) {
+      if (!ovf[i] && rc[i] == TRG_OK && trees[i]) trg_tree_free(c->shard_ctx[i], trees[i]);
+      trees[i] = nullptr;
+      trg_ctx* cx = c->shard_ctx[i];
+      const double ratio = std::max(v[2], (double)need[i].Emax / (double)std::max<size_t>(n[i], 1));
+      cx->build_growth = std::max(cx->build_growth, 1.25 * ratio);
+      al[i].Emax = (int)std::min<double>((double)INT32_MAX / 16,
+                                         std::max<double>(2.0 * al[i].Emax, 1.25 * ratio * (double)n[i] + 1024.0));
+      al[i].Kmax = std::max(al[i].Kmax, (int)v[3]);
+      al[i].Tmax = al[i].Emax / kTile + al[i].Kmax + 8;
+    }
+  }
+  set_error("build_tree (sharded): entry buffer growth did not converge");
+  return TRG_ERUNTIME;
+}
+
+}  // namespace trg
+
+extern "C" int trg_build_tree_sharded(trg_comm* comm, const double* const* xyz, const size_t* n,
+                                      int on_device, const trg_model_config* cfg,
+                                      trg_tree_dev** out, trg_build_diag* diag) {
+  if (!comm || !xyz || !n || !out) {
+    set_error("build_tree_sharded: bad argument");
+    return TRG_EINVAL;
+  }
+  TRG_TRY(validate_model_config(cfg));
+  const int S = comm->local;
+  std::vector<double> tot((size_t)S, 0.0);
+  for (int i = 0; i < S; ++i) {
+    if (n[i] > (size_t)INT32_MAX / 8) {
+      set_error("point cloud too large for int32 entry indexing");
+      return TRG_EINVAL;
+    }
+    tot[i] = (double)n[i];
+  }
+  TRG_TRY(comm_host_reduce(comm, tot.data(), 1, 0));
+  if (!(tot[0] > 0.0)) {
+    set_error("point cloud is empty");
+    return TRG_EINVAL;
+  }
+  TRG_CU(cudaSetDevice(comm->ctx->device));
+  std::vector<const double*> dev(S);
+  for (int i = 0; i < S; ++i)
+    TRG_TRY(stage_points_public(comm->shard_ctx[i], xyz[i], n[i], on_device, kSlotPoints, &dev[i]));
+  std::vector<trg_tree_dev*> trees(S, nullptr);
+  TRG_TRY(build_sharded_dev(comm, dev.data(), n, cfg, trees.data(), diag));
+  for (int i = 1; i < S; ++i) trg_tree_free(comm->shard_ctx[i], trees[i]);
+  *out = trees[0];
+  return TRG_OK;
 }

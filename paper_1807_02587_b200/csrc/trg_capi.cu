@@ -229,7 +229,7 @@ int trg_ctx_destroy(trg_ctx* ctx) {
   }
   cudaFree(ctx->status);
   cudaFree(ctx->dev_timeline);
-  cudaStreamDestroy(ctx->stream);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TRG_OK;
 }

@@ -31,6 +31,12 @@ struct EmParams {
   double rot_tol;
   uint32_t epoch0;
   Timeline* tl;
+  // Point-sharded mode: seg = it >= 0 finishes iteration it-1
+  // from the all-reduced moments in xmom ([J][4] + evals, outliers) and runs
+  // the E-step of iteration it up to the local per-node combine, then exits.
+  int seg;
+  double* xmom;
+  double n_total;  // total source points over all shards (mass floor)
 };
 
 constexpr int kAccStride = kNormalEq + 2;
@@ -53,31 +59,58 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
   const int lane = tid & 31, warp = tid >> 5;
   const int J = p.a.n_nodes;
   const int P2 = min(G, (J + (kAssocBlock / 32) - 1) / (kAssocBlock / 32));  // producer CTAs
-  const double n_total = (double)p.a.n;
+  const bool sharded = p.seg >= 0;
+  const double n_total = sharded ? p.n_total : (double)p.a.n;
   if (tid < 12) rt[tid] = ldcg(&p.st->Rt[tid]);
   if (tid == 0) {
-    s_done = 0;
-    s_fails = 0;
-    s_conv = 0;
-    s_iters = 0;
+    s_done = sharded ? *(volatile int*)&p.st->done : 0;
+    s_fails = sharded ? *(volatile int*)&p.st->fails : 0;
+    s_conv = sharded ? *(volatile int*)&p.st->converged : 0;
+    s_iters = sharded ? *(volatile int*)&p.st->iterations : 0;
   }
   __syncthreads();
+  if (s_done) return;
   const double trans_limit = ldcg(&p.st->trans_limit);
   for (int it = 0; it < p.max_iters; ++it) {
-    // ---- P1: E-step over this CTA's point tiles
+    const bool run_e = !sharded || p.seg == it;      // E-step of iteration it
+    const bool run_m = !sharded || p.seg == it + 1;  // combine/solve of iteration it
+    if (!run_e && !run_m) continue;
     AssocParams a = p.a;
     a.epoch = p.epoch0 + (uint32_t)it;
-    tl_mark(p.tl, 2000 + it * 10);
-    assoc_pass<4>(sm, a, rt, G, cta);
-    grid_sync(p.bar, G);
-    tl_mark(p.tl, 2000 + it * 10 + 1);
+    if (run_e) {
+      // ---- P1: E-step over this CTA's point tiles
+      tl_mark(p.tl, 2000 + it * 10);
+      assoc_pass<4>(sm, a, rt, G, cta);
+      grid_sync(p.bar, G);
+      tl_mark(p.tl, 2000 + it * 10 + 1);
+      if (sharded) {
+        // this shard's per-node moments + counters, for the all-reduce
+        for (int j = cta * (kAssocBlock / 32) + warp; j < J; j += G * (kAssocBlock / 32)) {
+          double m[4];
+          combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
+          if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) p.xmom[(size_t)j * 4 + k] = m[k];
+        }
+        if (cta == 0 && tid == 0) {
+          p.xmom[(size_t)J * 4] = (double)atomicExch(&a.counters[1], 0ull);
+          p.xmom[(size_t)J * 4 + 1] = (double)atomicExch(&a.counters[0], 0ull);
+        }
+        return;
+      }
+    }
     // ---- P2: per-node combine over CTAs + virtual-point rows
     if (cta < P2) {
       SolveAcc acc;
       acc_zero(acc);
       for (int j = cta * (kAssocBlock / 32) + warp; j < J; j += P2 * (kAssocBlock / 32)) {
         double m[4];
-        combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
+        if (sharded) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) m[k] = ldcg(p.xmom + (size_t)j * 4 + k);
+        } else {
+          combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
+        }
         if (lane == 0) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) p.moments[(size_t)j * 4 + k] = m[k];
@@ -128,7 +161,8 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
       }
       c = block_sum(c, ss);
       if (tid == 0) {
-        p.evals[it] = atomicExch(&a.counters[1], 0ull);
+        p.evals[it] = sharded ? (unsigned long long)ldcg(p.xmom + (size_t)J * 4)
+                              : atomicExch(&a.counters[1], 0ull);
         p.crit_before[it] = so.crit_before;
         p.crit_after[it] = so.degenerate ? so.crit_before : c;
       }
@@ -169,9 +203,22 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
       }
     }
     __syncthreads();
+    if (sharded) {
+      // the running state crosses the launch boundary through EmState
+      if (cta == 0 && tid == 0) {
+        EmState* st = p.st;
+        for (int k = 0; k < 12; ++k) st->Rt[k] = rt[k];
+        st->iterations = s_iters;
+        st->converged = s_conv;
+        st->fails = s_fails;
+        st->done = s_done || it + 1 >= p.max_iters;
+      }
+      if (s_done) return;
+      continue;  // on to the E-step of iteration it+1 (run_e of the next pass)
+    }
     if (s_done) break;
   }
-  if (cta == 0 && tid == 0) {
+  if (!sharded && cta == 0 && tid == 0) {
     EmState* st = p.st;
     for (int k = 0; k < 12; ++k) st->Rt[k] = rt[k];
     st->iterations = s_iters;
@@ -326,8 +373,17 @@ int stage_points_public(trg_ctx* ctx, const double* xyz, size_t n, int on_device
 
 namespace {
 
-int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t n,
-           const trg_reg_config* cfg, double target_diag, trg_reg_result* out) {
+struct EmJob {
+  EmParams p;
+  int G = 0, J = 0, K = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+// Parameters, workspace and initial state of one EM run (sharded: seg mode
+// with the exchange buffer xmom and the global point count).
+int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t n,
+               const trg_reg_config* cfg, double target_diag, bool sharded, double n_total,
+               EmJob* job) {
   const int J = tree->n_nodes;
   const int G = persistent_grid(ctx, (const void*)k_register, kAssocBlock, 0);
   EmParams p{};
@@ -340,7 +396,7 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   p.a.pts = src_dev;
   p.a.n = n;
   p.a.status = ctx->status;
-  void *part, *stamps, *mom, *cnt, *em, *tr;
+  void *part, *stamps, *mom, *cnt, *em, *tr, *xm;
   TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * 4 * (size_t)J * G, &part));
   TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)J * G, &stamps));
   TRG_TRY(ws_get(ctx, kSlotMoments, sizeof(double) * 4 * (size_t)J, &mom));
@@ -349,6 +405,7 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   TRG_TRY(ws_get(ctx, kSlotEm, em_bytes, &em));
   const int K = cfg->max_em_iterations;
   TRG_TRY(ws_get(ctx, kSlotEmTrace, (sizeof(double) * 2 + 8) * (size_t)K, &tr));
+  TRG_TRY(ws_get(ctx, kSlotBuild10, sizeof(double) * (4 * (size_t)J + 2), &xm));
   p.a.partials = static_cast<double*>(part);
   p.a.stamps = static_cast<uint32_t*>(stamps);
   p.a.counters = static_cast<unsigned long long*>(cnt);
@@ -362,6 +419,9 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   p.max_iters = K;
   p.rot_tol = cfg->rotation_tol;
   p.tl = ctx->dev_timeline;
+  p.seg = sharded ? 0 : -1;
+  p.xmom = static_cast<double*>(xm);
+  p.n_total = sharded ? n_total : (double)n;
   TRG_TRY(timeline_reset(ctx));
   p.epoch0 = ctx->epoch + 1;
   ctx->epoch += (uint32_t)K + 1;
@@ -371,27 +431,43 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   TRG_CU(cudaMemsetAsync(em, 0, 64, ctx->stream));
   TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
   TRG_CU(trg_memcpy(ctx, p.st, &st, sizeof st, cudaMemcpyHostToDevice));
-  k_check_finite<<<64, 256, 0, ctx->stream>>>(src_dev, 3 * n, ctx->status);
+  if (n > 0) k_check_finite<<<64, 256, 0, ctx->stream>>>(src_dev, 3 * n, ctx->status);
   k_extent<<<1, 256, 0, ctx->stream>>>(tree->nodes, J, p.st, target_diag, cfg->translation_tol);
-  cudaEvent_t e0, e1;
-  TRG_CU(cudaEventCreate(&e0));
-  TRG_CU(cudaEventCreate(&e1));
-  TRG_CU(cudaEventRecord(e0, ctx->stream));
-  void* args[] = {&p};
-  TRG_CU(launch_persistent(ctx, (const void*)k_register, G, kAssocBlock, args));
-  TRG_CU(cudaEventRecord(e1, ctx->stream));
-  ctx->launches += 3;
+  ctx->launches += 2;
+  job->p = p;
+  job->G = G;
+  job->J = J;
+  job->K = K;
+  TRG_CU(cudaEventCreate(&job->e0));
+  TRG_CU(cudaEventCreate(&job->e1));
+  TRG_CU(cudaEventRecord(job->e0, ctx->stream));
+  return TRG_OK;
+}
+
+int em_launch(trg_ctx* ctx, EmJob* job, int seg) {
+  if (job->p.seg >= 0) job->p.seg = seg;
+  void* args[] = {&job->p};
+  TRG_CU(launch_persistent(ctx, (const void*)k_register, job->G, kAssocBlock, args));
+  ctx->launches += 1;
+  return TRG_OK;
+}
+
+int em_collect(trg_ctx* ctx, EmJob* job, trg_reg_result* out) {
+  EmParams& p = job->p;
+  const int K = job->K;
+  TRG_CU(cudaEventRecord(job->e1, ctx->stream));
+  EmState st{};
   TRG_CU(trg_memcpy(ctx, &st, p.st, sizeof st, cudaMemcpyDeviceToHost));
   std::vector<double> cb(K), ca(K);
   std::vector<unsigned long long> ev(K);
   TRG_CU(trg_memcpy(ctx, cb.data(), p.crit_before, sizeof(double) * K, cudaMemcpyDeviceToHost));
   TRG_CU(trg_memcpy(ctx, ca.data(), p.crit_after, sizeof(double) * K, cudaMemcpyDeviceToHost));
   TRG_CU(trg_memcpy(ctx, ev.data(), p.evals, sizeof(unsigned long long) * K, cudaMemcpyDeviceToHost));
-  TRG_CU(cudaEventSynchronize(e1));
+  TRG_CU(cudaEventSynchronize(job->e1));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  cudaEventElapsedTime(&ms, job->e0, job->e1);
+  cudaEventDestroy(job->e0);
+  cudaEventDestroy(job->e1);
   TRG_TRY(check_status(ctx, "register_with_tree"));
   TRG_TRY(timeline_fetch(ctx));
   for (int k = 0; k < 9; ++k) out->R[k] = st.Rt[k];
@@ -399,7 +475,7 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
   out->iterations = st.iterations;
   out->converged = st.converged;
   out->em_seconds = ms * 1e-3;
-  out->model_components = (size_t)J;
+  out->model_components = (size_t)job->J;
   const int m = std::min(st.iterations, out->trace_capacity);
   for (int i = 0; i < m; ++i) {
     if (out->criterion_trace) out->criterion_trace[i] = cb[i];
@@ -407,6 +483,14 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
     if (out->eval_counts) out->eval_counts[i] = ev[i];
   }
   return TRG_OK;
+}
+
+int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t n,
+           const trg_reg_config* cfg, double target_diag, trg_reg_result* out) {
+  EmJob job;
+  TRG_TRY(em_prepare(ctx, tree, src_dev, n, cfg, target_diag, false, 0.0, &job));
+  TRG_TRY(em_launch(ctx, &job, -1));
+  return em_collect(ctx, &job, out);
 }
 
 // Bounding-box diagonal of a cloud (cloud_io.cpp:21-33): per-block min/max,
@@ -457,26 +541,84 @@ __global__ void k_bbox(const double* __restrict__ p, size_t n, double* part, uns
     s += (h[1] - l[1]) * (h[1] - l[1]);
     s += (h[2] - l[2]) * (h[2] - l[2]);
     *out = sqrt(s);
+    for (int k = 0; k < 3; ++k) {
+      out[2 + k] = l[k];
+      out[5 + k] = h[k];
+    }
     *cnt = 0u;
   }
 }
 
-double target_bbox_diagonal(trg_ctx* ctx, const double* dev, size_t n) {
+// bbox of a device cloud: out[0] = diagonal, out[2..4] = min, out[5..7] = max
+int target_bbox(trg_ctx* ctx, const double* dev, size_t n, double out8[8]) {
   void* o = nullptr;
   const int nb = 64;
-  if (ws_get(ctx, kSlotBuild11, 64 + sizeof(double) * 6 * nb, &o) != TRG_OK) return 0.0;
+  TRG_TRY(ws_get(ctx, kSlotBuild11, 64 + sizeof(double) * 6 * nb, &o));
   double* od = static_cast<double*>(o);
-  cudaMemsetAsync(static_cast<char*>(o) + 8, 0, 8, ctx->stream);
+  TRG_CU(cudaMemsetAsync(static_cast<char*>(o) + 8, 0, 8, ctx->stream));
   k_bbox<<<nb, 256, 0, ctx->stream>>>(dev, n, od + 8, reinterpret_cast<unsigned*>(od + 1),
                                       od);
   ctx->launches += 1;
-  double d = 0.0;
-  trg_memcpy(ctx, &d, o, sizeof d, cudaMemcpyDeviceToHost);
-  cudaStreamSynchronize(ctx->stream);
-  return d;
+  TRG_CU(trg_memcpy(ctx, out8, o, sizeof(double) * 8, cudaMemcpyDeviceToHost));
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  return TRG_OK;
+}
+
+double target_bbox_diagonal(trg_ctx* ctx, const double* dev, size_t n) {
+  double o[8];
+  if (target_bbox(ctx, dev, n, o) != TRG_OK) return 0.0;
+  return o[0];
 }
 
 }  // namespace
+
+namespace trg {
+// registration.cpp:174-209 / registration.hpp:29-32 argument checks
+int validate_reg_config(const trg_reg_config* cfg) {
+  if (!cfg) {
+    set_error("register: config is null");
+    return TRG_EINVAL;
+  }
+  if (!(cfg->rotation_tol > 0.0) || !(cfg->translation_tol > 0.0)) {
+    set_error("register: tolerances must be positive");
+    return TRG_EINVAL;
+  }
+  if (cfg->max_em_iterations < 1) {
+    set_error("register: max_em_iterations must be >= 1");
+    return TRG_EINVAL;
+  }
+  if (cfg->variant_param < 1) {
+    set_error("register: variant parameter must be >= 1");
+    return TRG_EINVAL;
+  }
+  if (cfg->variant_kind != TRG_VARIANT_ADAPTIVE && cfg->variant_kind != TRG_VARIANT_TREE) {
+    set_error("register: this path implements adaptive:L and tree:L");
+    return TRG_EINVAL;
+  }
+  {  // initial_transform.is_valid(1e-9) (geometry.cpp:22-38)
+    const double* R = cfg->initial_R;
+    double o = 0.0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double s = R[i] * R[j];
+        s += R[3 + i] * R[3 + j];
+        s += R[6 + i] * R[6 + j];
+        const double d = s - (i == j ? 1.0 : 0.0);
+        o += d * d;
+      }
+    const double det = R[0] * (R[4] * R[8] - R[7] * R[5]) - R[3] * (R[1] * R[8] - R[7] * R[2]) +
+                       R[6] * (R[1] * R[5] - R[4] * R[2]);
+    bool fin = true;
+    for (int k = 0; k < 9; ++k) fin = fin && std::isfinite(R[k]);
+    for (int k = 0; k < 3; ++k) fin = fin && std::isfinite(cfg->initial_t[k]);
+    if (!fin || !(std::sqrt(o) <= 1e-9) || !(std::fabs(det - 1.0) <= 1e-9)) {
+      set_error("register: invalid initial transform");
+      return TRG_EINVAL;
+    }
+  }
+  return TRG_OK;
+}
+}  // namespace trg
 
 extern "C" {
 
@@ -659,43 +801,7 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
     set_error("register: empty cloud");
     return TRG_EINVAL;
   }
-  if (!(cfg->rotation_tol > 0.0) || !(cfg->translation_tol > 0.0)) {
-    set_error("register: tolerances must be positive");
-    return TRG_EINVAL;
-  }
-  if (cfg->max_em_iterations < 1) {
-    set_error("register: max_em_iterations must be >= 1");
-    return TRG_EINVAL;
-  }
-  if (cfg->variant_param < 1) {
-    set_error("register: variant parameter must be >= 1");
-    return TRG_EINVAL;
-  }
-  if (cfg->variant_kind != TRG_VARIANT_ADAPTIVE && cfg->variant_kind != TRG_VARIANT_TREE) {
-    set_error("register: this path implements adaptive:L and tree:L");
-    return TRG_EINVAL;
-  }
-  {  // initial_transform.is_valid(1e-9) (geometry.cpp:22-38)
-    const double* R = cfg->initial_R;
-    double o = 0.0;
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) {
-        double s = R[i] * R[j];
-        s += R[3 + i] * R[3 + j];
-        s += R[6 + i] * R[6 + j];
-        const double d = s - (i == j ? 1.0 : 0.0);
-        o += d * d;
-      }
-    const double det = R[0] * (R[4] * R[8] - R[7] * R[5]) - R[3] * (R[1] * R[8] - R[7] * R[2]) +
-                       R[6] * (R[1] * R[5] - R[4] * R[2]);
-    bool fin = true;
-    for (int k = 0; k < 9; ++k) fin = fin && std::isfinite(R[k]);
-    for (int k = 0; k < 3; ++k) fin = fin && std::isfinite(cfg->initial_t[k]);
-    if (!fin || !(std::sqrt(o) <= 1e-9) || !(std::fabs(det - 1.0) <= 1e-9)) {
-      set_error("register: invalid initial transform");
-      return TRG_EINVAL;
-    }
-  }
+  TRG_TRY(validate_reg_config(cfg));
   TRG_CU(cudaSetDevice(ctx->device));
   const double* src = nullptr;
   const double* tgt = nullptr;
@@ -726,3 +832,94 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ sharded EM
+extern "C" int trg_register_clouds_sharded(trg_comm* comm, const double* const* target,
+                                           const size_t* n_target, const double* const* source,
+                                           const size_t* n_source, int on_device,
+                                           const trg_reg_config* cfg, trg_reg_result* out) {
+  if (!comm || !target || !source || !n_target || !n_source || !out) {
+    set_error("register_sharded: bad argument");
+    return TRG_EINVAL;
+  }
+  TRG_TRY(validate_reg_config(cfg));
+  const int S = comm->local;
+  trg_ctx* ctx = comm->ctx;
+  TRG_CU(cudaSetDevice(ctx->device));
+  // global point counts
+  std::vector<double> cnt((size_t)S * 2);
+  for (int i = 0; i < S; ++i) {
+    cnt[(size_t)i * 2] = (double)n_target[i];
+    cnt[(size_t)i * 2 + 1] = (double)n_source[i];
+  }
+  TRG_TRY(comm_host_reduce(comm, cnt.data(), 2, 0));
+  if (!(cnt[0] > 0.0) || !(cnt[1] > 0.0)) {
+    set_error("register: empty cloud");
+    return TRG_EINVAL;
+  }
+  const double n_total = cnt[1];
+  std::vector<const double*> tdev(S), sdev(S);
+  for (int i = 0; i < S; ++i) {
+    TRG_TRY(stage_points_public(comm->shard_ctx[i], source[i], n_source[i], on_device,
+                                kSlotPoints2, &sdev[i]));
+    TRG_TRY(stage_points_public(comm->shard_ctx[i], target[i], n_target[i], on_device, kSlotPoints,
+                                &tdev[i]));
+  }
+  cudaEvent_t e0, e1;
+  TRG_CU(cudaEventCreate(&e0));
+  TRG_CU(cudaEventCreate(&e1));
+  TRG_CU(cudaEventRecord(e0, ctx->stream));
+  // ---- sharded build (trees owned by the shard contexts)
+  trg_model_config mc = cfg->model_config;
+  mc.max_level = cfg->variant_param;
+  TRG_TRY(check_model_config(&mc));
+  std::vector<trg_tree_dev*> trees(S, nullptr);
+  for (int i = 0; i < S; ++i) comm->shard_ctx[i]->build_into_scratch = true;
+  int rc = build_sharded_dev(comm, tdev.data(), n_target, &mc, trees.data(), nullptr);
+  for (int i = 0; i < S; ++i) comm->shard_ctx[i]->build_into_scratch = false;
+  if (rc != TRG_OK) return rc;
+  TRG_CU(cudaEventRecord(e1, ctx->stream));
+  // ---- global bounding-box diagonal of the target (cloud_io.cpp:21-33)
+  std::vector<double> lo((size_t)S * 3, INFINITY), hi((size_t)S * 3, -INFINITY);
+  for (int i = 0; i < S; ++i) {
+    if (n_target[i] == 0) continue;
+    double o[8];
+    TRG_TRY(target_bbox(comm->shard_ctx[i], tdev[i], n_target[i], o));
+    for (int k = 0; k < 3; ++k) {
+      lo[(size_t)i * 3 + k] = o[2 + k];
+      hi[(size_t)i * 3 + k] = o[5 + k];
+    }
+  }
+  TRG_TRY(comm_host_reduce(comm, lo.data(), 3, 2));
+  TRG_TRY(comm_host_reduce(comm, hi.data(), 3, 1));
+  double dd = (hi[0] - lo[0]) * (hi[0] - lo[0]);
+  dd += (hi[1] - lo[1]) * (hi[1] - lo[1]);
+  dd += (hi[2] - lo[2]) * (hi[2] - lo[2]);
+  const double diag = std::sqrt(dd);
+  // ---- sharded EM: per iteration the per-node (m0, m1) + counters are
+  // all-reduced; every shard solves and updates T identically
+  std::vector<EmJob> job(S);
+  for (int i = 0; i < S; ++i)
+    TRG_TRY(em_prepare(comm->shard_ctx[i], trees[i], sdev[i], n_source[i], cfg, diag, true,
+                       n_total, &job[i]));
+  std::vector<double*> xm(S);
+  for (int i = 0; i < S; ++i) xm[i] = job[i].p.xmom;
+  const int K = cfg->max_em_iterations;
+  const size_t nx = 4 * (size_t)job[0].J + 2;
+  for (int it = 0; it <= K; ++it) {
+    for (int i = 0; i < S; ++i) TRG_TRY(em_launch(comm->shard_ctx[i], &job[i], it));
+    if (it < K) TRG_TRY(comm_allreduce_sum(comm, xm.data(), nx));
+  }
+  rc = em_collect(comm->shard_ctx[0], &job[0], out);
+  for (int i = 1; i < S; ++i) {
+    trg_reg_result tmp{};
+    const int r2 = em_collect(comm->shard_ctx[i], &job[i], &tmp);
+    if (rc == TRG_OK) rc = r2;
+  }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  out->model_build_seconds = ms * 1e-3;
+  return rc;
+}

@@ -107,6 +107,7 @@ struct trg_ctx {
   bool build_into_scratch = false;
   bool timeline_pending = false;
   std::vector<trg_ctx*> workers;  // trg_register_batch: SM-budgeted sub-contexts
+  bool own_stream = true;         // false: a shard context on its parent's stream
   static constexpr int kSlots = 32;
   void* slot_ptr[kSlots] = {};
   size_t slot_size[kSlots] = {};
@@ -116,6 +117,20 @@ struct trg_ctx {
   trg::Timeline* dev_timeline = nullptr;      // device buffer (reset per call)
   std::vector<unsigned long long> timeline;  // last call: globaltimer ns per mark
   std::vector<int> timeline_lab;
+};
+
+// Point-sharded execution (trg_comm_*).  NCCL mode: one shard
+// per process, `world` processes (one per GPU).  Local mode: `world` shards
+// driven by this process on one device (each on its own shard context that
+// shares the parent's stream), exchanged by a device reduction in fixed
+// shard order — the same segmented algorithm, runnable on one GPU.
+struct trg_comm {
+  trg_ctx* ctx = nullptr;
+  int rank = 0, world = 1;
+  int local = 1;                       // shards this process drives
+  std::vector<trg_ctx*> shard_ctx;     // [local]; shard_ctx[0] == ctx
+  void* nccl = nullptr;                // ncclComm_t (NCCL mode)
+  double* dscratch = nullptr;          // device scratch for host-value reductions
 };
 
 namespace trg {
@@ -159,6 +174,17 @@ int ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
 // complete before the call returns.
 cudaError_t trg_memcpy(trg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind);
 int host_ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
+// Collectives over a trg_comm, stream-ordered on comm->ctx->stream.  bufs /
+// src / dst hold one device pointer per local shard.
+int comm_allreduce_sum(trg_comm* c, double* const* bufs, size_t n);
+int comm_allgather(trg_comm* c, double* const* src, double* const* dst, size_t n);
+// vals: [local][n] host values (one row per local shard); on return row 0
+// (and every row) holds the reduction over all shards.  op: 0 sum, 1 max, 2 min.
+int comm_host_reduce(trg_comm* c, double* vals, int n, int op);
+int check_model_config(const trg_model_config* cfg);  // validate_config gmm.cpp:465-477
+// Sharded build over device-resident shard clouds (trg_build.cu).
+int build_sharded_dev(trg_comm* c, const double* const* dev, const size_t* n,
+                      const trg_model_config* cfg, trg_tree_dev** trees, trg_build_diag* diag);
 int check_status(trg_ctx* ctx, const char* where);
 int timeline_reset(trg_ctx* ctx);
 int timeline_fetch(trg_ctx* ctx);

@@ -520,6 +520,136 @@ def register_batch(targets, sources, config: RegistrationConfig = RegistrationCo
     return [_result(arr[i], cb, ca, ev) for i, (_, cb, ca, ev) in enumerate(bufs)]
 
 
+# ------------------------------------------------------------------ sharding
+def shard_bounds(n: int, world: int, rank: int) -> tuple:
+    """Contiguous block [lo, hi) of an n-point cloud held by `rank` of `world`
+    (the block order is the global entry order the sharded build assumes)."""
+    if world < 1 or not 0 <= rank < world:
+        raise InvalidArgument("shard_bounds: bad rank/world")
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def share_unique_id(dist, make_id) -> bytes:
+    """Rank 0 makes the 128-byte communicator id, every rank receives it
+    (torch.distributed object broadcast; any backend)."""
+    obj = [make_id() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    uid = obj[0]
+    if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
+        raise InvalidArgument("share_unique_id: malformed id")
+    return bytes(uid)
+
+
+class Comm:
+    """Point-sharded communicator (trg_comm).  ``Comm.local(k)``: k shards
+    driven by this process on one GPU (fixed-order device reduction);
+    ``Comm.nccl(...)`` / ``Comm.from_torch_distributed()``: one shard per
+    process over NCCL."""
+
+    def __init__(self, handle, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _chk(_lib.lib().trg_comm_unique_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def local(shards: int, ctx: Context | None = None) -> "Comm":
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _chk(_lib.lib().trg_comm_create_local(ctx.h, int(shards), C.byref(h)))
+        return Comm(h, ctx)
+
+    @staticmethod
+    def nccl(rank: int, world: int, uid: bytes, ctx: Context | None = None) -> "Comm":
+        ctx = ctx or default_context()
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _chk(_lib.lib().trg_comm_create_nccl(ctx.h, buf, int(rank), int(world), C.byref(h)))
+        return Comm(h, ctx)
+
+    @staticmethod
+    def from_torch_distributed(ctx: Context | None = None) -> "Comm":
+        import torch.distributed as dist
+        uid = share_unique_id(dist, Comm.unique_id)
+        return Comm.nccl(dist.get_rank(), dist.get_world_size(), uid, ctx)
+
+    @property
+    def rank(self) -> int:
+        return _lib.lib().trg_comm_rank(self.h)
+
+    @property
+    def world(self) -> int:
+        return _lib.lib().trg_comm_world(self.h)
+
+    @property
+    def local_shards(self) -> int:
+        return _lib.lib().trg_comm_local_shards(self.h)
+
+    def close(self):
+        if self.h:
+            _lib.lib().trg_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _shard_arrays(clouds, comm: Comm):
+    if len(clouds) != comm.local_shards:
+        raise InvalidArgument(f"expected {comm.local_shards} shard clouds, got {len(clouds)}")
+    keep, sides = [], set()
+    ptr = (C.c_void_p * len(clouds))()
+    cnt = (C.c_size_t * len(clouds))()
+    for i, c in enumerate(clouds):
+        p, n, d, k = _cloud_ptr(c)
+        keep.append(k)
+        sides.add(d)
+        ptr[i], cnt[i] = p.value, n
+    if len(sides) > 1:
+        raise InvalidArgument("all shard clouds must live on the same side")
+    return ptr, cnt, sides.pop(), keep
+
+
+def build_tree_sharded(shards: list, comm: Comm, config: ModelConfig = ModelConfig(),
+                       diagnostics: BuildDiagnostics | None = None) -> GmmTree:
+    """build_tree over the union of the shards' clouds (this process's local
+    shards; contiguous blocks of one cloud in shard order)."""
+    ptr, cnt, on_dev, _keep = _shard_arrays(shards, comm)
+    cfg = config.c()
+    h = C.c_void_p()
+    d = BuildDiagC()
+    _chk(_lib.lib().trg_build_tree_sharded(comm.h, ptr, cnt, on_dev, C.byref(cfg), C.byref(h),
+                                           C.byref(d)))
+    if diagnostics is not None:
+        diagnostics.calibration_drift = d.calibration_drift
+        diagnostics.calibration_passes = d.calibration_passes
+        L = config.max_level
+        diagnostics.entries_per_round = list(d.entries_per_round)[:L]
+        diagnostics.expanded_per_round = list(d.expanded_per_round)[:L]
+    return GmmTree(h, comm.ctx)
+
+
+def register_clouds_sharded(targets: list, sources: list, comm: Comm,
+                            config: RegistrationConfig = RegistrationConfig()) -> RegistrationResult:
+    """register_clouds over sharded target / source clouds."""
+    tp, tn, dt, _k1 = _shard_arrays(targets, comm)
+    sp, sn, ds, _k2 = _shard_arrays(sources, comm)
+    if dt != ds:
+        raise InvalidArgument("register_clouds_sharded: targets and sources on different sides")
+    r, cb, ca, ev = _result_buffers(config)
+    cfg = config.c()
+    _chk(_lib.lib().trg_register_clouds_sharded(comm.h, tp, tn, sp, sn, dt, C.byref(cfg),
+                                                C.byref(r)))
+    return _result(r, cb, ca, ev)
+
+
 # ------------------------------------------------------------------ inputs
 def synthetic(kind: str, n: int, seed: int) -> np.ndarray:
     """synthetic.cpp generators (bit-identical restatement)."""
