@@ -59,11 +59,11 @@ typedef struct {
 } trg_assoc_config;
 
 /* treereg::Variant::Kind, registration.hpp:19-20 */
-enum { TRG_VARIANT_ADAPTIVE = 0, TRG_VARIANT_TREE = 1 };
+enum { TRG_VARIANT_ADAPTIVE = 0, TRG_VARIANT_TREE = 1, TRG_VARIANT_FLAT = 2 };
 
 /* treereg::RegistrationConfig, registration.hpp:27-36 */
 typedef struct {
-  int variant_kind;        /* TRG_VARIANT_ADAPTIVE | TRG_VARIANT_TREE */
+  int variant_kind;        /* TRG_VARIANT_ADAPTIVE | TRG_VARIANT_TREE | TRG_VARIANT_FLAT */
   int variant_param;       /* tree depth L */
   double lambda_c;         /* 0.01 */
   int max_em_iterations;   /* 50 */
@@ -184,6 +184,23 @@ int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, siz
                   int xyz_on_device, const double R[9], const double t[3],
                   const trg_assoc_config* cfg, trg_moments* out, int* point_node,
                   double* point_weight);
+
+/* ---- flat mixture ("GMM J=n") --------------------
+ * treereg::build_flat_gmm (gmm.hpp:74-76, gmm.cpp:659-736): list_moments,
+ * D^2-weighted seeding from mt19937_64(cfg->rng_seed) (the reference's
+ * stream and libstdc++ distributions, reproduced on the device), J
+ * components at sigma^2 I, em_iterations_per_node * max_level EM
+ * iterations.  The mixture comes back as a depth-1 "tree" of J roots (all
+ * leaves), so trg_tree_download / trg_responsibilities_dense / the EM loop
+ * take it as is.  diag: entries_per_round[0] = N; no ll traces. */
+int trg_build_flat_gmm(trg_ctx* ctx, const double* xyz, size_t n, int xyz_on_device, size_t J,
+                       const trg_model_config* cfg, trg_tree_dev** out, trg_build_diag* diag);
+/* treereg::responsibilities_dense (association.hpp:44-47, association.cpp:54-89):
+ * every node of `comps` is a component (a flat mixture, or a tree's nodes).
+ * Moments as trg_associate (m2 when out->m2 != NULL). */
+int trg_responsibilities_dense(trg_ctx* ctx, const trg_tree_dev* comps, const double* xyz,
+                               size_t n, int xyz_on_device, const double R[9], const double t[3],
+                               double outlier_floor, trg_moments* out);
 
 /* ---- M-step ----------------------------------------------------------- */
 /* treereg::make_virtual_points + treereg::solve_mstep (mstep.hpp:46-47, 67)

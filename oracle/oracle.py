@@ -96,6 +96,10 @@ class Ref:
         L.ref_subsample.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_uint64, _dp]
         L.ref_build_tree.argtypes = [_dp, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_double,
                                      C.c_double, C.POINTER(C.c_void_p)]
+        L.ref_build_flat_gmm.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_int, C.c_int, C.c_double,
+                                         C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.ref_responsibilities_dense.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, _dp, C.c_double,
+                                                 _dp, _dp, _dp, _u64p, _dp]
         L.ref_tree_free.argtypes = [C.c_void_p]
         for f in ("ref_tree_size", "ref_tree_max_level", "ref_tree_calibration_drift",
                   "ref_tree_num_traces"):
@@ -163,6 +167,36 @@ class Ref:
         finally:
             self.L.ref_tree_free(h)
         return t
+
+    def build_flat_gmm(self, pts, j, max_level=3, em_iters=8, eps=1e-4, abs_floor=1e-12, seed=0):
+        p = np.ascontiguousarray(pts, dtype=np.float64)
+        h = C.c_void_p()
+        self._chk(self.L.ref_build_flat_gmm(_d(p), len(p), j, max_level, em_iters, eps, abs_floor,
+                                            C.c_uint64(seed), C.byref(h)))
+        try:
+            t = self._export(h)
+            buf = np.zeros(4096)
+            k = self.L.ref_tree_trace(h, 0, _d(buf), 4096) if self.L.ref_tree_num_traces(h) else 0
+            t["ll_trace"] = buf[:k].copy()
+        finally:
+            self.L.ref_tree_free(h)
+        return t
+
+    def responsibilities_dense(self, comps, pts, R=None, t=None, floor=1e-300) -> Moments:
+        R = np.eye(3) if R is None else np.ascontiguousarray(R, dtype=np.float64)
+        t = np.zeros(3) if t is None else np.ascontiguousarray(t, dtype=np.float64)
+        p = np.ascontiguousarray(pts, dtype=np.float64)
+        J = len(comps["weight"])
+        m0, m1, m2 = np.zeros(J), np.zeros((J, 3)), np.zeros((J, 3, 3))
+        cnt = np.zeros(3, np.uint64)
+        tm = np.zeros(1)
+        h = self._import(comps)
+        try:
+            self._chk(self.L.ref_responsibilities_dense(h, _d(p), len(p), _d(R), _d(t), floor,
+                                                        _d(m0), _d(m1), _d(m2), _u(cnt), _d(tm)))
+        finally:
+            self.L.ref_tree_free(h)
+        return Moments(m0, m1, m2, int(cnt[0]), int(cnt[1]), int(cnt[2]), float(tm[0]))
 
     def _export(self, h):
         n = self.L.ref_tree_size(h)
@@ -253,7 +287,8 @@ class Ref:
         it, conv = C.c_int(), C.c_int()
         bs, es = np.zeros(1), np.zeros(1)
         self._chk(self.L.ref_register_clouds(_d(a), len(a), _d(b), len(b),
-                                             1 if variant == "tree" else 0, level, lambda_c,
+                                             {"adaptive": 0, "tree": 1, "flat": 2}[variant], level,
+                                             lambda_c,
                                              max_iters, _d(R), _d(t), C.byref(it), C.byref(conv),
                                              _d(bs), _d(es)))
         return dict(R=R, t=t, iterations=it.value, converged=bool(conv.value),

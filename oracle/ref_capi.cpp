@@ -148,6 +148,56 @@ int ref_build_tree(const double* xyz, std::size_t n, int max_level, int em_iters
   })
 }
 
+// build_flat_gmm (gmm.cpp:659-736) as a depth-1 handle of J roots, so the
+// tree export / dense association wrappers serve it too.
+int ref_build_flat_gmm(const double* xyz, std::size_t n, std::size_t j, int max_level,
+                       int em_iters, double eps, double abs_floor, std::uint64_t seed,
+                       void** out) {
+  GUARD({
+    ModelConfig cfg;
+    cfg.max_level = max_level;
+    cfg.em_iterations_per_node = em_iters;
+    cfg.cov_regularization_epsilon = eps;
+    cfg.cov_regularization_absolute = abs_floor;
+    cfg.rng_seed = seed;
+    auto* h = new RefTree;
+    try {
+      h->tree.nodes = build_flat_gmm(to_cloud(xyz, n), j, cfg, &h->diag);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    const std::size_t J = h->tree.nodes.size();
+    h->tree.parent.assign(J, -1);
+    h->tree.first_child.assign(J, -1);
+    h->tree.child_count.assign(J, 0);
+    h->tree.level.assign(J, 0);
+    h->tree.max_level = 1;
+    *out = h;
+  })
+}
+
+// responsibilities_dense (association.cpp:54-89) over the handle's nodes.
+int ref_responsibilities_dense(void* h, const double* xyz, std::size_t n, const double* R,
+                               const double* t, double floor, double* m0, double* m1, double* m2,
+                               std::uint64_t* counters, double* total_mass) {
+  GUARD({
+    const MomentSet m = responsibilities_dense(to_cloud(xyz, n), static_cast<RefTree*>(h)->tree.nodes,
+                                               to_tf(R, t), floor);
+    for (std::size_t q = 0; q < m.components(); ++q) {
+      m0[q] = m.m0[q];
+      for (int r = 0; r < 3; ++r) {
+        m1[3 * q + r] = m.m1[q](r);
+        for (int c = 0; c < 3; ++c) m2[9 * q + 3 * r + c] = m.m2[q](r, c);
+      }
+    }
+    counters[0] = m.total_points;
+    counters[1] = m.outliers;
+    counters[2] = m.density_evaluations;
+    *total_mass = m.total_mass;
+  })
+}
+
 void ref_tree_free(void* h) { delete static_cast<RefTree*>(h); }
 int ref_tree_size(void* h) { return static_cast<int>(static_cast<RefTree*>(h)->tree.size()); }
 int ref_tree_max_level(void* h) { return static_cast<RefTree*>(h)->tree.max_level; }
@@ -307,7 +357,9 @@ int ref_register_with_tree(void* h, const double* xyz, std::size_t n, int varian
                            std::uint64_t* evals, double* em_seconds) {
   GUARD({
     RegistrationConfig cfg;
-    cfg.variant.kind = variant_kind == 1 ? Variant::Kind::kGmmTree : Variant::Kind::kAdaptive;
+    cfg.variant.kind = variant_kind == 2   ? Variant::Kind::kFlatGmm
+                       : variant_kind == 1 ? Variant::Kind::kGmmTree
+                                           : Variant::Kind::kAdaptive;
     cfg.variant.param = static_cast<RefTree*>(h)->tree.max_level;
     cfg.lambda_c = lambda_c;
     cfg.max_em_iterations = max_iters;
@@ -334,7 +386,9 @@ int ref_register_clouds(const double* tgt, std::size_t nt, const double* src, st
                         double* em_s) {
   GUARD({
     RegistrationConfig cfg;
-    cfg.variant.kind = variant_kind == 1 ? Variant::Kind::kGmmTree : Variant::Kind::kAdaptive;
+    cfg.variant.kind = variant_kind == 2   ? Variant::Kind::kFlatGmm
+                       : variant_kind == 1 ? Variant::Kind::kGmmTree
+                                           : Variant::Kind::kAdaptive;
     cfg.variant.param = level;
     cfg.lambda_c = lambda_c;
     cfg.max_em_iterations = max_iters;

@@ -104,6 +104,10 @@ SIGNATURES = {
     "trg_register_with_tree": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int,
                                          C.POINTER(RegConfigC), C.c_double,
                                          C.POINTER(RegResultC)]),
+    "trg_build_flat_gmm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_size_t,
+                                     C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p]),
+    "trg_responsibilities_dense": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int,
+                                             dp, dp, C.c_double, C.c_void_p]),
     "trg_comm_unique_id": (C.c_int, [C.c_void_p]),
     "trg_comm_create_nccl": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "trg_comm_create_local": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),

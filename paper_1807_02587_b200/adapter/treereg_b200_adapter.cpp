@@ -16,8 +16,11 @@
 //   solve_mstep             mstep.hpp:67           -> trg_solve_mstep_vps
 //   register_with_tree      registration.hpp:59-62 -> trg_register_with_tree
 //   register_clouds         registration.hpp:53-55 -> trg_register_clouds
-//                           (flat:J / icp variants forward to the reference's
-//                            own implementation, linked as register_clouds_ref)
+//                           (adaptive:L, tree:L, flat:J; the icp variant
+//                            forwards to the reference's own implementation,
+//                            linked as register_clouds_ref)
+//   build_flat_gmm          gmm.hpp:74-76          -> trg_build_flat_gmm
+//   responsibilities_dense  association.hpp:44-47  -> trg_responsibilities_dense
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -34,8 +37,8 @@
 
 namespace treereg {
 
-// The reference's own register_clouds for the variants this path does not
-// cover (flat GMM, ICP); see INTEGRATION.md for how it is kept linkable.
+// The reference's own register_clouds for the variant this path does not
+// cover (ICP); see INTEGRATION.md for how it is kept linkable.
 RegistrationResult register_clouds_ref(const PointCloud& target, const PointCloud& source,
                                        const RegistrationConfig& config);
 
@@ -177,8 +180,9 @@ trg_model_config model_cfg(const ModelConfig& m) {
 
 trg_reg_config reg_cfg(const RegistrationConfig& cfg) {
   trg_reg_config c{};
-  c.variant_kind =
-      cfg.variant.kind == Variant::Kind::kGmmTree ? TRG_VARIANT_TREE : TRG_VARIANT_ADAPTIVE;
+  c.variant_kind = cfg.variant.kind == Variant::Kind::kGmmTree   ? TRG_VARIANT_TREE
+                   : cfg.variant.kind == Variant::Kind::kFlatGmm ? TRG_VARIANT_FLAT
+                                                                 : TRG_VARIANT_ADAPTIVE;
   c.variant_param = cfg.variant.param;
   c.lambda_c = cfg.lambda_c;
   c.max_em_iterations = cfg.max_em_iterations;
@@ -348,10 +352,65 @@ RegistrationResult register_with_tree(const GmmTree& tree, const PointCloud& sou
   return result_of(r, cb, ca, ev);
 }
 
+std::vector<GaussianComponent> build_flat_gmm(const PointCloud& cloud, std::size_t j,
+                                              const ModelConfig& config,
+                                              BuildDiagnostics* diagnostics) {
+  if (cloud.empty()) throw std::invalid_argument("point cloud is empty");
+  if (!cloud.all_finite()) throw std::invalid_argument("point cloud has non-finite coordinates");
+  const trg_model_config mc = model_cfg(config);
+  DevTree dt;
+  check(trg_build_flat_gmm(ctx(), xyz(cloud), cloud.size(), 0, j, &mc, &dt.h, nullptr),
+        "build_flat_gmm");
+  if (diagnostics != nullptr) diagnostics->node_ll_traces.emplace_back();
+  return download(dt.h).nodes;
+}
+
+MomentSet responsibilities_dense(const PointCloud& cloud,
+                                 const std::vector<GaussianComponent>& components,
+                                 const RigidTransform& t, double outlier_floor) {
+  if (cloud.empty()) throw std::invalid_argument("association: empty point cloud");
+  if (components.empty()) throw std::invalid_argument("association: empty model");
+  GmmTree flat;
+  flat.nodes = components;
+  const std::size_t J = components.size();
+  flat.parent.assign(J, -1);
+  flat.first_child.assign(J, -1);
+  flat.child_count.assign(J, 0);
+  flat.level.assign(J, 0);
+  flat.max_level = 1;
+  DevTree dt;
+  upload(flat, dt);
+  std::vector<double> m0(J), m1(3 * J), m2(9 * J);
+  trg_moments m{};
+  m.m0 = m0.data();
+  m.m1 = m1.data();
+  m.m2 = m2.data();
+  double R[9], tr[3];
+  for (int i = 0; i < 3; ++i) {
+    tr[i] = t.translation(i);
+    for (int k = 0; k < 3; ++k) R[3 * i + k] = t.rotation(i, k);
+  }
+  check(trg_responsibilities_dense(ctx(), dt.h, xyz(cloud), cloud.size(), 0, R, tr, outlier_floor,
+                                   &m),
+        "responsibilities_dense");
+  MomentSet out(J);
+  for (std::size_t q = 0; q < J; ++q) {
+    out.m0[q] = m0[q];
+    for (int r = 0; r < 3; ++r) {
+      out.m1[q](r) = m1[3 * q + r];
+      for (int c = 0; c < 3; ++c) out.m2[q](r, c) = m2[9 * q + 3 * r + c];
+    }
+  }
+  out.total_points = m.total_points;
+  out.total_mass = m.total_mass;
+  out.outliers = m.outliers;
+  out.density_evaluations = m.density_evaluations;
+  return out;
+}
+
 RegistrationResult register_clouds(const PointCloud& target, const PointCloud& source,
                                    const RegistrationConfig& config) {
-  if (config.variant.kind == Variant::Kind::kFlatGmm ||
-      config.variant.kind == Variant::Kind::kIcpPointToPoint)
+  if (config.variant.kind == Variant::Kind::kIcpPointToPoint)
     return register_clouds_ref(target, source, config);  // not on this path
   if (target.empty() || source.empty()) throw std::invalid_argument("register: empty cloud");
   if (!target.all_finite() || !source.all_finite())

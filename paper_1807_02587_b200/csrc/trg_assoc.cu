@@ -54,4 +54,16 @@ int launch_associate(trg_ctx* ctx, const AssocParams& p, int nm, double* moments
   return TRG_OK;
 }
 
+int launch_combine(trg_ctx* ctx, const double* partials, const uint32_t* stamps, uint32_t epoch,
+                   int G, int J, int nm, double* out) {
+  const int cblocks = (J * 32 + 255) / 256;
+  if (nm == 4)
+    k_combine<4><<<cblocks, 256, 0, ctx->stream>>>(partials, stamps, epoch, G, J, out);
+  else
+    k_combine<10><<<cblocks, 256, 0, ctx->stream>>>(partials, stamps, epoch, G, J, out);
+  ctx->launches += 1;
+  TRG_CU(cudaGetLastError());
+  return TRG_OK;
+}
+
 }  // namespace trg

@@ -19,7 +19,7 @@
 #include <cstdlib>
 #include <vector>
 
-#include "trg_solve.cuh"
+#include "trg_gmm.cuh"
 
 namespace trg {
 
@@ -32,17 +32,7 @@ constexpr int kOffMom1 = 182;  // m0, m1[3], wmax, wmax index
 constexpr int kOffMom2 = 188;  // m2[6]
 constexpr int kOffCnt = 194;   // partition: count[8], mass[8]
 
-// One mixture component during a node fit (gmm.hpp:12-23 + log weight).
-struct GComp {
-  double w, lw;
-  double mean[3];
-  double axT[9];
-  double lam[3];
-  double log_norm;
-  double cov[9];
-  double il[3];  // 1 / lam
-};
-static_assert(sizeof(GComp) == 240, "GComp layout");
+
 
 struct RoundNodes {  // per expanding node k of a round (ping-pong by round parity)
   int* tree_id;      // tree node being expanded (-1: virtual root)
@@ -168,64 +158,6 @@ __device__ __forceinline__ double comp_log(const double r[18], double x0, double
   }
   const double q = fast_q(r + 2, r + 5, r + 14, x0, x1, x2);
   return r[1] + __fma_rn(-0.5, q, r[17]);
-}
-
-// set_floored_cov (gmm.cpp:143-150) into a GComp.
-__device__ __forceinline__ int comp_set_cov(GComp& g, const double sc[3][3], double floor_value) {
-  double lam[3], ax[3][3], cov[3][3];
-  const int rc = eig_sym3_floored(sc, floor_value, lam, ax);
-  if (rc) return rc;
-  reconstruct(lam, ax, cov);
-  for (int i = 0; i < 3; ++i) {
-    g.lam[i] = lam[i];
-    g.il[i] = 1.0 / lam[i];
-    for (int j = 0; j < 3; ++j) {
-      g.axT[3 * i + j] = ax[j][i];
-      g.cov[3 * i + j] = cov[i][j];
-    }
-  }
-  g.log_norm = log_norm_of(lam);
-  return kOk;
-}
-
-__device__ __forceinline__ void write_dnode_from_comp(DNode& d, double* cov9, const GComp& g,
-                                                      double w, int level, int parent) {
-  for (int i = 0; i < 3; ++i) d.mean[i] = g.mean[i];
-  for (int i = 0; i < 9; ++i) {
-    d.axT[i] = g.axT[i];
-    cov9[i] = g.cov[i];
-  }
-  for (int i = 0; i < 3; ++i) {
-    d.lam[i] = g.lam[i];
-    d.il[i] = 1.0 / g.lam[i];
-  }
-  d.pad = 0.0;
-  d.log_norm = g.log_norm;
-  d.weight = w;
-  const double tr = (g.lam[0] + g.lam[1]) + g.lam[2];
-  d.cplx = tr > 0.0 ? g.lam[2] / tr : -1.0;
-  d.first_child = -1;
-  d.child_count = 0;
-  d.level = level;
-  d.parent = parent;
-}
-
-// refresh_eig (gmm.cpp:31-35) of a tree node from its cov.
-__device__ __forceinline__ int refresh_node(DNode& d, const double* cov9) {
-  double m[3][3], lam[3], ax[3][3];
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) m[i][j] = cov9[3 * i + j];
-  const int rc = eig_sym3(m, lam, ax);
-  if (rc) return rc;
-  for (int i = 0; i < 3; ++i) {
-    d.lam[i] = lam[i];
-    d.il[i] = 1.0 / lam[i];
-    for (int j = 0; j < 3; ++j) d.axT[3 * i + j] = ax[j][i];
-  }
-  d.log_norm = log_norm_of(lam);
-  const double tr = (lam[0] + lam[1]) + lam[2];
-  d.cplx = tr > 0.0 ? lam[2] / tr : -1.0;
-  return kOk;
 }
 
 // Deterministic block sum of NV values per thread; results in out[0..NV) (smem).

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <vector>
 
+#include "trg_dense.cuh"
 #include "trg_solve.cuh"
 
 namespace trg {
@@ -37,6 +38,7 @@ struct EmParams {
   int seg;
   double* xmom;
   double n_total;  // total source points over all shards (mass floor)
+  double* psum;    // dense (flat mixture) E-step: per-point score sums
 };
 
 constexpr int kAccStride = kNormalEq + 2;
@@ -47,6 +49,9 @@ constexpr int kAccStride = kNormalEq + 2;
 // order and solves redundantly (identical bits everywhere), so the running
 // transform and the stop decision need no third barrier.  CTA 0 alone adds
 // the criterion-after trace and publishes the state for the host.
+// DENSE: the flat-mixture variant (registration.cpp:191-202): the E-step is
+// responsibilities_dense over the J components instead of the tree descent.
+template <bool DENSE>
 __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
   __shared__ AssocSmem<4> sm;
   __shared__ SolveSmem ss;
@@ -80,7 +85,25 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
     if (run_e) {
       // ---- P1: E-step over this CTA's point tiles
       tl_mark(p.tl, 2000 + it * 10);
-      assoc_pass<4>(sm, a, rt, G, cta);
+      if constexpr (DENSE) {
+        DenseParams d{};
+        d.pts = a.pts;
+        d.n = a.n;
+        d.comps = a.nodes;
+        d.J = J;
+        d.outlier_floor = a.outlier_floor;
+        d.psum = p.psum;
+        d.partials = a.partials;
+        d.stamps = a.stamps;
+        d.epoch = a.epoch;
+        d.counters = a.counters;
+        d.status = a.status;
+        dense_pass1(d, rt, G, cta);
+        grid_sync(p.bar, G);
+        dense_pass2<4>(d, rt, G, cta);
+      } else {
+        assoc_pass<4>(sm, a, rt, G, cta);
+      }
       grid_sync(p.bar, G);
       tl_mark(p.tl, 2000 + it * 10 + 1);
       if (sharded) {
@@ -374,6 +397,7 @@ int stage_points_public(trg_ctx* ctx, const double* xyz, size_t n, int on_device
 namespace {
 
 struct EmJob {
+  const void* kernel = nullptr;
   EmParams p;
   int G = 0, J = 0, K = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -383,9 +407,10 @@ struct EmJob {
 // with the exchange buffer xmom and the global point count).
 int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t n,
                const trg_reg_config* cfg, double target_diag, bool sharded, double n_total,
-               EmJob* job) {
+               EmJob* job, bool dense = false) {
   const int J = tree->n_nodes;
-  const int G = persistent_grid(ctx, (const void*)k_register, kAssocBlock, 0);
+  job->kernel = dense ? (const void*)k_register<true> : (const void*)k_register<false>;
+  const int G = persistent_grid(ctx, job->kernel, kAssocBlock, 0);
   EmParams p{};
   p.a.nodes = tree->nodes;
   p.a.n_nodes = J;
@@ -421,6 +446,11 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   p.tl = ctx->dev_timeline;
   p.seg = sharded ? 0 : -1;
   p.xmom = static_cast<double*>(xm);
+  if (dense) {
+    void* ps = nullptr;
+    TRG_TRY(ws_get(ctx, kSlotDense, sizeof(double) * std::max<size_t>(n, 1), &ps));
+    p.psum = static_cast<double*>(ps);
+  }
   p.n_total = sharded ? n_total : (double)n;
   TRG_TRY(timeline_reset(ctx));
   p.epoch0 = ctx->epoch + 1;
@@ -447,7 +477,7 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
 int em_launch(trg_ctx* ctx, EmJob* job, int seg) {
   if (job->p.seg >= 0) job->p.seg = seg;
   void* args[] = {&job->p};
-  TRG_CU(launch_persistent(ctx, (const void*)k_register, job->G, kAssocBlock, args));
+  TRG_CU(launch_persistent(ctx, job->kernel, job->G, kAssocBlock, args));
   ctx->launches += 1;
   return TRG_OK;
 }
@@ -486,9 +516,9 @@ int em_collect(trg_ctx* ctx, EmJob* job, trg_reg_result* out) {
 }
 
 int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t n,
-           const trg_reg_config* cfg, double target_diag, trg_reg_result* out) {
+           const trg_reg_config* cfg, double target_diag, trg_reg_result* out, bool dense = false) {
   EmJob job;
-  TRG_TRY(em_prepare(ctx, tree, src_dev, n, cfg, target_diag, false, 0.0, &job));
+  TRG_TRY(em_prepare(ctx, tree, src_dev, n, cfg, target_diag, false, 0.0, &job, dense));
   TRG_TRY(em_launch(ctx, &job, -1));
   return em_collect(ctx, &job, out);
 }
@@ -573,6 +603,16 @@ double target_bbox_diagonal(trg_ctx* ctx, const double* dev, size_t n) {
 }  // namespace
 
 namespace trg {
+// Non-finite coordinates -> TRG_EINVAL with `msg` (validate_cloud).
+int check_finite_dev(trg_ctx* ctx, const double* dev, size_t n, const char* msg) {
+  if (n == 0) return TRG_OK;
+  k_check_finite<<<64, 256, 0, ctx->stream>>>(dev, 3 * n, ctx->status);
+  ctx->launches += 1;
+  const int rc = check_status(ctx, "check_finite");
+  if (rc == TRG_EINVAL) set_error(msg);
+  return rc;
+}
+
 // registration.cpp:174-209 / registration.hpp:29-32 argument checks
 int validate_reg_config(const trg_reg_config* cfg) {
   if (!cfg) {
@@ -591,8 +631,9 @@ int validate_reg_config(const trg_reg_config* cfg) {
     set_error("register: variant parameter must be >= 1");
     return TRG_EINVAL;
   }
-  if (cfg->variant_kind != TRG_VARIANT_ADAPTIVE && cfg->variant_kind != TRG_VARIANT_TREE) {
-    set_error("register: this path implements adaptive:L and tree:L");
+  if (cfg->variant_kind != TRG_VARIANT_ADAPTIVE && cfg->variant_kind != TRG_VARIANT_TREE &&
+      cfg->variant_kind != TRG_VARIANT_FLAT) {
+    set_error("register: this path implements adaptive:L, tree:L and flat:J");
     return TRG_EINVAL;
   }
   {  // initial_transform.is_valid(1e-9) (geometry.cpp:22-38)
@@ -811,16 +852,23 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
   TRG_CU(cudaEventCreate(&e0));
   TRG_CU(cudaEventCreate(&e1));
   TRG_CU(cudaEventRecord(e0, ctx->stream));
+  const bool flat = cfg->variant_kind == TRG_VARIANT_FLAT;
   trg_model_config mc = cfg->model_config;
-  mc.max_level = cfg->variant_param;
+  if (!flat) mc.max_level = cfg->variant_param;
   trg_tree_dev* tree = nullptr;
   ctx->build_into_scratch = true;
-  int rc = trg_build_tree(ctx, tgt, n_target, 1, &mc, &tree, nullptr);
+  int rc;
+  if (flat) {  // registration.cpp:191-202: build_flat_gmm + dense E-step
+    rc = check_finite_dev(ctx, tgt, n_target, "point cloud has non-finite coordinates");
+    if (rc == TRG_OK) rc = flat_build(ctx, tgt, n_target, (size_t)cfg->variant_param, &mc, &tree, nullptr);
+  } else {
+    rc = trg_build_tree(ctx, tgt, n_target, 1, &mc, &tree, nullptr);
+  }
   ctx->build_into_scratch = false;
   if (rc != TRG_OK) return rc;
   TRG_CU(cudaEventRecord(e1, ctx->stream));
   const double diag = target_bbox_diagonal(ctx, tgt, n_target);
-  rc = run_em(ctx, tree, src, n_source, cfg, diag, out);
+  rc = run_em(ctx, tree, src, n_source, cfg, diag, out, flat);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
@@ -843,6 +891,10 @@ extern "C" int trg_register_clouds_sharded(trg_comm* comm, const double* const* 
     return TRG_EINVAL;
   }
   TRG_TRY(validate_reg_config(cfg));
+  if (cfg->variant_kind == TRG_VARIANT_FLAT) {
+    set_error("register_sharded: the sharded path implements adaptive:L and tree:L");
+    return TRG_EINVAL;
+  }
   const int S = comm->local;
   trg_ctx* ctx = comm->ctx;
   TRG_CU(cudaSetDevice(ctx->device));

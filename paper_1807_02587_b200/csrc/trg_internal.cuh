@@ -160,6 +160,7 @@ enum Slot : int {
   kSlotBuild10,
   kSlotBuild11,
   kSlotPoints2,
+  kSlotDense,         // dense association: per-point score sums
   kSlotHostStage,     // host slots only: pinned staging for pageable copies
   kSlotTimelineHost,  // host slots only: last device timeline
 };
@@ -182,6 +183,13 @@ int comm_allgather(trg_comm* c, double* const* src, double* const* dst, size_t n
 // (and every row) holds the reduction over all shards.  op: 0 sum, 1 max, 2 min.
 int comm_host_reduce(trg_comm* c, double* vals, int n, int op);
 int check_model_config(const trg_model_config* cfg);  // validate_config gmm.cpp:465-477
+int check_finite_dev(trg_ctx* ctx, const double* dev, size_t n, const char* msg);
+// Device pointer to N x 3 points: the caller's (on_device) or a staged copy.
+int stage_points_public(trg_ctx* ctx, const double* xyz, size_t n, int on_device, int slot,
+                        const double** dev);
+// build_flat_gmm (gmm.cpp:659-736) over a device cloud -> J-root mixture.
+int flat_build(trg_ctx* ctx, const double* dev, size_t n, size_t J, const trg_model_config* cfg,
+               trg_tree_dev** out, trg_build_diag* diag);
 // Sharded build over device-resident shard clouds (trg_build.cu).
 int build_sharded_dev(trg_comm* c, const double* const* dev, const size_t* n,
                       const trg_model_config* cfg, trg_tree_dev** trees, trg_build_diag* diag);
@@ -219,5 +227,8 @@ struct AssocParams {
 int launch_associate(trg_ctx* ctx, const AssocParams& p, int nm, double* moments /*[J][nm]*/,
                      int grid);
 int assoc_grid(trg_ctx* ctx, int nm);
+// Per-node fixed-order combine of epoch-stamped partial rows -> out[J][nm].
+int launch_combine(trg_ctx* ctx, const double* partials, const uint32_t* stamps, uint32_t epoch,
+                   int G, int J, int nm, double* out);
 
 }  // namespace trg

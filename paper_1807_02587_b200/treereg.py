@@ -152,14 +152,14 @@ class AssocConfig:  # association.hpp:34-40
 
 @dataclass
 class Variant:  # registration.hpp:17-25
-    kind: str = "adaptive"  # "adaptive" | "tree"
+    kind: str = "adaptive"  # "adaptive" | "tree" | "flat"
     param: int = 3
 
     @staticmethod
     def parse(text: str) -> "Variant":
         head, _, tail = text.partition(":")
-        if head not in ("adaptive", "tree"):
-            raise InvalidArgument(f"unsupported variant '{text}' (this path: adaptive:L, tree:L)")
+        if head not in ("adaptive", "tree", "flat"):
+            raise InvalidArgument(f"unsupported variant '{text}' (this path: adaptive:L, tree:L, flat:J)")
         if not tail:
             raise InvalidArgument(f"variant '{head}' needs a parameter, e.g. {head}:3")
         try:
@@ -171,6 +171,8 @@ class Variant:  # registration.hpp:17-25
         return Variant(head, p)
 
     def name(self) -> str:
+        if self.kind == "flat":
+            return f"GMM J={self.param}"
         return ("Adaptive L" if self.kind == "adaptive" else "GMM-Tree L") + str(self.param)
 
 
@@ -212,7 +214,7 @@ class RegistrationConfig:  # registration.hpp:27-36
 
     def c(self) -> RegConfigC:
         r = RegConfigC()
-        r.variant_kind = 1 if self.variant.kind == "tree" else 0
+        r.variant_kind = {"adaptive": 0, "tree": 1, "flat": 2}[self.variant.kind]
         r.variant_param = self.variant.param
         r.lambda_c = self.lambda_c
         r.max_em_iterations = self.max_em_iterations
@@ -518,6 +520,45 @@ def register_batch(targets, sources, config: RegistrationConfig = RegistrationCo
     _chk(_lib.lib().trg_register_batch(ctx.h, n, tp, tn, sp, sn, sides.pop() if sides else 0,
                                        C.byref(cfg), int(streams), arr))
     return [_result(arr[i], cb, ca, ev) for i, (_, cb, ca, ev) in enumerate(bufs)]
+
+
+# ------------------------------------------------------------------ flat mixture
+def build_flat_gmm(cloud, j: int, config: ModelConfig = ModelConfig(),
+                   diagnostics: BuildDiagnostics | None = None,
+                   ctx: Context | None = None) -> GmmTree:
+    """gmm.hpp:74-76 build_flat_gmm on the GPU: the J components come back as
+    a depth-1 GmmTree of J roots (``.host()`` gives the component arrays)."""
+    ctx = ctx or default_context()
+    ptr, n, on_dev, _keep = _cloud_ptr(cloud)
+    cfg = config.c()
+    h = C.c_void_p()
+    d = BuildDiagC()
+    _chk(_lib.lib().trg_build_flat_gmm(ctx.h, ptr, n, on_dev, int(j), C.byref(cfg), C.byref(h),
+                                       C.byref(d)))
+    if diagnostics is not None:
+        diagnostics.entries_per_round = [int(d.entries_per_round[0])]
+    return GmmTree(h, ctx)
+
+
+def responsibilities_dense(cloud, components: GmmTree, t: "RigidTransform" = None,
+                           outlier_floor: float = 1e-300, with_m2: bool = True) -> "MomentSet":
+    """association.hpp:44-47 responsibilities_dense: every node of
+    `components` (a flat mixture or any tree's nodes) against every point."""
+    t = t or RigidTransform.identity()
+    ptr, n, on_dev, _keep = _cloud_ptr(cloud)
+    J = components.size()
+    m0, m1 = np.zeros(J), np.zeros((J, 3))
+    m2 = np.zeros((J, 3, 3)) if with_m2 else None
+    mc = MomentsC()
+    mc.m0, mc.m1 = _d(m0), _d(m1)
+    mc.m2 = _d(m2) if with_m2 else None
+    R = np.ascontiguousarray(t.rotation, dtype=np.float64)
+    tt = np.ascontiguousarray(t.translation, dtype=np.float64)
+    _chk(_lib.lib().trg_responsibilities_dense(components.ctx.h, components.h, ptr, n, on_dev,
+                                               _d(R), _d(tt), float(outlier_floor),
+                                               C.byref(mc)))
+    return MomentSet(m0, m1, m2, int(mc.total_points), float(mc.total_mass), int(mc.outliers),
+                     int(mc.density_evaluations))
 
 
 # ------------------------------------------------------------------ sharding

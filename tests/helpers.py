@@ -10,9 +10,22 @@ TREE_KEYS = ("weight", "mean", "cov", "lambdas", "axes", "log_norm", "parent", "
 
 
 def golden_names():
-    """Fixtures that carry their input cloud (c4_* regenerate theirs)."""
+    """Tree fixtures that carry their input cloud (c4_* regenerate theirs;
+    flat_* are the flat-mixture fixtures)."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith("c4_"))
+                  if not os.path.basename(p).startswith(("c4_", "flat_")))
+
+
+def flat_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "flat_*.npz")))
+
+
+def load_flat(name):
+    z = np.load(os.path.join(GOLDEN, name + ".npz"))
+    g = {k: z[k] for k in z.files}
+    g["mix"] = {k: g["mix_" + k] for k in TREE_KEYS}
+    g["mix"]["max_level"] = 1
+    return g
 
 
 def load_golden(name):
