@@ -359,8 +359,71 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
   for (int k = 0; k < 11; ++k) acc[k] = 0.0;
   const int slot = lane / gsz;
   const bool want_ll = mode == 2 || (mode == 1 && p.want_traces);
+  const bool any_ll = __any_sync(0xffffffffu, want_ll);
+  // EM iterations (mode 1 on every lane, no trace): two warp steps per loop
+  // trip, so the shuffle / exp latency chains of two entries overlap
+  const bool em_fast = __all_sync(0xffffffffu, mode == 1) && !any_ll;
+  if (em_fast) {
+    const double n0 = sm.nmean[0], n1 = sm.nmean[1], n2 = sm.nmean[2];
+    for (int base = warp * 32; base < warp * 32 + 32; base += 2 * per_step) {
+      const int ea = base + slot, eb = base + per_step + slot;
+      const bool aa = ea < sm.tlen, ab = eb < sm.tlen;
+      const double xa0 = aa ? sm.ent[0][ea] : 0.0, xa1 = aa ? sm.ent[1][ea] : 0.0,
+                   xa2 = aa ? sm.ent[2][ea] : 0.0, wa = aa ? sm.ent[3][ea] : 0.0;
+      const double xb0 = ab ? sm.ent[0][eb] : 0.0, xb1 = ab ? sm.ent[1][eb] : 0.0,
+                   xb2 = ab ? sm.ent[2][eb] : 0.0, wb = ab ? sm.ent[3][eb] : 0.0;
+      const double la = aa ? comp_log(r, xa0, xa1, xa2, p.status) : -INFINITY;
+      const double lb = ab ? comp_log(r, xb0, xb1, xb2, p.status) : -INFINITY;
+      double ma = la, mb = lb;
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) {
+        const double ta = __shfl_xor_sync(0xffffffffu, ma, off);
+        const double tb = __shfl_xor_sync(0xffffffffu, mb, off);
+        ma = fmax(ma, ta);
+        mb = fmax(mb, tb);
+      }
+      const bool fa = aa && isfinite(ma), fb = ab && isfinite(mb);
+      const double ka = fa ? exp(la - ma) : 0.0, kb = fb ? exp(lb - mb) : 0.0;
+      double sa = ka, sb = kb;
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) {
+        const double ta = __shfl_xor_sync(0xffffffffu, sa, off);
+        const double tb = __shfl_xor_sync(0xffffffffu, sb, off);
+        sa += ta;
+        sb += tb;
+      }
+      const double ga = fa ? ka * rcp_sum(sa) * wa : 0.0;
+      const double gb = fb ? kb * rcp_sum(sb) * wb : 0.0;
+      if (ga > 0.0) {
+        const double d0 = xa0 - n0, d1 = xa1 - n1, d2 = xa2 - n2;
+        acc[0] += ga;
+        acc[1] += ga * d0;
+        acc[2] += ga * d1;
+        acc[3] += ga * d2;
+        acc[4] += ga * (d0 * d0);
+        acc[5] += ga * (d0 * d1);
+        acc[6] += ga * (d0 * d2);
+        acc[7] += ga * (d1 * d1);
+        acc[8] += ga * (d1 * d2);
+        acc[9] += ga * (d2 * d2);
+      }
+      if (gb > 0.0) {
+        const double d0 = xb0 - n0, d1 = xb1 - n1, d2 = xb2 - n2;
+        acc[0] += gb;
+        acc[1] += gb * d0;
+        acc[2] += gb * d1;
+        acc[3] += gb * d2;
+        acc[4] += gb * (d0 * d0);
+        acc[5] += gb * (d0 * d1);
+        acc[6] += gb * (d0 * d2);
+        acc[7] += gb * (d1 * d1);
+        acc[8] += gb * (d1 * d2);
+        acc[9] += gb * (d2 * d2);
+      }
+    }
+  }
   // entries of this warp: [warp*32, warp*32+32) of the tile
-  for (int base = warp * 32; base < warp * 32 + 32; base += per_step) {
+  for (int base = warp * 32; base < (em_fast ? warp * 32 : warp * 32 + 32); base += per_step) {
     const int ei = base + slot;
     const bool act = ei < sm.tlen;
     const int e = sm.tstart + ei;
@@ -377,10 +440,9 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
 #pragma unroll
     for (int off = 1; off < 8; off <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
     const bool fin = act && isfinite(m);  // uniform within the 8-lane group
-    // each lane exponentiates its own term (exp_nonpos: the shifted argument
-    // is <= 0); the 8-term sum is a butterfly (the reference's sequential
-    // order, gmm.cpp:183, differs by rounding only)
-    const double ek = fin ? exp_nonpos(lg - m) : 0.0;
+    // each lane exponentiates its own term; the 8-term sum is a butterfly
+    // (the reference's sequential order, gmm.cpp:183, differs by rounding)
+    const double ek = fin ? exp(lg - m) : 0.0;
     double s = ek;
 #pragma unroll
     for (int off = 1; off < 8; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -390,7 +452,9 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     // the per-iteration log-likelihood only feeds the diagnostics trace
     // (gmm.cpp:240); the final pass (mode 2) always needs it (gmm.cpp:394)
     double lt = 0.0;
-    if (want_ll && fin) lt = m + log(s);
+    if (any_ll) {  // warp-uniform: no predicated log in the EM iterations
+      if (want_ll && fin) lt = m + log(s);
+    }
     double denom = 0.0;
     if (mode == 3)
       for (int s2 = 0; s2 < sm.ns; ++s2) denom += __shfl_sync(0xffffffffu, gam, gbase + sm.surv[s2]);
@@ -1128,13 +1192,23 @@ __global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
       if (mine) {
         // (a) tile pass
         const int T = __ldcg(&st->Tp[par]);
+        const bool tl6 = p.dbg == 6 && round == 2 && ph_i == 4;  // experiments: tile anatomy
+        if (tl6 && tid == 0) tl_mark_any(p.tl, 6000);
+        int ntl = 0, nent = 0;
         for (int t = cta; t < T; t += G) {
           load_tile_ctx(p, sm, ph, par, t);
           double* rec = p.partial + (size_t)t * kRec;
           tile_entry_pass(p, sm, ph, par, rec);
           if (ph.mode[0] || ph.mode[1]) tile_comp_pass(p, sm, ph, par, rec, false);
           if (ph.pcount) tile_comp_pass(p, sm, ph, par, rec, true);
+          ++ntl;
+          nent += sm.tlen;
           __syncthreads();
+        }
+        // per-CTA finish: label 6100 + tiles, entries in the next mark
+        if (tl6 && tid == 0) {
+          tl_mark_any(p.tl, 6100 + ntl);
+          tl_mark_any(p.tl, 200000 + nent);
         }
         grid_sync(p.bar, G);
         tl_mark(p.tl, round * 100 + ph_i);
@@ -1300,7 +1374,9 @@ __global__ void __launch_bounds__(kTile, 3) k_calibrate(BuildParams p) {
           GComp g;
           g.w = nd.weight;
           for (int q = 0; q < 3; ++q) g.mean[q] = mu[q];
-          if (comp_set_cov(g, S2, cov_floor(S2, p.eps, p.abs_floor))) atomicCAS(p.status, 0, kEInval);
+          double w[9];
+          for (int q = 0; q < 9; ++q) w[q] = nd.axT[q];
+          if (comp_set_cov(g, S2, cov_floor(S2, p.eps, p.abs_floor), w)) atomicCAS(p.status, 0, kEInval);
           double dc[3][3];
           for (int r = 0; r < 3; ++r)
             for (int c = 0; c < 3; ++c) dc[r][c] = g.cov[3 * r + c] - before[r][c];
@@ -1378,7 +1454,7 @@ __global__ void __launch_bounds__(kTile, 3) k_calibrate(BuildParams p) {
           }
         }
         __syncwarp();
-        if (lane == 0 && refresh_node(p.nodes[par], p.cov + 9 * (size_t)par))  // gmm.cpp:576-578
+        if (lane == 0 && refresh_node(p.nodes[par], p.cov + 9 * (size_t)par, true))  // gmm.cpp:576-578
           atomicCAS(p.status, 0, kEInval);
         __syncwarp();
         node = par;
