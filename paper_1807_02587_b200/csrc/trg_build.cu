@@ -246,9 +246,11 @@ struct BuildSmem {
       double red[16];
       double am[2];
     } s;
-    struct {
-      double acc[kTile / 32][2][8][11];
-    } e;
+    struct {                 // tile_comp_pass (entry-per-thread E-step)
+      double gam[16][kTile];  // responsibilities, component-major
+      double lt[2][kTile];    // w * log-likelihood per entry and candidate
+      int best;               // heaviest survivor (partition fallback)
+    } g;
     typename cub::BlockScan<unsigned long long, kTile>::TempStorage scan;
   } u;
   int nitems;
@@ -333,224 +335,145 @@ __device__ void tile_entry_pass(const BuildParams& p, BuildSmem& sm, const Phase
   }
 }
 
-// Lane-per-component E-step over the tile for the active candidates
-// (e_step_moments gmm.cpp:159-206, final pass :331-358, partition :430-454).
-// mode_pc: 0 = per phase modes, 3 = partition count (kept candidate).
+// E-step over one tile (e_step_moments gmm.cpp:159-206, final pass
+// :331-358, partition :430-454), in two block-wide steps:
+//  (1) entry per thread: the 8 (or 16, both candidates) component
+//      log-densities are independent (ILP, no shuffles), max / sum / log run
+//      in component order exactly like the reference, responsibilities go to
+//      shared memory component-major;
+//  (2) (candidate, component) per warp, entries over the lanes: the moments
+//      (mode 1), masses (mode 2) or survivor-normalised partition (mode 3),
+//      then a fixed butterfly over the lanes.
 __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase& ph, int par,
                                double* rec, bool pcount) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nc = pcount ? 1 : sm.ncand;
-  const int gsz = 8 * nc;          // lanes per entry
-  const int per_step = 32 / gsz;   // entries per warp step
-  const int comp = lane & 7;
-  const int ci = (lane >> 3) % nc;  // index into active candidate list
-  const int cand = pcount ? sm.kept : sm.cand_list[ci];
-  const int mode = pcount ? 3 : ph.mode[cand];
-  const int gbase = lane & ~7;  // first lane of my 8-lane group
-  double r[18];
-  comp_to_regs(sm.comp[cand][comp], r);
-  // survivor slot of my component (partition)
-  int my_s = -1;
-  if (pcount)
-    for (int s = 0; s < sm.ns; ++s)
-      if (sm.surv[s] == comp) my_s = s;
-  double acc[11];
+  const int tlen = sm.tlen;
+  auto& G = sm.u.g;
+  // ---- (1)
+  if (tid < tlen) {
+    const double x0 = sm.ent[0][tid], x1 = sm.ent[1][tid], x2 = sm.ent[2][tid], w = sm.ent[3][tid];
+    for (int ci = 0; ci < nc; ++ci) {
+      const int cand = pcount ? sm.kept : sm.cand_list[ci];
+      const int mode = pcount ? 3 : ph.mode[cand];
+      double lg[8];
+      double m = -INFINITY;
 #pragma unroll
-  for (int k = 0; k < 11; ++k) acc[k] = 0.0;
-  const int slot = lane / gsz;
-  const bool want_ll = mode == 2 || (mode == 1 && p.want_traces);
-  const bool any_ll = __any_sync(0xffffffffu, want_ll);
-  // EM iterations (mode 1 on every lane, no trace): two warp steps per loop
-  // trip, so the shuffle / exp latency chains of two entries overlap
-  const bool em_fast = __all_sync(0xffffffffu, mode == 1) && !any_ll;
-  if (em_fast) {
-    const double n0 = sm.nmean[0], n1 = sm.nmean[1], n2 = sm.nmean[2];
-    for (int base = warp * 32; base < warp * 32 + 32; base += 2 * per_step) {
-      const int ea = base + slot, eb = base + per_step + slot;
-      const bool aa = ea < sm.tlen, ab = eb < sm.tlen;
-      const double xa0 = aa ? sm.ent[0][ea] : 0.0, xa1 = aa ? sm.ent[1][ea] : 0.0,
-                   xa2 = aa ? sm.ent[2][ea] : 0.0, wa = aa ? sm.ent[3][ea] : 0.0;
-      const double xb0 = ab ? sm.ent[0][eb] : 0.0, xb1 = ab ? sm.ent[1][eb] : 0.0,
-                   xb2 = ab ? sm.ent[2][eb] : 0.0, wb = ab ? sm.ent[3][eb] : 0.0;
-      const double la = aa ? comp_log(r, xa0, xa1, xa2, p.status) : -INFINITY;
-      const double lb = ab ? comp_log(r, xb0, xb1, xb2, p.status) : -INFINITY;
-      double ma = la, mb = lb;
+      for (int k = 0; k < 8; ++k) {
+        double r[18];
+        comp_to_regs(sm.comp[cand][k], r);
+        lg[k] = comp_log(r, x0, x1, x2, p.status);
+        m = fmax(m, lg[k]);
+      }
+      const bool fin = isfinite(m);
+      double ek[8], s = 0.0;
 #pragma unroll
-      for (int off = 1; off < 8; off <<= 1) {
-        const double ta = __shfl_xor_sync(0xffffffffu, ma, off);
-        const double tb = __shfl_xor_sync(0xffffffffu, mb, off);
-        ma = fmax(ma, ta);
-        mb = fmax(mb, tb);
+      for (int k = 0; k < 8; ++k) {
+        ek[k] = fin ? exp(lg[k] - m) : 0.0;
+        s += ek[k];
       }
-      const bool fa = aa && isfinite(ma), fb = ab && isfinite(mb);
-      const double ka = fa ? exp(la - ma) : 0.0, kb = fb ? exp(lb - mb) : 0.0;
-      double sa = ka, sb = kb;
+      // gamma_k = exp(log_k - log_total) = e_k / s (gmm.cpp:189, 354): one
+      // reciprocal per entry instead of a second exp per component
+      const double rs = fin ? rcp_sum(s) : 0.0;
 #pragma unroll
-      for (int off = 1; off < 8; off <<= 1) {
-        const double ta = __shfl_xor_sync(0xffffffffu, sa, off);
-        const double tb = __shfl_xor_sync(0xffffffffu, sb, off);
-        sa += ta;
-        sb += tb;
-      }
-      const double ga = fa ? ka * rcp_sum(sa) * wa : 0.0;
-      const double gb = fb ? kb * rcp_sum(sb) * wb : 0.0;
-      if (ga > 0.0) {
-        const double d0 = xa0 - n0, d1 = xa1 - n1, d2 = xa2 - n2;
-        acc[0] += ga;
-        acc[1] += ga * d0;
-        acc[2] += ga * d1;
-        acc[3] += ga * d2;
-        acc[4] += ga * (d0 * d0);
-        acc[5] += ga * (d0 * d1);
-        acc[6] += ga * (d0 * d2);
-        acc[7] += ga * (d1 * d1);
-        acc[8] += ga * (d1 * d2);
-        acc[9] += ga * (d2 * d2);
-      }
-      if (gb > 0.0) {
-        const double d0 = xb0 - n0, d1 = xb1 - n1, d2 = xb2 - n2;
-        acc[0] += gb;
-        acc[1] += gb * d0;
-        acc[2] += gb * d1;
-        acc[3] += gb * d2;
-        acc[4] += gb * (d0 * d0);
-        acc[5] += gb * (d0 * d1);
-        acc[6] += gb * (d0 * d2);
-        acc[7] += gb * (d1 * d1);
-        acc[8] += gb * (d1 * d2);
-        acc[9] += gb * (d2 * d2);
-      }
+      for (int k = 0; k < 8; ++k) G.gam[ci * 8 + k][tid] = ek[k] * rs;
+      // the per-iteration log-likelihood only feeds the diagnostics trace
+      // (gmm.cpp:240); the final pass (mode 2) always needs it (gmm.cpp:394)
+      const bool want_ll = mode == 2 || (mode == 1 && p.want_traces);
+      G.lt[ci][tid] = (fin && want_ll) ? w * (m + log(s)) : 0.0;
     }
   }
-  // entries of this warp: [warp*32, warp*32+32) of the tile
-  for (int base = warp * 32; base < (em_fast ? warp * 32 : warp * 32 + 32); base += per_step) {
-    const int ei = base + slot;
-    const bool act = ei < sm.tlen;
-    const int e = sm.tstart + ei;
-    double x0 = 0, x1 = 0, x2 = 0, w = 0;
-    if (act) {
-      x0 = sm.ent[0][ei];
-      x1 = sm.ent[1][ei];
-      x2 = sm.ent[2][ei];
-      w = sm.ent[3][ei];
-    }
-    const double lg = act ? comp_log(r, x0, x1, x2, p.status) : -INFINITY;
-    // max over the 8 components (order-free; lg is never NaN)
-    double m = lg;
+  if (pcount && tid == 0) {  // heaviest survivor: the partition's fallback
+    int best = 0;
+    for (int s2 = 1; s2 < sm.ns; ++s2)
+      if (p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[s2]] >
+          p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[best]])
+        best = s2;
+    G.best = best;
+  }
+  __syncthreads();
+  // ---- (2)
+  if (!pcount) {
+    for (int item = warp; item < nc * 8; item += kTile / 32) {
+      const int ci = item >> 3, k = item & 7;
+      const int cand = sm.cand_list[ci];
+      const int mode = ph.mode[cand];
+      const double n0 = sm.nmean[0], n1 = sm.nmean[1], n2 = sm.nmean[2];
+      double a[11];
 #pragma unroll
-    for (int off = 1; off < 8; off <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    const bool fin = act && isfinite(m);  // uniform within the 8-lane group
-    // each lane exponentiates its own term; the 8-term sum is a butterfly
-    // (the reference's sequential order, gmm.cpp:183, differs by rounding)
-    const double ek = fin ? exp(lg - m) : 0.0;
-    double s = ek;
-#pragma unroll
-    for (int off = 1; off < 8; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    // gamma_k = exp(log_k - log_total) = e_k / s (gmm.cpp:189, 354): one
-    // reciprocal per entry instead of a second exp per component (ulp-level)
-    const double gam = fin ? ek * rcp_sum(s) : 0.0;
-    // the per-iteration log-likelihood only feeds the diagnostics trace
-    // (gmm.cpp:240); the final pass (mode 2) always needs it (gmm.cpp:394)
-    double lt = 0.0;
-    if (any_ll) {  // warp-uniform: no predicated log in the EM iterations
-      if (want_ll && fin) lt = m + log(s);
-    }
-    double denom = 0.0;
-    if (mode == 3)
-      for (int s2 = 0; s2 < sm.ns; ++s2) denom += __shfl_sync(0xffffffffu, gam, gbase + sm.surv[s2]);
-    if (!act) continue;
-    if (!fin) {
-      // gmm.cpp:348: the entry keeps gamma = 0; the partition then hands it
-      // whole to the heaviest survivor (gmm.cpp:444-453)
-      if (mode == 3 && my_s >= 0) {
-        int best = 0;
-        for (int s2 = 1; s2 < sm.ns; ++s2)
-          if (p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[s2]] >
-              p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[best]])
-            best = s2;
-        p.emit[(size_t)e * 8 + my_s] = my_s == best ? w : 0.0;
-        if (my_s == best) {
-          acc[0] += 1.0;
-          acc[1] += w;
+      for (int q = 0; q < 11; ++q) a[q] = 0.0;
+      for (int e = lane; e < tlen; e += 32) {
+        const double w = sm.ent[3][e];
+        const double g = G.gam[item][e] * w;
+        if (k == 0) a[10] += G.lt[ci][e];
+        if (mode == 1) {
+          if (g > 0.0) {
+            const double d0 = sm.ent[0][e] - n0, d1 = sm.ent[1][e] - n1, d2 = sm.ent[2][e] - n2;
+            a[0] += g;
+            a[1] += g * d0;
+            a[2] += g * d1;
+            a[3] += g * d2;
+            a[4] += g * (d0 * d0);
+            a[5] += g * (d0 * d1);
+            a[6] += g * (d0 * d2);
+            a[7] += g * (d1 * d1);
+            a[8] += g * (d1 * d2);
+            a[9] += g * (d2 * d2);
+          }
+        } else {
+          a[0] += g;  // mode 2: child mass (gmm.cpp:355)
         }
       }
-      continue;
-    }
-    if (mode == 1) {
-      if (comp == 0) acc[10] += w * lt;
-      const double g = gam * w;
-      if (g > 0.0) {
-        const double d0 = x0 - sm.nmean[0], d1 = x1 - sm.nmean[1], d2 = x2 - sm.nmean[2];
-        acc[0] += g;
-        acc[1] += g * d0;
-        acc[2] += g * d1;
-        acc[3] += g * d2;
-        acc[4] += g * (d0 * d0);
-        acc[5] += g * (d0 * d1);
-        acc[6] += g * (d0 * d2);
-        acc[7] += g * (d1 * d1);
-        acc[8] += g * (d1 * d2);
-        acc[9] += g * (d2 * d2);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < 11; ++q) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+      if (lane == 0) {
+        if (mode == 1) {
+          for (int q = 0; q < 10; ++q) rec[kOffEm + cand * 81 + k * 10 + q] = a[q];
+          if (k == 0) rec[kOffEm + cand * 81 + 80] = a[10];
+        } else {
+          rec[kOffFin + cand * 9 + 1 + k] = a[0];
+          if (k == 0) rec[kOffFin + cand * 9] = a[10];
+        }
       }
-    } else if (mode == 2) {
-      if (comp == 0) acc[10] += w * lt;
-      acc[0] += w * gam;
-    } else if (mode == 3) {
-      // survivor-normalised soft partition (gmm.cpp:434-454)
-      double* em = p.emit + (size_t)e * 8;
-      if (denom > 0.0) {
-        if (my_s >= 0) {
-          const double g = gam / denom;
-          double out = 0.0;
+    }
+  } else {
+    // survivor-normalised soft partition (gmm.cpp:434-454): warp = survivor
+    if (tid < 16) rec[kOffCnt + tid] = 0.0;
+    __syncthreads();
+    const int ns = sm.ns;
+    if (warp < ns) {
+      const int sv = warp, comp = sm.surv[sv], best = G.best;
+      double cnt = 0.0, mass = 0.0;
+      for (int e = lane; e < tlen; e += 32) {
+        const double w = sm.ent[3][e];
+        double denom = 0.0;
+        for (int s2 = 0; s2 < ns; ++s2) denom += G.gam[sm.surv[s2]][e];
+        double out = 0.0;
+        if (denom > 0.0) {
+          const double g = G.gam[comp][e] / denom;
           if (!(g < 1e-12)) {
             out = w * g;
-            acc[0] += 1.0;
-            acc[1] += out;
+            cnt += 1.0;
+            mass += out;
           }
-          em[my_s] = out;
+        } else if (sv == best) {  // all on pruned children, or no finite density
+          out = w;
+          cnt += 1.0;
+          mass += w;
         }
-      } else {
-        int best = 0;
-        for (int s2 = 1; s2 < sm.ns; ++s2)
-          if (p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[s2]] >
-              p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[best]])
-            best = s2;
-        if (my_s >= 0) {
-          const double out = my_s == best ? w : 0.0;
-          if (my_s == best) {
-            acc[0] += 1.0;
-            acc[1] += w;
-          }
-          em[my_s] = out;
-        }
+        p.emit[(size_t)(sm.tstart + e) * 8 + sv] = out;
       }
-    }
-  }
-  // reduce over entry slots (lanes with the same (cand, comp))
 #pragma unroll
-  for (int off = gsz; off < 32; off <<= 1)
-#pragma unroll
-    for (int k = 0; k < 11; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
-  if (lane < gsz)
-#pragma unroll
-    for (int k = 0; k < 11; ++k) sm.u.e.acc[warp][ci][comp][k] = acc[k];
-  __syncthreads();
-  // combine warps in order
-  for (int idx = tid; idx < nc * 8 * 11; idx += blockDim.x) {
-    const int c2 = idx / 88, cm = (idx / 11) % 8, k = idx % 11;
-    double s = sm.u.e.acc[0][c2][cm][k];
-    for (int w2 = 1; w2 < kTile / 32; ++w2) s += sm.u.e.acc[w2][c2][cm][k];
-    const int cand2 = pcount ? sm.kept : sm.cand_list[c2];
-    const int md = pcount ? 3 : ph.mode[cand2];
-    if (md == 1) {
-      if (k < 10) rec[kOffEm + cand2 * 81 + cm * 10 + k] = s;
-      else if (cm == 0) rec[kOffEm + cand2 * 81 + 80] = s;
-    } else if (md == 2) {
-      if (k == 0) rec[kOffFin + cand2 * 9 + 1 + cm] = s;
-      else if (k == 10 && cm == 0) rec[kOffFin + cand2 * 9] = s;
-    } else if (md == 3) {
-      if (k == 0) rec[kOffCnt + cm] = s;      // indexed by comp; remapped below
-      else if (k == 1) rec[kOffCnt + 8 + cm] = s;
+      for (int o = 16; o > 0; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        mass += __shfl_xor_sync(0xffffffffu, mass, o);
+      }
+      if (lane == 0) {
+        rec[kOffCnt + comp] = cnt;
+        rec[kOffCnt + 8 + comp] = mass;
+      }
     }
   }
   __syncthreads();
@@ -1145,8 +1068,12 @@ __device__ void write_xarg(const BuildParams& p, const Phase& ph, int par, int K
   }
 }
 
-__global__ void __launch_bounds__(kTile, 3) k_build(BuildParams p) {
-  __shared__ BuildSmem sm;
+#ifndef TRG_KBUILD_MINB
+#define TRG_KBUILD_MINB 3
+#endif
+__global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p) {
+  extern __shared__ __align__(16) unsigned char k_build_smem[];  // BuildSmem (> 48 KB static)
+  BuildSmem& sm = *reinterpret_cast<BuildSmem*>(k_build_smem);
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   BuildState* st = p.st;
@@ -1272,7 +1199,10 @@ inline int build_exchange_points_per_round(int em_iters) {
 // the same stream): parent moment match + refresh_eig, then the leaf
 // calibration passes.  Separate so its 3x3 eigen chains get a full register
 // budget while k_build's E-step passes keep 3 CTAs per SM.
-__global__ void __launch_bounds__(kTile, 3) k_calibrate(BuildParams p) {
+#ifndef TRG_KCAL_MINB
+#define TRG_KCAL_MINB 3
+#endif
+__global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams p) {
   __shared__ AssocSmem<10> asm_;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -1568,7 +1498,9 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
                o_kex = carve(sizeof(int) * (size_t)cap),
                o_car = carve(sizeof(unsigned) * ((size_t)cap + 1)), o_dbits = carve(16),
                o_state = carve(sizeof(BuildState));
-  const int G = persistent_grid(ctx, (const void*)k_build, kTile, 0);
+  TRG_CU(cudaFuncSetAttribute((const void*)k_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sizeof(BuildSmem)));
+  const int G = persistent_grid(ctx, (const void*)k_build, kTile, sizeof(BuildSmem));
   const int Gc = persistent_grid(ctx, (const void*)k_calibrate, kTile, 0);
   const size_t o_cd = carve(sizeof(double) * std::max(G, Gc));
   const int W = std::max(world, 1);
@@ -1699,7 +1631,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
 int build_launch(trg_ctx* ctx, BuildJob* job, int seg) {
   job->p.seg = seg;
   void* args[] = {&job->p};
-  TRG_CU(launch_persistent(ctx, (const void*)k_build, job->G, kTile, args));
+  TRG_CU(launch_persistent(ctx, (const void*)k_build, job->G, kTile, args, sizeof(BuildSmem)));
   ctx->launches += 1;
   return TRG_OK;
 }

@@ -119,10 +119,11 @@ int persistent_grid(trg_ctx* ctx, const void* kernel, int block, size_t smem) {
   return ctx->sms * per_sm;
 }
 
-cudaError_t launch_persistent(trg_ctx* ctx, const void* kernel, int G, int block, void** args) {
+cudaError_t launch_persistent(trg_ctx* ctx, const void* kernel, int G, int block, void** args,
+                              size_t smem) {
   if (ctx->sms < ctx->device_sms)
-    return cudaLaunchKernel(kernel, dim3(G), dim3(block), args, 0, ctx->stream);
-  return cudaLaunchCooperativeKernel(kernel, dim3(G), dim3(block), args, 0, ctx->stream);
+    return cudaLaunchKernel(kernel, dim3(G), dim3(block), args, smem, ctx->stream);
+  return cudaLaunchCooperativeKernel(kernel, dim3(G), dim3(block), args, smem, ctx->stream);
 }
 
 int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out) {

@@ -205,7 +205,8 @@ int persistent_grid(trg_ctx* ctx, const void* kernel, int block, size_t smem);
 // the driver).  SM-budgeted contexts (trg_ctx_set_sm_budget) use a plain
 // launch so several contexts' persistent kernels run concurrently: their
 // budgets sum to at most the device's SMs, so every grid stays co-resident.
-cudaError_t launch_persistent(trg_ctx* ctx, const void* kernel, int G, int block, void** args);
+cudaError_t launch_persistent(trg_ctx* ctx, const void* kernel, int G, int block, void** args,
+                              size_t smem = 0);
 
 // ---- association (trg_assoc.cu)
 struct AssocParams {
