@@ -507,7 +507,11 @@ __device__ void node_mstep(const BuildParams& p, int k, int c, const double* red
   g.lw = log(g.w);
   const double* mean = p.nf.mean + 3 * k;
   for (int i = 0; i < 3; ++i) g.mean[i] = mean[i] + d[i];
-  if (comp_set_cov(g, sc, p.nf.floorv[k])) atomicCAS(p.status, 0, kEInval);
+  // the eigensolve starts from the component's previous axes: EM moves the
+  // covariance a little per iteration, so the warm Jacobi needs ~1 sweep
+  double warm[9];
+  for (int i = 0; i < 9; ++i) warm[i] = g.axT[i];
+  if (comp_set_cov(g, sc, p.nf.floorv[k], warm)) atomicCAS(p.status, 0, kEInval);
 }
 
 // Candidate init (fit_candidate gmm.cpp:319-326) for component `comp`.
