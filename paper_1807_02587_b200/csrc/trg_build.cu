@@ -113,6 +113,7 @@ struct BuildParams {
   double* cal_moments;  // [J][10]
   double* cta_drift;    // [G]
   unsigned* cal_arrive;  // [capacity + 1] last-arriver counters (+ virtual root)
+  int2* cal_up;          // [capacity] (parent, parent's child count) for the climb
   unsigned long long* drift_bits;  // [2] per-pass max drift (bits of a double >= 0)
   int* layout_scratch;  // [6 * 8 * Kmax]
   double* ll_trace;     // [capacity][2][em_iters + 1] per expansion, both candidates
@@ -1224,8 +1225,11 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
     if (cta == 0) reset_parents(p, lvl);
     grid_sync(p.bar, G);
     tl_mark(p.tl, 901);
-    for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x)
+    for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x) {
       if (refresh_node(p.nodes[j], p.cov + 9 * (size_t)j)) atomicCAS(p.status, 0, kEInval);
+      const int par = p.nodes[j].parent;
+      p.cal_up[j] = make_int2(par, par >= 0 ? p.nodes[par].child_count : lvl[1] - lvl[0]);
+    }
     grid_sync(p.bar, G);
     tl_mark(p.tl, 902);
   }
@@ -1328,9 +1332,10 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
       for (;;) {
         int par = 0, last = 0, need = 0;
         if (lane == 0) {
-          par = __ldcg(&p.nodes[node].parent);
+          const int2 up = __ldcg(&p.cal_up[node]);
+          par = up.x;
+          need = up.y;
           unsigned* ctr = par >= 0 ? &p.cal_arrive[par] : &p.cal_arrive[p.capacity];
-          need = par >= 0 ? __ldcg(&p.nodes[par].child_count) : root_count;
           __threadfence();
           last = atomicAdd(ctr, 1u) == (unsigned)need - 1;
           if (last) {
@@ -1344,18 +1349,22 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
         need = __shfl_sync(0xffffffffu, need, 0);
         const int first = par >= 0 ? __ldcg(&p.nodes[par].first_child) : 0;
         const int count = need;
-        // lane c < count holds child c: branch mass, weight, mean, cov
-        const int ci = first + (lane < count ? lane : 0);
-        const double cb = lane < count ? __ldcg(&branch[(size_t)ci * 10]) : 0.0;
-        double cwt = __ldcg(&p.nodes[ci].weight);
+        // lane c < count holds child c (<= 8 children); sums over the
+        // children are fixed full-warp butterflies (idle lanes add 0), so
+        // every lane holds the same totals
+        const bool own = lane < count;
+        const int ci = first + (own ? lane : 0);
+        const double cb = own ? __ldcg(&branch[(size_t)ci * 10]) : 0.0;
+        double cwt = own ? __ldcg(&p.nodes[ci].weight) : 0.0;
         double cm[3], cc[9];
-        for (int k = 0; k < 3; ++k) cm[k] = __ldcg(&p.nodes[ci].mean[k]);
-        for (int k = 0; k < 9; ++k) cc[k] = __ldcg(&p.cov[9 * (size_t)ci + k]);
-        // branch mass and sibling reweight (gmm.cpp:547-566): sequential sum
-        double sb = 0.0;
-        for (int c = 0; c < count; ++c) sb += __shfl_sync(0xffffffffu, cb, c);
+        for (int k = 0; k < 3; ++k) cm[k] = own ? __ldcg(&p.nodes[ci].mean[k]) : 0.0;
+        for (int k = 0; k < 9; ++k) cc[k] = own ? __ldcg(&p.cov[9 * (size_t)ci + k]) : 0.0;
+        // branch mass and sibling reweight (gmm.cpp:547-566)
+        double sb = cb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) sb += __shfl_xor_sync(0xffffffffu, sb, o);
         if (par >= 0 && lane == 0) branch[(size_t)par * 10] = sb;
-        if (sb > 0.0 && lane < count) {
+        if (sb > 0.0 && own) {
           const double w = cb / sb;
           drift = smax(drift, fabs(cwt - w));
           cwt = w;
@@ -1363,32 +1372,35 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
         }
         if (tl5 && lane == 0) tl_mark_any(p.tl, par < 0 ? 5020 : 5010 + __ldcg(&p.nodes[par].level));
         if (par < 0) break;  // top octet done
-        // parent moment match (gmm.cpp:489-513), sums in child order
-        double w = 0.0, mu[3] = {0.0, 0.0, 0.0};
-        for (int c = 0; c < count; ++c) {
-          const double wc = __shfl_sync(0xffffffffu, cwt, c);
-          w += wc;
-          for (int k = 0; k < 3; ++k) mu[k] = mu[k] + wc * __shfl_sync(0xffffffffu, cm[k], c);
-        }
+        // parent moment match (gmm.cpp:489-513)
+        double v[4] = {cwt, cwt * cm[0], cwt * cm[1], cwt * cm[2]};
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+        const double w = v[0];
+        double cvn[9];
         if (w > 0.0) {
-          for (int k = 0; k < 3; ++k) mu[k] = mu[k] / w;
-          double cv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-          for (int c = 0; c < count; ++c) {
-            const double wc = __shfl_sync(0xffffffffu, cwt, c);
-            double d[3], cov9[9];
-            for (int k = 0; k < 3; ++k) d[k] = __shfl_sync(0xffffffffu, cm[k], c) - mu[k];
-            for (int k = 0; k < 9; ++k) cov9[k] = __shfl_sync(0xffffffffu, cc[k], c);
-            for (int r = 0; r < 3; ++r)
-              for (int q = 0; q < 3; ++q)
-                cv[3 * r + q] = cv[3 * r + q] + wc * (cov9[3 * r + q] + d[r] * d[q]);
-          }
+          const double mu[3] = {v[1] / w, v[2] / w, v[3] / w};
+          const double d[3] = {cm[0] - mu[0], cm[1] - mu[1], cm[2] - mu[2]};
+          double cv[9];
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) cv[3 * r + q] = cwt * (cc[3 * r + q] + d[r] * d[q]);
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+            for (int k = 0; k < 9; ++k) cv[k] += __shfl_xor_sync(0xffffffffu, cv[k], o);
+          for (int k = 0; k < 9; ++k) cvn[k] = cv[k] / w;
           if (lane == 0) {
-            for (int k = 0; k < 9; ++k) p.cov[9 * (size_t)par + k] = cv[k] / w;
+            for (int k = 0; k < 9; ++k) p.cov[9 * (size_t)par + k] = cvn[k];
             for (int k = 0; k < 3; ++k) p.nodes[par].mean[k] = mu[k];
           }
+        } else {
+          for (int k = 0; k < 9; ++k) cvn[k] = __ldcg(&p.cov[9 * (size_t)par + k]);
         }
-        __syncwarp();
-        if (lane == 0 && refresh_node(p.nodes[par], p.cov + 9 * (size_t)par, true))  // gmm.cpp:576-578
+        if (lane == 0 && refresh_node(p.nodes[par], cvn, true))  // gmm.cpp:576-578
           atomicCAS(p.status, 0, kEInval);
         __syncwarp();
         node = par;
@@ -1501,6 +1513,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
                o_llt = carve(sizeof(double) * (size_t)cap * 2 * (cfg->em_iterations_per_node + 1)),
                o_kex = carve(sizeof(int) * (size_t)cap),
                o_car = carve(sizeof(unsigned) * ((size_t)cap + 1)), o_dbits = carve(16),
+               o_up = carve(sizeof(int2) * (size_t)cap),
                o_state = carve(sizeof(BuildState));
   TRG_CU(cudaFuncSetAttribute((const void*)k_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)sizeof(BuildSmem)));
@@ -1556,6 +1569,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   p.ll_trace = (double*)(A + o_llt);
   p.kept_exp = (int*)(A + o_kex);
   p.cal_arrive = (unsigned*)(A + o_car);
+  p.cal_up = (int2*)(A + o_up);
   p.drift_bits = (unsigned long long*)(A + o_dbits);
   p.bar = (unsigned*)(A + o_bar);
   p.st = (BuildState*)(A + o_state);

@@ -4,7 +4,7 @@
 # exited 0 without ncu).
 set -x
 mkdir -p gpurun_out
-CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --batch 0"
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --batch 0 --c4 0"
 $CMD > gpurun_out/plain.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
