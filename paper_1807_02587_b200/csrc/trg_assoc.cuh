@@ -35,6 +35,19 @@ __device__ __forceinline__ double node_score(const DNode* __restrict__ g, double
   return sc;
 }
 
+// Score for the descent without an early return, so the <= 8 sibling
+// evaluations are straight-line code; `bad` collects the non-PD error.
+__device__ __forceinline__ double node_score_nb(const DNode* __restrict__ g, double y0, double y1,
+                                                double y2, bool& bad) {
+  const double w = g->weight;
+  const double lam2 = g->lam[2];
+  const double q = fast_q(g->mean, g->axT, g->il, y0, y1, y2);
+  const double sc = __dmul_rn(w, exp(__fma_rn(-0.5, q, g->log_norm)));
+  const bool live = w > 0.0;
+  bad = bad || (live && !(lam2 > 0.0));
+  return (live && lam2 > 0.0) ? sc : 0.0;
+}
+
 struct Descent {
   int node;       // stop node, -1 = outlier
   double path;    // product of sibling-normalised responsibilities
@@ -42,20 +55,33 @@ struct Descent {
 };
 
 // association.cpp:117-150 for one transformed point y.
-__device__ __forceinline__ Descent descend(const DNode* __restrict__ nodes, int root_count,
-                                           int depth, double lambda_c, double outlier_floor,
-                                           double y0, double y1, double y2, int* status) {
+__device__ __forceinline__ Descent descend(const DNode* __restrict__ nodes, const DNode* snodes,
+                                           int n_snodes, int root_count, int depth,
+                                           double lambda_c, double outlier_floor, double y0,
+                                           double y1, double y2, int* status) {
   Descent r{-1, 1.0, 0};
   int node = -1;
+#ifdef TRG_DESCENT_PROBE
+  long long tp[8];
+  int np = 0;
+  tp[np++] = clock64();
+#endif
   for (int l = 0; l < depth; ++l) {
-    const int first = node < 0 ? 0 : nodes[node].first_child;
-    const int count = node < 0 ? root_count : nodes[node].child_count;
+    const DNode* cur = node < n_snodes ? snodes + node : nodes + node;
+    const int first = node < 0 ? 0 : cur->first_child;
+    const int count = node < 0 ? root_count : cur->child_count;
+    // siblings from the shared-memory stage when the whole run is staged
+    const DNode* sib = first + count <= n_snodes ? snodes + first : nodes + first;
     // the <= 8 sibling scores are independent: evaluate them together (ILP),
     // then sum and arg-max in sibling order exactly like the reference
     double sc[8];
+    bool bad = false;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      sc[k] = k < count ? node_score(nodes + first + k, y0, y1, y2, status) : 0.0;
+    for (int k = 0; k < 8; ++k) {
+      const double v = node_score_nb(sib + (k < count ? k : 0), y0, y1, y2, bad);
+      sc[k] = k < count ? v : 0.0;
+    }
+    if (bad) atomicCAS(status, 0, kEDomain);  // log_density: covariance is not PD
     double sum = 0.0, best_s = 0.0;
     int best = 0;
 #pragma unroll
@@ -75,16 +101,39 @@ __device__ __forceinline__ Descent descend(const DNode* __restrict__ nodes, int 
     if (!(sum > 0.0)) break;  // deeper underflow: keep the current node
     node = first + best;
     r.path *= best_s / sum;
-    const DNode* nd = nodes + node;
+    const DNode* nd = sib + best;
     if (nd->child_count == 0) break;
     if (nd->cplx < 0.0) {
       atomicCAS(status, 0, kEDomain);  // node_complexity: no positive trace
       break;
     }
     if (nd->cplx <= lambda_c) break;
+#ifdef TRG_DESCENT_PROBE
+    tp[np++] = clock64();
+#endif
   }
+#ifdef TRG_DESCENT_PROBE
+  tp[np++] = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0 && lambda_c == 0.0)
+    printf("descent cycles: %lld %lld %lld (levels %d)\n", np > 1 ? tp[1] - tp[0] : -1LL,
+           np > 2 ? tp[2] - tp[1] : -1LL, np > 3 ? tp[3] - tp[2] : -1LL, np - 1);
+#endif
   r.node = node;
   return r;
+}
+
+// Upper levels staged per CTA (18 KB): the descent's first L-1 levels then
+// read shared memory; the last level reads global memory.
+constexpr int kStageNodes = 96;
+
+// Copies nodes [0, S) into the stage (16-byte loads through L2: another CTA
+// may have rewritten them since this SM last read them).  Block-wide.
+__device__ __forceinline__ void stage_nodes(DNode* snodes, const DNode* __restrict__ nodes, int S) {
+  const int4* src = reinterpret_cast<const int4*>(nodes);
+  int4* dst = reinterpret_cast<int4*>(snodes);
+  const int n16 = S * (int)(sizeof(DNode) / 16);
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldcg(src + i);
+  __syncthreads();
 }
 
 // Deposit vector of one point (association.cpp:20-23): NM = 4 -> (g, g y),
@@ -249,8 +298,8 @@ __device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double
         d.path = 0.5;
         d.evals = 1;
       } else {
-        d = descend(p.nodes, p.root_count, p.depth, p.lambda_c, p.outlier_floor, y0, y1, y2,
-                    p.status);
+        d = descend(p.nodes, p.snodes, p.n_snodes, p.root_count, p.depth, p.lambda_c,
+                    p.outlier_floor, y0, y1, y2, p.status);
       }
       my_ev += d.evals;
       if (d.node < 0) {

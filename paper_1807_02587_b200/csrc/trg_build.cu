@@ -1245,6 +1245,9 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
   // all-reduced leaf moments in xcal) and stage 1 of pass s up to the local
   // leaf combine, then exits for the exchange.
   const int root_count = lvl[1] - lvl[0];
+  extern __shared__ __align__(16) unsigned char k_cal_stage[];  // upper levels for the descent
+  DNode* cal_stage = reinterpret_cast<DNode*>(k_cal_stage);
+  const int n_stage = min(p.L >= 2 ? lvl[p.L - 1] : 0, kStageNodes);
   for (int pass = 0; pass < 40; ++pass) {
     const bool run_s1 = !sharded || p.seg == pass;
     const bool run_s2 = !sharded || p.seg == pass + 1;
@@ -1253,6 +1256,8 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
     a.n_nodes = J;
     a.root_count = root_count;
     a.epoch = p.a.epoch + (uint32_t)pass;
+    a.snodes = cal_stage;
+    a.n_snodes = n_stage;
     const bool tl5 = p.dbg == 5 && pass == 10;  // experiments: fine marks of one pass
     if (run_s1) {
       if (pass > 0) {
@@ -1263,6 +1268,7 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
         }
       }
       if (cta == 0 && tid == 0) p.drift_bits[pass & 1] = 0ull;
+      stage_nodes(cal_stage, p.nodes, n_stage);  // stage 2 rewrote them
       assoc_pass<10>(asm_, a, nullptr, G, cta);
       if (tl5) tl_mark(p.tl, 5001);
       grid_sync(p.bar, G);
@@ -1518,7 +1524,10 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   TRG_CU(cudaFuncSetAttribute((const void*)k_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)sizeof(BuildSmem)));
   const int G = persistent_grid(ctx, (const void*)k_build, kTile, sizeof(BuildSmem));
-  const int Gc = persistent_grid(ctx, (const void*)k_calibrate, kTile, 0);
+  const size_t cal_smem = sizeof(DNode) * kStageNodes;
+  TRG_CU(cudaFuncSetAttribute((const void*)k_calibrate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)cal_smem));
+  const int Gc = persistent_grid(ctx, (const void*)k_calibrate, kTile, cal_smem);
   const size_t o_cd = carve(sizeof(double) * std::max(G, Gc));
   const int W = std::max(world, 1);
   const size_t o_xa = carve(sizeof(double) * 8 * K), o_xaa = carve(sizeof(double) * 8 * K * W),
@@ -1657,7 +1666,8 @@ int build_launch(trg_ctx* ctx, BuildJob* job, int seg) {
 int calibrate_launch(trg_ctx* ctx, BuildJob* job, int seg) {
   job->p.seg = seg;
   void* args[] = {&job->p};
-  TRG_CU(launch_persistent(ctx, (const void*)k_calibrate, job->Gc, kTile, args));
+  TRG_CU(launch_persistent(ctx, (const void*)k_calibrate, job->Gc, kTile, args,
+                           sizeof(DNode) * kStageNodes));
   ctx->launches += 1;
   return TRG_OK;
 }
@@ -1686,6 +1696,7 @@ int build_collect(trg_ctx* ctx, BuildJob* job, const trg_model_config* cfg, trg_
   }
   tree->n_nodes = st.J;
   tree->root_count = st.root_count;
+  tree->n_upper = L >= 2 ? st.lvl_start[L - 1] : 0;
   TRG_TRY(timeline_fetch(ctx));
   if (diag) {
     for (int r = 0; r < 8; ++r) {

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "trg_internal.cuh"
+#include "trg_assoc.cuh"
 
 namespace {
 thread_local std::string g_last_error;
@@ -312,6 +313,11 @@ int trg_tree_upload(trg_ctx* ctx, const trg_tree* h, trg_tree_dev** out) {
   t->n_nodes = J;
   t->max_level = h->max_level;
   t->root_count = root_count;
+  {
+    int up = 0;  // BFS prefix above the deepest level
+    while (up < J && h->level[up] < h->max_level - 1) ++up;
+    t->n_upper = up;
+  }
   TRG_CU(trg_memcpy(ctx, t->nodes, nodes.data(), sizeof(DNode) * J, cudaMemcpyHostToDevice));
   TRG_CU(trg_memcpy(ctx, t->cov, h->cov, sizeof(double) * 9 * J, cudaMemcpyHostToDevice));
   TRG_CU(cudaStreamSynchronize(ctx->stream));
@@ -393,6 +399,7 @@ int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, siz
   p.nodes = tree->nodes;
   p.n_nodes = J;
   p.root_count = tree->root_count;
+  p.n_snodes = std::min(tree->n_upper, kStageNodes);
   p.depth = depth;
   p.lambda_c = cfg->lambda_c;
   p.outlier_floor = cfg->outlier_floor;

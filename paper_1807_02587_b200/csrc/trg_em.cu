@@ -76,12 +76,17 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
   __syncthreads();
   if (s_done) return;
   const double trans_limit = ldcg(&p.st->trans_limit);
+  // the model is fixed during the EM: stage its upper levels once
+  extern __shared__ __align__(16) unsigned char k_reg_stage[];
+  DNode* reg_stage = reinterpret_cast<DNode*>(k_reg_stage);
+  if (!DENSE) stage_nodes(reg_stage, p.a.nodes, p.a.n_snodes);
   for (int it = 0; it < p.max_iters; ++it) {
     const bool run_e = !sharded || p.seg == it;      // E-step of iteration it
     const bool run_m = !sharded || p.seg == it + 1;  // combine/solve of iteration it
     if (!run_e && !run_m) continue;
     AssocParams a = p.a;
     a.epoch = p.epoch0 + (uint32_t)it;
+    a.snodes = reg_stage;
     if (run_e) {
       // ---- P1: E-step over this CTA's point tiles
       tl_mark(p.tl, 2000 + it * 10);
@@ -398,6 +403,7 @@ namespace {
 
 struct EmJob {
   const void* kernel = nullptr;
+  size_t smem = 0;
   EmParams p;
   int G = 0, J = 0, K = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -410,11 +416,15 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
                EmJob* job, bool dense = false) {
   const int J = tree->n_nodes;
   job->kernel = dense ? (const void*)k_register<true> : (const void*)k_register<false>;
-  const int G = persistent_grid(ctx, job->kernel, kAssocBlock, 0);
+  job->smem = dense ? 0 : sizeof(DNode) * kStageNodes;
+  TRG_CU(cudaFuncSetAttribute(job->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)std::max<size_t>(job->smem, 1)));
+  const int G = persistent_grid(ctx, job->kernel, kAssocBlock, job->smem);
   EmParams p{};
   p.a.nodes = tree->nodes;
   p.a.n_nodes = J;
   p.a.root_count = tree->root_count;
+  p.a.n_snodes = dense ? 0 : std::min(tree->n_upper, kStageNodes);
   p.a.depth = tree->max_level;
   p.a.lambda_c = cfg->variant_kind == TRG_VARIANT_TREE ? 0.0 : cfg->lambda_c;
   p.a.outlier_floor = 1e-300;
@@ -477,7 +487,7 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
 int em_launch(trg_ctx* ctx, EmJob* job, int seg) {
   if (job->p.seg >= 0) job->p.seg = seg;
   void* args[] = {&job->p};
-  TRG_CU(launch_persistent(ctx, job->kernel, job->G, kAssocBlock, args));
+  TRG_CU(launch_persistent(ctx, job->kernel, job->G, kAssocBlock, args, job->smem));
   ctx->launches += 1;
   return TRG_OK;
 }

@@ -63,6 +63,7 @@ __device__ __forceinline__ double fast_q(const double* mean, const double* axT, 
 
 struct trg_tree_dev {
   int n_nodes = 0, max_level = 0, capacity = 0, root_count = 0;
+  int n_upper = 0;  // nodes above the deepest level (BFS prefix; staged in smem by the descent)
   trg::DNode* nodes = nullptr;  // [capacity]
   double* cov = nullptr;        // [capacity*9] row-major
   int* owner_ctx_device = nullptr;
@@ -224,6 +225,10 @@ struct AssocParams {
   double* point_w;               // nullable
   int* status;
   int dbg_mode;                  // 0 normal; experiments: 1 skip reduction, 2 skip descent
+  // nodes [0, n_snodes) read from a shared-memory copy (the calling kernel
+  // stages them): the tree's upper levels, visited by every point
+  const trg::DNode* snodes;
+  int n_snodes;
 };
 int launch_associate(trg_ctx* ctx, const AssocParams& p, int nm, double* moments /*[J][nm]*/,
                      int grid);
