@@ -333,6 +333,9 @@ __device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double
 }
 
 // Sum node j's partial rows over CTAs in fixed order (one warp per node).
+// Rows are read in batches of 4 per lane with the stamp test as a select,
+// so the loads of a batch are all in flight together (a branch per row
+// serialises the L2 round trips); skipped rows add exactly 0.
 template <int NM>
 __device__ __forceinline__ void combine_node(const double* __restrict__ partials,
                                              const uint32_t* __restrict__ stamps, uint32_t epoch,
@@ -341,12 +344,27 @@ __device__ __forceinline__ void combine_node(const double* __restrict__ partials
   double acc[NM];
 #pragma unroll
   for (int m = 0; m < NM; ++m) acc[m] = 0.0;
-  for (int c = lane; c < G; c += 32) {
-    const size_t row = (size_t)j * G + c;
-    if (stamps[row] == epoch) {
+  const size_t base = (size_t)j * G;
+  for (int c0 = lane; c0 < G; c0 += 128) {
+    uint32_t st[4];
 #pragma unroll
-      for (int m = 0; m < NM; ++m) acc[m] += partials[row * NM + m];
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 32 * u;
+      st[u] = c < G ? __ldcg(stamps + base + c) : 0u;
     }
+    double v[4][NM];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 32 * u;
+      const bool ok = c < G && st[u] == epoch;
+      const double* row = partials + (base + (ok ? c : 0)) * NM;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) v[u][m] = ok ? __ldcg(row + m) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int m = 0; m < NM; ++m) acc[m] += v[u][m];
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1)
