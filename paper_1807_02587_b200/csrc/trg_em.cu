@@ -87,6 +87,10 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
     AssocParams a = p.a;
     a.epoch = p.epoch0 + (uint32_t)it;
     a.snodes = reg_stage;
+    // per-iteration counters alternate between two slots: CTA 0 reads and
+    // clears slot it&1 in P3 while faster CTAs may already count iteration
+    // it+1's evaluations (slot (it+1)&1); nobody reaches it+2 before that
+    a.counters = p.a.counters + 2 * (it & 1);
     if (run_e) {
       // ---- P1: E-step over this CTA's point tiles
       tl_mark(p.tl, 2000 + it * 10);
