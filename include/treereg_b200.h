@@ -300,6 +300,12 @@ int trg_synth_kinect_pair(uint64_t seed, double* target, double* source, double 
 int trg_synth_kinect_pair_ex(uint64_t seed, double noise_scale, double rot_range_deg,
                              double trans_range, double* target, double* source, double R_gt[9],
                              double t_gt[3]);
+/* A Kinect-style frame sequence (frames x 76,800 points): camera k is
+ * camera k-1 moved by random_rigid_transform({step_rot_deg, step_trans},
+ * trial k) in its own frame; R_gt/t_gt [frames][9]/[3] map frame k into
+ * frame 0 (the trajectory a sequence registration recovers). */
+int trg_synth_kinect_sequence(uint64_t seed, int frames, double step_rot_deg, double step_trans,
+                              double* out, double* R_gt, double* t_gt);
 /* HDL-32-style sweep pair (72,000 points each). */
 int trg_synth_lidar_pair(uint64_t seed, double* target, double* source, double R_gt[9],
                          double t_gt[3]);

@@ -131,6 +131,7 @@ SIGNATURES = {
     "trg_bbox_diagonal": (C.c_double, [dp, C.c_size_t]),
     "trg_random_rigid_transform": (C.c_int, [C.c_double, C.c_double, C.c_uint64, C.c_int, dp,
                                              dp]),
+    "trg_synth_kinect_sequence": (C.c_int, [C.c_uint64, C.c_int, C.c_double, C.c_double, dp, dp, dp]),
     "trg_synth_kinect_pair": (C.c_int, [C.c_uint64, dp, dp, dp, dp]),
     "trg_synth_kinect_pair_ex": (C.c_int, [C.c_uint64, C.c_double, C.c_double, C.c_double, dp, dp,
                                            dp, dp]),

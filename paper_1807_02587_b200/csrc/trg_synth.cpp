@@ -510,6 +510,31 @@ int trg_synth_kinect_pair_ex(uint64_t seed, double noise_scale, double rot_deg, 
   return TRG_OK;
 }
 
+int trg_synth_kinect_sequence(uint64_t seed, int frames, double step_rot_deg, double step_trans,
+                              double* out, double* R_gt, double* t_gt) {
+  if (frames < 1 || !out || !R_gt || !t_gt) return TRG_EINVAL;
+  double R0[9], t0[3];
+  look_at({3.4, 1.5, 2.6}, {1.2, 0.7, 0.9}, R0, t0);
+  double Rk[9], tk[3];
+  for (int i = 0; i < 9; ++i) Rk[i] = R0[i];
+  for (int i = 0; i < 3; ++i) tk[i] = t0[i];
+  Rng rng(splitmix64(seed + 0x53657175656e6365ull));
+  for (int k = 0; k < frames; ++k) {
+    if (k > 0) {  // camera k = camera k-1 moved by a random step in its own frame
+      double dR[9], dt[3], Rn[9], tn[3];
+      rigid(step_rot_deg, step_trans, seed, k, dR, dt);
+      matmul(Rk, dR, Rn);
+      for (int i = 0; i < 3; ++i)
+        tn[i] = tk[i] + Rk[3 * i] * dt[0] + Rk[3 * i + 1] * dt[1] + Rk[3 * i + 2] * dt[2];
+      for (int i = 0; i < 9; ++i) Rk[i] = Rn[i];
+      for (int i = 0; i < 3; ++i) tk[i] = tn[i];
+    }
+    render_kinect(Rk, tk, rng, out + (size_t)k * 76800 * 3, 1.0);
+    relative(R0, t0, Rk, tk, R_gt + 9 * (size_t)k, t_gt + 3 * (size_t)k);  // frame k -> frame 0
+  }
+  return TRG_OK;
+}
+
 int trg_synth_kinect_pair(uint64_t seed, double* target, double* source, double R_gt[9],
                           double t_gt[3]) {
   return trg_synth_kinect_pair_ex(seed, 1.0, 5.0, 0.05, target, source, R_gt, t_gt);

@@ -522,6 +522,23 @@ def register_batch(targets, sources, config: RegistrationConfig = RegistrationCo
     return [_result(arr[i], cb, ca, ev) for i, (_, cb, ca, ev) in enumerate(bufs)]
 
 
+def register_sequence(frames, config: RegistrationConfig = RegistrationConfig(),
+                      ctx: Context | None = None, streams: int = 0):
+    """Frame-to-frame sequence (the reference harness's run_sequence core,
+    harness.cpp:334-389): pair k registers frame k (source) to frame k-1
+    (target) and the trajectory chains T_k = T_{k-1} * pairwise_k (frame k ->
+    frame 0).  All pairs go through register_batch, so the GPU overlaps the
+    tree builds and EM loops of consecutive pairs.  Returns (pairwise
+    results, trajectory)."""
+    if len(frames) < 2:
+        raise InvalidArgument("sequence: need at least 2 frames")
+    res = register_batch(list(frames[:-1]), list(frames[1:]), config, ctx, streams)
+    traj = [RigidTransform.identity()]
+    for r in res:
+        traj.append(traj[-1] * r.transform)
+    return res, traj
+
+
 # ------------------------------------------------------------------ flat mixture
 def build_flat_gmm(cloud, j: int, config: ModelConfig = ModelConfig(),
                    diagnostics: BuildDiagnostics | None = None,
@@ -723,6 +740,16 @@ def kinect_pair(seed: int):
     tg, sr, R, t = np.zeros((76800, 3)), np.zeros((76800, 3)), np.zeros((3, 3)), np.zeros(3)
     _chk(_lib.lib().trg_synth_kinect_pair(seed, _d(tg), _d(sr), _d(R), _d(t)))
     return tg, sr, RigidTransform(R, t)
+
+
+def kinect_sequence(seed: int, frames: int, step_rot_deg: float = 2.0, step_trans: float = 0.02):
+    """Kinect-style frame sequence -> (frames [F, 76800, 3], gt [F] RigidTransform
+    mapping frame k into frame 0)."""
+    out = np.zeros((frames, 76800, 3))
+    R, t = np.zeros((frames, 3, 3)), np.zeros((frames, 3))
+    _chk(_lib.lib().trg_synth_kinect_sequence(seed, frames, step_rot_deg, step_trans, _d(out), _d(R),
+                                              _d(t)))
+    return out, [RigidTransform(R[k], t[k]) for k in range(frames)]
 
 
 def lidar_pair(seed: int):

@@ -60,3 +60,28 @@ def test_batch_errors(ctx):
     with pytest.raises(tr.InvalidArgument):
         tr.register_batch([g["points"]], [g["src"]], cfg, ctx, 17)
     assert tr.register_batch([], [], cfg, ctx) == []
+
+
+def test_register_sequence_matches_reference(ctx):
+    """Frame-to-frame sequence: every link and the chained
+    trajectory against the reference's register_clouds on the same frames
+    (tests/golden/make_golden_seq.py); each link also equals a one-pair call."""
+    import os
+    from tests.helpers import GOLDEN
+    tr = _tr()
+    z = np.load(os.path.join(GOLDEN, "seq_kinect5.npz"))
+    frames, gt = tr.kinect_sequence(11, 5, step_rot_deg=2.0, step_trans=0.02)
+    assert np.array_equal(np.array([[f.sum(), np.abs(f).sum()] for f in frames]), z["frames_sum"])
+    cfg = tr.RegistrationConfig(variant=tr.Variant("adaptive", 3))
+    res, traj = tr.register_sequence(frames, cfg, ctx, streams=2)
+    assert len(res) == 4 and len(traj) == 5
+    ext = float(np.linalg.norm(frames[0].max(0) - frames[0].min(0)))
+    for k, r in enumerate(res):
+        assert rotation_angle_between(r.transform.rotation, z["link_R"][k]) <= 1e-4
+        assert np.linalg.norm(r.transform.translation - z["link_t"][k]) <= 1e-4 * ext
+        assert r.converged == bool(z["link_meta"][k][1])
+        one = tr.register_clouds(frames[k], frames[k + 1], cfg, ctx)
+        assert np.abs(r.transform.rotation - one.transform.rotation).max() <= 1e-8
+    for k in range(5):
+        assert rotation_angle_between(traj[k].rotation, z["traj_R"][k]) <= 4e-4
+        assert np.linalg.norm(traj[k].translation - z["traj_t"][k]) <= 4e-4 * ext
