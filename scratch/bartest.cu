@@ -53,13 +53,32 @@ __device__ __forceinline__ void nofence_sync(unsigned* bar, unsigned nb) {
   }
   __syncthreads();
 }
+// counting barrier: arrivals only add (no return value), every CTA polls the
+// monotonic counter until it reaches epoch * nb
+template <bool SLEEP>
+__device__ __forceinline__ void count_sync(unsigned* bar, unsigned nb, unsigned& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned target = (++epoch) * nb;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (SLEEP && v < target) __nanosleep(32);
+    } while (v < target);
+  }
+  __syncthreads();
+}
 template <int MODE>
 __global__ void k(unsigned* bar, int iters, long long* out) {
+  unsigned epoch = 0;
   long long t0 = clock64();
   for (int i = 0; i < iters; ++i) {
     if (MODE == 0) flat_sync(bar, gridDim.x);
     else if (MODE == 1) tree_sync<16>(bar, gridDim.x);
-    else nofence_sync(bar, gridDim.x);
+    else if (MODE == 2) nofence_sync(bar, gridDim.x);
+    else if (MODE == 3) count_sync<false>(bar, gridDim.x, epoch);
+    else count_sync<true>(bar, gridDim.x, epoch);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *out = (clock64() - t0) / iters;
 }
@@ -67,10 +86,10 @@ int main() {
   unsigned* bar; long long* out; cudaMalloc(&bar, 1 << 16); cudaMalloc(&out, 8);
   for (int per : {1, 2, 3, 4}) {
     const int G = 148 * per;
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
       cudaMemset(bar, 0, 1 << 16);
       int it = 2000; void* args[] = {&bar, &it, &out};
-      void* fn = mode == 0 ? (void*)k<0> : mode == 1 ? (void*)k<1> : (void*)k<2>;
+      void* fn = mode == 0 ? (void*)k<0> : mode == 1 ? (void*)k<1> : mode == 2 ? (void*)k<2> : mode == 3 ? (void*)k<3> : (void*)k<4>;
       cudaLaunchCooperativeKernel(fn, G, 256, args, 0, 0);
       cudaError_t e = cudaDeviceSynchronize();
       long long c; cudaMemcpy(&c, out, 8, cudaMemcpyDeviceToHost);
