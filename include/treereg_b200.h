@@ -59,11 +59,11 @@ typedef struct {
 } trg_assoc_config;
 
 /* treereg::Variant::Kind, registration.hpp:19-20 */
-enum { TRG_VARIANT_ADAPTIVE = 0, TRG_VARIANT_TREE = 1, TRG_VARIANT_FLAT = 2 };
+enum { TRG_VARIANT_ADAPTIVE = 0, TRG_VARIANT_TREE = 1, TRG_VARIANT_FLAT = 2, TRG_VARIANT_ICP = 3 };
 
 /* treereg::RegistrationConfig, registration.hpp:27-36 */
 typedef struct {
-  int variant_kind;        /* TRG_VARIANT_ADAPTIVE | TRG_VARIANT_TREE | TRG_VARIANT_FLAT */
+  int variant_kind;        /* TRG_VARIANT_ADAPTIVE | TRG_VARIANT_TREE | TRG_VARIANT_FLAT | TRG_VARIANT_ICP */
   int variant_param;       /* tree depth L */
   double lambda_c;         /* 0.01 */
   int max_em_iterations;   /* 50 */

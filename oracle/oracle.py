@@ -287,7 +287,7 @@ class Ref:
         it, conv = C.c_int(), C.c_int()
         bs, es = np.zeros(1), np.zeros(1)
         self._chk(self.L.ref_register_clouds(_d(a), len(a), _d(b), len(b),
-                                             {"adaptive": 0, "tree": 1, "flat": 2}[variant], level,
+                                             {"adaptive": 0, "tree": 1, "flat": 2, "icp": 3}[variant], level,
                                              lambda_c,
                                              max_iters, _d(R), _d(t), C.byref(it), C.byref(conv),
                                              _d(bs), _d(es)))

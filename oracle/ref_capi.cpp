@@ -357,7 +357,8 @@ int ref_register_with_tree(void* h, const double* xyz, std::size_t n, int varian
                            std::uint64_t* evals, double* em_seconds) {
   GUARD({
     RegistrationConfig cfg;
-    cfg.variant.kind = variant_kind == 2   ? Variant::Kind::kFlatGmm
+    cfg.variant.kind = variant_kind == 3   ? Variant::Kind::kIcpPointToPoint
+                       : variant_kind == 2 ? Variant::Kind::kFlatGmm
                        : variant_kind == 1 ? Variant::Kind::kGmmTree
                                            : Variant::Kind::kAdaptive;
     cfg.variant.param = static_cast<RefTree*>(h)->tree.max_level;
@@ -386,7 +387,8 @@ int ref_register_clouds(const double* tgt, std::size_t nt, const double* src, st
                         double* em_s) {
   GUARD({
     RegistrationConfig cfg;
-    cfg.variant.kind = variant_kind == 2   ? Variant::Kind::kFlatGmm
+    cfg.variant.kind = variant_kind == 3   ? Variant::Kind::kIcpPointToPoint
+                       : variant_kind == 2 ? Variant::Kind::kFlatGmm
                        : variant_kind == 1 ? Variant::Kind::kGmmTree
                                            : Variant::Kind::kAdaptive;
     cfg.variant.param = level;

@@ -16,9 +16,8 @@
 //   solve_mstep             mstep.hpp:67           -> trg_solve_mstep_vps
 //   register_with_tree      registration.hpp:59-62 -> trg_register_with_tree
 //   register_clouds         registration.hpp:53-55 -> trg_register_clouds
-//                           (adaptive:L, tree:L, flat:J; the icp variant
-//                            forwards to the reference's own implementation,
-//                            linked as register_clouds_ref)
+//                           (adaptive:L, tree:L, flat:J, icp)
+//   register_icp_pt2pt      registration.hpp:64-66 -> trg_register_clouds (icp)
 //   build_flat_gmm          gmm.hpp:74-76          -> trg_build_flat_gmm
 //   responsibilities_dense  association.hpp:44-47  -> trg_responsibilities_dense
 #include <chrono>
@@ -36,11 +35,6 @@
 #include "treereg_b200.h"
 
 namespace treereg {
-
-// The reference's own register_clouds for the variant this path does not
-// cover (ICP); see INTEGRATION.md for how it is kept linkable.
-RegistrationResult register_clouds_ref(const PointCloud& target, const PointCloud& source,
-                                       const RegistrationConfig& config);
 
 namespace {
 
@@ -180,9 +174,10 @@ trg_model_config model_cfg(const ModelConfig& m) {
 
 trg_reg_config reg_cfg(const RegistrationConfig& cfg) {
   trg_reg_config c{};
-  c.variant_kind = cfg.variant.kind == Variant::Kind::kGmmTree   ? TRG_VARIANT_TREE
-                   : cfg.variant.kind == Variant::Kind::kFlatGmm ? TRG_VARIANT_FLAT
-                                                                 : TRG_VARIANT_ADAPTIVE;
+  c.variant_kind = cfg.variant.kind == Variant::Kind::kGmmTree          ? TRG_VARIANT_TREE
+                   : cfg.variant.kind == Variant::Kind::kFlatGmm        ? TRG_VARIANT_FLAT
+                   : cfg.variant.kind == Variant::Kind::kIcpPointToPoint ? TRG_VARIANT_ICP
+                                                                        : TRG_VARIANT_ADAPTIVE;
   c.variant_param = cfg.variant.param;
   c.lambda_c = cfg.lambda_c;
   c.max_em_iterations = cfg.max_em_iterations;
@@ -410,8 +405,6 @@ MomentSet responsibilities_dense(const PointCloud& cloud,
 
 RegistrationResult register_clouds(const PointCloud& target, const PointCloud& source,
                                    const RegistrationConfig& config) {
-  if (config.variant.kind == Variant::Kind::kIcpPointToPoint)
-    return register_clouds_ref(target, source, config);  // not on this path
   if (target.empty() || source.empty()) throw std::invalid_argument("register: empty cloud");
   if (!target.all_finite() || !source.all_finite())
     throw std::invalid_argument("register: non-finite coordinates");
@@ -428,6 +421,13 @@ RegistrationResult register_clouds(const PointCloud& target, const PointCloud& s
                             &r),
         "register_clouds");
   return result_of(r, cb, ca, ev);
+}
+
+RegistrationResult register_icp_pt2pt(const PointCloud& target, const PointCloud& source,
+                                      const RegistrationConfig& config) {
+  RegistrationConfig c = config;
+  c.variant.kind = Variant::Kind::kIcpPointToPoint;
+  return register_clouds(target, source, c);
 }
 
 }  // namespace treereg

@@ -641,13 +641,13 @@ int validate_reg_config(const trg_reg_config* cfg) {
     set_error("register: max_em_iterations must be >= 1");
     return TRG_EINVAL;
   }
-  if (cfg->variant_param < 1) {
+  if (cfg->variant_param < 1 && cfg->variant_kind != TRG_VARIANT_ICP) {
     set_error("register: variant parameter must be >= 1");
     return TRG_EINVAL;
   }
   if (cfg->variant_kind != TRG_VARIANT_ADAPTIVE && cfg->variant_kind != TRG_VARIANT_TREE &&
-      cfg->variant_kind != TRG_VARIANT_FLAT) {
-    set_error("register: this path implements adaptive:L, tree:L and flat:J");
+      cfg->variant_kind != TRG_VARIANT_FLAT && cfg->variant_kind != TRG_VARIANT_ICP) {
+    set_error("register: unknown variant");
     return TRG_EINVAL;
   }
   {  // initial_transform.is_valid(1e-9) (geometry.cpp:22-38)
@@ -862,6 +862,12 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
   const double* tgt = nullptr;
   TRG_TRY(stage_points_public(ctx, source, n_source, on_device, kSlotPoints2, &src));
   TRG_TRY(stage_points_public(ctx, target, n_target, on_device, kSlotPoints, &tgt));
+  if (cfg->variant_kind == TRG_VARIANT_ICP) {  // registration.cpp:205-206
+    TRG_TRY(check_finite_dev(ctx, tgt, n_target, "register: non-finite coordinates"));
+    TRG_TRY(check_finite_dev(ctx, src, n_source, "register: non-finite coordinates"));
+    return register_icp_dev(ctx, tgt, n_target, src, n_source, cfg,
+                            target_bbox_diagonal(ctx, tgt, n_target), out);
+  }
   cudaEvent_t e0, e1;
   TRG_CU(cudaEventCreate(&e0));
   TRG_CU(cudaEventCreate(&e1));
@@ -905,7 +911,7 @@ extern "C" int trg_register_clouds_sharded(trg_comm* comm, const double* const* 
     return TRG_EINVAL;
   }
   TRG_TRY(validate_reg_config(cfg));
-  if (cfg->variant_kind == TRG_VARIANT_FLAT) {
+  if (cfg->variant_kind == TRG_VARIANT_FLAT || cfg->variant_kind == TRG_VARIANT_ICP) {
     set_error("register_sharded: the sharded path implements adaptive:L and tree:L");
     return TRG_EINVAL;
   }

@@ -188,6 +188,9 @@ int check_finite_dev(trg_ctx* ctx, const double* dev, size_t n, const char* msg)
 // Device pointer to N x 3 points: the caller's (on_device) or a staged copy.
 int stage_points_public(trg_ctx* ctx, const double* xyz, size_t n, int on_device, int slot,
                         const double** dev);
+// register_icp_pt2pt (registration.cpp:211-298) over device clouds.
+int register_icp_dev(trg_ctx* ctx, const double* tgt, size_t nt, const double* src, size_t ns,
+                     const trg_reg_config* cfg, double diag, trg_reg_result* out);
 // build_flat_gmm (gmm.cpp:659-736) over a device cloud -> J-root mixture.
 int flat_build(trg_ctx* ctx, const double* dev, size_t n, size_t J, const trg_model_config* cfg,
                trg_tree_dev** out, trg_build_diag* diag);

@@ -152,14 +152,16 @@ class AssocConfig:  # association.hpp:34-40
 
 @dataclass
 class Variant:  # registration.hpp:17-25
-    kind: str = "adaptive"  # "adaptive" | "tree" | "flat"
+    kind: str = "adaptive"  # "adaptive" | "tree" | "flat" | "icp"
     param: int = 3
 
     @staticmethod
     def parse(text: str) -> "Variant":
         head, _, tail = text.partition(":")
+        if head == "icp" and not tail:
+            return Variant("icp", 0)
         if head not in ("adaptive", "tree", "flat"):
-            raise InvalidArgument(f"unsupported variant '{text}' (this path: adaptive:L, tree:L, flat:J)")
+            raise InvalidArgument(f"unsupported variant '{text}' (adaptive:L, tree:L, flat:J, icp)")
         if not tail:
             raise InvalidArgument(f"variant '{head}' needs a parameter, e.g. {head}:3")
         try:
@@ -171,6 +173,8 @@ class Variant:  # registration.hpp:17-25
         return Variant(head, p)
 
     def name(self) -> str:
+        if self.kind == "icp":
+            return "ICP"
         if self.kind == "flat":
             return f"GMM J={self.param}"
         return ("Adaptive L" if self.kind == "adaptive" else "GMM-Tree L") + str(self.param)
@@ -214,7 +218,7 @@ class RegistrationConfig:  # registration.hpp:27-36
 
     def c(self) -> RegConfigC:
         r = RegConfigC()
-        r.variant_kind = {"adaptive": 0, "tree": 1, "flat": 2}[self.variant.kind]
+        r.variant_kind = {"adaptive": 0, "tree": 1, "flat": 2, "icp": 3}[self.variant.kind]
         r.variant_param = self.variant.param
         r.lambda_c = self.lambda_c
         r.max_em_iterations = self.max_em_iterations

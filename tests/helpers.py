@@ -13,7 +13,7 @@ def golden_names():
     """Tree fixtures that carry their input cloud (c2_/c3_/c4_* regenerate
     theirs; flat_* are the flat-mixture fixtures)."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith(("c2_", "c3_", "c4_", "flat_", "seq_")))
+                  if not os.path.basename(p).startswith(("c2_", "c3_", "c4_", "flat_", "seq_", "icp_")))
 
 
 def flat_names():
