@@ -73,3 +73,32 @@ def test_far_points_are_outliers(ctx):
     pts = np.vstack([g["points"], [[1e6, 1e6, 1e6]]])
     m, node, _ = tr.associate_adaptive(pts, tree, per_point=True)
     assert node[-1] == -1 and m.outliers >= 1 and m.total_points == len(pts)
+
+
+@pytest.mark.parametrize("gen", ["kinect", "lidar"])
+def test_association_full_size_vs_port(ctx, gen):
+    """Size-scaled parity at the C2 / C3 configurations: the GPU descent on
+    the full 76,800 / 72,000-point clouds (GPU-built tree, the pair's
+    ground-truth pose) against the C oracle on the same tree, point by point."""
+    tr = _tr()
+    try:
+        from oracle.oracle import Port
+        port = Port()
+    except (ImportError, FileNotFoundError):
+        pytest.skip("C oracle not built")
+    tg, sr, gt = (tr.kinect_pair if gen == "kinect" else tr.lidar_pair)(2)
+    tree = tr.build_tree(tg, tr.ModelConfig(max_level=3), ctx=ctx)
+    h = tree.host()
+    for lc in (0.0, 0.01):
+        m, node, w = tr.associate_adaptive(sr, tree, gt, tr.AssocConfig(lambda_c=lc), per_point=True)
+        o = port.associate(h, sr, gt.rotation, gt.translation, lambda_c=lc, per_point=True)
+        ref_node, ref_w = o[1], o[2]
+        bad = np.nonzero(node != ref_node)[0]
+        y = sr @ gt.rotation.T + gt.translation
+        for i in bad:
+            assert near_tie_on_path(h, y[i], lc), f"point {i}: {node[i]} vs {ref_node[i]}"
+        ok = node == ref_node
+        assert ok.mean() > 0.999
+        assert rel_err(w[ok], ref_w[ok]) <= 1e-12
+        if len(bad) == 0:
+            assert rel_err(m.m0, o[0].m0) <= 1e-10
