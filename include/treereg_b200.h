@@ -284,6 +284,17 @@ int trg_register_clouds_sharded(trg_comm* comm, const double* const* target,
                                 const size_t* n_source, int on_device, const trg_reg_config* cfg,
                                 trg_reg_result* out);
 
+/* ---- ingest (host code) ---------------------------
+ * treereg::read_cloud (cloud_io.hpp, cloud_io.cpp:401-427): format 0 = by
+ * content ("ply" magic, else XYZ text), 1 = PLY ascii, 2 = PLY
+ * binary_little_endian, 3 = XYZ text.  *xyz is malloc'd (N x 3, free with
+ * trg_free_cloud); parse errors return TRG_ERUNTIME (ParseError). */
+int trg_read_cloud(const char* path, int format, double** xyz, size_t* n);
+void trg_free_cloud(double* xyz);
+/* treereg::subsample (cloud_io.cpp:477-498): selection sampling of m of n
+ * points in index order, std::mt19937_64(seed) -- identical picks. */
+int trg_subsample(const double* xyz, size_t n, size_t m, uint64_t seed, double* out);
+
 /* ---- host-side data (synthetic inputs; the reference's generators,
  *      synthetic.cpp / cloud_io.cpp, restated + the new Kinect / LiDAR
  *      frame-pair generators of SURVEY.md §8d) -------------------------- */

@@ -100,6 +100,8 @@ class Ref:
                                          C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]
         L.ref_responsibilities_dense.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, _dp, C.c_double,
                                                  _dp, _dp, _dp, _u64p, _dp]
+        L.ref_read_cloud.argtypes = [C.c_char_p, C.c_int, _dp, C.c_size_t]
+        L.ref_read_cloud.restype = C.c_longlong
         L.ref_tree_free.argtypes = [C.c_void_p]
         for f in ("ref_tree_size", "ref_tree_max_level", "ref_tree_calibration_drift",
                   "ref_tree_num_traces"):
@@ -197,6 +199,21 @@ class Ref:
         finally:
             self.L.ref_tree_free(h)
         return Moments(m0, m1, m2, int(cnt[0]), int(cnt[1]), int(cnt[2]), float(tm[0]))
+
+    def read_cloud(self, path, fmt=0):
+        n = self.L.ref_read_cloud(str(path).encode(), fmt, None, 0)
+        if n < 0:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        out = np.zeros((n, 3))
+        self.L.ref_read_cloud(str(path).encode(), fmt, _d(out), n)
+        return out
+
+    def subsample(self, pts, n, seed):
+        p = np.ascontiguousarray(pts, dtype=np.float64)
+        out = np.zeros((int(n), 3))
+        if self.L.ref_subsample(_d(p), len(p), int(n), int(seed), _d(out)) != 0:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        return out
 
     def _export(self, h):
         n = self.L.ref_tree_size(h)

@@ -198,6 +198,23 @@ int ref_responsibilities_dense(void* h, const double* xyz, std::size_t n, const 
   })
 }
 
+// read_cloud (cloud_io.cpp:401-427): format 0 = by content, 1 = ply ascii,
+// 2 = ply binary_le, 3 = xyz.  Returns the point count, fills at most cap.
+long long ref_read_cloud(const char* path, int format, double* out, std::size_t cap) {
+  try {
+    const PointCloud c = format == 0 ? read_cloud(path)
+                                     : read_cloud(path, format == 1   ? CloudFormat::kPlyAscii
+                                                        : format == 2 ? CloudFormat::kPlyBinaryLe
+                                                                      : CloudFormat::kXyzText);
+    for (std::size_t i = 0; i < c.size() && i < cap; ++i)
+      for (int k = 0; k < 3; ++k) out[3 * i + k] = c.points[i](k);
+    return static_cast<long long>(c.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 void ref_tree_free(void* h) { delete static_cast<RefTree*>(h); }
 int ref_tree_size(void* h) { return static_cast<int>(static_cast<RefTree*>(h)->tree.size()); }
 int ref_tree_max_level(void* h) { return static_cast<RefTree*>(h)->tree.max_level; }

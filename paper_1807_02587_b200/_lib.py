@@ -131,6 +131,9 @@ SIGNATURES = {
     "trg_bbox_diagonal": (C.c_double, [dp, C.c_size_t]),
     "trg_random_rigid_transform": (C.c_int, [C.c_double, C.c_double, C.c_uint64, C.c_int, dp,
                                              dp]),
+    "trg_read_cloud": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(dp), C.POINTER(C.c_size_t)]),
+    "trg_free_cloud": (None, [dp]),
+    "trg_subsample": (C.c_int, [dp, C.c_size_t, C.c_size_t, C.c_uint64, dp]),
     "trg_synth_kinect_sequence": (C.c_int, [C.c_uint64, C.c_int, C.c_double, C.c_double, dp, dp, dp]),
     "trg_synth_kinect_pair": (C.c_int, [C.c_uint64, dp, dp, dp, dp]),
     "trg_synth_kinect_pair_ex": (C.c_int, [C.c_uint64, C.c_double, C.c_double, C.c_double, dp, dp,

@@ -713,6 +713,27 @@ def register_clouds_sharded(targets: list, sources: list, comm: Comm,
 
 
 # ------------------------------------------------------------------ inputs
+def read_cloud(path, fmt: str = "auto") -> np.ndarray:
+    """cloud_io read_cloud: fmt in auto | ply_ascii | ply_binary | xyz."""
+    code = {"auto": 0, "ply_ascii": 1, "ply_binary": 2, "xyz": 3}[fmt]
+    p = dp()
+    n = C.c_size_t()
+    _chk(_lib.lib().trg_read_cloud(str(path).encode(), code, C.byref(p), C.byref(n)))
+    try:
+        return np.ctypeslib.as_array(p, shape=(n.value * 3,)).reshape(n.value, 3).copy() \
+            if n.value else np.zeros((0, 3))
+    finally:
+        _lib.lib().trg_free_cloud(p)
+
+
+def subsample(cloud, n: int, seed: int) -> np.ndarray:
+    """cloud_io subsample: n points in index order, reference-identical picks."""
+    p = _points(cloud)
+    out = np.zeros((int(n), 3))
+    _chk(_lib.lib().trg_subsample(_d(p), len(p), int(n), seed, _d(out)))
+    return out
+
+
 def synthetic(kind: str, n: int, seed: int) -> np.ndarray:
     """synthetic.cpp generators (bit-identical restatement)."""
     out = np.zeros((n, 3))
