@@ -112,8 +112,7 @@ struct BuildParams {
   AssocParams a;
   double* cal_moments;  // [J][10]
   double* cta_drift;    // [G]
-  unsigned* cal_arrive;  // [capacity + 1] last-arriver counters (+ virtual root)
-  int2* cal_up;          // [capacity] (parent, parent's child count) for the climb
+  unsigned* cal_arrive;  // [capacity + 1]; slot capacity: leaf arrivals of a calibration pass
   unsigned long long* drift_bits;  // [2] per-pass max drift (bits of a double >= 0)
   int* layout_scratch;  // [6 * 8 * Kmax]
   double* ll_trace;     // [capacity][2][em_iters + 1] per expansion, both candidates
@@ -676,16 +675,11 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
   if (ph.pcount) {
     // per-child totals + per-tile child base offsets (stable order); lane s
     const int ns = nf.ns[k];
+    // (tile_base / next_seg: the kind-2 reduction items; layout turns the
+    // child entry counts into segments)
     if (lane < ns) {
       const int s = lane;
       const int comp = nf.surv[8 * k + s];
-      const int t0 = p.rn[par].tile0[k], nt = p.rn[par].ntiles[k];
-      double base = 0.0;
-      for (int t = 0; t < nt; ++t) {
-        p.tile_base[(size_t)(t0 + t) * 8 + s] = base;
-        base += __ldcg(p.partial + (size_t)(t0 + t) * kRec + kOffCnt + comp);
-      }
-      nf.next_seg[8 * k + s] = (int)base;  // child entry count (layout turns it into a segment)
       nf.smass[8 * k + s] = __ldcg(red + kOffCnt + 8 + comp);
     }
     __syncwarp();
@@ -1015,7 +1009,13 @@ __device__ int phase_items(const Phase& ph, int* off, int* kind) {
     if (ph.mode[c] == 1) sum_range(kOffEm + 81 * c, 81);
     if (ph.mode[c] == 2) sum_range(kOffFin + 9 * c, 9);
   }
-  if (ph.pcount) sum_range(kOffCnt + 8, 8);
+  if (ph.pcount) {
+    sum_range(kOffCnt + 8, 8);
+    for (int q = 0; q < 8; ++q) {  // per-survivor tile prefix (child base offsets)
+      off[n] = q;
+      kind[n++] = 2;
+    }
+  }
   return n;
 }
 
@@ -1032,6 +1032,30 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) out[off] = v;
+  } else if (kind == 2) {
+    // survivor `off`'s per-tile child base offsets: exclusive prefix over the
+    // node's tiles of its integer entry counts (exact in any order), lanes
+    // own contiguous tile runs
+    const int s = off, ns = __ldcg(&p.nf.ns[k]);
+    if (s >= ns) return;
+    const int comp = __ldcg(&p.nf.surv[8 * k + s]);
+    const double* cnt = p.partial + (size_t)t0 * kRec + kOffCnt + comp;
+    const int per = (nt + 31) / 32;
+    const int q0 = min(nt, lane * per), q1 = min(nt, q0 + per);
+    double loc = 0.0;
+    for (int q = q0; q < q1; ++q) loc += __ldcg(cnt + (size_t)q * kRec);
+    double inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    double base = inc - loc;
+    for (int q = q0; q < q1; ++q) {
+      p.tile_base[(size_t)(t0 + q) * 8 + s] = base;
+      base += __ldcg(cnt + (size_t)q * kRec);
+    }
+    if (lane == 31) p.nf.next_seg[8 * k + s] = (int)inc;  // child entry count
   } else {
     double bs = -INFINITY, bi = 1e300;
     for (int q = lane; q < nt; q += 32)
@@ -1200,6 +1224,97 @@ inline int build_exchange_points_per_round(int em_iters) {
   return n;
 }
 
+// calibrate_pass's tree update (gmm.cpp:547-578) by one CTA, after the leaf
+// refits: per level bottom-up, an 8-lane group per parent (lane c holds child
+// c) sums its children's branch masses, reweights them (mass shares;
+// shadowed octets keep theirs) and moment-matches the parent from them, every
+// sum running in child order like the reference's loops; the top octet is
+// reweighted last; then every parent's refresh_eig runs in parallel
+// (warm-started from its previous axes).
+__device__ __forceinline__ double group8_sum(double v, int gbase) {
+  double t = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) t += __shfl_sync(0xffffffffu, v, gbase + q);
+  return t;
+}
+
+constexpr int kTopoCap = 640;  // parents whose (first_child, child_count) CTA 0 keeps in smem
+
+__device__ __forceinline__ int2 cal_topo(const BuildParams& p, const int2* topo, int n_topo, int i) {
+  return i < n_topo ? topo[i] : make_int2(__ldcg(&p.nodes[i].first_child), __ldcg(&p.nodes[i].child_count));
+}
+
+__device__ void cal_tree_update(const BuildParams& p, const int* lvl, int root_count,
+                                const int2* topo, int n_topo, double& drift, bool marks) {
+  const int tid = threadIdx.x, c = tid & 7, gbase = (tid & 31) & ~7;
+  const int groups = blockDim.x / 8;
+  double* branch = p.cal_moments;  // slot 0 of each node
+  for (int l = p.L - 2; l >= 0; --l) {
+    const int n = lvl[l + 1] - lvl[l];
+    for (int b = 0; b < n; b += groups) {  // uniform across the CTA (full-warp shuffles)
+      const int i = lvl[l] + b + (tid >> 3);
+      const bool act = b + (tid >> 3) < n;
+      const int2 tp = act ? cal_topo(p, topo, n_topo, i) : make_int2(0, 0);
+      const int f = tp.x, cc = tp.y;
+      const bool own = c < cc;
+      const int ci = f + (own ? c : 0);
+      const double cb = own ? __ldcg(&branch[(size_t)ci * 10]) : 0.0;
+      double cw = own ? __ldcg(&p.nodes[ci].weight) : 0.0;
+      double cm[3], cv[9];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) cm[k] = own ? __ldcg(&p.nodes[ci].mean[k]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) cv[k] = own ? __ldcg(&p.cov[9 * (size_t)ci + k]) : 0.0;
+      const double sb = group8_sum(cb, gbase);
+      if (cc > 0 && c == 0) branch[(size_t)i * 10] = sb;
+      if (own && sb > 0.0) {
+        const double nw = cb / sb;
+        drift = smax(drift, fabs(cw - nw));
+        cw = nw;
+        p.nodes[ci].weight = nw;
+      }
+      const double w = group8_sum(cw, gbase);
+      double mu[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) mu[k] = group8_sum(cw * cm[k], gbase);
+      const bool upd = cc > 0 && w > 0.0;  // group-uniform; shuffles stay warp-uniform
+      for (int k = 0; k < 3; ++k) mu[k] = upd ? mu[k] / w : 0.0;
+      const double d[3] = {cm[0] - mu[0], cm[1] - mu[1], cm[2] - mu[2]};
+      double m2[9];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) m2[3 * r + q] = cw * (cv[3 * r + q] + d[r] * d[q]);
+      double out[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) out[k] = group8_sum(m2[k], gbase);
+      if (upd && c == 0) {
+        for (int k = 0; k < 9; ++k) p.cov[9 * (size_t)i + k] = out[k] / w;
+        for (int k = 0; k < 3; ++k) p.nodes[i].mean[k] = mu[k];
+      }
+    }
+    __syncthreads();
+    if (marks && tid == 0) tl_mark_any(p.tl, 5030 + l);
+  }
+  if (tid < 32) {  // top octet: lane r < 8 holds root r (root_count <= 8)
+    const bool own = tid < root_count;
+    const double cb = own ? __ldcg(&branch[(size_t)tid * 10]) : 0.0;
+    const double sb = group8_sum(cb, 0);
+    if (own && sb > 0.0) {
+      const double nw = cb / sb;
+      drift = smax(drift, fabs(__ldcg(&p.nodes[tid].weight) - nw));
+      p.nodes[tid].weight = nw;
+    }
+  }
+  const int n_par = p.L >= 2 ? lvl[p.L - 1] : 0;  // parents sit above the deepest level
+  for (int i = tid; i < n_par; i += blockDim.x) {
+    if (cal_topo(p, topo, n_topo, i).y == 0) continue;
+    double cv[9];
+    for (int k = 0; k < 9; ++k) cv[k] = __ldcg(&p.cov[9 * (size_t)i + k]);
+    if (refresh_node(p.nodes[i], cv, true)) atomicCAS(p.status, 0, kEInval);
+  }
+}
+
 // Second persistent kernel of the build (launched right behind k_build on
 // the same stream): parent moment match + refresh_eig, then the leaf
 // calibration passes.  Separate so its 3x3 eigen chains get a full register
@@ -1225,26 +1340,37 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
     if (cta == 0) reset_parents(p, lvl);
     grid_sync(p.bar, G);
     tl_mark(p.tl, 901);
-    for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x) {
+    for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x)
       if (refresh_node(p.nodes[j], p.cov + 9 * (size_t)j)) atomicCAS(p.status, 0, kEInval);
-      const int par = p.nodes[j].parent;
-      p.cal_up[j] = make_int2(par, par >= 0 ? p.nodes[par].child_count : lvl[1] - lvl[0]);
-    }
     grid_sync(p.bar, G);
     tl_mark(p.tl, 902);
   }
   // ------------------------------------------------ leaf calibration
   // calibrate_pass (gmm.cpp:523-580) per pass: association at identity with
   // m2 (stage 1); then leaf refits and the whole bottom-up tree update
-  // (branch masses, octet reweights, parent moment match, refresh_eig) run as
-  // a last-arriver climb: each leaf's warp refits it and arrives at its
-  // parent; the parent's last-arriving child processes the parent and climbs
-  // on.  Every node is updated from the same inputs, in the same order, as
-  // the reference's level loops.  2 grid barriers per pass.
+  // (branch masses, octet reweights, parent moment match, refresh_eig): each
+  // leaf's warp refits it and arrives on a counter; CTA 0 waits for all
+  // leaves and runs the tree update (cal_tree_update) in the reference's
+  // level order, while the other CTAs go on to the pass's closing barrier.
+  // 2 grid barriers per pass.
   // Sharded (p.seg >= 0): segment s runs stage 2 of pass s-1 (from the
   // all-reduced leaf moments in xcal) and stage 1 of pass s up to the local
   // leaf combine, then exits for the exchange.
   const int root_count = lvl[1] - lvl[0];
+  __shared__ int n_leaf_s;
+  if (tid == 0) n_leaf_s = 0;
+  __syncthreads();
+  {
+    int c = 0;
+    for (int j = tid; j < J; j += blockDim.x) c += __ldcg(&p.nodes[j].child_count) == 0;
+    if (c) atomicAdd(&n_leaf_s, c);
+  }
+  __syncthreads();
+  const int n_leaf = n_leaf_s;
+  __shared__ int2 topo[kTopoCap];  // CTA 0's copy of the parents' topology
+  const int n_topo = cta == 0 ? min(lvl[p.L >= 2 ? p.L - 1 : 0], kTopoCap) : 0;
+  for (int i = tid; i < n_topo; i += blockDim.x)
+    topo[i] = make_int2(__ldcg(&p.nodes[i].first_child), __ldcg(&p.nodes[i].child_count));
   extern __shared__ __align__(16) unsigned char k_cal_stage[];  // upper levels for the descent
   DNode* cal_stage = reinterpret_cast<DNode*>(k_cal_stage);
   const int n_stage = min(p.L >= 2 ? lvl[p.L - 1] : 0, kStageNodes);
@@ -1295,7 +1421,6 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
         combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
       }
       if (tl5 && lane == 0 && j % 16 == 0) tl_mark_any(p.tl, 5002);
-      if (p.dbg == 1) continue;
       double* branch = p.cal_moments;  // slot 0 of each node
       if (lane == 0) {
         branch[(size_t)j * 10] = m[0];
@@ -1330,87 +1455,26 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
       }
       __syncwarp();
       if (tl5 && lane == 0 && j % 16 == 0) tl_mark_any(p.tl, 5003);
-      if (p.dbg == 2) continue;
-      // climb: arrive at the parent; the parent's last-arriving child's warp
-      // processes it (lanes load one child each; sums run in child order on
-      // every lane, so the arithmetic is the reference's), then climbs on
-      int node = j;
-      for (;;) {
-        int par = 0, last = 0, need = 0;
-        if (lane == 0) {
-          const int2 up = __ldcg(&p.cal_up[node]);
-          par = up.x;
-          need = up.y;
-          unsigned* ctr = par >= 0 ? &p.cal_arrive[par] : &p.cal_arrive[p.capacity];
-          __threadfence();
-          last = atomicAdd(ctr, 1u) == (unsigned)need - 1;
-          if (last) {
-            *ctr = 0u;
-            __threadfence();
-          }
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (!last) break;
-        par = __shfl_sync(0xffffffffu, par, 0);
-        need = __shfl_sync(0xffffffffu, need, 0);
-        const int first = par >= 0 ? __ldcg(&p.nodes[par].first_child) : 0;
-        const int count = need;
-        // lane c < count holds child c (<= 8 children); sums over the
-        // children are fixed full-warp butterflies (idle lanes add 0), so
-        // every lane holds the same totals
-        const bool own = lane < count;
-        const int ci = first + (own ? lane : 0);
-        const double cb = own ? __ldcg(&branch[(size_t)ci * 10]) : 0.0;
-        double cwt = own ? __ldcg(&p.nodes[ci].weight) : 0.0;
-        double cm[3], cc[9];
-        for (int k = 0; k < 3; ++k) cm[k] = own ? __ldcg(&p.nodes[ci].mean[k]) : 0.0;
-        for (int k = 0; k < 9; ++k) cc[k] = own ? __ldcg(&p.cov[9 * (size_t)ci + k]) : 0.0;
-        // branch mass and sibling reweight (gmm.cpp:547-566)
-        double sb = cb;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) sb += __shfl_xor_sync(0xffffffffu, sb, o);
-        if (par >= 0 && lane == 0) branch[(size_t)par * 10] = sb;
-        if (sb > 0.0 && own) {
-          const double w = cb / sb;
-          drift = smax(drift, fabs(cwt - w));
-          cwt = w;
-          p.nodes[ci].weight = w;
-        }
-        if (tl5 && lane == 0) tl_mark_any(p.tl, par < 0 ? 5020 : 5010 + __ldcg(&p.nodes[par].level));
-        if (par < 0) break;  // top octet done
-        // parent moment match (gmm.cpp:489-513)
-        double v[4] = {cwt, cwt * cm[0], cwt * cm[1], cwt * cm[2]};
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-          for (int k = 0; k < 4; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-        const double w = v[0];
-        double cvn[9];
-        if (w > 0.0) {
-          const double mu[3] = {v[1] / w, v[2] / w, v[3] / w};
-          const double d[3] = {cm[0] - mu[0], cm[1] - mu[1], cm[2] - mu[2]};
-          double cv[9];
-#pragma unroll
-          for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int q = 0; q < 3; ++q) cv[3 * r + q] = cwt * (cc[3 * r + q] + d[r] * d[q]);
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-            for (int k = 0; k < 9; ++k) cv[k] += __shfl_xor_sync(0xffffffffu, cv[k], o);
-          for (int k = 0; k < 9; ++k) cvn[k] = cv[k] / w;
-          if (lane == 0) {
-            for (int k = 0; k < 9; ++k) p.cov[9 * (size_t)par + k] = cvn[k];
-            for (int k = 0; k < 3; ++k) p.nodes[par].mean[k] = mu[k];
-          }
-        } else {
-          for (int k = 0; k < 9; ++k) cvn[k] = __ldcg(&p.cov[9 * (size_t)par + k]);
-        }
-        if (lane == 0 && refresh_node(p.nodes[par], cvn, true))  // gmm.cpp:576-578
-          atomicCAS(p.status, 0, kEInval);
-        __syncwarp();
-        node = par;
+      if (lane == 0) {  // this leaf is refit: arrive for CTA 0's tree update
+        __threadfence();
+        atomicAdd(&p.cal_arrive[p.capacity], 1u);
       }
+    }
+    if (cta == 0) {
+      // tree update of the pass (gmm.cpp:547-578), in the reference's level
+      // order, once every leaf has arrived: branch masses, octet reweights
+      // and the parent moment match bottom-up, one thread per parent with
+      // sums in child order; then refresh_eig of all parents in parallel.
+      if (tid == 0) {
+        volatile unsigned* ctr = &p.cal_arrive[p.capacity];
+        while (*ctr < (unsigned)n_leaf) __nanosleep(20);
+        __threadfence();
+        *ctr = 0u;
+      }
+      __syncthreads();
+      if (tl5 && tid == 0) tl_mark_any(p.tl, 5010);
+      cal_tree_update(p, lvl, root_count, topo, n_topo, drift, tl5);
+      if (tl5 && tid == 0) tl_mark_any(p.tl, 5020);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) drift = smax(drift, __shfl_xor_sync(0xffffffffu, drift, off));
@@ -1519,7 +1583,6 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
                o_llt = carve(sizeof(double) * (size_t)cap * 2 * (cfg->em_iterations_per_node + 1)),
                o_kex = carve(sizeof(int) * (size_t)cap),
                o_car = carve(sizeof(unsigned) * ((size_t)cap + 1)), o_dbits = carve(16),
-               o_up = carve(sizeof(int2) * (size_t)cap),
                o_state = carve(sizeof(BuildState));
   TRG_CU(cudaFuncSetAttribute((const void*)k_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)sizeof(BuildSmem)));
@@ -1578,7 +1641,6 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   p.ll_trace = (double*)(A + o_llt);
   p.kept_exp = (int*)(A + o_kex);
   p.cal_arrive = (unsigned*)(A + o_car);
-  p.cal_up = (int2*)(A + o_up);
   p.drift_bits = (unsigned long long*)(A + o_dbits);
   p.bar = (unsigned*)(A + o_bar);
   p.st = (BuildState*)(A + o_state);

@@ -13,6 +13,6 @@ t = t[:n].astype(np.int64); lab = lab[:n]
 t0 = t[lab == 1000 + 9 * 10 + 2][0]  # end of pass 9 = start of pass 10
 print("n marks", n)
 def rel(L): return (t[lab == L] - t0) / 1e3
-for L in (1101, 5001, 5002, 5003, 5010, 5011, 5012, 5020, 1102):
+for L in (1101, 5001, 5002, 5003, 5010, 5040, 5041, 5042, 5043, 5031, 5030, 5020, 1102):
     v = rel(L)
     if len(v): print(L, "count", len(v), "min %.2f med %.2f max %.2f us" % (v.min(), np.median(v), v.max()))
