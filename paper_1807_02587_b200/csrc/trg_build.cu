@@ -258,6 +258,7 @@ struct BuildSmem {
   int item_kind[192];
   int tnode, tstart, tlen, tidx;
   double ent[4][kTile];  // the tile's entries (x, y, z, w), staged once per tile
+  double sred[kTile / 32][11][33];  // per-warp cross-lane sums of tile_comp_pass (padded rows)
   double nref[3], nmean[3], seed[3];
   GComp comp[2][8];
   int cand_list[2];
@@ -322,7 +323,7 @@ __device__ void tile_entry_pass(const BuildParams& p, BuildSmem& sm, const Phase
       double d2 = a * a;
       d2 += b * b;
       d2 += c * c;
-      const double md = ph.fps == 1 ? d2 : smin(p.min_d2[e], d2);
+      const double md = ph.fps == 1 ? d2 : smin(__ldcg(&p.min_d2[e]), d2);
       p.min_d2[e] = md;
       sc = w * md;
     }
@@ -386,8 +387,8 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
   if (pcount && tid == 0) {  // heaviest survivor: the partition's fallback
     int best = 0;
     for (int s2 = 1; s2 < sm.ns; ++s2)
-      if (p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[s2]] >
-          p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[best]])
+      if (__ldcg(&p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[s2]]) >
+          __ldcg(&p.nf.cmass[(size_t)sm.tnode * 16 + sm.kept * 8 + sm.surv[best]]))
         best = s2;
     G.best = best;
   }
@@ -424,19 +425,30 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
           a[0] += g;  // mode 2: child mass (gmm.cpp:355)
         }
       }
+      // Cross-lane sums through shared memory: lane q adds value q of all
+      // 32 lanes in the halving tree (16, 8, 4, 2, 1) - the very tree lane
+      // 0 of an xor butterfly computes, so the sums are bit-identical to it,
+      // at ~half the issue slots of 11 x 5 double shuffles.
+      double(*sr)[33] = sm.sred[warp];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+      for (int q = 0; q < 11; ++q) sr[q][lane] = a[q];
+      __syncwarp();
+      const bool need = mode == 1 ? (lane < 10 || (lane == 10 && k == 0))
+                                  : (lane == 0 || (lane == 10 && k == 0));
+      if (need) {
+        double t[16];
 #pragma unroll
-        for (int q = 0; q < 11; ++q) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
-      if (lane == 0) {
-        if (mode == 1) {
-          for (int q = 0; q < 10; ++q) rec[kOffEm + cand * 81 + k * 10 + q] = a[q];
-          if (k == 0) rec[kOffEm + cand * 81 + 80] = a[10];
-        } else {
-          rec[kOffFin + cand * 9 + 1 + k] = a[0];
-          if (k == 0) rec[kOffFin + cand * 9] = a[10];
-        }
+        for (int i = 0; i < 16; ++i) t[i] = sr[lane][i] + sr[lane][i + 16];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+          for (int i = 0; i < o; ++i) t[i] += t[i + o];
+        if (mode == 1)
+          rec[kOffEm + cand * 81 + (lane < 10 ? k * 10 + lane : 80)] = t[0];
+        else
+          rec[kOffFin + cand * 9 + (lane == 0 ? 1 + k : 0)] = t[0];
       }
+      __syncwarp();
     }
   } else {
     // survivor-normalised soft partition (gmm.cpp:434-454): warp = survivor
@@ -506,12 +518,12 @@ __device__ void node_mstep(const BuildParams& p, int k, int c, const double* red
   g.w = m0 / total;
   g.lw = log(g.w);
   const double* mean = p.nf.mean + 3 * k;
-  for (int i = 0; i < 3; ++i) g.mean[i] = mean[i] + d[i];
+  for (int i = 0; i < 3; ++i) g.mean[i] = __ldcg(&mean[i]) + d[i];
   // the eigensolve starts from the component's previous axes: EM moves the
   // covariance a little per iteration, so the warm Jacobi needs ~1 sweep
   double warm[9];
-  for (int i = 0; i < 9; ++i) warm[i] = g.axT[i];
-  if (comp_set_cov(g, sc, p.nf.floorv[k], warm)) atomicCAS(p.status, 0, kEInval);
+  for (int i = 0; i < 9; ++i) warm[i] = __ldcg(&g.axT[i]);
+  if (comp_set_cov(g, sc, __ldcg(&p.nf.floorv[k]), warm)) atomicCAS(p.status, 0, kEInval);
 }
 
 // Candidate init (fit_candidate gmm.cpp:319-326) for component `comp`.
@@ -582,7 +594,7 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
   }
   if (ph.mom2) {
     if (lane == 0) {
-      const double mass = nf.mass[k];
+      const double mass = __ldcg(&nf.mass[k]);
       double m[6];
       for (int q = 0; q < 6; ++q) m[q] = __ldcg(red + kOffMom2 + q);
       const double M[3][3] = {{m[0], m[1], m[2]}, {m[1], m[3], m[4]}, {m[2], m[4], m[5]}};
@@ -650,14 +662,14 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
   __syncwarp();
   if (ph.mode[1] == 2 && lane == 0) {
     // candidate choice (gmm.cpp:394) and survivors (gmm.cpp:414-428)
-    const int kept = (nf.final_ll[2 * k + 1] > nf.final_ll[2 * k + 0]) ? 1 : 0;
+    const int kept = (__ldcg(&nf.final_ll[2 * k + 1]) > __ldcg(&nf.final_ll[2 * k + 0])) ? 1 : 0;
     nf.kept[k] = kept;
     p.kept_exp[p.st->exp_base + k] = kept;
     const double* cm = nf.cmass + 16 * k + 8 * kept;
-    const double thr = smax(4.0, nf.mass[k] * 1e-6);
+    const double thr = smax(4.0, __ldcg(&nf.mass[k]) * 1e-6);
     int ns = 0;
     for (int j = 0; j < 8; ++j)
-      if (cm[j] > thr) nf.surv[8 * k + ns++] = j;
+      if (__ldcg(&cm[j]) > thr) nf.surv[8 * k + ns++] = j;
     int ok = 1;
     if (ns == 0) {
       if (round != 0) {
@@ -665,7 +677,7 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
       } else {
         int best = 0;
         for (int j = 1; j < 8; ++j)
-          if (cm[j] > cm[best]) best = j;
+          if (__ldcg(&cm[j]) > __ldcg(&cm[best])) best = j;
         nf.surv[8 * k + ns++] = best;
       }
     }
@@ -709,10 +721,10 @@ __device__ void load_tile_ctx(const BuildParams& p, BuildSmem& sm, const Phase& 
   }
   if (!ph.pwrite && tid < tlen) {
     const int e = tstart + tid;
-    sm.ent[0][tid] = p.ex[par][e];
-    sm.ent[1][tid] = p.ey[par][e];
-    sm.ent[2][tid] = p.ez[par][e];
-    sm.ent[3][tid] = p.ew[par][e];
+    sm.ent[0][tid] = __ldcg(&p.ex[par][e]);  // (other CTAs wrote them: L2, not L1)
+    sm.ent[1][tid] = __ldcg(&p.ey[par][e]);
+    sm.ent[2][tid] = __ldcg(&p.ez[par][e]);
+    sm.ent[3][tid] = __ldcg(&p.ew[par][e]);
   }
   if (tid < 3) {
     if (ph.mom1) {
@@ -720,17 +732,17 @@ __device__ void load_tile_ctx(const BuildParams& p, BuildSmem& sm, const Phase& 
       // a point every shard knows: the node's fitted mean (0 for the root)
       double v;
       if (p.seg < 0) {
-        const int e0 = p.rn[par].seg[k];
-        v = tid == 0 ? p.ex[par][e0] : (tid == 1 ? p.ey[par][e0] : p.ez[par][e0]);
+        const int e0 = __ldcg(&p.rn[par].seg[k]);
+        v = __ldcg(tid == 0 ? &p.ex[par][e0] : (tid == 1 ? &p.ey[par][e0] : &p.ez[par][e0]));
       } else {
-        const int id = p.rn[par].tree_id[k];
-        v = id >= 0 ? p.nodes[id].mean[tid] : 0.0;
+        const int id = __ldcg(&p.rn[par].tree_id[k]);
+        v = id >= 0 ? __ldcg(&p.nodes[id].mean[tid]) : 0.0;
       }
       sm.nref[tid] = v;
       p.nf.ref[3 * k + tid] = v;
     }
-    sm.nmean[tid] = p.nf.mean[3 * k + tid];
-    if (ph.fps) sm.seed[tid] = p.nf.seeds[24 * k + 3 * (ph.fps - 1) + tid];
+    sm.nmean[tid] = __ldcg(&p.nf.mean[3 * k + tid]);
+    if (ph.fps) sm.seed[tid] = __ldcg(&p.nf.seeds[24 * k + 3 * (ph.fps - 1) + tid]);
   }
   if (tid == 0) {
     int nc = 0;
@@ -738,9 +750,9 @@ __device__ void load_tile_ctx(const BuildParams& p, BuildSmem& sm, const Phase& 
       if (ph.mode[c]) sm.cand_list[nc++] = c;
     sm.ncand = nc;
     if (ph.pcount) {
-      sm.kept = p.nf.kept[k];
-      sm.ns = p.nf.ns[k];
-      for (int s = 0; s < sm.ns; ++s) sm.surv[s] = p.nf.surv[8 * k + s];
+      sm.kept = __ldcg(&p.nf.kept[k]);
+      sm.ns = __ldcg(&p.nf.ns[k]);
+      for (int s = 0; s < sm.ns; ++s) sm.surv[s] = __ldcg(&p.nf.surv[8 * k + s]);
     }
   }
   const bool need_comps = ph.mode[0] || ph.mode[1] || ph.pcount;
@@ -1170,6 +1182,8 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
         tl_mark(p.tl, round * 100 + ph_i);
         // (b) per-node reduction of the tile records (+ node update when the
         // whole cloud is here)
+        const bool tl7 = p.dbg == 7 && round == 2 && ph_i == 5;  // experiments: reduce anatomy
+        if (tl7 && tid == 0) tl_mark_any(p.tl, 6999);
         if (tid == 0) sm.nitems = phase_items(ph, sm.item_off, sm.item_kind);
         __syncthreads();
         const int NI = sm.nitems;
@@ -1188,7 +1202,13 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
             }
           }
           last = __shfl_sync(0xffffffffu, last, 0);
+          if (last && tl7 && lane == 0) tl_mark_any(p.tl, 7100);
           if (last) node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
+          if (last && tl7 && lane == 0) tl_mark_any(p.tl, 7200);
+        }
+        if (tl7) {
+          __syncthreads();
+          if (tid == 0) tl_mark_any(p.tl, 7000);
         }
         if (sharded) {
           grid_sync(p.bar, G);
@@ -1590,7 +1610,8 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   const size_t cal_smem = sizeof(DNode) * kStageNodes;
   TRG_CU(cudaFuncSetAttribute((const void*)k_calibrate, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)cal_smem));
-  const int Gc = persistent_grid(ctx, (const void*)k_calibrate, kTile, cal_smem);
+  int Gc = persistent_grid(ctx, (const void*)k_calibrate, kTile, cal_smem);
+  if (const char* e = getenv("TRG_KCAL_PER_SM")) Gc = std::min(Gc, ctx->sms * atoi(e));  // experiments
   const size_t o_cd = carve(sizeof(double) * std::max(G, Gc));
   const int W = std::max(world, 1);
   const size_t o_xa = carve(sizeof(double) * 8 * K), o_xaa = carve(sizeof(double) * 8 * K * W),
