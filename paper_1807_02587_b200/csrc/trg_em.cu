@@ -4,6 +4,7 @@
 // point rows, single-block 6-DoF solve (K8), T <- delta o T, convergence and
 // degenerate-streak control -- with grid barriers between phases, so the
 // host never sees an iteration boundary.
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <vector>
@@ -423,7 +424,13 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   job->smem = dense ? 0 : sizeof(DNode) * kStageNodes;
   TRG_CU(cudaFuncSetAttribute(job->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)std::max<size_t>(job->smem, 1)));
-  const int G = persistent_grid(ctx, job->kernel, kAssocBlock, job->smem);
+  // 2 CTAs per SM (of the 3 that fit): the per-node combine over CTAs and
+  // the redundant per-CTA solve get cheaper faster than the E-step slows
+  // (C2, 16 iterations: 0.72 ms at 2/SM vs 0.80 at 1/SM and 0.90 at 3/SM)
+  int per_sm = 2;
+  if (const char* e = getenv("TRG_KREG_PER_SM")) per_sm = atoi(e);  // experiments
+  const int G = std::min(persistent_grid(ctx, job->kernel, kAssocBlock, job->smem),
+                         ctx->sms * std::max(1, per_sm));
   EmParams p{};
   p.a.nodes = tree->nodes;
   p.a.n_nodes = J;

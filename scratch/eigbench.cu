@@ -36,6 +36,20 @@ __global__ void kjac(DNode* nodes, double* cov, long long* out, int mode, int re
   out[0] = (t1 - t0) / reps;
   nodes[1].lam[0] = c[1];
 }
+__global__ void kldlt(double* A0, long long* out, int mode, int reps) {
+  double A[6][6], b[6], x[6], tr, mind;
+  for (int i = 0; i < 6; ++i) { b[i] = A0[36 + i]; for (int j = 0; j < 6; ++j) A[i][j] = A0[6 * i + j]; }
+  long long t0 = clock64();
+  double acc = 0;
+  for (int r = 0; r < reps; ++r) {
+    if (mode == 0) { ldlt_solve6_tr(A, b, x, &tr, &mind); acc = x[0] + tr; }
+    if (mode == 1) { double w[3] = {x[0] + 1e-3, x[1], x[2]}, R[9]; small_angle_rotation(w, R); acc = R[1]; x[0] = acc * 1e-9; }
+    b[0] += acc * 1e-30;
+  }
+  long long t1 = clock64();
+  out[0] = (t1 - t0) / reps;
+  A0[50] = acc;
+}
 __global__ void klog(double* x, long long* out, int reps) {
   double v = x[0];
   long long t0 = clock64();
@@ -103,6 +117,16 @@ int main() {
   for (int m = 0; m < 3; ++m) {
     kjac<<<1, 1>>>(dn, dc, dout, m, 50); cudaMemcpy(&o, dout, 8, cudaMemcpyDeviceToHost);
     printf("mode %d (0 jacobi warm, 1 eig_sym3 warm, 2 jacobi cold): %lld cycles\n", m, o);
+  }
+  {
+    double hA[64];
+    for (int i = 0; i < 6; ++i) for (int j = 0; j < 6; ++j) hA[6 * i + j] = (i == j ? 10.0 + i : 0.0) + 1.0 / (1 + i + j);
+    for (int i = 0; i < 6; ++i) hA[36 + i] = 1.0 + i;
+    double* dA; cudaMalloc(&dA, 64 * 8); cudaMemcpy(dA, hA, 64 * 8, cudaMemcpyHostToDevice);
+    for (int m = 0; m < 2; ++m) {
+      kldlt<<<1, 1>>>(dA, dout, m, 50); cudaMemcpy(&o, dout, 8, cudaMemcpyDeviceToHost);
+      printf("%s: %lld cycles\n", m == 0 ? "ldlt_solve6_tr" : "small_angle_rotation", o);
+    }
   }
   klog<<<1, 1>>>(dx, dout, 200); cudaMemcpy(&o, dout, 8, cudaMemcpyDeviceToHost); printf("log: %lld\n", o);
   kfma<<<1, 1>>>(dx, dout, 1000); cudaMemcpy(&o, dout, 8, cudaMemcpyDeviceToHost); printf("dfma: %lld\n", o);
