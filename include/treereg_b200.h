@@ -167,7 +167,27 @@ void* trg_ctx_stream(trg_ctx* ctx);
 int trg_tree_capacity(int max_level);
 /* Upload a host tree (e.g. a load_tree() result, gmm.cpp:798-896). */
 int trg_tree_upload(trg_ctx* ctx, const trg_tree* host, trg_tree_dev** out);
+/* load_tree's model from its JSON fields (gmm.cpp:798-896): weight, mean,
+ * cov and the topology are read from `host`; lambdas / axes / log_norm are
+ * ignored and recomputed on the device (refresh_eig, gmm.cpp:31-35, for every
+ * node).  TRG_EINVAL when eig_sym3 rejects a covariance, TRG_EDOMAIN when one
+ * is not positive definite (the lowest such node decides, like the
+ * reference's in-order loop). */
+int trg_tree_upload_refresh(trg_ctx* ctx, const trg_tree* host, trg_tree_dev** out);
 int trg_tree_download(trg_ctx* ctx, const trg_tree_dev* tree, trg_tree* host);
+/* treereg::save_tree / load_tree (gmm.cpp:769-896): the reference's JSON
+ * model file ("gmm-tree" v1), written with the reference's JSON library so
+ * the bytes match.  Bad files return TRG_ERUNTIME with the reference's
+ * "bad model file <path>: ..." message; a covariance eig_sym3 rejects,
+ * TRG_EINVAL.  trg_load_tree computes every node's eigen fields on the
+ * device (trg_tree_upload_refresh). */
+int trg_save_tree(trg_ctx* ctx, const trg_tree_dev* tree, const char* path);
+int trg_load_tree(trg_ctx* ctx, const char* path, trg_tree_dev** out);
+/* Host halves (no device): save from / parse into a host tree.  Parse with
+ * host->capacity < nodes returns TRG_ERANGE and sets host->n_nodes to the
+ * size needed (lambdas / axes / log_norm are not touched). */
+int trg_save_tree_host(const trg_tree* host, const char* path);
+int trg_load_tree_host(const char* path, trg_tree* host);
 int trg_tree_free(trg_ctx* ctx, trg_tree_dev* tree);
 int trg_tree_size(const trg_tree_dev* tree);
 

@@ -122,6 +122,8 @@ class Ref:
                                           C.c_double, C.c_int, _dp, _dp, _ip, _ip, _dp, _dp]
         L.ref_eig_sym3.argtypes = [_dp, C.c_int, C.c_double, _dp, _dp]
         L.ref_set_threads.argtypes = [C.c_uint]
+        L.ref_save_tree.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_load_tree.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
 
     def _chk(self, rc):
         if rc != 0:
@@ -214,6 +216,23 @@ class Ref:
         if self.L.ref_subsample(_d(p), len(p), int(n), int(seed), _d(out)) != 0:
             raise RuntimeError(self.L.ref_last_error().decode())
         return out
+
+    def save_tree(self, tree: dict, path):
+        """gmm.cpp:769-796 save_tree of a host tree (exported layout)."""
+        h = self._import(tree)
+        try:
+            self._chk(self.L.ref_save_tree(h, str(path).encode()))
+        finally:
+            self.L.ref_tree_free(h)
+
+    def load_tree(self, path) -> dict:
+        """gmm.cpp:798-896 load_tree; raises OracleError (code 1/3) like the reference."""
+        h = C.c_void_p()
+        self._chk(self.L.ref_load_tree(str(path).encode(), C.byref(h)))
+        try:
+            return self._export(h)
+        finally:
+            self.L.ref_tree_free(h)
 
     def _export(self, h):
         n = self.L.ref_tree_size(h)

@@ -215,6 +215,24 @@ long long ref_read_cloud(const char* path, int format, double* out, std::size_t 
   }
 }
 
+// gmm.cpp:769-796 save_tree / 798-896 load_tree
+int ref_save_tree(void* h, const char* path) {
+  GUARD({ save_tree(static_cast<RefTree*>(h)->tree, path); })
+}
+
+int ref_load_tree(const char* path, void** out) {
+  GUARD({
+    auto* t = new RefTree;
+    try {
+      t->tree = load_tree(path);
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    *out = t;
+  })
+}
+
 void ref_tree_free(void* h) { delete static_cast<RefTree*>(h); }
 int ref_tree_size(void* h) { return static_cast<int>(static_cast<RefTree*>(h)->tree.size()); }
 int ref_tree_max_level(void* h) { return static_cast<RefTree*>(h)->tree.max_level; }

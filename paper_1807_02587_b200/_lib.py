@@ -87,6 +87,11 @@ SIGNATURES = {
     "trg_ctx_transfer_bytes": (None, [C.c_void_p, u64p, u64p]),
     "trg_tree_capacity": (C.c_int, [C.c_int]),
     "trg_tree_upload": (C.c_int, [C.c_void_p, C.POINTER(TreeC), C.POINTER(C.c_void_p)]),
+    "trg_tree_upload_refresh": (C.c_int, [C.c_void_p, C.POINTER(TreeC), C.POINTER(C.c_void_p)]),
+    "trg_save_tree": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p]),
+    "trg_load_tree": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "trg_save_tree_host": (C.c_int, [C.POINTER(TreeC), C.c_char_p]),
+    "trg_load_tree_host": (C.c_int, [C.c_char_p, C.POINTER(TreeC)]),
     "trg_tree_download": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(TreeC)]),
     "trg_tree_free": (C.c_int, [C.c_void_p, C.c_void_p]),
     "trg_tree_size": (C.c_int, [C.c_void_p]),

@@ -1,14 +1,17 @@
 // C-ABI entry points (include/treereg_b200.h): context, workspace, tree
 // upload/download and the E-step.  Host code here only validates, stages
 // and launches; all arithmetic on the hot path runs in the kernels.
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "trg_internal.cuh"
 #include "trg_assoc.cuh"
+#include "trg_gmm.cuh"
 
 namespace {
 thread_local std::string g_last_error;
@@ -280,7 +283,29 @@ int trg_tree_capacity(int max_level) {
 int trg_tree_size(const trg_tree_dev* tree) { return tree ? tree->n_nodes : 0; }
 
 // Host tree -> packed device records.
+// refresh_eig (gmm.cpp:31-35) of every node of an uploaded model, as
+// load_tree does (gmm.cpp:889-894); the lowest failing node's error wins
+// (key = node * 4 + code), like the reference's in-order loop.
+__global__ void k_refresh_nodes(DNode* nodes, const double* cov, int J, int* first_bad) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  int code = 0;
+  if (refresh_node(nodes[j], cov + 9 * (size_t)j)) code = 1;  // eig_sym3 rejected it
+  else if (!(nodes[j].lam[2] > 0.0)) code = 2;                 // not positive definite
+  if (code) atomicMin(first_bad, j * 4 + code);
+}
+
+static int tree_upload(trg_ctx* ctx, const trg_tree* h, bool refresh, trg_tree_dev** out);
+
 int trg_tree_upload(trg_ctx* ctx, const trg_tree* h, trg_tree_dev** out) {
+  return tree_upload(ctx, h, false, out);
+}
+
+int trg_tree_upload_refresh(trg_ctx* ctx, const trg_tree* h, trg_tree_dev** out) {
+  return tree_upload(ctx, h, true, out);
+}
+
+static int tree_upload(trg_ctx* ctx, const trg_tree* h, bool refresh, trg_tree_dev** out) {
   if (!h || h->n_nodes <= 0 || h->max_level < 1) {
     set_error("trg_tree_upload: empty model");
     return TRG_EINVAL;
@@ -294,12 +319,12 @@ int trg_tree_upload(trg_ctx* ctx, const trg_tree* h, trg_tree_dev** out) {
     DNode& d = nodes[i];
     for (int r = 0; r < 3; ++r) {
       d.mean[r] = h->mean[3 * i + r];
-      d.lam[r] = h->lambdas[3 * i + r];
-      for (int k = 0; k < 3; ++k) d.axT[3 * r + k] = h->axes[9 * i + 3 * k + r];
+      d.lam[r] = refresh ? 1.0 : h->lambdas[3 * i + r];  // (refresh: computed on the device)
+      for (int k = 0; k < 3; ++k) d.axT[3 * r + k] = refresh ? (r == k) : h->axes[9 * i + 3 * k + r];
     }
     for (int r = 0; r < 3; ++r) d.il[r] = 1.0 / d.lam[r];
     d.pad = 0.0;
-    d.log_norm = h->log_norm[i];
+    d.log_norm = refresh ? 0.0 : h->log_norm[i];
     d.weight = h->weight[i];
     const double tr = (d.lam[0] + d.lam[1]) + d.lam[2];
     d.cplx = tr > 0.0 ? d.lam[2] / tr : -1.0;
@@ -320,7 +345,31 @@ int trg_tree_upload(trg_ctx* ctx, const trg_tree* h, trg_tree_dev** out) {
   }
   TRG_CU(trg_memcpy(ctx, t->nodes, nodes.data(), sizeof(DNode) * J, cudaMemcpyHostToDevice));
   TRG_CU(trg_memcpy(ctx, t->cov, h->cov, sizeof(double) * 9 * J, cudaMemcpyHostToDevice));
-  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  if (refresh) {
+    int* bad = nullptr;
+    const int none = INT_MAX;
+    TRG_CU(cudaMallocAsync((void**)&bad, sizeof(int), ctx->stream));
+    TRG_CU(cudaMemcpyAsync(bad, &none, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    k_refresh_nodes<<<(J + 127) / 128, 128, 0, ctx->stream>>>(t->nodes, t->cov, J, bad);
+    ctx->launches += 1;
+    int key = none;
+    TRG_CU(cudaMemcpyAsync(&key, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TRG_CU(cudaFreeAsync(bad, ctx->stream));
+    TRG_CU(cudaStreamSynchronize(ctx->stream));
+    if (key != none) {
+      trg_tree_free(ctx, t);
+      const int node = key / 4;
+      if (key % 4 == 1) {
+        set_error("eig_sym3: non-finite, non-symmetric or corrupted covariance (node " +
+                  std::to_string(node) + ")");
+        return TRG_EINVAL;
+      }
+      set_error("a node covariance is not positive definite");
+      return TRG_EDOMAIN;
+    }
+  } else {
+    TRG_CU(cudaStreamSynchronize(ctx->stream));
+  }
   *out = t;
   return TRG_OK;
 }

@@ -306,6 +306,56 @@ class GmmTree:
         return GmmTree(h, ctx)
 
 
+# ------------------------------------------------------------------ model files
+def save_tree(tree, path) -> None:
+    """gmm.cpp:769-796 save_tree (trg_save_tree / trg_save_tree_host): the
+    reference's JSON model file, byte for byte.  `tree` is a GmmTree or a
+    host dict in the .host() layout."""
+    if isinstance(tree, GmmTree):
+        _chk(_lib.lib().trg_save_tree(tree.ctx.h, tree.h, str(path).encode()))
+        return
+    a = {k: np.ascontiguousarray(v) for k, v in tree.items() if isinstance(v, np.ndarray)}
+    for k in ("parent", "first_child", "child_count", "level"):
+        a[k] = a[k].astype(np.int32)
+    s = _tree_struct(a, int(tree["max_level"]), len(a["weight"]))
+    s.n_nodes = len(a["weight"])
+    _chk(_lib.lib().trg_save_tree_host(C.byref(s), str(path).encode()))
+
+
+def _empty_host_tree(J: int) -> dict:
+    return dict(weight=np.zeros(J), mean=np.zeros((J, 3)), cov=np.zeros((J, 3, 3)),
+                lambdas=np.zeros((J, 3)), axes=np.zeros((J, 3, 3)), log_norm=np.zeros(J),
+                parent=np.zeros(J, np.int32), first_child=np.zeros(J, np.int32),
+                child_count=np.zeros(J, np.int32), level=np.zeros(J, np.int32))
+
+
+def parse_tree_file(path) -> dict:
+    """The host half of load_tree (gmm.cpp:798-887; trg_load_tree_host): JSON
+    parse and every structural check with the reference's messages.  Returns
+    weight / mean / cov / topology (eigen fields unset)."""
+    L = _lib.lib()
+    s = _tree_struct(_empty_host_tree(0), 0, 0)
+    rc = L.trg_load_tree_host(str(path).encode(), C.byref(s))
+    if rc != _lib.TRG_ERANGE:
+        _chk(rc if rc != 0 else _lib.TRG_EINVAL)
+    t = _empty_host_tree(s.n_nodes)
+    s = _tree_struct(t, 0, s.n_nodes)
+    _chk(L.trg_load_tree_host(str(path).encode(), C.byref(s)))
+    t["max_level"] = s.max_level
+    return t
+
+
+def load_tree(path, ctx: Context | None = None) -> "GmmTree":
+    """gmm.cpp:798-896 load_tree onto the device (trg_load_tree): host parse
+    and validation, then refresh_eig of every node on the GPU.  Bad files
+    raise RuntimeError("bad model file <path>: ...") like the reference; a
+    covariance eig_sym3 rejects raises InvalidArgument."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    _chk(_lib.lib().trg_load_tree(ctx.h, str(path).encode(), C.byref(h)))
+    return GmmTree(h, ctx)
+
+
 def _tree_struct(t: dict, max_level: int, cap: int) -> TreeC:
     s = TreeC()
     s.n_nodes = 0
