@@ -212,6 +212,7 @@ __device__ __forceinline__ void block_argmax(double s, double i, double (*ws)[2]
 
 struct Phase {
   bool mom1, mom2, pcount, pwrite, layout;
+  bool emit;    // pcount: the partition is written next (not in the last round)
   int fps;      // FPS round 1..7 (0 = none)
   int mode[2];  // per candidate: 0 none, 1 EM, 2 final
   int em_it[2];
@@ -232,7 +233,10 @@ __device__ __forceinline__ Phase phase_of(int p, int I, bool last_round) {
     ph.em_it[1] = p - 7;
   }
   if (p == I + 8) ph.mode[1] = 2;
-  if (p == I + 9) ph.pcount = true;
+  if (p == I + 9) {
+    ph.pcount = true;
+    ph.emit = !last_round;  // the last round's children are leaves: counts only
+  }
   if (p == I + 10) ph.layout = true;
   if (p == I + 11 && !last_round) ph.pwrite = true;
   return ph;
@@ -475,7 +479,7 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
           cnt += 1.0;
           mass += w;
         }
-        p.emit[(size_t)(sm.tstart + e) * 8 + sv] = out;
+        if (ph.emit) p.emit[(size_t)(sm.tstart + e) * 8 + sv] = out;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1023,7 +1027,7 @@ __device__ int phase_items(const Phase& ph, int* off, int* kind) {
   }
   if (ph.pcount) {
     sum_range(kOffCnt + 8, 8);
-    for (int q = 0; q < 8; ++q) {  // per-survivor tile prefix (child base offsets)
+    for (int q = 0; q < (ph.emit ? 8 : 0); ++q) {  // per-survivor tile prefix (child base offsets)
       off[n] = q;
       kind[n++] = 2;
     }

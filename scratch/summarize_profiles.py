@@ -43,6 +43,18 @@ def details(k):
     for r in rows[1:]:
         if len(r) > iV and r[iN] in want and r[iN] not in out:
             out[r[iN]] = (r[iV], r[iU])
+    # FP64 pipe: the arithmetic roofline the path is closest to
+    raw = subprocess.run(["ncu", "-i", f"gpurun_out/prof_{k}.ncu-rep", "--page", "raw", "--csv"],
+                         capture_output=True, text=True).stdout
+    rr = list(csv.reader(raw.splitlines()))
+    if len(rr) > 2:
+        hh, vv = rr[0], rr[2]
+        for name, key in (("FP64 pipe inst executed (% of peak, active)",
+                           "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                          ("FP64 pipe cycles active (% of elapsed)",
+                           "TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")):
+            if key in hh:
+                out[name] = (f"{float(vv[hh.index(key)]):.2f}", "%")
     return out
 
 
