@@ -17,6 +17,7 @@
 //   p = I+11       partition write pass (skipped in the last round)
 #include <cub/block/block_scan.cuh>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "trg_gmm.cuh"
@@ -101,6 +102,7 @@ struct BuildParams {
   double* partial;    // [Tmax][kRec]
   double* nodered;    // [Kmax][kRec] per-node reduced record
   unsigned* fdone;    // [Kmax] fields reduced (per phase)
+  TreeMeta* meta;     // published by k_calibrate for work queued behind the build
   double* tile_base;  // [Tmax][8] child base offsets within node's child segment
   double* min_d2;     // [Emax]
   double* emit;       // [Emax][8]
@@ -1352,7 +1354,10 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
   const int lane = tid & 31, warp = tid >> 5;
   BuildState* st = p.st;
   const bool sharded = p.seg >= 0;
-  if (__ldcg(&st->status_overflow)) return;
+  if (__ldcg(&st->status_overflow)) {
+    if (cta == 0 && tid == 0) p.meta->ok = 0;
+    return;
+  }
   if (sharded && __ldcg(&st->cal_done)) return;
   const int J = __ldcg(&st->J);
   __shared__ int lvl[9];
@@ -1511,7 +1516,15 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
       st->cal_pass = pass + 1;
     }
   }
-  if (cta == 0 && tid == 0) st->cal_evals = __ldcg(&p.a.counters[1]);
+  if (cta == 0 && tid == 0) {
+    st->cal_evals = __ldcg(&p.a.counters[1]);
+    TreeMeta m;
+    m.J = J;
+    m.root_count = root_count;
+    m.n_upper = p.L >= 2 ? lvl[p.L - 1] : 0;
+    m.ok = __ldcg(p.status) == 0 ? 1 : 0;
+    *p.meta = m;
+  }
 }
 
 __global__ void k_init_entries(const double* __restrict__ pts, size_t n, double* ex, double* ey,
@@ -1607,6 +1620,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
                o_llt = carve(sizeof(double) * (size_t)cap * 2 * (cfg->em_iterations_per_node + 1)),
                o_kex = carve(sizeof(int) * (size_t)cap),
                o_car = carve(sizeof(unsigned) * ((size_t)cap + 1)), o_dbits = carve(16),
+               o_meta = carve(sizeof(TreeMeta)),
                o_state = carve(sizeof(BuildState));
   TRG_CU(cudaFuncSetAttribute((const void*)k_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)sizeof(BuildSmem)));
@@ -1658,6 +1672,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   p.partial = (double*)(A + o_part);
   p.nodered = (double*)(A + o_nred);
   p.fdone = (unsigned*)(A + o_fd);
+  p.meta = (TreeMeta*)(A + o_meta);
   p.tile_base = (double*)(A + o_tb);
   p.min_d2 = (double*)(A + o_md);
   p.emit = (double*)(A + o_emit);
@@ -1725,8 +1740,15 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   TRG_CU(cudaMemsetAsync(A + o_fd, 0, sizeof(unsigned) * K, ctx->stream));
   TRG_CU(cudaMemsetAsync(A + o_car, 0, sizeof(unsigned) * ((size_t)cap + 1), ctx->stream));
   TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
-  TRG_CU(trg_memcpy(ctx, p.st, &st, sizeof st, cudaMemcpyHostToDevice));
-  const int h_rn[5] = {-1, 0, (int)n, 0, st.Tp[0]};
+  // initial state through a dedicated pinned buffer: asynchronous copies, no
+  // staging syncs (the previous build's copies completed at its collect)
+  void* hinit = nullptr;
+  TRG_TRY(host_ws_get(ctx, kSlotHostBuildInit, sizeof(BuildState) + 8 * sizeof(int), &hinit));
+  std::memcpy(hinit, &st, sizeof st);
+  int* h_rn = reinterpret_cast<int*>(static_cast<char*>(hinit) + sizeof(BuildState));
+  const int rn0[5] = {-1, 0, (int)n, 0, st.Tp[0]};
+  std::memcpy(h_rn, rn0, sizeof rn0);
+  TRG_CU(trg_memcpy(ctx, p.st, hinit, sizeof st, cudaMemcpyHostToDevice));
   for (int q = 0; q < 5; ++q)
     TRG_CU(trg_memcpy(ctx, A + o_rn[0][q], &h_rn[q], sizeof(int), cudaMemcpyHostToDevice));
   k_init_entries<<<256, 256, 0, ctx->stream>>>(pts, n, p.ex[0], p.ey[0], p.ez[0], p.ew[0],
@@ -1907,6 +1929,66 @@ extern "C" int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz
   set_error("build_tree: entry buffer growth did not converge");
   return TRG_ERUNTIME;
 }
+
+// ------------------------------------------------------------ async build
+namespace trg {
+
+struct AsyncBuild {
+  BuildJob job;
+  BuildAlloc al;
+  trg_model_config cfg;
+  size_t n = 0;
+};
+
+int build_async_start(trg_ctx* ctx, const double* dev, size_t n, const trg_model_config* cfg,
+                      AsyncBuild** h, trg_tree_dev** tree, const TreeMeta** meta) {
+  if (!*h) {  // first attempt: trg_build_tree's argument checks
+    TRG_TRY(validate_model_config(cfg));
+    if (n == 0 || !dev) {
+      set_error("point cloud is empty");
+      return TRG_EINVAL;
+    }
+    if (n > (size_t)INT32_MAX / 8) {
+      set_error("point cloud too large for int32 entry indexing");
+      return TRG_EINVAL;
+    }
+    *h = new AsyncBuild;
+    (*h)->al = initial_alloc(ctx, n, cfg->max_level);
+    (*h)->cfg = *cfg;
+    (*h)->n = n;
+  }
+  AsyncBuild* b = *h;
+  b->job = BuildJob{};
+  TRG_TRY(build_prepare(ctx, dev, n, &b->cfg, b->al, nullptr, 0, &b->job));
+  TRG_TRY(build_launch(ctx, &b->job, -1));
+  TRG_TRY(calibrate_launch(ctx, &b->job, -1));
+  *tree = b->job.tree;
+  *meta = b->job.p.meta;
+  return TRG_OK;
+}
+
+int build_async_finish(trg_ctx* ctx, AsyncBuild* b, trg_tree_dev** out, bool* retry) {
+  bool overflow = false;
+  BuildAlloc need = b->al;
+  *retry = false;
+  const int rc = build_collect(ctx, &b->job, &b->cfg, out, nullptr, &overflow, &need);
+  if (rc != TRG_OK) {
+    if (rc == TRG_EINVAL && trg_last_error()[0] == 'b') set_error("point cloud has non-finite coordinates or no mass");
+    return rc;
+  }
+  if (overflow) {  // as trg_build_tree's retry loop
+    ctx->build_growth = std::max(ctx->build_growth, 1.25 * (double)need.Emax / (double)b->n);
+    b->al.Emax = std::max(b->al.Emax * 2, need.Emax + 1024);
+    b->al.Kmax = std::max(b->al.Kmax, need.Kmax);
+    b->al.Tmax = b->al.Emax / kTile + b->al.Kmax + 8;
+    *retry = true;
+  }
+  return TRG_OK;
+}
+
+void build_async_free(AsyncBuild* b) { delete b; }
+
+}  // namespace trg
 
 // ------------------------------------------------------------ sharded build
 namespace trg {

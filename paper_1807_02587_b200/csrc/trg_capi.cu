@@ -85,12 +85,14 @@ cudaError_t trg_memcpy(trg_ctx* ctx, void* dst, const void* src, size_t bytes, c
   return cudaSuccess;
 }
 
-int check_status(trg_ctx* ctx, const char* where) {
+int check_status(trg_ctx* ctx, const char* where) { return check_status_at(ctx, ctx->status, where); }
+
+int check_status_at(trg_ctx* ctx, int* dev_status, const char* where) {
   int st = 0;
-  TRG_CU(trg_memcpy(ctx, &st, ctx->status, sizeof(int), cudaMemcpyDeviceToHost));
+  TRG_CU(trg_memcpy(ctx, &st, dev_status, sizeof(int), cudaMemcpyDeviceToHost));
   TRG_CU(cudaStreamSynchronize(ctx->stream));
   if (st != 0) {
-    TRG_CU(cudaMemsetAsync(ctx->status, 0, sizeof(int), ctx->stream));
+    TRG_CU(cudaMemsetAsync(dev_status, 0, sizeof(int), ctx->stream));
     const char* what = st == kEDomain   ? "covariance is not positive definite / no positive trace"
                        : st == kEInval  ? "invalid argument"
                        : st == kERuntime ? "no responsibility mass"
@@ -210,8 +212,9 @@ int trg_ctx_create(int device, trg_ctx** out) {
   c->sms = prop.multiProcessorCount;
   c->device_sms = c->sms;
   TRG_CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-  TRG_CU(cudaMalloc(&c->status, sizeof(int)));
-  TRG_CU(cudaMemset(c->status, 0, sizeof(int)));
+  TRG_CU(cudaMalloc(&c->status, 2 * sizeof(int)));
+  TRG_CU(cudaMemset(c->status, 0, 2 * sizeof(int)));
+  c->status2 = c->status + 1;
   TRG_CU(cudaMalloc(&c->dev_timeline, sizeof(Timeline)));
   TRG_CU(cudaMemset(c->dev_timeline, 0, sizeof(Timeline)));
   *out = c;

@@ -40,6 +40,9 @@ struct EmParams {
   double* xmom;
   double n_total;  // total source points over all shards (mass floor)
   double* psum;    // dense (flat mixture) E-step: per-point score sums
+  // Queued behind an asynchronous build (register_clouds): the tree's size
+  // comes from the build's published meta (nothing to do unless meta->ok).
+  const TreeMeta* meta;
 };
 
 constexpr int kAccStride = kNormalEq + 2;
@@ -63,7 +66,13 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
   __shared__ int s_done, s_fails, s_conv, s_iters;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int J = p.a.n_nodes;
+  int J = p.a.n_nodes, root_count = p.a.root_count, n_snodes = p.a.n_snodes;
+  if (p.meta) {
+    if (!__ldcg(&p.meta->ok)) return;  // the build failed or overflowed: the host retries / reports
+    J = __ldcg(&p.meta->J);
+    root_count = __ldcg(&p.meta->root_count);
+    n_snodes = min(__ldcg(&p.meta->n_upper), kStageNodes);
+  }
   const int P2 = min(G, (J + (kAssocBlock / 32) - 1) / (kAssocBlock / 32));  // producer CTAs
   const bool sharded = p.seg >= 0;
   const double n_total = sharded ? p.n_total : (double)p.a.n;
@@ -80,12 +89,15 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
   // the model is fixed during the EM: stage its upper levels once
   extern __shared__ __align__(16) unsigned char k_reg_stage[];
   DNode* reg_stage = reinterpret_cast<DNode*>(k_reg_stage);
-  if (!DENSE) stage_nodes(reg_stage, p.a.nodes, p.a.n_snodes);
+  if (!DENSE) stage_nodes(reg_stage, p.a.nodes, n_snodes);
   for (int it = 0; it < p.max_iters; ++it) {
     const bool run_e = !sharded || p.seg == it;      // E-step of iteration it
     const bool run_m = !sharded || p.seg == it + 1;  // combine/solve of iteration it
     if (!run_e && !run_m) continue;
     AssocParams a = p.a;
+    a.n_nodes = J;
+    a.root_count = root_count;
+    a.n_snodes = n_snodes;
     a.epoch = p.epoch0 + (uint32_t)it;
     a.snodes = reg_stage;
     // per-iteration counters alternate between two slots: CTA 0 reads and
@@ -264,8 +276,13 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
 // registration.cpp:140-151 tree_extent_estimate (single block; min/max are
 // exact, so the result is bit-identical to the reference).
 __global__ void k_extent(const DNode* __restrict__ nodes, int J, EmState* st, double diag,
-                         double tol) {
+                         double tol, const TreeMeta* meta, const double* diag_dev) {
   __shared__ double lo[3][256], hi[3][256];
+  if (meta) {
+    if (!__ldcg(&meta->ok)) return;
+    J = __ldcg(&meta->J);
+  }
+  if (diag_dev) diag = __ldcg(diag_dev);
   double l[3] = {INFINITY, INFINITY, INFINITY}, h[3] = {-INFINITY, -INFINITY, -INFINITY};
   if (!(diag > 0.0)) {
     for (int j = threadIdx.x; j < J; j += blockDim.x) {
@@ -412,14 +429,22 @@ struct EmJob {
   EmParams p;
   int G = 0, J = 0, K = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int* status = nullptr;  // the status word this run reports through
 };
 
 // Parameters, workspace and initial state of one EM run (sharded: seg mode
 // with the exchange buffer xmom and the global point count).
+// meta / diag_dev (asynchronous register_clouds): the tree is still being
+// built; its size and the target diagonal are read on the device, workspace
+// is sized for the tree's capacity, and errors go to ctx->status2 so the
+// build's collect does not see them.  Nothing here synchronises the stream.
 int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t n,
                const trg_reg_config* cfg, double target_diag, bool sharded, double n_total,
-               EmJob* job, bool dense = false) {
-  const int J = tree->n_nodes;
+               EmJob* job, bool dense = false, const TreeMeta* meta = nullptr,
+               const double* diag_dev = nullptr) {
+  const int J = meta ? tree->capacity : tree->n_nodes;
+  int* status = meta ? ctx->status2 : ctx->status;
+  job->status = status;
   job->kernel = dense ? (const void*)k_register<true> : (const void*)k_register<false>;
   job->smem = dense ? 0 : sizeof(DNode) * kStageNodes;
   TRG_CU(cudaFuncSetAttribute(job->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -441,7 +466,8 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   p.a.outlier_floor = 1e-300;
   p.a.pts = src_dev;
   p.a.n = n;
-  p.a.status = ctx->status;
+  p.a.status = status;
+  p.meta = meta;
   void *part, *stamps, *mom, *cnt, *em, *tr, *xm;
   TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * 4 * (size_t)J * G, &part));
   TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)J * G, &stamps));
@@ -476,14 +502,20 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   TRG_TRY(timeline_reset(ctx));
   p.epoch0 = ctx->epoch + 1;
   ctx->epoch += (uint32_t)K + 1;
-  EmState st{};
+  // initial state through a dedicated pinned buffer: an asynchronous copy,
+  // no staging sync (the previous run's copy completed at its collect)
+  void* hst = nullptr;
+  TRG_TRY(host_ws_get(ctx, kSlotHostEmInit, sizeof(EmState), &hst));
+  EmState& st = *static_cast<EmState*>(hst);
+  st = EmState{};
   for (int k = 0; k < 9; ++k) st.Rt[k] = cfg->initial_R[k];
   for (int k = 0; k < 3; ++k) st.Rt[9 + k] = cfg->initial_t[k];
   TRG_CU(cudaMemsetAsync(em, 0, 64, ctx->stream));
   TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
   TRG_CU(trg_memcpy(ctx, p.st, &st, sizeof st, cudaMemcpyHostToDevice));
-  if (n > 0) k_check_finite<<<64, 256, 0, ctx->stream>>>(src_dev, 3 * n, ctx->status);
-  k_extent<<<1, 256, 0, ctx->stream>>>(tree->nodes, J, p.st, target_diag, cfg->translation_tol);
+  if (n > 0) k_check_finite<<<64, 256, 0, ctx->stream>>>(src_dev, 3 * n, status);
+  k_extent<<<1, 256, 0, ctx->stream>>>(tree->nodes, J, p.st, target_diag, cfg->translation_tol,
+                                       meta, diag_dev);
   ctx->launches += 2;
   job->p = p;
   job->G = G;
@@ -519,7 +551,7 @@ int em_collect(trg_ctx* ctx, EmJob* job, trg_reg_result* out) {
   cudaEventElapsedTime(&ms, job->e0, job->e1);
   cudaEventDestroy(job->e0);
   cudaEventDestroy(job->e1);
-  TRG_TRY(check_status(ctx, "register_with_tree"));
+  TRG_TRY(check_status_at(ctx, job->status ? job->status : ctx->status, "register_with_tree"));
   TRG_TRY(timeline_fetch(ctx));
   for (int k = 0; k < 9; ++k) out->R[k] = st.Rt[k];
   for (int k = 0; k < 3; ++k) out->t[k] = st.Rt[9 + k];
@@ -600,8 +632,9 @@ __global__ void k_bbox(const double* __restrict__ p, size_t n, double* part, uns
   }
 }
 
-// bbox of a device cloud: out[0] = diagonal, out[2..4] = min, out[5..7] = max
-int target_bbox(trg_ctx* ctx, const double* dev, size_t n, double out8[8]) {
+// bbox of a device cloud, left on the device: od[0] = diagonal, od[2..4] =
+// min, od[5..7] = max (stream-ordered, no synchronisation)
+int bbox_launch(trg_ctx* ctx, const double* dev, size_t n, double** od_out) {
   void* o = nullptr;
   const int nb = 64;
   TRG_TRY(ws_get(ctx, kSlotBuild11, 64 + sizeof(double) * 6 * nb, &o));
@@ -610,7 +643,15 @@ int target_bbox(trg_ctx* ctx, const double* dev, size_t n, double out8[8]) {
   k_bbox<<<nb, 256, 0, ctx->stream>>>(dev, n, od + 8, reinterpret_cast<unsigned*>(od + 1),
                                       od);
   ctx->launches += 1;
-  TRG_CU(trg_memcpy(ctx, out8, o, sizeof(double) * 8, cudaMemcpyDeviceToHost));
+  *od_out = od;
+  return TRG_OK;
+}
+
+// bbox of a device cloud: out[0] = diagonal, out[2..4] = min, out[5..7] = max
+int target_bbox(trg_ctx* ctx, const double* dev, size_t n, double out8[8]) {
+  double* od = nullptr;
+  TRG_TRY(bbox_launch(ctx, dev, n, &od));
+  TRG_CU(trg_memcpy(ctx, out8, od, sizeof(double) * 8, cudaMemcpyDeviceToHost));
   TRG_CU(cudaStreamSynchronize(ctx->stream));
   return TRG_OK;
 }
@@ -854,6 +895,70 @@ int trg_register_with_tree(trg_ctx* ctx, const trg_tree_dev* tree, const double*
   return rc;
 }
 
+// register_clouds for the tree variants with one host synchronisation: the
+// target's bbox, the build and the EM are queued back to back on the stream
+// (the EM reads the tree's size and the diagonal on the device), then the
+// build and the EM are collected.  An entry-buffer overflow (the EM saw
+// meta->ok == 0 and did nothing) re-queues both with the grown allocation.
+static int register_tree_async(trg_ctx* ctx, const double* tgt, size_t n_target,
+                               const double* src, size_t n_source, const trg_reg_config* cfg,
+                               trg_reg_result* out) {
+  trg_model_config mc = cfg->model_config;
+  mc.max_level = cfg->variant_param;
+  double* od = nullptr;
+  TRG_TRY(bbox_launch(ctx, tgt, n_target, &od));
+  AsyncBuild* ab = nullptr;
+  int rc = TRG_OK;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    cudaEvent_t e0, e1;
+    TRG_CU(cudaEventCreate(&e0));
+    TRG_CU(cudaEventCreate(&e1));
+    TRG_CU(cudaEventRecord(e0, ctx->stream));
+    trg_tree_dev* tree = nullptr;
+    const TreeMeta* meta = nullptr;
+    ctx->build_into_scratch = true;
+    rc = build_async_start(ctx, tgt, n_target, &mc, &ab, &tree, &meta);
+    ctx->build_into_scratch = false;
+    if (rc != TRG_OK) break;
+    TRG_CU(cudaEventRecord(e1, ctx->stream));
+    EmJob job;
+    rc = em_prepare(ctx, tree, src, n_source, cfg, 0.0, false, 0.0, &job, false, meta, od);
+    if (rc == TRG_OK) rc = em_launch(ctx, &job, -1);
+    if (rc != TRG_OK) break;
+    trg_tree_dev* built = nullptr;
+    bool retry = false;
+    rc = build_async_finish(ctx, ab, &built, &retry);  // synchronises the stream
+    if (rc == TRG_OK && retry) {
+      cudaEventDestroy(job.e0);
+      cudaEventDestroy(job.e1);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      continue;
+    }
+    if (rc != TRG_OK) {  // the EM's events / status word are dropped with it
+      cudaEventDestroy(job.e0);
+      cudaEventDestroy(job.e1);
+      cudaMemsetAsync(ctx->status2, 0, sizeof(int), ctx->stream);
+      break;
+    }
+    job.J = built->n_nodes;
+    rc = em_collect(ctx, &job, out);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc == TRG_OK) out->model_build_seconds = ms * 1e-3;
+    build_async_free(ab);
+    return rc;
+  }
+  build_async_free(ab);
+  if (rc == TRG_OK) {
+    set_error("build_tree: entry buffer growth did not converge");
+    rc = TRG_ERUNTIME;
+  }
+  return rc;
+}
+
 // registration.cpp:174-209 register_clouds (adaptive:L / tree:L):
 // validate, build the tree on the target, then the EM loop.
 int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
@@ -875,6 +980,7 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
     return register_icp_dev(ctx, tgt, n_target, src, n_source, cfg,
                             target_bbox_diagonal(ctx, tgt, n_target), out);
   }
+  if (cfg->variant_kind != TRG_VARIANT_FLAT) return register_tree_async(ctx, tgt, n_target, src, n_source, cfg, out);
   cudaEvent_t e0, e1;
   TRG_CU(cudaEventCreate(&e0));
   TRG_CU(cudaEventCreate(&e1));

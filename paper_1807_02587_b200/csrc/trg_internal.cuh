@@ -115,6 +115,7 @@ struct trg_ctx {
   void* host_slot_ptr[kSlots] = {};
   size_t host_slot_size[kSlots] = {};
   int* status = nullptr;  // device status word
+  int* status2 = nullptr;  // second word: the EM of an asynchronous register_clouds
   trg::Timeline* dev_timeline = nullptr;      // device buffer (reset per call)
   std::vector<unsigned long long> timeline;  // last call: globaltimer ns per mark
   std::vector<int> timeline_lab;
@@ -164,6 +165,8 @@ enum Slot : int {
   kSlotDense,         // dense association: per-point score sums
   kSlotHostStage,     // host slots only: pinned staging for pageable copies
   kSlotTimelineHost,  // host slots only: last device timeline
+  kSlotHostEmInit,    // host slots only: pinned EmState initialiser (no staging sync)
+  kSlotHostBuildInit, // host slots only: pinned BuildState initialiser
 };
 
 int ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
@@ -198,6 +201,21 @@ int flat_build(trg_ctx* ctx, const double* dev, size_t n, size_t J, const trg_mo
 int build_sharded_dev(trg_comm* c, const double* const* dev, const size_t* n,
                       const trg_model_config* cfg, trg_tree_dev** trees, trg_build_diag* diag);
 int check_status(trg_ctx* ctx, const char* where);
+int check_status_at(trg_ctx* ctx, int* dev_status, const char* where);
+// What k_calibrate publishes about the finished tree for work queued behind
+// it without a host round trip (ok = 0: the build failed or overflowed).
+struct TreeMeta {
+  int ok, J, root_count, n_upper;
+};
+// Asynchronous build (register_clouds): launch the build, queue work behind
+// it, then collect.  finish() sets *retry when the entry buffers overflowed
+// (the queued work saw meta->ok == 0 and did nothing); start() again reuses
+// the grown allocation.
+struct AsyncBuild;
+int build_async_start(trg_ctx* ctx, const double* dev, size_t n, const trg_model_config* cfg,
+                      AsyncBuild** h, trg_tree_dev** tree, const TreeMeta** meta);
+int build_async_finish(trg_ctx* ctx, AsyncBuild* h, trg_tree_dev** out, bool* retry);
+void build_async_free(AsyncBuild* h);
 int timeline_reset(trg_ctx* ctx);
 int timeline_fetch(trg_ctx* ctx);
 int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out);
