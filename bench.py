@@ -339,6 +339,18 @@ def run_c4(args, tr, ctx, dist, dev, world):
     dt = max_over_ranks(time.perf_counter() - t0, dist, dev)
     ang = float(np.degrees(np.arccos(np.clip((np.trace(res.transform.rotation.T @ T.rotation) - 1) / 2,
                                              -1, 1))))
+    roof = None
+    if world == 1:  # the HBM fraction is meaningful at C4 (entries exceed L2)
+        diag = tr.BuildDiagnostics()
+        tree = tr.build_tree(tg, tr.ModelConfig(max_level=4), diag, ctx)
+        b_build, _ = algorithmic_bytes(diag, len(pts), len(src), tree.size(), res.iterations)
+        t_build = float(np.median(builds))
+        peak, peak_kind = load_peaks()
+        ach = b_build / t_build / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "kernel": "tree build (k_build + k_calibrate), C4", "algorithmic_bytes": b_build,
+                "peak_kind": peak_kind, "E_per_round": list(diag.entries_per_round),
+                "calibration_passes": diag.calibration_passes}
     return {"workload": "C4 synthetic_scene(1M, seed 4), adaptive:4" +
                         (f", point-sharded over {world} GPUs (NCCL)" if world > 1 else ", one GPU"),
             "scaling": "strong" if world > 1 else None,
@@ -346,7 +358,7 @@ def run_c4(args, tr, ctx, dist, dev, world):
             "timing": "host wall clock around synchronous registrations, max over ranks",
             "tree_build_mpoints_per_s": len(pts) / float(np.median(builds)) / 1e6,
             "em_iterations": res.iterations, "converged": res.converged,
-            "rot_err_deg_vs_gt": ang,
+            "rot_err_deg_vs_gt": ang, "roofline": roof,
             "note": "the reference's own register_clouds does not converge on this pose either "
                     "(50 iterations, same answer: tests/test_c4_gpu.py)"}
 
@@ -392,9 +404,17 @@ def cpu_baseline(cfg_name):
         t0 = time.perf_counter()
         ref.register_clouds(tg, sr, level=L)
         dt = time.perf_counter() - t0
+        # the reference's serial run beside the all-cores one
+        ref.set_threads(1)
+        t0 = time.perf_counter()
+        ref.register_clouds(tg, sr, level=L)
+        dt1 = time.perf_counter() - t0
+        ref.set_threads(cores)
         return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "reference",
                 "sample": f"1 full registration (build+EM) of the {cfg_name.upper()} pair, "
-                          f"{cores} threads, {dt:.2f} s"}
+                          f"{cores} threads, {dt:.2f} s",
+                "serial": {"value": 1.0 / dt1, "unit": UNIT, "cores": 1,
+                           "sample": f"the same registration on 1 thread, {dt1:.2f} s"}}
     except Exception as e:  # the oracle build is test infrastructure; report, don't fail
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                 "sample": f"unavailable: {e}"}
