@@ -362,7 +362,7 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     const double x0 = sm.ent[0][tid], x1 = sm.ent[1][tid], x2 = sm.ent[2][tid], w = sm.ent[3][tid];
     for (int ci = 0; ci < nc; ++ci) {
       const int cand = pcount ? sm.kept : sm.cand_list[ci];
-      const int mode = pcount ? 3 : ph.mode[cand];
+      const int mode = pcount ? 3 : (cand == 0 ? ph.mode[0] : ph.mode[1]);  // (no local-memory index)
       double lg[8];
       double m = -INFINITY;
 #pragma unroll
@@ -404,7 +404,7 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     for (int item = warp; item < nc * 8; item += kTile / 32) {
       const int ci = item >> 3, k = item & 7;
       const int cand = sm.cand_list[ci];
-      const int mode = ph.mode[cand];
+      const int mode = cand == 0 ? ph.mode[0] : ph.mode[1];
       const double n0 = sm.nmean[0], n1 = sm.nmean[1], n2 = sm.nmean[2];
       double a[11];
 #pragma unroll

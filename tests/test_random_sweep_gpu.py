@@ -1,0 +1,93 @@
+"""Randomised parity sweep against the live reference (oracle/_ref, the
+reference's own sources): ragged sizes around the 32-point expansion gate
+and the 256-entry tile (1, 9, 31-33, 255-257, 1023, 3001, 4097), shapes
+that stress the covariance floor (lines, planes, duplicate points, mixed
+scales) and depths 1-3.  Per case: build_tree (structure exact, parameters
+1e-4), per-point association on the reference's tree (node ids equal except
+documented near-ties, path weights 1e-12) and register_clouds (1e-4 rad /
+1e-4 x extent)."""
+import numpy as np
+import pytest
+
+from tests.helpers import near_tie_on_path, rel_err, rotation_angle_between
+
+pytestmark = pytest.mark.gpu
+
+
+def _cloud(shape, n, rng):
+    if shape == "uniform":
+        return rng.uniform(-1, 1, size=(n, 3))
+    if shape == "blobs":
+        c = rng.normal(size=(4, 3)) * 2.0
+        return c[rng.integers(0, 4, n)] + rng.normal(size=(n, 3)) * 0.2
+    if shape == "plane":
+        u = rng.uniform(-1, 1, size=(n, 2))
+        return np.c_[u, 0.3 * u[:, 0] + 1e-3 * rng.normal(size=n)]
+    if shape == "line":
+        s = rng.uniform(-2, 2, size=n)
+        return np.c_[s, 0.5 * s, -s] + 1e-4 * rng.normal(size=(n, 3))
+    if shape == "duplicates":
+        base = rng.normal(size=(max(1, n // 8), 3))
+        return base[rng.integers(0, len(base), n)]
+    if shape == "mixed":  # far-apart clusters at very different scales
+        a = rng.normal(size=(n // 2, 3)) * 1e-2
+        b = rng.normal(size=(n - n // 2, 3)) * 5.0 + 40.0
+        return np.r_[a, b]
+    raise ValueError(shape)
+
+
+CASES = [(1, 1, "uniform", 2), (2, 9, "blobs", 2), (3, 31, "plane", 2), (4, 32, "uniform", 2),
+         (5, 33, "line", 3), (6, 255, "duplicates", 2), (7, 256, "blobs", 3), (8, 257, "plane", 3),
+         (9, 1023, "mixed", 3), (10, 3001, "uniform", 2), (11, 4097, "blobs", 1),
+         (12, 2500, "line", 3)]
+# plus drawn cases: size, shape and depth from the seed
+_SHAPES = ("uniform", "blobs", "plane", "line", "duplicates", "mixed")
+for _s in range(13, 37):
+    _r = np.random.default_rng(1000 + _s)
+    CASES.append((_s, int(_r.integers(1, 6000)), _SHAPES[int(_r.integers(0, 6))], int(_r.integers(1, 4))))
+
+
+@pytest.mark.parametrize("seed,n,shape,L", CASES)
+def test_random_cloud_parity(ctx, ref, seed, n, shape, L):
+    from paper_1807_02587_b200 import treereg as tr
+    rng = np.random.default_rng(seed)
+    pts = _cloud(shape, n, rng)
+    # build_tree
+    G = ref.build_tree(pts, max_level=L)
+    h = tr.build_tree(pts, tr.ModelConfig(max_level=L), ctx=ctx).host()
+    assert len(h["weight"]) == len(G["weight"])
+    for k in ("parent", "first_child", "child_count", "level"):
+        assert np.array_equal(h[k], G[k]), k
+    assert np.abs(h["weight"] - G["weight"]).max() <= 1e-4 * max(1.0, G["weight"].max())
+    scale = max(np.abs(G["mean"]).max(), 1e-300)
+    assert np.abs(h["mean"] - G["mean"]).max() <= 1e-4 * scale
+    # covariances within 1e-4 relative, plus the rounding floor of a scatter
+    # formed from raw moments (m2/m0 - mu mu^T): eps * |mu|^2 per entry.  A leaf
+    # holding one point (or duplicates) far from the origin has a covariance
+    # that IS that rounding noise clamped at the 1e-12 floor in both
+    # implementations ("mixed" clouds at |x| ~ 50: 1e-13 of noise on 1e-12).
+    cs = np.linalg.norm(G["cov"].reshape(len(G["cov"]), -1), axis=1)
+    noise = 64 * np.finfo(float).eps * (np.sum(G["mean"] ** 2, axis=1) + cs)
+    dc = np.linalg.norm((h["cov"] - G["cov"]).reshape(len(cs), -1), axis=1)
+    assert np.all(dc <= 1e-4 * cs + noise), np.max(dc / np.maximum(cs, 1e-300))
+    # per-point association on the reference's tree, under a small motion
+    R, t = ref.random_rigid_transform(5.0, 0.05, seed)
+    tree = tr.GmmTree.from_host(G, ctx)
+    lc = 0.01
+    _, node, w = tr.associate_adaptive(pts, tree, tr.RigidTransform(R, t), tr.AssocConfig(lambda_c=lc),
+                                       per_point=True)
+    rnode, rw = ref.associate_points(G, pts, R, t, lambda_c=lc)
+    y = pts @ R.T + t
+    for i in np.nonzero(node != rnode)[0]:
+        assert near_tie_on_path(G, y[i], lc), f"point {i}: {node[i]} vs {rnode[i]}"
+    ok = node == rnode
+    assert rel_err(w[ok], rw[ok]) <= 1e-12
+    # register_clouds end to end (source = target moved by the inverse motion)
+    if n >= 32:
+        src = (pts - t) @ R
+        want = ref.register_clouds(pts, src, level=L)
+        got = tr.register_clouds(pts, src, tr.RegistrationConfig(variant=tr.Variant("adaptive", L)), ctx)
+        diag = float(np.linalg.norm(pts.max(0) - pts.min(0)))
+        ang = rotation_angle_between(got.transform.rotation, want["R"])
+        assert ang <= 1e-4 or np.abs(got.transform.rotation - want["R"]).max() <= 1e-6
+        assert np.linalg.norm(got.transform.translation - want["t"]) <= 1e-4 * max(diag, 1e-12)
