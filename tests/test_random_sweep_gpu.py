@@ -85,8 +85,9 @@ def test_random_cloud_parity(ctx, ref, seed, n, shape, L):
     # register_clouds end to end (source = target moved by the inverse motion)
     if n >= 32:
         src = (pts - t) @ R
-        want = ref.register_clouds(pts, src, level=L)
-        got = tr.register_clouds(pts, src, tr.RegistrationConfig(variant=tr.Variant("adaptive", L)), ctx)
+        var = "tree" if seed % 2 else "adaptive"  # tree:L = lambda_c 0 (full-depth walks)
+        want = ref.register_clouds(pts, src, level=L, variant=var)
+        got = tr.register_clouds(pts, src, tr.RegistrationConfig(variant=tr.Variant(var, L)), ctx)
         diag = float(np.linalg.norm(pts.max(0) - pts.min(0)))
         ang = rotation_angle_between(got.transform.rotation, want["R"])
         assert ang <= 1e-4 or np.abs(got.transform.rotation - want["R"]).max() <= 1e-6
