@@ -1622,12 +1622,10 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
                o_car = carve(sizeof(unsigned) * ((size_t)cap + 1)), o_dbits = carve(16),
                o_meta = carve(sizeof(TreeMeta)),
                o_state = carve(sizeof(BuildState));
-  TRG_CU(cudaFuncSetAttribute((const void*)k_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)sizeof(BuildSmem)));
+  TRG_CU(set_dynamic_smem((const void*)k_build, sizeof(BuildSmem)));
   const int G = persistent_grid(ctx, (const void*)k_build, kTile, sizeof(BuildSmem));
   const size_t cal_smem = sizeof(DNode) * kStageNodes;
-  TRG_CU(cudaFuncSetAttribute((const void*)k_calibrate, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)cal_smem));
+  TRG_CU(set_dynamic_smem((const void*)k_calibrate, cal_smem));
   int Gc = persistent_grid(ctx, (const void*)k_calibrate, kTile, cal_smem);
   if (const char* e = getenv("TRG_KCAL_PER_SM")) Gc = std::min(Gc, ctx->sms * atoi(e));  // experiments
   const size_t o_cd = carve(sizeof(double) * std::max(G, Gc));

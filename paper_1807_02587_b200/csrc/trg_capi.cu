@@ -7,6 +7,9 @@
 #include <cstring>
 #include <algorithm>
 #include <string>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "trg_internal.cuh"
@@ -118,11 +121,42 @@ int timeline_fetch(trg_ctx* ctx) {
   return TRG_OK;
 }
 
+// Occupancy and the dynamic-smem attribute are per kernel and configuration,
+// not per call: both are cached (process-wide, thread-safe) so a
+// registration issues no driver queries on its way to the first launch.
+static std::mutex g_attr_mu;
+static std::map<std::tuple<const void*, int, size_t>, int> g_occ;
+static std::map<const void*, size_t> g_smem_attr;
+
 int persistent_grid(trg_ctx* ctx, const void* kernel, int block, size_t smem) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
-  if (per_sm < 1) per_sm = 1;
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_occ.find({kernel, block, smem});
+    if (it != g_occ.end()) per_sm = it->second;
+  }
+  if (per_sm == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+    if (per_sm < 1) per_sm = 1;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    g_occ[{kernel, block, smem}] = per_sm;
+  }
   return ctx->sms * per_sm;
+}
+
+cudaError_t set_dynamic_smem(const void* kernel, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_smem_attr.find(kernel);
+    if (it != g_smem_attr.end() && it->second >= bytes) return cudaSuccess;
+  }
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    size_t& v = g_smem_attr[kernel];
+    v = std::max(v, bytes);
+  }
+  return e;
 }
 
 cudaError_t launch_persistent(trg_ctx* ctx, const void* kernel, int G, int block, void** args,

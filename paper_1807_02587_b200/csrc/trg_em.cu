@@ -447,8 +447,7 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   job->status = status;
   job->kernel = dense ? (const void*)k_register<true> : (const void*)k_register<false>;
   job->smem = dense ? 0 : sizeof(DNode) * kStageNodes;
-  TRG_CU(cudaFuncSetAttribute(job->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)std::max<size_t>(job->smem, 1)));
+  TRG_CU(set_dynamic_smem(job->kernel, std::max<size_t>(job->smem, 1)));
   // 2 CTAs per SM (of the 3 that fit): the per-node combine over CTAs and
   // the redundant per-CTA solve get cheaper faster than the E-step slows
   // (C2, 16 iterations: 0.72 ms at 2/SM vs 0.80 at 1/SM and 0.90 at 3/SM)

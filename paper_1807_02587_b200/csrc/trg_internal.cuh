@@ -222,6 +222,8 @@ int tree_alloc(trg_ctx* ctx, int capacity, trg_tree_dev** out);
 
 // Grid size for persistent kernels: SMs x resident CTAs.
 int persistent_grid(trg_ctx* ctx, const void* kernel, int block, size_t smem);
+// cudaFuncAttributeMaxDynamicSharedMemorySize, set once per kernel (cached).
+cudaError_t set_dynamic_smem(const void* kernel, size_t bytes);
 // Launches a persistent (grid-barrier) kernel of G = persistent_grid() CTAs.
 // Whole-device contexts use a cooperative launch (co-residency checked by
 // the driver).  SM-budgeted contexts (trg_ctx_set_sm_budget) use a plain
