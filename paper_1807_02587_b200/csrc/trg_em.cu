@@ -918,12 +918,18 @@ static int register_tree_async(trg_ctx* ctx, const double* tgt, size_t n_target,
     ctx->build_into_scratch = true;
     rc = build_async_start(ctx, tgt, n_target, &mc, &ab, &tree, &meta);
     ctx->build_into_scratch = false;
-    if (rc != TRG_OK) break;
-    TRG_CU(cudaEventRecord(e1, ctx->stream));
+    if (rc == TRG_OK) rc = cudaEventRecord(e1, ctx->stream) == cudaSuccess ? TRG_OK : TRG_ECUDA;
     EmJob job;
-    rc = em_prepare(ctx, tree, src, n_source, cfg, 0.0, false, 0.0, &job, false, meta, od);
+    if (rc == TRG_OK) rc = em_prepare(ctx, tree, src, n_source, cfg, 0.0, false, 0.0, &job, false, meta, od);
     if (rc == TRG_OK) rc = em_launch(ctx, &job, -1);
-    if (rc != TRG_OK) break;
+    if (rc != TRG_OK) {
+      if (job.e0) cudaEventDestroy(job.e0);
+      if (job.e1) cudaEventDestroy(job.e1);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      cudaStreamSynchronize(ctx->stream);  // nothing queued may outlive the call
+      break;
+    }
     trg_tree_dev* built = nullptr;
     bool retry = false;
     rc = build_async_finish(ctx, ab, &built, &retry);  // synchronises the stream
@@ -937,6 +943,8 @@ static int register_tree_async(trg_ctx* ctx, const double* tgt, size_t n_target,
     if (rc != TRG_OK) {  // the EM's events / status word are dropped with it
       cudaEventDestroy(job.e0);
       cudaEventDestroy(job.e1);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
       cudaMemsetAsync(ctx->status2, 0, sizeof(int), ctx->stream);
       break;
     }
