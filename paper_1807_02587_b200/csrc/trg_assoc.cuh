@@ -26,7 +26,7 @@ __device__ __forceinline__ double node_score(const DNode* __restrict__ g, double
   const double w = g->weight;
   const double lam2 = g->lam[2];
   const double q = fast_q(g->mean, g->axT, g->il, y0, y1, y2);
-  const double sc = __dmul_rn(w, exp(__fma_rn(-0.5, q, g->log_norm)));
+  const double sc = __dmul_rn(w, trg_exp(__fma_rn(-0.5, q, g->log_norm)));
   if (!(w > 0.0)) return 0.0;
   if (!(lam2 > 0.0)) {
     atomicCAS(status, 0, kEDomain);  // log_density: covariance is not PD
@@ -42,7 +42,7 @@ __device__ __forceinline__ double node_score_nb(const DNode* __restrict__ g, dou
   const double w = g->weight;
   const double lam2 = g->lam[2];
   const double q = fast_q(g->mean, g->axT, g->il, y0, y1, y2);
-  const double sc = __dmul_rn(w, exp(__fma_rn(-0.5, q, g->log_norm)));
+  const double sc = __dmul_rn(w, trg_exp(__fma_rn(-0.5, q, g->log_norm)));
   const bool live = w > 0.0;
   bad = bad || (live && !(lam2 > 0.0));
   return (live && lam2 > 0.0) ? sc : 0.0;

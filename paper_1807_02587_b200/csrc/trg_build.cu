@@ -376,7 +376,7 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
       double ek[8], s = 0.0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        ek[k] = fin ? exp(lg[k] - m) : 0.0;
+        ek[k] = fin ? trg_exp(lg[k] - m) : 0.0;  // == exp(), bit for bit
         s += ek[k];
       }
       // gamma_k = exp(log_k - log_total) = e_k / s (gmm.cpp:189, 354): one

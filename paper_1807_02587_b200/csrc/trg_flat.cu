@@ -341,16 +341,16 @@ __global__ void __launch_bounds__(kFB, 2) k_flat_build(FlatParams p) {
         const double lg = flat_logp(p, k, x0, x1, x2);
         if (!(lg > -INFINITY)) continue;
         if (lg > m) {
-          s = s * exp(m - lg) + 1.0;
+          s = s * trg_exp(m - lg) + 1.0;
           m = lg;
         } else {
-          s += exp(lg - m);
+          s += trg_exp(lg - m);
         }
       }
       double M = m;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
-      double sl = (m > -INFINITY) ? s * exp(m - M) : 0.0;
+      double sl = (m > -INFINITY) ? s * trg_exp(m - M) : 0.0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xffffffffu, sl, o);
       const double ltot = isfinite(M) ? M + log(sl) : -INFINITY;
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(kFB, 2) k_flat_build(FlatParams p) {
             if (!(lti > -INFINITY)) continue;
             const double x0 = p.pts[3 * i], x1 = p.pts[3 * i + 1], x2 = p.pts[3 * i + 2];
             const double lg = flat_logp(p, k, x0, x1, x2);
-            const double g = lg > -INFINITY ? exp(lg - lti) : 0.0;
+            const double g = lg > -INFINITY ? trg_exp(lg - lti) : 0.0;
             if (!(g > 0.0)) continue;
             const double d0 = x0 - r0, d1 = x1 - r1, d2 = x2 - r2;
             a[0] += g;
