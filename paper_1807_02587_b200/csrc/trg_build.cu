@@ -365,13 +365,20 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
       const int mode = pcount ? 3 : (cand == 0 ? ph.mode[0] : ph.mode[1]);  // (no local-memory index)
       double lg[8];
       double m = -INFINITY;
+      bool nonpd = false;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
+        // comp_log without branches: the value is selected, the domain
+        // error (log_density on a non-PD covariance) flagged once below
         double r[18];
         comp_to_regs(sm.comp[cand][k], r);
-        lg[k] = comp_log(r, x0, x1, x2, p.status);
+        const double v = r[1] + __fma_rn(-0.5, fast_q(r + 2, r + 5, r + 14, x0, x1, x2), r[17]);
+        const bool live = r[0] > 0.0, pd = r[16] > 0.0;
+        nonpd |= live && !pd;
+        lg[k] = (live && pd) ? v : -INFINITY;
         m = fmax(m, lg[k]);
       }
+      if (nonpd) atomicCAS(p.status, 0, kEDomain);
       const bool fin = isfinite(m);
       double ek[8], s = 0.0;
 #pragma unroll
