@@ -150,18 +150,6 @@ __device__ __forceinline__ void comp_to_regs(const GComp& c, double r[18]) {
   r[17] = c.log_norm;
 }
 
-// gmm.cpp:176-178: log w + log_density, or -inf when w == 0.
-__device__ __forceinline__ double comp_log(const double r[18], double x0, double x1, double x2,
-                                           int* status) {
-  if (!(r[0] > 0.0)) return -INFINITY;
-  if (!(r[16] > 0.0)) {  // 1/lam3: log_density on a non-PD covariance
-    atomicCAS(status, 0, kEDomain);
-    return -INFINITY;
-  }
-  const double q = fast_q(r + 2, r + 5, r + 14, x0, x1, x2);
-  return r[1] + __fma_rn(-0.5, q, r[17]);
-}
-
 // Deterministic block sum of NV values per thread; results in out[0..NV) (smem).
 template <int NV>
 __device__ __forceinline__ void block_sum_vec(double v[NV], double (*wsum)[NV], double* out) {
@@ -368,8 +356,9 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
       bool nonpd = false;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        // comp_log without branches: the value is selected, the domain
-        // error (log_density on a non-PD covariance) flagged once below
+        // gmm.cpp:176-178 log w + log_density (-inf when w == 0), without
+        // branches: the value is selected, the domain error (log_density on
+        // a non-PD covariance) flagged once below
         double r[18];
         comp_to_regs(sm.comp[cand][k], r);
         const double v = r[1] + __fma_rn(-0.5, fast_q(r + 2, r + 5, r + 14, x0, x1, x2), r[17]);
