@@ -92,3 +92,42 @@ def test_random_cloud_parity(ctx, ref, seed, n, shape, L):
         ang = rotation_angle_between(got.transform.rotation, want["R"])
         assert ang <= 1e-4 or np.abs(got.transform.rotation - want["R"]).max() <= 1e-6
         assert np.linalg.norm(got.transform.translation - want["t"]) <= 1e-4 * max(diag, 1e-12)
+
+
+# ModelConfig away from the defaults (gmm.hpp:34-41): EM iterations per node,
+# the expansion gate, both covariance regularisers, and depths up to 4.
+CONFIGS = [dict(em_iters=1, min_points=32, eps=1e-4, abs_floor=1e-12, L=3),
+           dict(em_iters=3, min_points=100, eps=1e-4, abs_floor=1e-12, L=3),
+           dict(em_iters=12, min_points=8, eps=1e-4, abs_floor=1e-12, L=2),
+           dict(em_iters=8, min_points=32, eps=1e-2, abs_floor=1e-12, L=3),
+           dict(em_iters=8, min_points=32, eps=0.0, abs_floor=1e-6, L=3),
+           dict(em_iters=5, min_points=16, eps=1e-3, abs_floor=1e-9, L=4)]
+
+
+@pytest.mark.parametrize("ci", range(len(CONFIGS)))
+def test_model_config_parity(ctx, ref, ci):
+    from paper_1807_02587_b200 import treereg as tr
+    c = CONFIGS[ci]
+    pts = _cloud(("blobs", "plane", "uniform", "line", "mixed", "blobs")[ci], 4000,
+                 np.random.default_rng(100 + ci))
+    G = ref.build_tree(pts, max_level=c["L"], em_iters=c["em_iters"], min_points=c["min_points"],
+                       eps=c["eps"], abs_floor=c["abs_floor"])
+    mc = tr.ModelConfig(em_iterations_per_node=c["em_iters"], min_points_per_node=c["min_points"],
+                        cov_regularization_epsilon=c["eps"], cov_regularization_absolute=c["abs_floor"],
+                        max_level=c["L"])
+    d = tr.BuildDiagnostics()
+    h = tr.build_tree(pts, mc, d, ctx).host()
+    assert len(h["weight"]) == len(G["weight"])
+    for k in ("parent", "first_child", "child_count", "level"):
+        assert np.array_equal(h[k], G[k]), k
+    assert np.abs(h["weight"] - G["weight"]).max() <= 1e-4
+    assert np.abs(h["mean"] - G["mean"]).max() <= 1e-4 * max(np.abs(G["mean"]).max(), 1e-300)
+    cs = np.linalg.norm(G["cov"].reshape(len(G["cov"]), -1), axis=1)
+    noise = 64 * np.finfo(float).eps * (np.sum(G["mean"] ** 2, axis=1) + cs)
+    dc = np.linalg.norm((h["cov"] - G["cov"]).reshape(len(cs), -1), axis=1)
+    assert np.all(dc <= 1e-4 * cs + noise)
+    # BuildDiagnostics::node_ll_traces: one (em_iters + 1)-long trace per expansion
+    assert len(d.node_ll_traces) == len(G["ll_traces"])
+    for a, b in zip(d.node_ll_traces, G["ll_traces"]):
+        assert len(a) == len(b) == c["em_iters"] + 1
+        assert np.abs(np.asarray(a) - b).max() <= 1e-6 * max(1.0, np.abs(b).max())
