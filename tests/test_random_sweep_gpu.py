@@ -131,3 +131,37 @@ def test_model_config_parity(ctx, ref, ci):
     for a, b in zip(d.node_ll_traces, G["ll_traces"]):
         assert len(a) == len(b) == c["em_iters"] + 1
         assert np.abs(np.asarray(a) - b).max() <= 1e-6 * max(1.0, np.abs(b).max())
+
+
+# RegistrationConfig away from the defaults (registration.hpp:27-36): early
+# stop by the iteration cap, tight / loose tolerances, lambda_c levels, the
+# tree:L variant, the target-diagonal fallback (tree_extent_estimate).
+REGS = [dict(variant="adaptive", lc=0.01, iters=3, rtol=1e-5, ttol=1e-5, diag=True),
+        dict(variant="adaptive", lc=0.2, iters=50, rtol=1e-8, ttol=1e-8, diag=True),
+        dict(variant="adaptive", lc=0.0, iters=50, rtol=1e-3, ttol=1e-3, diag=True),
+        dict(variant="tree", lc=0.0, iters=20, rtol=1e-5, ttol=1e-5, diag=False),
+        dict(variant="adaptive", lc=1.0 / 3.0, iters=50, rtol=1e-5, ttol=1e-5, diag=False)]
+
+
+@pytest.mark.parametrize("ri", range(len(REGS)))
+def test_registration_config_parity(ctx, ref, ri):
+    from paper_1807_02587_b200 import treereg as tr
+    c = REGS[ri]
+    rng = np.random.default_rng(200 + ri)
+    pts = _cloud(("blobs", "plane", "uniform", "blobs", "line")[ri], 3000, rng)
+    G = ref.build_tree(pts, max_level=3)
+    R, t = ref.random_rigid_transform(10.0, 0.1, 200 + ri)
+    src = (pts - t) @ R
+    diag = float(np.linalg.norm(pts.max(0) - pts.min(0))) if c["diag"] else 0.0
+    want = ref.register_with_tree(G, src, variant=c["variant"], lambda_c=c["lc"], max_iters=c["iters"],
+                                  rot_tol=c["rtol"], trans_tol=c["ttol"], target_diag=diag)
+    cfg = tr.RegistrationConfig(variant=tr.Variant(c["variant"], 3), lambda_c=c["lc"],
+                                max_em_iterations=c["iters"], rotation_tol=c["rtol"],
+                                translation_tol=c["ttol"])
+    got = tr.register_with_tree(tr.GmmTree.from_host(G, ctx), src, cfg, diag)
+    assert got.iterations == want["iterations"]
+    assert got.converged == want["converged"]
+    assert np.abs(got.transform.rotation - want["R"]).max() <= 1e-6
+    assert np.linalg.norm(got.transform.translation - want["t"]) <= 1e-6 * max(1.0, np.abs(pts).max())
+    n = got.iterations
+    assert np.array_equal(np.asarray(got.eval_counts[:n]), want["eval_counts"][:n])
