@@ -214,6 +214,31 @@ int stage_points_public(trg_ctx* ctx, const double* xyz, size_t n, int on_device
   return TRG_OK;
 }
 
+int stage_points_side(trg_ctx* ctx, const double* xyz, size_t n, int on_device, int slot,
+                      const double** dev, bool* deferred) {
+  *deferred = false;
+  if (on_device || !is_pinned(xyz)) return stage_points_public(ctx, xyz, n, on_device, slot, dev);
+  if (!ctx->side) {
+    TRG_CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    TRG_CU(cudaEventCreateWithFlags(&ctx->side_done, cudaEventDisableTiming));
+  }
+  void* p = nullptr;
+  TRG_TRY(ws_get(ctx, slot, sizeof(double) * 3 * n, &p));
+  // the slot's previous reader (an earlier call on the main stream) is done:
+  // every call collects before returning
+  TRG_CU(cudaMemcpyAsync(p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->side));
+  TRG_CU(cudaEventRecord(ctx->side_done, ctx->side));
+  ctx->bytes_h2d += sizeof(double) * 3 * n;
+  *dev = static_cast<const double*>(p);
+  *deferred = true;
+  return TRG_OK;
+}
+
+int stage_wait(trg_ctx* ctx) {
+  TRG_CU(cudaStreamWaitEvent(ctx->stream, ctx->side_done, 0));
+  return TRG_OK;
+}
+
 }  // namespace trg
 
 using namespace trg;
@@ -271,6 +296,11 @@ int trg_ctx_destroy(trg_ctx* ctx) {
   }
   cudaFree(ctx->status);
   cudaFree(ctx->dev_timeline);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaEventDestroy(ctx->side_done);
+    cudaStreamDestroy(ctx->side);
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TRG_OK;

@@ -900,8 +900,8 @@ int trg_register_with_tree(trg_ctx* ctx, const trg_tree_dev* tree, const double*
 // build and the EM are collected.  An entry-buffer overflow (the EM saw
 // meta->ok == 0 and did nothing) re-queues both with the grown allocation.
 static int register_tree_async(trg_ctx* ctx, const double* tgt, size_t n_target,
-                               const double* src, size_t n_source, const trg_reg_config* cfg,
-                               trg_reg_result* out) {
+                               const double* src, size_t n_source, bool src_deferred,
+                               const trg_reg_config* cfg, trg_reg_result* out) {
   trg_model_config mc = cfg->model_config;
   mc.max_level = cfg->variant_param;
   double* od = nullptr;
@@ -919,6 +919,7 @@ static int register_tree_async(trg_ctx* ctx, const double* tgt, size_t n_target,
     rc = build_async_start(ctx, tgt, n_target, &mc, &ab, &tree, &meta);
     ctx->build_into_scratch = false;
     if (rc == TRG_OK) rc = cudaEventRecord(e1, ctx->stream) == cudaSuccess ? TRG_OK : TRG_ECUDA;
+    if (rc == TRG_OK && src_deferred) rc = stage_wait(ctx);
     EmJob job;
     if (rc == TRG_OK) rc = em_prepare(ctx, tree, src, n_source, cfg, 0.0, false, 0.0, &job, false, meta, od);
     if (rc == TRG_OK) rc = em_launch(ctx, &job, -1);
@@ -959,6 +960,7 @@ static int register_tree_async(trg_ctx* ctx, const double* tgt, size_t n_target,
     return rc;
   }
   build_async_free(ab);
+  if (src_deferred) cudaStreamSynchronize(ctx->side);  // no copy may outlive a failed call
   if (rc == TRG_OK) {
     set_error("build_tree: entry buffer growth did not converge");
     rc = TRG_ERUNTIME;
@@ -979,6 +981,14 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
   TRG_CU(cudaSetDevice(ctx->device));
   const double* src = nullptr;
   const double* tgt = nullptr;
+  if (cfg->variant_kind == TRG_VARIANT_ADAPTIVE || cfg->variant_kind == TRG_VARIANT_TREE) {
+    // target first; a pinned source streams in on the side stream under the
+    // build (the EM waits for it)
+    bool deferred = false;
+    TRG_TRY(stage_points_public(ctx, target, n_target, on_device, kSlotPoints, &tgt));
+    TRG_TRY(stage_points_side(ctx, source, n_source, on_device, kSlotPoints2, &src, &deferred));
+    return register_tree_async(ctx, tgt, n_target, src, n_source, deferred, cfg, out);
+  }
   TRG_TRY(stage_points_public(ctx, source, n_source, on_device, kSlotPoints2, &src));
   TRG_TRY(stage_points_public(ctx, target, n_target, on_device, kSlotPoints, &tgt));
   if (cfg->variant_kind == TRG_VARIANT_ICP) {  // registration.cpp:205-206
@@ -987,7 +997,6 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
     return register_icp_dev(ctx, tgt, n_target, src, n_source, cfg,
                             target_bbox_diagonal(ctx, tgt, n_target), out);
   }
-  if (cfg->variant_kind != TRG_VARIANT_FLAT) return register_tree_async(ctx, tgt, n_target, src, n_source, cfg, out);
   cudaEvent_t e0, e1;
   TRG_CU(cudaEventCreate(&e0));
   TRG_CU(cudaEventCreate(&e1));

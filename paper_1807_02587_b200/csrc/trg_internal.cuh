@@ -109,6 +109,8 @@ struct trg_ctx {
   bool timeline_pending = false;
   std::vector<trg_ctx*> workers;  // trg_register_batch: SM-budgeted sub-contexts
   bool own_stream = true;         // false: a shard context on its parent's stream
+  cudaStream_t side = nullptr;    // copy stream: a pinned source cloud's H2D under the build
+  cudaEvent_t side_done = nullptr;
   static constexpr int kSlots = 32;
   void* slot_ptr[kSlots] = {};
   size_t slot_size[kSlots] = {};
@@ -191,6 +193,12 @@ int check_finite_dev(trg_ctx* ctx, const double* dev, size_t n, const char* msg)
 // Device pointer to N x 3 points: the caller's (on_device) or a staged copy.
 int stage_points_public(trg_ctx* ctx, const double* xyz, size_t n, int on_device, int slot,
                         const double** dev);
+// As stage_points_public, but a pinned host cloud is copied on the context's
+// side stream (overlapping whatever the main stream runs meanwhile); *deferred
+// tells the caller to stage_wait() before the main stream reads it.
+int stage_points_side(trg_ctx* ctx, const double* xyz, size_t n, int on_device, int slot,
+                      const double** dev, bool* deferred);
+int stage_wait(trg_ctx* ctx);
 // register_icp_pt2pt (registration.cpp:211-298) over device clouds.
 int register_icp_dev(trg_ctx* ctx, const double* tgt, size_t nt, const double* src, size_t ns,
                      const trg_reg_config* cfg, double diag, trg_reg_result* out);
