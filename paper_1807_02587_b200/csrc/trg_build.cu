@@ -1782,9 +1782,17 @@ int build_collect(trg_ctx* ctx, BuildJob* job, const trg_model_config* cfg, trg_
   trg_tree_dev* tree = job->tree;
   const BuildAlloc al = job->al;
   const int L = cfg->max_level;
-  BuildState st{};
-  TRG_CU(trg_memcpy(ctx, &st, p.st, sizeof st, cudaMemcpyDeviceToHost));
-  int rc = check_status(ctx, "build_tree");
+  // state and status word in one round trip (pinned, one synchronisation)
+  void* hc = nullptr;
+  TRG_TRY(host_ws_get(ctx, kSlotHostCollect, sizeof(BuildState) + 16, &hc));
+  TRG_CU(cudaMemcpyAsync(hc, p.st, sizeof(BuildState), cudaMemcpyDeviceToHost, ctx->stream));
+  int* hstatus = reinterpret_cast<int*>(static_cast<char*>(hc) + sizeof(BuildState));
+  TRG_CU(cudaMemcpyAsync(hstatus, ctx->status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  ctx->bytes_d2h += sizeof(BuildState) + sizeof(int);
+  BuildState st;
+  std::memcpy(&st, hc, sizeof st);
+  int rc = status_result(ctx, *hstatus, ctx->status, "build_tree");
   if (rc == TRG_OK && st.status_overflow) {
     *overflow = true;
     need->Emax = std::max(al.Emax, st.need_E);

@@ -94,6 +94,10 @@ int check_status_at(trg_ctx* ctx, int* dev_status, const char* where) {
   int st = 0;
   TRG_CU(trg_memcpy(ctx, &st, dev_status, sizeof(int), cudaMemcpyDeviceToHost));
   TRG_CU(cudaStreamSynchronize(ctx->stream));
+  return status_result(ctx, st, dev_status, where);
+}
+
+int status_result(trg_ctx* ctx, int st, int* dev_status, const char* where) {
   if (st != 0) {
     TRG_CU(cudaMemsetAsync(dev_status, 0, sizeof(int), ctx->stream));
     const char* what = st == kEDomain   ? "covariance is not positive definite / no positive trace"

@@ -5,6 +5,7 @@
 // degenerate-streak control -- with grid barriers between phases, so the
 // host never sees an iteration boundary.
 #include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <cstdio>
 #include <vector>
@@ -538,19 +539,34 @@ int em_collect(trg_ctx* ctx, EmJob* job, trg_reg_result* out) {
   EmParams& p = job->p;
   const int K = job->K;
   TRG_CU(cudaEventRecord(job->e1, ctx->stream));
-  EmState st{};
-  TRG_CU(trg_memcpy(ctx, &st, p.st, sizeof st, cudaMemcpyDeviceToHost));
+  // state, traces and status word in one round trip (pinned, one synchronisation)
+  int* dev_status = job->status ? job->status : ctx->status;
+  const size_t tb = sizeof(double) * K;
+  void* hc = nullptr;
+  TRG_TRY(host_ws_get(ctx, kSlotHostCollect, sizeof(EmState) + 3 * tb + 16, &hc));
+  char* h = static_cast<char*>(hc);
+  TRG_CU(cudaMemcpyAsync(h, p.st, sizeof(EmState), cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(cudaMemcpyAsync(h + sizeof(EmState), p.crit_before, tb, cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(cudaMemcpyAsync(h + sizeof(EmState) + tb, p.crit_after, tb, cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(cudaMemcpyAsync(h + sizeof(EmState) + 2 * tb, p.evals, tb, cudaMemcpyDeviceToHost, ctx->stream));
+  TRG_CU(cudaMemcpyAsync(h + sizeof(EmState) + 3 * tb, dev_status, sizeof(int), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  ctx->bytes_d2h += sizeof(EmState) + 3 * tb + sizeof(int);
+  EmState st;
+  std::memcpy(&st, h, sizeof st);
   std::vector<double> cb(K), ca(K);
   std::vector<unsigned long long> ev(K);
-  TRG_CU(trg_memcpy(ctx, cb.data(), p.crit_before, sizeof(double) * K, cudaMemcpyDeviceToHost));
-  TRG_CU(trg_memcpy(ctx, ca.data(), p.crit_after, sizeof(double) * K, cudaMemcpyDeviceToHost));
-  TRG_CU(trg_memcpy(ctx, ev.data(), p.evals, sizeof(unsigned long long) * K, cudaMemcpyDeviceToHost));
-  TRG_CU(cudaEventSynchronize(job->e1));
+  std::memcpy(cb.data(), h + sizeof(EmState), tb);
+  std::memcpy(ca.data(), h + sizeof(EmState) + tb, tb);
+  std::memcpy(ev.data(), h + sizeof(EmState) + 2 * tb, tb);
+  int hst = 0;
+  std::memcpy(&hst, h + sizeof(EmState) + 3 * tb, sizeof(int));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, job->e0, job->e1);
   cudaEventDestroy(job->e0);
   cudaEventDestroy(job->e1);
-  TRG_TRY(check_status_at(ctx, job->status ? job->status : ctx->status, "register_with_tree"));
+  TRG_TRY(status_result(ctx, hst, dev_status, "register_with_tree"));
   TRG_TRY(timeline_fetch(ctx));
   for (int k = 0; k < 9; ++k) out->R[k] = st.Rt[k];
   for (int k = 0; k < 3; ++k) out->t[k] = st.Rt[9 + k];

@@ -169,6 +169,7 @@ enum Slot : int {
   kSlotTimelineHost,  // host slots only: last device timeline
   kSlotHostEmInit,    // host slots only: pinned EmState initialiser (no staging sync)
   kSlotHostBuildInit, // host slots only: pinned BuildState initialiser
+  kSlotHostCollect,   // host slots only: a call's results, fetched with one synchronisation
 };
 
 int ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
@@ -210,6 +211,9 @@ int build_sharded_dev(trg_comm* c, const double* const* dev, const size_t* n,
                       const trg_model_config* cfg, trg_tree_dev** trees, trg_build_diag* diag);
 int check_status(trg_ctx* ctx, const char* where);
 int check_status_at(trg_ctx* ctx, int* dev_status, const char* where);
+// A status word already fetched (value st): clears the device word and sets
+// the error like check_status_at.
+int status_result(trg_ctx* ctx, int st, int* dev_status, const char* where);
 // What k_calibrate publishes about the finished tree for work queued behind
 // it without a host round trip (ok = 0: the build failed or overflowed).
 struct TreeMeta {
