@@ -167,3 +167,20 @@ def test_registration_config_parity(ctx, ref, ri):
     assert np.linalg.norm(got.transform.translation - want["t"]) <= 1e-6 * max(1.0, np.abs(pts).max())
     n = got.iterations
     assert np.array_equal(np.asarray(got.eval_counts[:n]), want["eval_counts"][:n])
+
+
+@pytest.mark.parametrize("seed,n,shape,var,param", [(301, 3000, "blobs", "flat", 8), (302, 1500, "plane", "flat", 16),
+                                                    (303, 800, "uniform", "icp", 0), (304, 2000, "mixed", "icp", 0)])
+def test_flat_and_icp_random(ctx, ref, seed, n, shape, var, param):
+    # (ICP on collinear points is ill-posed: the reference's own Kabsch
+    # iterates to non-rotations there, so no parity is defined for it)
+    from paper_1807_02587_b200 import treereg as tr
+    pts = _cloud(shape, n, np.random.default_rng(seed))
+    R, t = ref.random_rigid_transform(6.0, 0.05, seed)
+    src = (pts - t) @ R
+    want = ref.register_clouds(pts, src, level=param, variant=var)
+    got = tr.register_clouds(pts, src, tr.RegistrationConfig(variant=tr.Variant(var, param)), ctx)
+    assert got.iterations == want["iterations"]
+    assert got.converged == want["converged"]
+    assert np.abs(got.transform.rotation - want["R"]).max() <= 1e-6
+    assert np.linalg.norm(got.transform.translation - want["t"]) <= 1e-6 * max(1.0, np.abs(pts).max())
