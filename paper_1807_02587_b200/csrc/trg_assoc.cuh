@@ -268,7 +268,10 @@ __device__ __forceinline__ void apply_rt(const double* Rt, double p0, double p1,
 // Association pass of one CTA over tiles cta, cta+G, ... (persistent).
 template <int NM>
 __device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double* Rt_smem, int G,
-                           int cta) {
+                           int cta, int tile_G = -1, int tile_cta = -1) {
+  // tiles are dealt over tile_G CTAs (default: all G); partial rows stay
+  // indexed by the CTA's own id among G
+  const int tG = tile_G < 0 ? G : tile_G, tc = tile_G < 0 ? cta : tile_cta;
   const int tid = threadIdx.x;
   const int J = p.n_nodes;
   const int kb = key_bits_for(J);
@@ -280,10 +283,10 @@ __device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double
   unsigned long long my_out = 0, my_ev = 0;
   // tiles of ts <= 256 points: when the cloud is small for the grid, spread
   // it evenly over all CTAs (every SM gets the same share of descents)
-  const size_t per_cta = (p.n + G - 1) / G;
+  const size_t per_cta = (p.n + tG - 1) / tG;
   const int ts = per_cta < (size_t)kAssocBlock ? (per_cta > 0 ? (int)per_cta : 1) : kAssocBlock;
   const size_t ntiles = (p.n + ts - 1) / ts;
-  for (size_t tile = cta; tile < ntiles; tile += G) {
+  for (size_t tile = tc; tile < ntiles; tile += tG) {
     const size_t i = tile * ts + tid;
     unsigned key = (unsigned)J;
     double v[NM];

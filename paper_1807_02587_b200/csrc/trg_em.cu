@@ -91,6 +91,32 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
   extern __shared__ __align__(16) unsigned char k_reg_stage[];
   DNode* reg_stage = reinterpret_cast<DNode*>(k_reg_stage);
   if (!DENSE) stage_nodes(reg_stage, p.a.nodes, n_snodes);
+  // criterion after the update of iteration k (trace only), CTA 0.  Single
+  // GPU (defer): CTA 0 takes no E-step tiles and computes it for iteration
+  // it-1 while the other CTAs run iteration it's E-step (the moments and
+  // the solve of it-1 are still in place then), so the trace leaves the
+  // iteration's critical path; the last iteration's is computed after the loop.
+  const bool defer = !sharded && !DENSE && G > 1;
+  auto crit_trace = [&](int k) {
+    unsigned long long* counters = p.a.counters + 2 * (k & 1);
+    double c = 0.0;
+    if (!so.degenerate) {
+      double dRt[12];
+      for (int i = 0; i < 9; ++i) dRt[i] = so.dR[i];
+      for (int i = 0; i < 3; ++i) dRt[9 + i] = so.dt[i];
+      for (int j = tid; j < J; j += blockDim.x) {
+        const double* m = p.moments + (size_t)j * 4;
+        c += crit_term(p.a.nodes + j, ldcg(m), ldcg(m + 1), ldcg(m + 2), ldcg(m + 3), n_total, dRt);
+      }
+    }
+    c = block_sum(c, ss);
+    if (tid == 0) {
+      p.evals[k] = sharded ? (unsigned long long)ldcg(p.xmom + (size_t)J * 4)
+                           : atomicExch(&counters[1], 0ull);
+      p.crit_before[k] = so.crit_before;
+      p.crit_after[k] = so.degenerate ? so.crit_before : c;
+    }
+  };
   for (int it = 0; it < p.max_iters; ++it) {
     const bool run_e = !sharded || p.seg == it;      // E-step of iteration it
     const bool run_m = !sharded || p.seg == it + 1;  // combine/solve of iteration it
@@ -124,8 +150,10 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
         dense_pass1(d, rt, G, cta);
         grid_sync(p.bar, G);
         dense_pass2<4>(d, rt, G, cta);
+      } else if (defer && cta == 0) {
+        if (it > 0) crit_trace(it - 1);
       } else {
-        assoc_pass<4>(sm, a, rt, G, cta);
+        assoc_pass<4>(sm, a, rt, G, cta, defer ? G - 1 : G, defer ? cta - 1 : cta);
       }
       grid_sync(p.bar, G);
       tl_mark(p.tl, 2000 + it * 10 + 1);
@@ -193,26 +221,7 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
     if (tid < 32) warp_solve_normal_eq(red, (int)red[kNormalEq + 1], &so, e6, p.tl, false);
     __syncthreads();
     tl_mark(p.tl, 2000 + it * 10 + 3);
-    if (cta == 0) {  // criterion after the update (trace only)
-      double c = 0.0;
-      if (!so.degenerate) {
-        double dRt[12];
-        for (int i = 0; i < 9; ++i) dRt[i] = so.dR[i];
-        for (int i = 0; i < 3; ++i) dRt[9 + i] = so.dt[i];
-        for (int j = tid; j < J; j += blockDim.x) {
-          const double* m = p.moments + (size_t)j * 4;
-          c += crit_term(a.nodes + j, ldcg(m), ldcg(m + 1), ldcg(m + 2), ldcg(m + 3), n_total,
-                         dRt);
-        }
-      }
-      c = block_sum(c, ss);
-      if (tid == 0) {
-        p.evals[it] = sharded ? (unsigned long long)ldcg(p.xmom + (size_t)J * 4)
-                              : atomicExch(&a.counters[1], 0ull);
-        p.crit_before[it] = so.crit_before;
-        p.crit_after[it] = so.degenerate ? so.crit_before : c;
-      }
-    }
+    if (cta == 0 && !defer) crit_trace(it);
     if (tid == 0) {
       s_iters = it + 1;
       if (!so.degenerate) {
@@ -264,6 +273,7 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
     }
     if (s_done) break;
   }
+  if (defer && cta == 0) crit_trace(s_iters - 1);
   if (!sharded && cta == 0 && tid == 0) {
     EmState* st = p.st;
     for (int k = 0; k < 12; ++k) st->Rt[k] = rt[k];
