@@ -184,3 +184,17 @@ def test_flat_and_icp_random(ctx, ref, seed, n, shape, var, param):
     assert got.converged == want["converged"]
     assert np.abs(got.transform.rotation - want["R"]).max() <= 1e-6
     assert np.linalg.norm(got.transform.translation - want["t"]) <= 1e-6 * max(1.0, np.abs(pts).max())
+
+
+def test_register_clouds_run_to_run_identical(ctx):
+    """The whole queued register_clouds (bbox -> build -> EM, side-stream
+    source copy) is bit-reproducible run to run, like the reference."""
+    from paper_1807_02587_b200 import treereg as tr
+    tg, sr, _ = tr.kinect_pair(3)
+    cfg = tr.RegistrationConfig(variant=tr.Variant("adaptive", 3))
+    a = tr.register_clouds(tg, sr, cfg, ctx)
+    b = tr.register_clouds(tg, sr, cfg, ctx)
+    assert np.array_equal(a.transform.rotation, b.transform.rotation)
+    assert np.array_equal(a.transform.translation, b.transform.translation)
+    assert a.iterations == b.iterations
+    assert np.array_equal(np.asarray(a.eval_counts[:a.iterations]), np.asarray(b.eval_counts[:b.iterations]))
