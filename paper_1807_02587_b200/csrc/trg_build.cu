@@ -1623,7 +1623,16 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   const size_t cal_smem = sizeof(DNode) * kStageNodes;
   TRG_CU(set_dynamic_smem((const void*)k_calibrate, cal_smem));
   int Gc = persistent_grid(ctx, (const void*)k_calibrate, kTile, cal_smem);
-  if (const char* e = getenv("TRG_KCAL_PER_SM")) Gc = std::min(Gc, ctx->sms * atoi(e));  // experiments
+  {
+    // CTAs per SM from the cloud size: each CTA's association tile should
+    // hold ~200 points; small clouds run fewer, fuller CTAs (cheaper grid
+    // barriers and per-leaf combines: C1 10k points 3.36 -> 2.89 ms build;
+    // C2 76.8k stays at 3/SM, its optimum)
+    int per_sm = (int)std::min<size_t>(3, std::max<size_t>(1, (n + 192 * (size_t)ctx->sms - 1) /
+                                                                  (192 * (size_t)ctx->sms)));
+    if (const char* e = getenv("TRG_KCAL_PER_SM")) per_sm = atoi(e);  // experiments
+    Gc = std::min(Gc, ctx->sms * std::max(1, per_sm));
+  }
   const size_t o_cd = carve(sizeof(double) * std::max(G, Gc));
   const int W = std::max(world, 1);
   const size_t o_xa = carve(sizeof(double) * 8 * K), o_xaa = carve(sizeof(double) * 8 * K * W),

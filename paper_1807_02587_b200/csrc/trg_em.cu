@@ -461,8 +461,9 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   TRG_CU(set_dynamic_smem(job->kernel, std::max<size_t>(job->smem, 1)));
   // 2 CTAs per SM (of the 3 that fit): the per-node combine over CTAs and
   // the redundant per-CTA solve get cheaper faster than the E-step slows
-  // (C2, 16 iterations: 0.72 ms at 2/SM vs 0.80 at 1/SM and 0.90 at 3/SM)
-  int per_sm = 2;
+  // (C2, 16 iterations: 0.72 ms at 2/SM vs 0.80 at 1/SM and 0.90 at 3/SM);
+  // clouds under 40k points: 1/SM (C1: 0.39 vs 0.44 ms)
+  int per_sm = n >= 40000 ? 2 : 1;
   if (const char* e = getenv("TRG_KREG_PER_SM")) per_sm = atoi(e);  // experiments
   const int G = std::min(persistent_grid(ctx, job->kernel, kAssocBlock, job->smem),
                          ctx->sms * std::max(1, per_sm));
