@@ -1,16 +1,15 @@
 // Device building blocks of the adaptive E-step (K7 associate_descend):
 // per-point log-time tree descent (association.cpp:91-157, Algorithm 1 of
-// the paper) and the deterministic per-CTA reduction of the deposits.
+// the paper) and the deposit of the per-point sufficient statistics.
 //
-// Reduction scheme (no float atomics anywhere): each CTA processes tiles of
-// 256 points; per tile the (stop node, deposit) pairs are stably radix-sorted
-// by node inside the block, reduced by a segmented scan, and each segment
-// tail adds its sum into this CTA's private row of the partial table
-// partials[node][cta][NM] (epoch-stamped, so nothing is zeroed between
-// calls).  A combine pass then sums each node over CTAs in fixed order.
+// Reduction scheme (no float atomics anywhere): points are processed in
+// fixed 32-point windows, one warp each; a window's runs of equal stop nodes
+// are summed by a segmented warp scan and each run adds its sums to the
+// node's exact fixed-point accumulator (trg_fx.cuh).  Integer addition is
+// associative, so the totals are bit-identical for any grid, SM budget or
+// CTA schedule -- the reference's thread-count invariance
+// (parallel.hpp:30-33) -- and nothing reads per-CTA partial rows.
 #pragma once
-#include <cub/block/block_radix_sort.cuh>
-
 #include "trg_internal.cuh"
 
 namespace trg {
@@ -142,107 +141,25 @@ template <int NM>
 __device__ __forceinline__ void deposit_values(double g, double y0, double y1, double y2,
                                                double v[NM]) {
   v[0] = g;
-  v[1] = g * y0;
-  v[2] = g * y1;
-  v[3] = g * y2;
+  v[1] = __dmul_rn(g, y0);
+  v[2] = __dmul_rn(g, y1);
+  v[3] = __dmul_rn(g, y2);
   if constexpr (NM == 10) {
-    v[4] = g * (y0 * y0);
-    v[5] = g * (y0 * y1);
-    v[6] = g * (y0 * y2);
-    v[7] = g * (y1 * y1);
-    v[8] = g * (y1 * y2);
-    v[9] = g * (y2 * y2);
+    v[4] = __dmul_rn(g, __dmul_rn(y0, y0));
+    v[5] = __dmul_rn(g, __dmul_rn(y0, y1));
+    v[6] = __dmul_rn(g, __dmul_rn(y0, y2));
+    v[7] = __dmul_rn(g, __dmul_rn(y1, y1));
+    v[8] = __dmul_rn(g, __dmul_rn(y1, y2));
+    v[9] = __dmul_rn(g, __dmul_rn(y2, y2));
   }
-}
-
-template <int NM>
-struct AssocSmem {
-  using Sort = cub::BlockRadixSort<unsigned, kAssocBlock, 1, int>;
-  typename Sort::TempStorage sort;
-  double vals_copy[kAssocBlock][NM];
-  unsigned skeys[kAssocBlock];
-  double warp_v[kAssocBlock / 32][NM];
-  int warp_f[kAssocBlock / 32];
-  double carry[kAssocBlock / 32][NM];
-  unsigned long long outliers, evals;
-};
-
-// Reduces one tile's deposits (key = node or >= J for "none") into the CTA's
-// row of the partial table.  Must be called by all threads of the block.
-template <int NM>
-__device__ void tile_reduce(AssocSmem<NM>& sm, unsigned key, const double v[NM], int J,
-                            int key_bits, double* __restrict__ partials,
-                            uint32_t* __restrict__ stamps, uint32_t epoch, int G, int cta) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-  for (int m = 0; m < NM; ++m) sm.vals_copy[tid][m] = v[m];
-  unsigned k1[1] = {key};
-  int i1[1] = {tid};
-  __syncthreads();
-  typename AssocSmem<NM>::Sort(sm.sort).Sort(k1, i1, 0, key_bits);
-  sm.skeys[tid] = k1[0];
-  __syncthreads();
-  const unsigned k = k1[0];
-  double x[NM];
-#pragma unroll
-  for (int m = 0; m < NM; ++m) x[m] = sm.vals_copy[i1[0]][m];
-  const bool head = (tid == 0) || sm.skeys[tid - 1] != k;
-  const bool tail = (tid == kAssocBlock - 1) || sm.skeys[tid + 1] != k;
-  // warp-level inclusive segmented scan: (v, f) op: f_r ? v_r : v_l + v_r
-  int f = head ? 1 : 0;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    double o[NM];
-#pragma unroll
-    for (int m = 0; m < NM; ++m) o[m] = __shfl_up_sync(0xffffffffu, x[m], off);
-    const int of = __shfl_up_sync(0xffffffffu, f, off);
-    if (lane >= off) {
-      if (!f) {
-#pragma unroll
-        for (int m = 0; m < NM; ++m) x[m] = o[m] + x[m];
-      }
-      f |= of;
-    }
-  }
-  if (lane == 31) {
-#pragma unroll
-    for (int m = 0; m < NM; ++m) sm.warp_v[warp][m] = x[m];
-    sm.warp_f[warp] = f;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    // carry into warp w = inclusive value at the last item of warp w-1
-#pragma unroll
-    for (int m = 0; m < NM; ++m) sm.carry[0][m] = 0.0;
-    for (int w = 1; w < kAssocBlock / 32; ++w)
-#pragma unroll
-      for (int m = 0; m < NM; ++m)
-        sm.carry[w][m] = sm.warp_f[w - 1] ? sm.warp_v[w - 1][m]
-                                          : sm.carry[w - 1][m] + sm.warp_v[w - 1][m];
-  }
-  __syncthreads();
-  if (!f && warp > 0) {
-#pragma unroll
-    for (int m = 0; m < NM; ++m) x[m] = sm.carry[warp][m] + x[m];
-  }
-  if (tail && k < (unsigned)J) {
-    const size_t row = (size_t)k * G + cta;
-    double* p = partials + row * NM;
-    if (stamps[row] == epoch) {
-#pragma unroll
-      for (int m = 0; m < NM; ++m) p[m] = p[m] + x[m];
-    } else {
-#pragma unroll
-      for (int m = 0; m < NM; ++m) p[m] = x[m];
-      stamps[row] = epoch;
-    }
-  }
-  __syncthreads();
 }
 
 __device__ __forceinline__ int key_bits_for(int J) { return 32 - __clz((unsigned)J); }
 
-// Transform y = R p + t (geometry.hpp:31) in the reference's order.
+// Transform y = R p + t (geometry.hpp:31) in the reference's order, with
+// explicit round-to-nearest operations: the result is the reference's bit
+// for bit whatever the including file's -fmad setting (the fused EM and
+// calibration kernels contract elsewhere; the descent must not).
 __device__ __forceinline__ void apply_rt(const double* Rt, double p0, double p1, double p2,
                                          double& y0, double& y1, double& y2) {
   if (Rt == nullptr) {
@@ -251,64 +168,58 @@ __device__ __forceinline__ void apply_rt(const double* Rt, double p0, double p1,
     y2 = p2;
     return;
   }
-  double s = Rt[0] * p0;
-  s += Rt[1] * p1;
-  s += Rt[2] * p2;
-  y0 = s + Rt[9];
-  s = Rt[3] * p0;
-  s += Rt[4] * p1;
-  s += Rt[5] * p2;
-  y1 = s + Rt[10];
-  s = Rt[6] * p0;
-  s += Rt[7] * p1;
-  s += Rt[8] * p2;
-  y2 = s + Rt[11];
+  double s = __dmul_rn(Rt[0], p0);
+  s = __dadd_rn(s, __dmul_rn(Rt[1], p1));
+  s = __dadd_rn(s, __dmul_rn(Rt[2], p2));
+  y0 = __dadd_rn(s, Rt[9]);
+  s = __dmul_rn(Rt[3], p0);
+  s = __dadd_rn(s, __dmul_rn(Rt[4], p1));
+  s = __dadd_rn(s, __dmul_rn(Rt[5], p2));
+  y1 = __dadd_rn(s, Rt[10]);
+  s = __dmul_rn(Rt[6], p0);
+  s = __dadd_rn(s, __dmul_rn(Rt[7], p1));
+  s = __dadd_rn(s, __dmul_rn(Rt[8], p2));
+  y2 = __dadd_rn(s, Rt[11]);
 }
 
-// Association pass of one CTA over tiles cta, cta+G, ... (persistent).
+// Scales of the association's accumulators (trg_fx.cuh): deposits are
+// g (<= 1), g y and g y y^T with |y| = |R p + t| <= sqrt(3) max|p| + max|t|.
+__device__ __forceinline__ void assoc_scales(const double* pmax, const double* Rt, FxScale sc[3]) {
+  double y = 1.7320508075688774 * __ldcg(pmax);
+  if (Rt) y += fmax(fabs(Rt[9]), fmax(fabs(Rt[10]), fabs(Rt[11])));
+  y *= 1.0000001;
+  sc[0] = fx_scale(1.0);
+  sc[1] = fx_scale(y);
+  sc[2] = fx_scale(y * y);
+}
+
+// Association pass of one warp over the fixed 32-point windows w = gwarp,
+// gwarp + nwarps, ... (association.cpp:91-157): per point the descent, then
+// the window's deposits go to the exact accumulators p.acc[J][NM][3]
+// (warp_run_deposit).  The totals do not depend on the grid.
 template <int NM>
-__device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double* Rt_smem, int G,
-                           int cta, int tile_G = -1, int tile_cta = -1) {
-  // tiles are dealt over tile_G CTAs (default: all G); partial rows stay
-  // indexed by the CTA's own id among G
-  const int tG = tile_G < 0 ? G : tile_G, tc = tile_G < 0 ? cta : tile_cta;
-  const int tid = threadIdx.x;
-  const int J = p.n_nodes;
-  const int kb = key_bits_for(J);
-  if (tid == 0) {
-    sm.outliers = 0;
-    sm.evals = 0;
-  }
-  __syncthreads();
+__device__ void assoc_fx_pass(const AssocParams& p, const double* Rt_smem, const FxScale* sc,
+                              int nwarps, int gwarp) {
+  constexpr int kOrd[10] = {0, 1, 1, 1, 2, 2, 2, 2, 2, 2};
+  const int lane = threadIdx.x & 31;
   unsigned long long my_out = 0, my_ev = 0;
-  // tiles of ts <= 256 points: when the cloud is small for the grid, spread
-  // it evenly over all CTAs (every SM gets the same share of descents)
-  const size_t per_cta = (p.n + tG - 1) / tG;
-  const int ts = per_cta < (size_t)kAssocBlock ? (per_cta > 0 ? (int)per_cta : 1) : kAssocBlock;
-  const size_t ntiles = (p.n + ts - 1) / ts;
-  for (size_t tile = tc; tile < ntiles; tile += tG) {
-    const size_t i = tile * ts + tid;
-    unsigned key = (unsigned)J;
+  const size_t nwin = (p.n + 31) / 32;
+  for (size_t w = gwarp; w < nwin; w += nwarps) {
+    const size_t i = w * 32 + lane;
+    int key = -1;
     double v[NM];
 #pragma unroll
     for (int m = 0; m < NM; ++m) v[m] = 0.0;
-    if (tid < ts && i < p.n) {
+    if (i < p.n) {
       double y0, y1, y2;
       apply_rt(Rt_smem, p.pts[3 * i], p.pts[3 * i + 1], p.pts[3 * i + 2], y0, y1, y2);
-      Descent d;
-      if (p.dbg_mode == 2) {
-        d.node = (int)(i % (size_t)J);
-        d.path = 0.5;
-        d.evals = 1;
-      } else {
-        d = descend(p.nodes, p.snodes, p.n_snodes, p.root_count, p.depth, p.lambda_c,
-                    p.outlier_floor, y0, y1, y2, p.status);
-      }
+      const Descent d = descend(p.nodes, p.snodes, p.n_snodes, p.root_count, p.depth, p.lambda_c,
+                                p.outlier_floor, y0, y1, y2, p.status);
       my_ev += d.evals;
       if (d.node < 0) {
         ++my_out;
       } else {
-        key = (unsigned)d.node;
+        key = d.node;
         deposit_values<NM>(d.path, y0, y1, y2, v);
       }
       if (p.point_node) {
@@ -316,65 +227,50 @@ __device__ void assoc_pass(AssocSmem<NM>& sm, const AssocParams& p, const double
         p.point_w[i] = d.node < 0 ? 0.0 : d.path;
       }
     }
-    // reconverge before the block-wide sort (CUB's warp-level steps assume
-    // converged warps; the descent above diverges per point)
     __syncwarp();
-    if (p.dbg_mode != 1) tile_reduce<NM>(sm, key, v, J, kb, p.partials, p.stamps, p.epoch, G, cta);
-    else if (key < (unsigned)J) p.partials[key] += v[0] * 0.0;
+#ifdef TRG_ASSOC_PROBE
+    if (lane == 0 && (gwarp % 32) == 0 && p.tl) tl_mark_any(p.tl, 5101);
+#endif
+    warp_run_deposit<NM>(key, v, p.acc, p.acc_stride, sc, kOrd);
+#ifdef TRG_ASSOC_PROBE
+    if (lane == 0 && (gwarp % 32) == 0 && p.tl) tl_mark_any(p.tl, 5102);
+#endif
   }
-  // integer counters: warp shuffle sums, then one add per warp (no 64-bit
-  // shared-memory CAS loops)
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     my_out += __shfl_xor_sync(0xffffffffu, my_out, off);
     my_ev += __shfl_xor_sync(0xffffffffu, my_ev, off);
   }
-  if ((tid & 31) == 0 && (my_out | my_ev)) {
+  if (lane == 0 && (my_out | my_ev)) {
     atomicAdd(&p.counters[0], my_out);
     atomicAdd(&p.counters[1], my_ev);
   }
 }
 
-// Sum node j's partial rows over CTAs in fixed order (one warp per node).
-// Rows are read in batches of 4 per lane with the stamp test as a select,
-// so the loads of a batch are all in flight together (a branch per row
-// serialises the L2 round trips); skipped rows add exactly 0.
-template <int NM>
-__device__ __forceinline__ void combine_node(const double* __restrict__ partials,
-                                             const uint32_t* __restrict__ stamps, uint32_t epoch,
-                                             int G, int j, double out[NM]) {
-  const int lane = threadIdx.x & 31;
-  double acc[NM];
-#pragma unroll
-  for (int m = 0; m < NM; ++m) acc[m] = 0.0;
-  const size_t base = (size_t)j * G;
-  for (int c0 = lane; c0 < G; c0 += 128) {
-    uint32_t st[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + 32 * u;
-      st[u] = c < G ? __ldcg(stamps + base + c) : 0u;
-    }
-    double v[4][NM];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + 32 * u;
-      const bool ok = c < G && st[u] == epoch;
-      const double* row = partials + (base + (ok ? c : 0)) * NM;
-#pragma unroll
-      for (int m = 0; m < NM; ++m) v[u][m] = ok ? __ldcg(row + m) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int m = 0; m < NM; ++m) acc[m] += v[u][m];
+// Stages nodes [0, S) into shared memory with one bulk copy (TMA engine),
+// completing on `bar` (phase bit `phase`, flipped on return).  Block-wide;
+// the nodes may have been rewritten by other CTAs before the caller's last
+// grid barrier.
+__device__ __forceinline__ void stage_nodes_bulk(DNode* snodes, const DNode* nodes, int S,
+                                                 uint64_t* bar, unsigned& phase) {
+  if (S <= 0) return;
+  __syncthreads();  // every reader of the previous stage is done
+  if (threadIdx.x == 0) {
+    fence_proxy_async_shared();
+    fence_proxy_async_global();
+    bulk_g2s_issue(snodes, nodes, (unsigned)(S * sizeof(DNode)), bar);
   }
+  mbar_wait(bar, phase);
+  phase ^= 1u;
+}
+
+// Node j's NM values from the planar accumulators.
+template <int NM>
+__device__ __forceinline__ void fx_row(const long long* acc, size_t stride, int j, const FxScale* sc,
+                                       double out[NM]) {
+  constexpr int kOrd[10] = {0, 1, 1, 1, 2, 2, 2, 2, 2, 2};
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-    for (int m = 0; m < NM; ++m) acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], off);
-#pragma unroll
-  for (int m = 0; m < NM; ++m) out[m] = acc[m];
+  for (int m = 0; m < NM; ++m) out[m] = fx_load(acc, stride, j, m, sc[kOrd[m]].down);
 }
 
 }  // namespace trg

@@ -113,7 +113,9 @@ struct BuildParams {
   int capacity;
   // calibration association
   AssocParams a;
-  double* cal_moments;  // [J][10]
+  double* cal_moments;  // [capacity] branch masses of a calibration pass
+  long long* cal_acc;   // [3][capacity][10][3] exact leaf accumulators (trg_fx.cuh)
+  unsigned long long* pmax_bits;  // max |coordinate| of the cloud (bits; k_init_entries)
   double* cta_drift;    // [G]
   unsigned* cal_arrive;  // [capacity + 1]; slot capacity: leaf arrivals of a calibration pass
   unsigned long long* drift_bits;  // [2] per-pass max drift (bits of a double >= 0)
@@ -124,7 +126,6 @@ struct BuildParams {
   BuildState* st;
   Timeline* tl;
   int* status;
-  int dbg;  // experiments only (TRG_BUILD_DBG): 1 = calibration combine only, 2 = + leaf refit
   int want_traces;  // per-iteration log-likelihoods only feed BuildDiagnostics (gmm.cpp:240)
   // Point-sharded mode (trg_build_tree_sharded): seg >= 0 runs
   // one segment between two exchange points (k_build: the per-node phase
@@ -1163,8 +1164,6 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
       if (mine) {
         // (a) tile pass
         const int T = __ldcg(&st->Tp[par]);
-        const bool tl6 = p.dbg == 6 && round == 2 && ph_i == 4;  // experiments: tile anatomy
-        if (tl6 && tid == 0) tl_mark_any(p.tl, 6000);
         int ntl = 0, nent = 0;
         for (int t = cta; t < T; t += G) {
           load_tile_ctx(p, sm, ph, par, t);
@@ -1176,17 +1175,10 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
           nent += sm.tlen;
           __syncthreads();
         }
-        // per-CTA finish: label 6100 + tiles, entries in the next mark
-        if (tl6 && tid == 0) {
-          tl_mark_any(p.tl, 6100 + ntl);
-          tl_mark_any(p.tl, 200000 + nent);
-        }
         grid_sync(p.bar, G);
         tl_mark(p.tl, round * 100 + ph_i);
         // (b) per-node reduction of the tile records (+ node update when the
         // whole cloud is here)
-        const bool tl7 = p.dbg == 7 && round == 2 && ph_i == 5;  // experiments: reduce anatomy
-        if (tl7 && tid == 0) tl_mark_any(p.tl, 6999);
         if (tid == 0) sm.nitems = phase_items(ph, sm.item_off, sm.item_kind);
         __syncthreads();
         const int NI = sm.nitems;
@@ -1205,13 +1197,7 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
             }
           }
           last = __shfl_sync(0xffffffffu, last, 0);
-          if (last && tl7 && lane == 0) tl_mark_any(p.tl, 7100);
           if (last) node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
-          if (last && tl7 && lane == 0) tl_mark_any(p.tl, 7200);
-        }
-        if (tl7) {
-          __syncthreads();
-          if (tid == 0) tl_mark_any(p.tl, 7000);
         }
         if (sharded) {
           grid_sync(p.bar, G);
@@ -1247,106 +1233,208 @@ inline int build_exchange_points_per_round(int em_iters) {
   return n;
 }
 
-// calibrate_pass's tree update (gmm.cpp:547-578) by one CTA, after the leaf
-// refits: per level bottom-up, an 8-lane group per parent (lane c holds child
-// c) sums its children's branch masses, reweights them (mass shares;
-// shadowed octets keep theirs) and moment-matches the parent from them, every
-// sum running in child order like the reference's loops; the top octet is
-// reweighted last; then every parent's refresh_eig runs in parallel
-// (warm-started from its previous axes).
-__device__ __forceinline__ double group8_sum(double v, int gbase) {
+// ----------------------------------------------------------------- calibration
+// calibrate_pass (gmm.cpp:523-580) as a dataflow over the tree: after the
+// pass's association (exact per-leaf accumulators) and one grid barrier,
+// every node is finished by the thread that completes it:
+//   leaf j (thread j / G of CTA j % G): branch mass = its m0, refit of mean
+//     and floored covariance from its deposits (gmm.cpp:532-545), then
+//     arrival on its parent's counter;
+//   internal node P (by the thread whose arrival completes P's children):
+//     branch mass = sum of the children's in child order (gmm.cpp:547-556),
+//     reweight of P's octet (mass shares; a shadowed octet keeps its shares,
+//     gmm.cpp:557-566), the moment match of P from its children
+//     (reset_parents_to_child_moments, gmm.cpp:489-513), then arrival on P's
+//     parent; P's refresh_eig (gmm.cpp:576-578) runs after the climb, since
+//     nothing above P needs P's eigen fields;
+//   the top octet is reweighted by the thread completing the level-0 set.
+// The reference's loops run level by level; every value here comes from
+// the same operands in the same order (child order for every sum), so the
+// pass computes the same tree, with a critical path of one leaf refit, the
+// chain of moment matches and the eigensolves of the completing thread.
+// Drift is the max over all of it (atomicMax on the bits of a double >= 0).
+// A second grid barrier closes the pass.
+struct CalCtx {
+  double* branch;    // [capacity] subtree deposit mass of this pass
+  unsigned* arrive;  // [capacity + 1] (slot capacity: the top octet)
+  int root_count;
+};
+
+__device__ __forceinline__ void cal_reweight(const BuildParams& p, const double* branch, int first,
+                                             int count, double& drift) {
+  double s = 0.0;
+  for (int c = 0; c < count; ++c) s += __ldcg(&branch[first + c]);
+  if (!(s > 0.0)) return;  // shadowed octet: keep the fitted shares
+  for (int c = 0; c < count; ++c) {
+    const double w = __ldcg(&branch[first + c]) / s;
+    drift = smax(drift, fabs(__ldcg(&p.nodes[first + c].weight) - w));
+    p.nodes[first + c].weight = w;
+  }
+}
+
+// Node i is final for this pass: arrive on its parent.  Returns the parent
+// when this arrival completed it (its node work is then this thread's), -1
+// otherwise (or after reweighting the top octet).
+__device__ __forceinline__ int cal_arrive(const BuildParams& p, const CalCtx& cx, int i,
+                                          double& drift) {
+  const int par = __ldcg(&p.nodes[i].parent);
+  const int slot = par >= 0 ? par : p.capacity;
+  const int need = par >= 0 ? __ldcg(&p.nodes[par].child_count) : cx.root_count;
+  __threadfence();
+  const unsigned old = atomicAdd(&cx.arrive[slot], 1u);
+  if (old + 1 != (unsigned)need) return -1;
+  __threadfence();
+  cx.arrive[slot] = 0u;
+  if (par < 0) {  // top octet (gmm.cpp:567-571)
+    cal_reweight(p, cx.branch, 0, cx.root_count, drift);
+    return -1;
+  }
+  return par;
+}
+
+// Sum of v over lanes [0, cc) of the warp in lane (= child) order, the
+// reference's serial loop order; the result is uniform.
+__device__ __forceinline__ double child_sum(double v, int cc) {
   double t = 0.0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) t += __shfl_sync(0xffffffffu, v, gbase + q);
+  for (int q = 0; q < cc; ++q) t += __shfl_sync(0xffffffffu, v, q);
   return t;
 }
 
-constexpr int kTopoCap = 640;  // parents whose (first_child, child_count) CTA 0 keeps in smem
-
-__device__ __forceinline__ int2 cal_topo(const BuildParams& p, const int2* topo, int n_topo, int i) {
-  return i < n_topo ? topo[i] : make_int2(__ldcg(&p.nodes[i].first_child), __ldcg(&p.nodes[i].child_count));
+// Internal node P, all children final, by one warp (lane c holds child c):
+// branch mass, octet reweight, moment match of P (no eigensolve).  Every
+// sum runs in child order.
+__device__ void cal_internal(const BuildParams& p, const CalCtx& cx, int P, double& drift) {
+  const int lane = threadIdx.x & 31;
+  const int f = __ldcg(&p.nodes[P].first_child), cc = __ldcg(&p.nodes[P].child_count);
+  const bool own = lane < cc;
+  const int ci = f + (own ? lane : 0);
+  const double cb = own ? __ldcg(&cx.branch[ci]) : 0.0;
+  double cw = own ? __ldcg(&p.nodes[ci].weight) : 0.0;
+  double cm[3], cv[9];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) cm[k] = own ? __ldcg(&p.nodes[ci].mean[k]) : 0.0;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) cv[k] = own ? __ldcg(&p.cov[9 * (size_t)ci + k]) : 0.0;
+  const double b = child_sum(cb, cc);  // branch (gmm.cpp:547-556) = the octet's share sum
+  if (lane == 0) cx.branch[P] = b;
+  if (b > 0.0 && own) {  // reweight (gmm.cpp:557-566); a shadowed octet keeps its shares
+    const double nw = cb / b;
+    drift = smax(drift, fabs(cw - nw));
+    cw = nw;
+    p.nodes[ci].weight = nw;
+  }
+  const double w = child_sum(cw, cc);
+  if (!(w > 0.0)) return;
+  double mu[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) mu[k] = child_sum(__dmul_rn(cw, cm[k]), cc) / w;
+  const double d[3] = {cm[0] - mu[0], cm[1] - mu[1], cm[2] - mu[2]};
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double v = child_sum(__dmul_rn(cw, __dadd_rn(cv[3 * r + q], __dmul_rn(d[r], d[q]))), cc);
+      if (lane == 3 * r + q) p.cov[9 * (size_t)P + 3 * r + q] = v / w;
+    }
+  if (lane < 3) p.nodes[P].mean[lane] = mu[lane];
 }
 
-__device__ void cal_tree_update(const BuildParams& p, const int* lvl, int root_count,
-                                const int2* topo, int n_topo, double& drift, bool marks) {
-  const int tid = threadIdx.x, c = tid & 7, gbase = (tid & 31) & ~7;
-  const int groups = blockDim.x / 8;
-  double* branch = p.cal_moments;  // slot 0 of each node
-  for (int l = p.L - 2; l >= 0; --l) {
-    const int n = lvl[l + 1] - lvl[l];
-    for (int b = 0; b < n; b += groups) {  // uniform across the CTA (full-warp shuffles)
-      const int i = lvl[l] + b + (tid >> 3);
-      const bool act = b + (tid >> 3) < n;
-      const int2 tp = act ? cal_topo(p, topo, n_topo, i) : make_int2(0, 0);
-      const int f = tp.x, cc = tp.y;
-      const bool own = c < cc;
-      const int ci = f + (own ? c : 0);
-      const double cb = own ? __ldcg(&branch[(size_t)ci * 10]) : 0.0;
-      double cw = own ? __ldcg(&p.nodes[ci].weight) : 0.0;
-      double cm[3], cv[9];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) cm[k] = own ? __ldcg(&p.nodes[ci].mean[k]) : 0.0;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) cv[k] = own ? __ldcg(&p.cov[9 * (size_t)ci + k]) : 0.0;
-      const double sb = group8_sum(cb, gbase);
-      if (cc > 0 && c == 0) branch[(size_t)i * 10] = sb;
-      if (own && sb > 0.0) {
-        const double nw = cb / sb;
-        drift = smax(drift, fabs(cw - nw));
-        cw = nw;
-        p.nodes[ci].weight = nw;
-      }
-      const double w = group8_sum(cw, gbase);
-      double mu[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) mu[k] = group8_sum(cw * cm[k], gbase);
-      const bool upd = cc > 0 && w > 0.0;  // group-uniform; shuffles stay warp-uniform
-      for (int k = 0; k < 3; ++k) mu[k] = upd ? mu[k] / w : 0.0;
-      const double d[3] = {cm[0] - mu[0], cm[1] - mu[1], cm[2] - mu[2]};
-      double m2[9];
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) m2[3 * r + q] = cw * (cv[3 * r + q] + d[r] * d[q]);
-      double out[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) out[k] = group8_sum(m2[k], gbase);
-      if (upd && c == 0) {
-        for (int k = 0; k < 9; ++k) p.cov[9 * (size_t)i + k] = out[k] / w;
-        for (int k = 0; k < 3; ++k) p.nodes[i].mean[k] = mu[k];
-      }
-    }
-    __syncthreads();
-    if (marks && tid == 0) tl_mark_any(p.tl, 5030 + l);
+// Leaf refit (gmm.cpp:532-545) from the leaf's deposits m[10].
+__device__ void cal_leaf(const BuildParams& p, const CalCtx& cx, int j, const double m[10],
+                         double& drift) {
+  cx.branch[j] = m[0];
+  DNode& nd = p.nodes[j];
+  if (!(m[0] > 0.0)) return;
+  const double mu[3] = {m[1] / m[0], m[2] / m[0], m[3] / m[0]};
+  const double M[3][3] = {{m[4], m[5], m[6]}, {m[5], m[7], m[8]}, {m[6], m[8], m[9]}};
+  double S[3][3], S2[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) S[r][c] = M[r][c] / m[0] - mu[r] * mu[c];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) S2[r][c] = 0.5 * (S[r][c] + S[c][r]);
+  double dm = (nd.mean[0] - mu[0]) * (nd.mean[0] - mu[0]);
+  dm += (nd.mean[1] - mu[1]) * (nd.mean[1] - mu[1]);
+  dm += (nd.mean[2] - mu[2]) * (nd.mean[2] - mu[2]);
+  drift = smax(drift, sqrt(dm));
+  double before[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) before[r][c] = p.cov[9 * (size_t)j + 3 * r + c];
+  GComp g;
+  g.w = nd.weight;
+  for (int q = 0; q < 3; ++q) g.mean[q] = mu[q];
+  double w[9];
+  for (int q = 0; q < 9; ++q) w[q] = nd.axT[q];
+  if (comp_set_cov(g, S2, cov_floor(S2, p.eps, p.abs_floor), w)) atomicCAS(p.status, 0, kEInval);
+  double dc[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) dc[r][c] = g.cov[3 * r + c] - before[r][c];
+  drift = smax(drift, norm33(dc));
+  // every field but weight (the parent's octet reweight owns it this pass)
+  for (int i = 0; i < 3; ++i) nd.mean[i] = g.mean[i];
+  for (int i = 0; i < 9; ++i) {
+    nd.axT[i] = g.axT[i];
+    p.cov[9 * (size_t)j + i] = g.cov[i];
   }
-  if (tid < 32) {  // top octet: lane r < 8 holds root r (root_count <= 8)
-    const bool own = tid < root_count;
-    const double cb = own ? __ldcg(&branch[(size_t)tid * 10]) : 0.0;
-    const double sb = group8_sum(cb, 0);
-    if (own && sb > 0.0) {
-      const double nw = cb / sb;
-      drift = smax(drift, fabs(__ldcg(&p.nodes[tid].weight) - nw));
-      p.nodes[tid].weight = nw;
-    }
+  for (int i = 0; i < 3; ++i) {
+    nd.lam[i] = g.lam[i];
+    nd.il[i] = 1.0 / g.lam[i];
   }
-  const int n_par = p.L >= 2 ? lvl[p.L - 1] : 0;  // parents sit above the deepest level
-  for (int i = tid; i < n_par; i += blockDim.x) {
-    if (cal_topo(p, topo, n_topo, i).y == 0) continue;
+  nd.log_norm = g.log_norm;
+  const double tr = (g.lam[0] + g.lam[1]) + g.lam[2];
+  nd.cplx = tr > 0.0 ? g.lam[2] / tr : -1.0;
+}
+
+#ifndef TRG_PROBE_PASS
+#define TRG_PROBE_PASS 10
+#endif
+#ifdef TRG_CAL_PROBE
+#define CAL_PROBE(cond, lab) \
+  if ((cond) && __ldcg(&p.st->cal_pass) == TRG_PROBE_PASS) tl_mark_any(p.tl, lab)
+#else
+#define CAL_PROBE(cond, lab)
+#endif
+// Leaf j final (its warp; lane 0 did the refit): climb as long as this warp
+// completes ancestors, then the refresh_eig of every node it matched, one
+// lane each.
+__device__ void cal_finish_leaf(const BuildParams& p, const CalCtx& cx, int j, double& drift) {
+  const int lane = threadIdx.x & 31;
+  int done[8];
+  int nd = 0;
+  int P = -1;
+  if (lane == 0) P = cal_arrive(p, cx, j, drift);
+  P = __shfl_sync(0xffffffffu, P, 0);
+  CAL_PROBE(lane == 0 && j % 16 == 0, 5003);
+  while (P >= 0) {
+    cal_internal(p, cx, P, drift);
+    __syncwarp();
+    CAL_PROBE(lane == 0, 5010);
+    done[nd++] = P;
+    if (lane == 0) P = cal_arrive(p, cx, P, drift);
+    P = __shfl_sync(0xffffffffu, P, 0);
+    CAL_PROBE(lane == 0, 5011);
+  }
+  int mine = -1;  // the refreshes run on different lanes, concurrently
+  for (int k = 0; k < nd; ++k)
+    if (lane == k) mine = done[k];
+  if (mine >= 0) {
     double cv[9];
-    for (int k = 0; k < 9; ++k) cv[k] = __ldcg(&p.cov[9 * (size_t)i + k]);
-    if (refresh_node(p.nodes[i], cv, true)) atomicCAS(p.status, 0, kEInval);
+    for (int q = 0; q < 9; ++q) cv[q] = __ldcg(&p.cov[9 * (size_t)mine + q]);
+    if (refresh_node(p.nodes[mine], cv, true)) atomicCAS(p.status, 0, kEInval);
+    CAL_PROBE(true, 5030);
   }
+  __syncwarp();
 }
 
 // Second persistent kernel of the build (launched right behind k_build on
 // the same stream): parent moment match + refresh_eig, then the leaf
-// calibration passes.  Separate so its 3x3 eigen chains get a full register
-// budget while k_build's E-step passes keep 3 CTAs per SM.
+// calibration passes.
 #ifndef TRG_KCAL_MINB
 #define TRG_KCAL_MINB 3
 #endif
 __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams p) {
-  __shared__ AssocSmem<10> asm_;
+  __shared__ FxScale sc[3];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ int lvl[9];
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   BuildState* st = p.st;
@@ -1357,8 +1445,12 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
   }
   if (sharded && __ldcg(&st->cal_done)) return;
   const int J = __ldcg(&st->J);
-  __shared__ int lvl[9];
   if (tid < 9) lvl[tid] = __ldcg(&st->lvl_start[tid]);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    mbar_fence_init();
+    assoc_scales(p.a.pmax, nullptr, sc);
+  }
   __syncthreads();
   // ------------------------------------------------ rematch + refresh_eig
   if (!sharded || p.seg == 0) {
@@ -1372,45 +1464,33 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
     tl_mark(p.tl, 902);
   }
   // ------------------------------------------------ leaf calibration
-  // calibrate_pass (gmm.cpp:523-580) per pass: association at identity with
-  // m2 (stage 1); then leaf refits and the whole bottom-up tree update
-  // (branch masses, octet reweights, parent moment match, refresh_eig): each
-  // leaf's warp refits it and arrives on a counter; CTA 0 waits for all
-  // leaves and runs the tree update (cal_tree_update) in the reference's
-  // level order, while the other CTAs go on to the pass's closing barrier.
-  // 2 grid barriers per pass.
   // Sharded (p.seg >= 0): segment s runs stage 2 of pass s-1 (from the
   // all-reduced leaf moments in xcal) and stage 1 of pass s up to the local
-  // leaf combine, then exits for the exchange.
-  const int root_count = lvl[1] - lvl[0];
-  __shared__ int n_leaf_s;
-  if (tid == 0) n_leaf_s = 0;
-  __syncthreads();
-  {
-    int c = 0;
-    for (int j = tid; j < J; j += blockDim.x) c += __ldcg(&p.nodes[j].child_count) == 0;
-    if (c) atomicAdd(&n_leaf_s, c);
-  }
-  __syncthreads();
-  const int n_leaf = n_leaf_s;
-  __shared__ int2 topo[kTopoCap];  // CTA 0's copy of the parents' topology
-  const int n_topo = cta == 0 ? min(lvl[p.L >= 2 ? p.L - 1 : 0], kTopoCap) : 0;
-  for (int i = tid; i < n_topo; i += blockDim.x)
-    topo[i] = make_int2(__ldcg(&p.nodes[i].first_child), __ldcg(&p.nodes[i].child_count));
-  extern __shared__ __align__(16) unsigned char k_cal_stage[];  // upper levels for the descent
+  // leaf moments, then exits for the exchange.
+  CalCtx cx;
+  cx.branch = p.cal_moments;
+  cx.arrive = p.cal_arrive;
+  cx.root_count = lvl[1] - lvl[0];
+  extern __shared__ __align__(128) unsigned char k_cal_stage[];  // upper levels for the descent
   DNode* cal_stage = reinterpret_cast<DNode*>(k_cal_stage);
   const int n_stage = min(p.L >= 2 ? lvl[p.L - 1] : 0, kStageNodes);
+  const size_t accJ = (size_t)p.capacity * 30;  // limbs per accumulator buffer
+  unsigned mphase = 0;
+  constexpr int WPB = kTile / 32;
   for (int pass = 0; pass < 40; ++pass) {
     const bool run_s1 = !sharded || p.seg == pass;
     const bool run_s2 = !sharded || p.seg == pass + 1;
     if (!run_s1 && !run_s2) continue;
     AssocParams a = p.a;
     a.n_nodes = J;
-    a.root_count = root_count;
-    a.epoch = p.a.epoch + (uint32_t)pass;
+    a.root_count = cx.root_count;
     a.snodes = cal_stage;
     a.n_snodes = n_stage;
-    const bool tl5 = p.dbg == 5 && pass == 10;  // experiments: fine marks of one pass
+    a.acc = p.cal_acc + (size_t)(pass % 3) * accJ;
+#ifdef TRG_ASSOC_PROBE
+    a.tl = pass == TRG_PROBE_PASS ? p.tl : nullptr;
+    if (pass == TRG_PROBE_PASS && tid == 0 && cta % 32 == 0) tl_mark_any(p.tl, 5100);
+#endif
     if (run_s1) {
       if (pass > 0) {
         const double dprev = __longlong_as_double((long long)__ldcg(&p.drift_bits[(pass - 1) & 1]));
@@ -1420,87 +1500,49 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
         }
       }
       if (cta == 0 && tid == 0) p.drift_bits[pass & 1] = 0ull;
-      stage_nodes(cal_stage, p.nodes, n_stage);  // stage 2 rewrote them
-      assoc_pass<10>(asm_, a, nullptr, G, cta);
-      if (tl5) tl_mark(p.tl, 5001);
+      stage_nodes_bulk(cal_stage, p.nodes, n_stage, &mbar, mphase);  // stage 2 rewrote them
+#ifdef TRG_ASSOC_PROBE
+      if (pass == TRG_PROBE_PASS && tid == 0 && cta % 32 == 0) tl_mark_any(p.tl, 5103);
+#endif
+      assoc_fx_pass<10>(a, nullptr, sc, G * WPB, cta * WPB + warp);
       grid_sync(p.bar, G);
       tl_mark(p.tl, 1000 + pass * 10 + 1);
       if (sharded) {
-        // this shard's leaf moments, for the all-reduce
-        for (int j = cta * (kTile / 32) + warp; j < J; j += G * (kTile / 32)) {
-          if (__ldcg(&p.nodes[j].child_count) != 0) continue;
+        // this shard's leaf moments, for the all-reduce (rows zeroed for
+        // the next segment)
+        for (int j = cta * WPB + warp; j < J; j += G * WPB) {
           double m[10];
-          combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
-          if (lane == 0)
+          fx_row<10>(a.acc, a.acc_stride, j, sc, m);
+          __syncwarp();
+          if (lane < 30) a.acc[(size_t)lane * a.acc_stride + j] = 0;
+          if (lane == 0 && __ldcg(&p.nodes[j].child_count) == 0)
             for (int q = 0; q < 10; ++q) p.xcal[(size_t)j * 10 + q] = m[q];
         }
         return;
       }
     }
+    if (!sharded) {
+      // zero this CTA's slice of the buffer pass+2 writes
+      long long* z = p.cal_acc + (size_t)((pass + 2) % 3) * accJ;
+      for (size_t q = (size_t)cta * blockDim.x + tid; q < accJ; q += (size_t)G * blockDim.x) z[q] = 0;
+    }
     double drift = 0.0;
-    for (int j = cta * (kTile / 32) + warp; j < J; j += G * (kTile / 32)) {
+    for (int j = warp * G + cta; j < J; j += G * WPB) {  // a warp per leaf, spread over SMs
       if (__ldcg(&p.nodes[j].child_count) != 0) continue;  // leaves only
-      double m[10];
-      if (sharded) {
-        for (int q = 0; q < 10; ++q) m[q] = __ldcg(p.xcal + (size_t)j * 10 + q);
-      } else {
-        combine_node<10>(a.partials, a.stamps, a.epoch, G, j, m);
-      }
-      if (tl5 && lane == 0 && j % 16 == 0) tl_mark_any(p.tl, 5002);
-      double* branch = p.cal_moments;  // slot 0 of each node
       if (lane == 0) {
-        branch[(size_t)j * 10] = m[0];
-        DNode& nd = p.nodes[j];
-        if (m[0] > 0.0) {  // leaf refit (gmm.cpp:532-545)
-          const double mu[3] = {m[1] / m[0], m[2] / m[0], m[3] / m[0]};
-          const double M[3][3] = {{m[4], m[5], m[6]}, {m[5], m[7], m[8]}, {m[6], m[8], m[9]}};
-          double S[3][3], S2[3][3];
-          for (int r = 0; r < 3; ++r)
-            for (int c = 0; c < 3; ++c) S[r][c] = M[r][c] / m[0] - mu[r] * mu[c];
-          for (int r = 0; r < 3; ++r)
-            for (int c = 0; c < 3; ++c) S2[r][c] = 0.5 * (S[r][c] + S[c][r]);
-          double dm = (nd.mean[0] - mu[0]) * (nd.mean[0] - mu[0]);
-          dm += (nd.mean[1] - mu[1]) * (nd.mean[1] - mu[1]);
-          dm += (nd.mean[2] - mu[2]) * (nd.mean[2] - mu[2]);
-          drift = smax(drift, sqrt(dm));
-          double before[3][3];
-          for (int r = 0; r < 3; ++r)
-            for (int c = 0; c < 3; ++c) before[r][c] = p.cov[9 * (size_t)j + 3 * r + c];
-          GComp g;
-          g.w = nd.weight;
-          for (int q = 0; q < 3; ++q) g.mean[q] = mu[q];
-          double w[9];
-          for (int q = 0; q < 9; ++q) w[q] = nd.axT[q];
-          if (comp_set_cov(g, S2, cov_floor(S2, p.eps, p.abs_floor), w)) atomicCAS(p.status, 0, kEInval);
-          double dc[3][3];
-          for (int r = 0; r < 3; ++r)
-            for (int c = 0; c < 3; ++c) dc[r][c] = g.cov[3 * r + c] - before[r][c];
-          drift = smax(drift, norm33(dc));
-          write_dnode_from_comp(nd, p.cov + 9 * (size_t)j, g, nd.weight, nd.level, nd.parent);
+        CAL_PROBE(j % 16 == 0, 5000);
+        double m[10];
+        if (sharded) {
+          for (int q = 0; q < 10; ++q) m[q] = __ldcg(p.xcal + (size_t)j * 10 + q);
+        } else {
+          fx_row<10>(a.acc, a.acc_stride, j, sc, m);
         }
+        CAL_PROBE(j % 16 == 0, 5001);
+        cal_leaf(p, cx, j, m, drift);
+        CAL_PROBE(j % 16 == 0, 5002);
       }
       __syncwarp();
-      if (tl5 && lane == 0 && j % 16 == 0) tl_mark_any(p.tl, 5003);
-      if (lane == 0) {  // this leaf is refit: arrive for CTA 0's tree update
-        __threadfence();
-        atomicAdd(&p.cal_arrive[p.capacity], 1u);
-      }
-    }
-    if (cta == 0) {
-      // tree update of the pass (gmm.cpp:547-578), in the reference's level
-      // order, once every leaf has arrived: branch masses, octet reweights
-      // and the parent moment match bottom-up, one thread per parent with
-      // sums in child order; then refresh_eig of all parents in parallel.
-      if (tid == 0) {
-        volatile unsigned* ctr = &p.cal_arrive[p.capacity];
-        while (*ctr < (unsigned)n_leaf) __nanosleep(20);
-        __threadfence();
-        *ctr = 0u;
-      }
-      __syncthreads();
-      if (tl5 && tid == 0) tl_mark_any(p.tl, 5010);
-      cal_tree_update(p, lvl, root_count, topo, n_topo, drift, tl5);
-      if (tl5 && tid == 0) tl_mark_any(p.tl, 5020);
+      cal_finish_leaf(p, cx, j, drift);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) drift = smax(drift, __shfl_xor_sync(0xffffffffu, drift, off));
@@ -1517,7 +1559,7 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
     st->cal_evals = __ldcg(&p.a.counters[1]);
     TreeMeta m;
     m.J = J;
-    m.root_count = root_count;
+    m.root_count = cx.root_count;
     m.n_upper = p.L >= 2 ? lvl[p.L - 1] : 0;
     m.ok = __ldcg(p.status) == 0 ? 1 : 0;
     *p.meta = m;
@@ -1526,11 +1568,13 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
 
 __global__ void k_init_entries(const double* __restrict__ pts, size_t n, double* ex, double* ey,
                                double* ez, double* ew, int* tile_node, int* tile_start,
-                               int* tile_len, int* status) {
+                               int* tile_len, int* status, unsigned long long* pmax_bits) {
+  double am = 0.0;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
     const double x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
     if (!isfinite(x) || !isfinite(y) || !isfinite(z)) atomicCAS(status, 0, kEInval);
+    am = fmax(am, fmax(fabs(x), fmax(fabs(y), fabs(z))));
     ex[i] = x;
     ey[i] = y;
     ez[i] = z;
@@ -1542,6 +1586,10 @@ __global__ void k_init_entries(const double* __restrict__ pts, size_t n, double*
       tile_len[t] = (int)min((size_t)kTile, n - i);
     }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) am = fmax(am, __shfl_xor_sync(0xffffffffu, am, o));
+  if ((threadIdx.x & 31) == 0 && am > 0.0)
+    atomicMax(pmax_bits, (unsigned long long)__double_as_longlong(am));
 }
 
 }  // namespace trg
@@ -1613,6 +1661,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
                o_tb = carve(sizeof(double) * 8 * T),
                o_md = carve(sizeof(double) * E), o_emit = carve(sizeof(double) * 8 * E),
                o_calm = carve(sizeof(double) * 10 * cap), o_bar = carve(64),
+               o_cacc = carve(sizeof(long long) * 3 * 30 * (size_t)cap), o_pmax = carve(64),
                o_lay = carve(sizeof(int) * 48 * K),
                o_llt = carve(sizeof(double) * (size_t)cap * 2 * (cfg->em_iterations_per_node + 1)),
                o_kex = carve(sizeof(int) * (size_t)cap),
@@ -1628,7 +1677,6 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
     // records are reduced in tile order).
     const double est_tiles = (double)n * std::pow(4.0, (double)(L - 1)) / kTile;
     int per_sm = (int)std::min(3.0, std::max(1.0, std::ceil(est_tiles / (4.0 * ctx->sms))));
-    if (const char* e = getenv("TRG_KBUILD_PER_SM")) per_sm = atoi(e);  // experiments
     G = std::min(G, ctx->sms * std::max(1, per_sm));
   }
   const size_t cal_smem = sizeof(DNode) * kStageNodes;
@@ -1641,7 +1689,6 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
     // C2 76.8k stays at 3/SM, its optimum)
     int per_sm = (int)std::min<size_t>(3, std::max<size_t>(1, (n + 192 * (size_t)ctx->sms - 1) /
                                                                   (192 * (size_t)ctx->sms)));
-    if (const char* e = getenv("TRG_KCAL_PER_SM")) per_sm = atoi(e);  // experiments
     Gc = std::min(Gc, ctx->sms * std::max(1, per_sm));
   }
   const size_t o_cd = carve(sizeof(double) * std::max(G, Gc));
@@ -1691,6 +1738,8 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   p.min_d2 = (double*)(A + o_md);
   p.emit = (double*)(A + o_emit);
   p.cal_moments = (double*)(A + o_calm);
+  p.cal_acc = (long long*)(A + o_cacc);
+  p.pmax_bits = (unsigned long long*)(A + o_pmax);
   p.layout_scratch = (int*)(A + o_lay);
   p.ll_trace = (double*)(A + o_llt);
   p.kept_exp = (int*)(A + o_kex);
@@ -1706,11 +1755,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   p.xarg = (double*)(A + o_xa);
   p.xarg_all = (double*)(A + o_xaa);
   p.xcal = (double*)(A + o_xc);
-  {
-    const char* dbg = getenv("TRG_BUILD_DBG");
-    p.dbg = dbg ? atoi(dbg) : 0;
-    p.want_traces = (diag && diag->ll_traces && diag->ll_trace_capacity > 0) ? 1 : 0;
-  }
+  p.want_traces = (diag && diag->ll_traces && diag->ll_trace_capacity > 0) ? 1 : 0;
   TRG_TRY(timeline_reset(ctx));
   // tree
   trg_tree_dev* tree = nullptr;
@@ -1719,9 +1764,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   p.nodes = tree->nodes;
   p.cov = tree->cov;
   // calibration association (NM = 10, identity, lambda_c = 0, full depth)
-  void *part, *stamps, *cnt;
-  TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * 10 * (size_t)cap * Gc, &part));
-  TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)cap * Gc, &stamps));
+  void* cnt;
   TRG_TRY(ws_get(ctx, kSlotCounters, 64, &cnt));
   p.a.nodes = tree->nodes;
   p.a.depth = L;
@@ -1730,16 +1773,10 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   p.a.pts = pts;
   p.a.n = n;
   p.a.Rt = nullptr;
-  p.a.partials = (double*)part;
-  p.a.stamps = (uint32_t*)stamps;
   p.a.counters = (unsigned long long*)cnt;
+  p.a.pmax = reinterpret_cast<const double*>(p.pmax_bits);
+  p.a.acc_stride = (size_t)cap;
   p.a.status = ctx->status;
-  p.a.epoch = ctx->epoch + 1;
-  {
-    const char* dm = getenv("TRG_ASSOC_DBG");  // experiments only
-    p.a.dbg_mode = dm ? atoi(dm) : 0;
-  }
-  ctx->epoch += 41;
   // ---- initial state
   BuildState st{};
   st.Kp[0] = 1;
@@ -1753,6 +1790,8 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   TRG_CU(cudaMemsetAsync(A + o_arr, 0, sizeof(unsigned) * K, ctx->stream));
   TRG_CU(cudaMemsetAsync(A + o_fd, 0, sizeof(unsigned) * K, ctx->stream));
   TRG_CU(cudaMemsetAsync(A + o_car, 0, sizeof(unsigned) * ((size_t)cap + 1), ctx->stream));
+  TRG_CU(cudaMemsetAsync(A + o_cacc, 0, sizeof(long long) * 3 * 30 * (size_t)cap, ctx->stream));
+  TRG_CU(cudaMemsetAsync(A + o_pmax, 0, 64, ctx->stream));
   TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
   // initial state through a dedicated pinned buffer: asynchronous copies, no
   // staging syncs (the previous build's copies completed at its collect)
@@ -1767,7 +1806,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
     TRG_CU(trg_memcpy(ctx, A + o_rn[0][q], &h_rn[q], sizeof(int), cudaMemcpyHostToDevice));
   k_init_entries<<<256, 256, 0, ctx->stream>>>(pts, n, p.ex[0], p.ey[0], p.ez[0], p.ew[0],
                                                p.tile_node[0], p.tile_start[0], p.tile_len[0],
-                                               ctx->status);
+                                               ctx->status, p.pmax_bits);
   ctx->launches += 1;
   job->p = p;
   job->tree = tree;

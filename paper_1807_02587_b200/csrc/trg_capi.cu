@@ -524,21 +524,18 @@ int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, siz
   p.lambda_c = cfg->lambda_c;
   p.outlier_floor = cfg->outlier_floor;
   p.n = n;
-  p.epoch = ++ctx->epoch;
   p.status = ctx->status;
-  {
-    const char* dm = getenv("TRG_ASSOC_DBG");
-    p.dbg_mode = dm ? atoi(dm) : 0;
-  }
   TRG_TRY(stage_points_public(ctx, xyz, n, xyz_on_device, kSlotPoints, &p.pts));
-  void *part, *stamps, *mom, *cnt, *rt;
-  TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * nm * (size_t)J * G, &part));
-  TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)J * G, &stamps));
+  void *accv, *mom, *cnt, *rt;
+  const size_t acc_bytes = sizeof(long long) * 3 * nm * (size_t)J;
+  TRG_TRY(ws_get(ctx, kSlotPartials, acc_bytes, &accv));
   TRG_TRY(ws_get(ctx, kSlotMoments, sizeof(double) * nm * (size_t)J, &mom));
-  TRG_TRY(ws_get(ctx, kSlotCounters, 64 + 12 * sizeof(double), &cnt));
+  TRG_TRY(ws_get(ctx, kSlotCounters, 64 + 12 * sizeof(double) + 64, &cnt));
   rt = static_cast<char*>(cnt) + 64;
-  p.partials = static_cast<double*>(part);
-  p.stamps = static_cast<uint32_t*>(stamps);
+  unsigned long long* pmax = reinterpret_cast<unsigned long long*>(static_cast<char*>(cnt) + 64 + 12 * sizeof(double));
+  p.acc = static_cast<long long*>(accv);
+  p.acc_stride = (size_t)J;
+  p.pmax = reinterpret_cast<const double*>(pmax);
   p.counters = static_cast<unsigned long long*>(cnt);
   double hrt[12];
   for (int k = 0; k < 9; ++k) hrt[k] = R[k];
@@ -546,6 +543,9 @@ int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, siz
   TRG_CU(trg_memcpy(ctx, rt, hrt, sizeof hrt, cudaMemcpyHostToDevice));
   p.Rt = static_cast<const double*>(rt);
   TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
+  TRG_CU(cudaMemsetAsync(pmax, 0, 8, ctx->stream));
+  TRG_CU(cudaMemsetAsync(accv, 0, acc_bytes, ctx->stream));
+  TRG_TRY(launch_absmax(ctx, p.pts, n, pmax, nullptr));
   if (point_node) {
     void *pn, *pw;
     TRG_TRY(ws_get(ctx, kSlotPointNode, sizeof(int) * n, &pn));

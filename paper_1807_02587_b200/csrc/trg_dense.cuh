@@ -8,6 +8,49 @@
 
 namespace trg {
 
+// Sum node j's partial rows over CTAs in fixed order (one warp per node).
+// Rows are read in batches of 4 per lane with the stamp test as a select,
+// so the loads of a batch are all in flight together (a branch per row
+// serialises the L2 round trips); skipped rows add exactly 0.
+template <int NM>
+__device__ __forceinline__ void combine_node(const double* __restrict__ partials,
+                                             const uint32_t* __restrict__ stamps, uint32_t epoch,
+                                             int G, int j, double out[NM]) {
+  const int lane = threadIdx.x & 31;
+  double acc[NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) acc[m] = 0.0;
+  const size_t base = (size_t)j * G;
+  for (int c0 = lane; c0 < G; c0 += 128) {
+    uint32_t st[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 32 * u;
+      st[u] = c < G ? __ldcg(stamps + base + c) : 0u;
+    }
+    double v[4][NM];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 32 * u;
+      const bool ok = c < G && st[u] == epoch;
+      const double* row = partials + (base + (ok ? c : 0)) * NM;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) v[u][m] = ok ? __ldcg(row + m) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int m = 0; m < NM; ++m) acc[m] += v[u][m];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int m = 0; m < NM; ++m) acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], off);
+#pragma unroll
+  for (int m = 0; m < NM; ++m) out[m] = acc[m];
+}
+
+
 // -------------------------------------------------------- dense association
 struct DenseParams {
   const double* pts;

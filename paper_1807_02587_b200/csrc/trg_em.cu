@@ -11,7 +11,7 @@
 #include <vector>
 
 #include "trg_dense.cuh"
-#include "trg_solve.cuh"
+#include "trg_roles.cuh"
 
 namespace trg {
 
@@ -23,8 +23,11 @@ struct EmState {
 
 struct EmParams {
   AssocParams a;
-  double* moments;  // [J][4]
-  double* cta_acc;  // [G][kNormalEq + 2]
+  double* moments;  // [J][4] (dense path)
+  double* cta_acc;  // [G][kNormalEq + 2] (dense path)
+  long long* acc;   // tree path: [2][12][acc_stride] exact planar accumulators (trg_fx.cuh)
+  unsigned* sync;   // [16]: grid barrier, flag, arrivals (zeroed per launch)
+  unsigned* smtab;  // [G] SM id per CTA (roles)
   unsigned* bar;
   EmState* st;
   double* crit_before;
@@ -48,25 +51,44 @@ struct EmParams {
 
 constexpr int kAccStride = kNormalEq + 2;
 
-// One EM iteration = E-step (all CTAs) | grid barrier | per-node combine +
-// virtual-point rows (the first ceil(J/8) CTAs, one warp per node) | grid
-// barrier | EVERY CTA folds those per-CTA normal equations in the same fixed
-// order and solves redundantly (identical bits everywhere), so the running
-// transform and the stop decision need no third barrier.  CTA 0 alone adds
-// the criterion-after trace and publishes the state for the host.
+// Per-node (m0, m1) of iteration `it`: the exchanged doubles (sharded) or
+// the iteration's exact accumulators.
+__device__ __forceinline__ void em_node_moments(const EmParams& p, bool sharded, const long long* acc,
+                                                const FxScale* sc, int j, double m[4]) {
+  if (sharded) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m[k] = ldcg(p.xmom + (size_t)j * 4 + k);
+  } else {
+    fx_row<4>(acc, p.a.acc_stride, j, sc, m);
+  }
+}
+
+// One EM iteration (tree model) = E-step: every CTA's warps descend their
+// fixed 32-point windows and add each window's runs to the iteration's exact
+// per-node accumulators | ONE grid barrier | EVERY CTA reads all J nodes'
+// moments, forms the virtual-point rows (27-term normal equations) in the
+// same thread mapping, reduces them in a fixed order and solves (identical
+// bits everywhere), so T <- delta o T and the stop decision need no second
+// barrier.  The accumulators rotate over three buffers: iteration it writes
+// acc[it % 3], and after its barrier every CTA zeroes its slice of
+// acc[(it + 2) % 3] (last read before that barrier, next written after the
+// following one).
 // DENSE: the flat-mixture variant (registration.cpp:191-202): the E-step is
-// responsibilities_dense over the J components instead of the tree descent.
+// responsibilities_dense over the J components (per-component rows + a
+// per-node combine on ceil(J/8) CTAs, then a second barrier).
 template <bool DENSE>
-__global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
-  __shared__ AssocSmem<4> sm;
+__global__ void __launch_bounds__(kAssocBlock, 2) k_register(EmParams p) {
   __shared__ SolveSmem ss;
   __shared__ Eig6Smem e6;
   __shared__ SolveOut so;
   __shared__ double rt[12];
   __shared__ double red[kAccStride];
+  __shared__ FxScale sc[3], sc_prev[3];
+  __shared__ __align__(8) uint64_t mbar;
   __shared__ int s_done, s_fails, s_conv, s_iters;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  constexpr int WPB = kAssocBlock / 32;
   int J = p.a.n_nodes, root_count = p.a.root_count, n_snodes = p.a.n_snodes;
   if (p.meta) {
     if (!__ldcg(&p.meta->ok)) return;  // the build failed or overflowed: the host retries / reports
@@ -74,39 +96,49 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
     root_count = __ldcg(&p.meta->root_count);
     n_snodes = min(__ldcg(&p.meta->n_upper), kStageNodes);
   }
-  const int P2 = min(G, (J + (kAssocBlock / 32) - 1) / (kAssocBlock / 32));  // producer CTAs
+  const int P2 = min(G, (J + WPB - 1) / WPB);  // DENSE: producer CTAs of the per-node rows
   const bool sharded = p.seg >= 0;
   const double n_total = sharded ? p.n_total : (double)p.a.n;
+  const size_t accJ = p.a.acc_stride * 4 * 3;  // limbs per accumulator buffer
   if (tid < 12) rt[tid] = ldcg(&p.st->Rt[tid]);
   if (tid == 0) {
     s_done = sharded ? *(volatile int*)&p.st->done : 0;
     s_fails = sharded ? *(volatile int*)&p.st->fails : 0;
     s_conv = sharded ? *(volatile int*)&p.st->converged : 0;
     s_iters = sharded ? *(volatile int*)&p.st->iterations : 0;
+    mbar_init(&mbar, 1);
+    mbar_fence_init();
   }
   __syncthreads();
   if (s_done) return;
   const double trans_limit = ldcg(&p.st->trans_limit);
-  // the model is fixed during the EM: stage its upper levels once
-  extern __shared__ __align__(16) unsigned char k_reg_stage[];
+  // the model is fixed during the EM: stage its upper levels once (bulk copy)
+  extern __shared__ __align__(128) unsigned char k_reg_stage[];
   DNode* reg_stage = reinterpret_cast<DNode*>(k_reg_stage);
-  if (!DENSE) stage_nodes(reg_stage, p.a.nodes, n_snodes);
+  unsigned mphase = 0;
+  if (!DENSE) stage_nodes_bulk(reg_stage, p.a.nodes, n_snodes, &mbar, mphase);
   // criterion after the update of iteration k (trace only), CTA 0.  Single
-  // GPU (defer): CTA 0 takes no E-step tiles and computes it for iteration
-  // it-1 while the other CTAs run iteration it's E-step (the moments and
-  // the solve of it-1 are still in place then), so the trace leaves the
+  // GPU (defer): CTA 0 takes no E-step windows and computes it for iteration
+  // it-1 while the other CTAs run iteration it's E-step (the moments of it-1
+  // and its solve are still in place then), so the trace leaves the
   // iteration's critical path; the last iteration's is computed after the loop.
   const bool defer = !sharded && !DENSE && G > 1;
-  auto crit_trace = [&](int k) {
+  auto crit_trace = [&](int k, const FxScale* s) {
     unsigned long long* counters = p.a.counters + 2 * (k & 1);
     double c = 0.0;
     if (!so.degenerate) {
       double dRt[12];
       for (int i = 0; i < 9; ++i) dRt[i] = so.dR[i];
       for (int i = 0; i < 3; ++i) dRt[9 + i] = so.dt[i];
+      const long long* acc = p.acc + (size_t)(k % 3) * accJ;
       for (int j = tid; j < J; j += blockDim.x) {
-        const double* m = p.moments + (size_t)j * 4;
-        c += crit_term(p.a.nodes + j, ldcg(m), ldcg(m + 1), ldcg(m + 2), ldcg(m + 3), n_total, dRt);
+        double m[4];
+        if (DENSE) {
+          for (int q = 0; q < 4; ++q) m[q] = ldcg(p.moments + (size_t)j * 4 + q);
+        } else {
+          em_node_moments(p, sharded, acc, s, j, m);
+        }
+        c += crit_term(p.a.nodes + j, m[0], m[1], m[2], m[3], n_total, dRt);
       }
     }
     c = block_sum(c, ss);
@@ -119,7 +151,7 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
   };
   for (int it = 0; it < p.max_iters; ++it) {
     const bool run_e = !sharded || p.seg == it;      // E-step of iteration it
-    const bool run_m = !sharded || p.seg == it + 1;  // combine/solve of iteration it
+    const bool run_m = !sharded || p.seg == it + 1;  // solve of iteration it
     if (!run_e && !run_m) continue;
     AssocParams a = p.a;
     a.n_nodes = J;
@@ -127,12 +159,17 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
     a.n_snodes = n_snodes;
     a.epoch = p.epoch0 + (uint32_t)it;
     a.snodes = reg_stage;
+    a.acc = p.acc + (size_t)(it % 3) * accJ;
     // per-iteration counters alternate between two slots: CTA 0 reads and
-    // clears slot it&1 in P3 while faster CTAs may already count iteration
-    // it+1's evaluations (slot (it+1)&1); nobody reaches it+2 before that
+    // clears slot it&1 while faster CTAs may already count iteration it+1's
+    // evaluations (slot (it+1)&1); nobody reaches it+2 before that
     a.counters = p.a.counters + 2 * (it & 1);
+    if (tid < 3) sc_prev[tid] = sc[tid];
+    __syncthreads();
+    if (tid == 0) assoc_scales(p.a.pmax, rt, sc);
+    __syncthreads();
     if (run_e) {
-      // ---- P1: E-step over this CTA's point tiles
+      // ---- E-step
       tl_mark(p.tl, 2000 + it * 10);
       if constexpr (DENSE) {
         DenseParams d{};
@@ -151,17 +188,26 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
         grid_sync(p.bar, G);
         dense_pass2<4>(d, rt, G, cta);
       } else if (defer && cta == 0) {
-        if (it > 0) crit_trace(it - 1);
+        if (it > 0) crit_trace(it - 1, sc_prev);
       } else {
-        assoc_pass<4>(sm, a, rt, G, cta, defer ? G - 1 : G, defer ? cta - 1 : cta);
+        const int ctas = defer ? G - 1 : G, c = defer ? cta - 1 : cta;
+        assoc_fx_pass<4>(a, rt, sc, ctas * WPB, c * WPB + warp);
       }
       grid_sync(p.bar, G);
       tl_mark(p.tl, 2000 + it * 10 + 1);
       if (sharded) {
         // this shard's per-node moments + counters, for the all-reduce
-        for (int j = cta * (kAssocBlock / 32) + warp; j < J; j += G * (kAssocBlock / 32)) {
+        // (the accumulator rows are zeroed for the next segment)
+        for (int j = cta * WPB + warp; j < J; j += G * WPB) {
           double m[4];
-          combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
+          if constexpr (DENSE) {
+            combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
+          } else {
+            fx_row<4>(a.acc, a.acc_stride, j, sc, m);
+          }
+          __syncwarp();
+          if (!DENSE)
+            if (lane < 12) a.acc[(size_t)lane * a.acc_stride + j] = 0;
           if (lane == 0)
 #pragma unroll
             for (int k = 0; k < 4; ++k) p.xmom[(size_t)j * 4 + k] = m[k];
@@ -173,55 +219,75 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
         return;
       }
     }
-    // ---- P2: per-node combine over CTAs + virtual-point rows
-    if (cta < P2) {
+    // ---- normal equations of iteration it
+    if constexpr (DENSE) {
+      if (cta < P2) {
+        SolveAcc acc;
+        acc_zero(acc);
+        for (int j = cta * WPB + warp; j < J; j += P2 * WPB) {
+          double m[4];
+          if (sharded) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) m[k] = ldcg(p.xmom + (size_t)j * 4 + k);
+          } else {
+            combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
+          }
+          if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) p.moments[(size_t)j * 4 + k] = m[k];
+            vp_accumulate(a.nodes + j, m[0], m[1], m[2], m[3], n_total, acc, a.status);
+          }
+        }
+        block_reduce_acc(acc, ss);
+        if (tid == 0) {
+          double* o = p.cta_acc + (size_t)cta * kAccStride;
+#pragma unroll
+          for (int k = 0; k < kNormalEq; ++k) o[k] = acc.v[k];
+          o[kNormalEq] = acc.crit;
+          o[kNormalEq + 1] = (double)acc.nvp;
+        }
+      }
+      grid_sync(p.bar, G);
+      tl_mark(p.tl, 2000 + it * 10 + 2);
+      {
+        const int v = tid >> 3, sub = tid & 7;
+        double s = 0.0;
+        if (v < kAccStride)
+          for (int c = sub; c < P2; c += 8) s += ldcg(p.cta_acc + (size_t)c * kAccStride + v);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        if (v < kAccStride && sub == 0) red[v] = s;
+      }
+    } else {
+      if (!sharded) {
+        // zero this CTA's slice of the buffer iteration it+2 writes
+        long long* z = p.acc + (size_t)((it + 2) % 3) * accJ;
+        for (size_t q = (size_t)cta * blockDim.x + tid; q < accJ; q += (size_t)G * blockDim.x) z[q] = 0;
+      }
+      // every CTA: all nodes' rows, fixed thread mapping and reduction order
       SolveAcc acc;
       acc_zero(acc);
-      for (int j = cta * (kAssocBlock / 32) + warp; j < J; j += P2 * (kAssocBlock / 32)) {
+      for (int j = tid; j < J; j += blockDim.x) {
         double m[4];
-        if (sharded) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) m[k] = ldcg(p.xmom + (size_t)j * 4 + k);
-        } else {
-          combine_node<4>(a.partials, a.stamps, a.epoch, G, j, m);
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) p.moments[(size_t)j * 4 + k] = m[k];
-          vp_accumulate(a.nodes + j, m[0], m[1], m[2], m[3], n_total, acc, a.status);
-        }
+        em_node_moments(p, sharded, a.acc, sc, j, m);
+        vp_accumulate(a.nodes + j, m[0], m[1], m[2], m[3], n_total, acc, a.status);
       }
       block_reduce_acc(acc, ss);
       if (tid == 0) {
-        double* o = p.cta_acc + (size_t)cta * kAccStride;
 #pragma unroll
-        for (int k = 0; k < kNormalEq; ++k) o[k] = acc.v[k];
-        o[kNormalEq] = acc.crit;
-        o[kNormalEq + 1] = (double)acc.nvp;
+        for (int k = 0; k < kNormalEq; ++k) red[k] = acc.v[k];
+        red[kNormalEq] = acc.crit;
+        red[kNormalEq + 1] = (double)acc.nvp;
       }
     }
-    grid_sync(p.bar, G);
-    tl_mark(p.tl, 2000 + it * 10 + 2);
-    // ---- P3 (every CTA): fold the P2 partials (8 lanes per value, strided,
-    // fixed shuffle tree), solve, update T
-    {
-      const int v = tid >> 3, sub = tid & 7;
-      double s = 0.0;
-      if (v < kAccStride)
-        for (int c = sub; c < P2; c += 8) s += ldcg(p.cta_acc + (size_t)c * kAccStride + v);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      if (v < kAccStride && sub == 0) red[v] = s;
-    }
     __syncthreads();
-    tl_mark(p.tl, 7000);
     if (tid == 0) so.crit_before = red[kNormalEq];
     __syncthreads();
-    if (tid < 32) warp_solve_normal_eq(red, (int)red[kNormalEq + 1], &so, e6, p.tl, false);
+    if (tid < 32) warp_solve_normal_eq(red, (int)red[kNormalEq + 1], &so, e6, nullptr, false);
     __syncthreads();
     tl_mark(p.tl, 2000 + it * 10 + 3);
-    if (cta == 0 && !defer) crit_trace(it);
+    if (cta == 0 && !defer) crit_trace(it, sc);
     if (tid == 0) {
       s_iters = it + 1;
       if (!so.degenerate) {
@@ -273,7 +339,7 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
     }
     if (s_done) break;
   }
-  if (defer && cta == 0) crit_trace(s_iters - 1);
+  if (defer && cta == 0) crit_trace(s_iters - 1, sc);
   if (!sharded && cta == 0 && tid == 0) {
     EmState* st = p.st;
     for (int k = 0; k < 12; ++k) st->Rt[k] = rt[k];
@@ -281,6 +347,258 @@ __global__ void __launch_bounds__(kAssocBlock, 3) k_register(EmParams p) {
     st->converged = s_conv;
     st->fails = s_fails;
     st->done = 1;
+  }
+}
+
+// ---------------------------------------------------------------- tree EM
+constexpr int kEmBlock = 320;  // 10 warps: 2 CTAs x 147 worker SMs >= 2,400 windows (C2)
+// Registration EM with a tree model (registration.cpp:47-82) as ONE
+// persistent launch with roles (trg_roles.cuh): WORKER CTAs run each
+// iteration's E-step -- the descent of their fixed 32-point windows and the
+// exact per-node deposits into acc[it % 2] -- and arrive on a counter; ONE
+// SOLVER CTA (on an updater SM, its instruction cache holding the solver)
+// waits for the arrivals, forms the virtual-point rows of all J nodes
+// (make_virtual_points + the 27-term normal equations, mstep.cpp:8-75),
+// solves (mstep.cpp:76-98), applies T <- delta o T and the stop tests
+// (registration.cpp:66-78), zeroes acc[(it + 1) % 2], publishes the new
+// state with a flag, and only then computes the criterion-after trace of
+// the iteration (diagnostics, off the critical path).  No grid barrier per
+// iteration.
+// Sharded (p.seg >= 0): segment s finishes iteration s-1 from the
+// all-reduced moments in xmom, publishes iteration s, waits for the local
+// E-step and exports this shard's per-node moments for the all-reduce.
+__device__ __forceinline__ void em_apply_update(const SolveOut& so, double* rt, const EmParams& p,
+                                                double trans_limit, int& s_fails, int& s_conv,
+                                                int& s_done) {
+  if (!so.degenerate) {
+    // T = delta * T (geometry.hpp:42-47)
+    double nR[9], nt[3];
+    for (int i = 0; i < 3; ++i)
+      for (int jj = 0; jj < 3; ++jj) {
+        double q = so.dR[3 * i] * rt[jj];
+        q += so.dR[3 * i + 1] * rt[3 + jj];
+        q += so.dR[3 * i + 2] * rt[6 + jj];
+        nR[3 * i + jj] = q;
+      }
+    for (int i = 0; i < 3; ++i) {
+      double q = so.dR[3 * i] * rt[9];
+      q += so.dR[3 * i + 1] * rt[10];
+      q += so.dR[3 * i + 2] * rt[11];
+      nt[i] = q + so.dt[i];
+    }
+    for (int k = 0; k < 9; ++k) rt[k] = nR[k];
+    for (int k = 0; k < 3; ++k) rt[9 + k] = nt[k];
+    s_fails = 0;
+    // rotation_angle (geometry.cpp:17-20) and |t| (registration.cpp:68-69)
+    double cth = ((so.dR[0] + so.dR[4]) + so.dR[8] - 1.0) * 0.5;
+    cth = cth < -1.0 ? -1.0 : (cth > 1.0 ? 1.0 : cth);
+    double tn = so.trans[0] * so.trans[0];
+    tn += so.trans[1] * so.trans[1];
+    tn += so.trans[2] * so.trans[2];
+    if (acos(cth) < p.rot_tol && sqrt(tn) < trans_limit) {
+      s_conv = 1;
+      s_done = 1;
+    }
+  } else if (++s_fails >= 3) {
+    s_done = 1;
+  }
+}
+
+#ifndef TRG_KEM_MINB
+#define TRG_KEM_MINB 2
+#endif
+__global__ void __launch_bounds__(kEmBlock, TRG_KEM_MINB) k_em_tree(EmParams p) {
+  __shared__ SolveSmem ss;
+  __shared__ Eig6Smem e6;
+  __shared__ SolveOut so;
+  __shared__ double rt[12];
+  __shared__ double red[kAccStride];
+  __shared__ FxScale sc[3];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ int s_done, s_fails, s_conv, s_iters;
+  extern __shared__ __align__(128) unsigned char k_em_stage[];
+  const int G = gridDim.x, tid = threadIdx.x, warp = tid >> 5;
+  constexpr int WPB = kEmBlock / 32;
+  int J = p.a.n_nodes, root_count = p.a.root_count, n_snodes = p.a.n_snodes;
+  if (p.meta) {
+    if (!__ldcg(&p.meta->ok)) return;  // the build failed or overflowed: the host retries / reports
+    J = __ldcg(&p.meta->J);
+    root_count = __ldcg(&p.meta->root_count);
+    n_snodes = min(__ldcg(&p.meta->n_upper), kStageNodes);
+  }
+  const bool sharded = p.seg >= 0;
+  const int it0 = sharded ? p.seg : 0;
+  const double n_total = sharded ? p.n_total : (double)p.a.n;
+  const size_t S = p.a.acc_stride;
+  unsigned* flag = p.sync + 2;
+  unsigned* arrived = p.sync + 3;
+  const Roles r = assign_roles(p.smtab, p.sync, G, 1);
+  if (r.upd && r.idx != 0) return;  // the solver's SM stays free of E-step work
+  EmState* st = p.st;
+  if (!r.upd) {
+    // ------------------------------------------------ workers: E-steps
+    if (tid == 0) {
+      mbar_init(&mbar, 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    DNode* stage = reinterpret_cast<DNode*>(k_em_stage);
+    unsigned mphase = 0;
+    stage_nodes_bulk(stage, p.a.nodes, n_snodes, &mbar, mphase);  // the model is fixed
+    AssocParams a = p.a;
+    a.n_nodes = J;
+    a.root_count = root_count;
+    a.n_snodes = n_snodes;
+    a.snodes = stage;
+    for (int k = 0;; ++k) {
+      const int it = it0 + k;
+      wait_flag(flag, (unsigned)k + 1);
+      if (tid == 0) s_done = __ldcg(&st->done);
+      if (tid < 12) rt[tid] = __ldcg(&st->Rt[tid]);
+      __syncthreads();
+      if (s_done || it >= p.max_iters) return;
+      if (tid == 0) assoc_scales(p.a.pmax, rt, sc);
+      __syncthreads();
+      a.acc = p.acc + (size_t)(it & 1) * S * 12;
+      a.counters = p.a.counters + 2 * (it & 1);
+      assoc_fx_pass<4>(a, rt, sc, r.n_work * WPB, r.idx * WPB + warp);
+      arrive_count(arrived);
+      if (sharded) return;  // one E-step per segment
+    }
+  }
+  // -------------------------------------------------- the solver CTA
+  if (tid == 0) {
+    s_done = __ldcg(&st->done);
+    s_fails = __ldcg(&st->fails);
+    s_conv = __ldcg(&st->converged);
+    s_iters = __ldcg(&st->iterations);
+  }
+  if (tid < 12) rt[tid] = __ldcg(&st->Rt[tid]);
+  __syncthreads();
+  const double trans_limit = __ldcg(&st->trans_limit);
+  // moments of iteration `it` (exchanged doubles when sharded)
+  auto node_m = [&](int it, int j, double m[4]) {
+    if (sharded) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) m[q] = __ldcg(p.xmom + (size_t)j * 4 + q);
+    } else {
+      fx_row<4>(p.acc + (size_t)(it & 1) * S * 12, S, j, sc, m);
+    }
+  };
+  // criterion after the update of iteration it (trace only)
+  auto crit_trace = [&](int it) {
+    double c = 0.0;
+    if (!so.degenerate) {
+      double dRt[12];
+      for (int i = 0; i < 9; ++i) dRt[i] = so.dR[i];
+      for (int i = 0; i < 3; ++i) dRt[9 + i] = so.dt[i];
+      for (int j = tid; j < J; j += blockDim.x) {
+        double m[4];
+        node_m(it, j, m);
+        c += crit_term(p.a.nodes + j, m[0], m[1], m[2], m[3], n_total, dRt);
+      }
+    }
+    c = block_sum(c, ss);
+    if (tid == 0) {
+      p.evals[it] = sharded ? (unsigned long long)__ldcg(p.xmom + (size_t)J * 4)
+                            : atomicExch(&p.a.counters[2 * (it & 1) + 1], 0ull);
+      p.crit_before[it] = so.crit_before;
+      p.crit_after[it] = so.degenerate ? so.crit_before : c;
+    }
+  };
+  // solve of iteration it from its moments; state update
+  auto solve = [&](int it) {
+    SolveAcc acc;
+    acc_zero(acc);
+    for (int j = tid; j < J; j += blockDim.x) {
+      double m[4];
+      node_m(it, j, m);
+      vp_accumulate(p.a.nodes + j, m[0], m[1], m[2], m[3], n_total, acc, p.a.status);
+    }
+#ifdef TRG_EM_PROBE
+    if (tid == 0) tl_mark_any(p.tl, 7100);
+#endif
+    block_reduce_acc(acc, ss);
+    if (tid == 0) {
+#pragma unroll
+      for (int k = 0; k < kNormalEq; ++k) red[k] = acc.v[k];
+      red[kNormalEq] = acc.crit;
+      red[kNormalEq + 1] = (double)acc.nvp;
+      so.crit_before = acc.crit;
+    }
+    __syncthreads();
+#ifdef TRG_EM_PROBE
+    if (tid == 0) tl_mark_any(p.tl, 7101);
+#endif
+#ifdef TRG_EM_PROBE
+    if (tid < 32) warp_solve_normal_eq(red, (int)red[kNormalEq + 1], &so, e6, p.tl, false);
+#else
+    if (tid < 32) warp_solve_normal_eq(red, (int)red[kNormalEq + 1], &so, e6, nullptr, false);
+#endif
+    __syncthreads();
+#ifdef TRG_EM_PROBE
+    if (tid == 0) tl_mark_any(p.tl, 7102);
+#endif
+    if (tid == 0) {
+      s_iters = it + 1;
+      em_apply_update(so, rt, p, trans_limit, s_fails, s_conv, s_done);
+      if (it + 1 >= p.max_iters) s_done = 1;
+    }
+    __syncthreads();
+  };
+  auto publish_state = [&](unsigned f) {
+    if (tid == 0) {
+      for (int k = 0; k < 12; ++k) st->Rt[k] = rt[k];
+      st->iterations = s_iters;
+      st->converged = s_conv;
+      st->fails = s_fails;
+      st->done = s_done;
+      publish_flag(flag, f);
+    }
+  };
+  if (sharded && it0 > 0 && !s_done) {
+    // finish iteration it0-1 from the all-reduced moments
+    solve(it0 - 1);
+    publish_state(1u);
+    crit_trace(it0 - 1);
+  } else {
+    if (tid == 0 && it0 >= p.max_iters) s_done = 1;
+    __syncthreads();
+    publish_state(1u);
+  }
+  if (s_done) return;
+  for (int k = 0;; ++k) {
+    const int it = it0 + k;
+    if (tid == 0) assoc_scales(p.a.pmax, rt, sc);  // the scales the workers used
+    wait_count(arrived, (unsigned)r.n_work * (unsigned)(k + 1));
+    if (tid == 0) tl_mark_any(p.tl, 2000 + it * 10 + 1);
+    if (sharded) {
+      // this shard's per-node moments + counters, for the all-reduce (the
+      // accumulator rows are zeroed for the next segment)
+      long long* acc = p.acc + (size_t)(it & 1) * S * 12;
+      for (int j = tid; j < J; j += blockDim.x) {
+        double m[4];
+        fx_row<4>(acc, S, j, sc, m);
+        for (int q = 0; q < 12; ++q) acc[(size_t)q * S + j] = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) p.xmom[(size_t)j * 4 + q] = m[q];
+      }
+      if (tid == 0) {
+        p.xmom[(size_t)J * 4] = (double)atomicExch(&p.a.counters[2 * (it & 1) + 1], 0ull);
+        p.xmom[(size_t)J * 4 + 1] = (double)atomicExch(&p.a.counters[2 * (it & 1)], 0ull);
+      }
+      return;
+    }
+    solve(it);
+    {  // the buffer iteration it+1 writes (last read by iteration it-1)
+      long long* z = p.acc + (size_t)((it + 1) & 1) * S * 12;
+      for (size_t q = tid; q < S * 12; q += blockDim.x) z[q] = 0;
+    }
+    __syncthreads();
+    publish_state((unsigned)k + 2);
+    if (tid == 0) tl_mark_any(p.tl, 2000 + it * 10 + 3);
+    crit_trace(it);
+    if (s_done) break;
   }
 }
 
@@ -436,6 +754,7 @@ namespace {
 
 struct EmJob {
   const void* kernel = nullptr;
+  int block = 0;
   size_t smem = 0;
   EmParams p;
   int G = 0, J = 0, K = 0;
@@ -456,16 +775,21 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   const int J = meta ? tree->capacity : tree->n_nodes;
   int* status = meta ? ctx->status2 : ctx->status;
   job->status = status;
-  job->kernel = dense ? (const void*)k_register<true> : (const void*)k_register<false>;
+  job->kernel = dense ? (const void*)k_register<true> : (const void*)k_em_tree;
+  job->block = dense ? kAssocBlock : kEmBlock;
   job->smem = dense ? 0 : sizeof(DNode) * kStageNodes;
   TRG_CU(set_dynamic_smem(job->kernel, std::max<size_t>(job->smem, 1)));
-  // 2 CTAs per SM (of the 3 that fit): the per-node combine over CTAs and
-  // the redundant per-CTA solve get cheaper faster than the E-step slows
-  // (C2, 16 iterations: 0.72 ms at 2/SM vs 0.80 at 1/SM and 0.90 at 3/SM);
-  // clouds under 40k points: 1/SM (C1: 0.39 vs 0.44 ms)
+  // dense: 2 CTAs per SM (of the 3 that fit).  tree: enough worker warps
+  // for one 32-point window each (a second window per warp doubles the
+  // E-step's latency), at most 2 CTAs per SM, plus the solver's SM
   int per_sm = n >= 40000 ? 2 : 1;
-  if (const char* e = getenv("TRG_KREG_PER_SM")) per_sm = atoi(e);  // experiments
-  const int G = std::min(persistent_grid(ctx, job->kernel, kAssocBlock, job->smem),
+  if (!dense) {
+    const size_t windows = (n + 31) / 32;
+    const size_t wpc = kEmBlock / 32;
+    per_sm = (int)std::min<size_t>(2, std::max<size_t>(1, (windows + wpc * (ctx->sms - 1) - 1) /
+                                                              (wpc * std::max(1, ctx->sms - 1))));
+  }
+  const int G = std::min(persistent_grid(ctx, job->kernel, job->block, job->smem),
                          ctx->sms * std::max(1, per_sm));
   EmParams p{};
   p.a.nodes = tree->nodes;
@@ -479,12 +803,16 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   p.a.n = n;
   p.a.status = status;
   p.meta = meta;
-  void *part, *stamps, *mom, *cnt, *em, *tr, *xm;
-  TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * 4 * (size_t)J * G, &part));
-  TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)J * G, &stamps));
+  void *part = nullptr, *stamps = nullptr, *mom, *cnt, *em, *tr, *xm, *accv = nullptr;
+  if (dense) {
+    TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(double) * 4 * (size_t)J * G, &part));
+    TRG_TRY(ws_get(ctx, kSlotStamps, sizeof(uint32_t) * (size_t)J * G, &stamps));
+  } else {
+    TRG_TRY(ws_get(ctx, kSlotPartials, sizeof(long long) * 2 * 12 * (size_t)J, &accv));
+  }
   TRG_TRY(ws_get(ctx, kSlotMoments, sizeof(double) * 4 * (size_t)J, &mom));
-  TRG_TRY(ws_get(ctx, kSlotCounters, 64, &cnt));
-  const size_t em_bytes = 256 + sizeof(EmState) + sizeof(double) * kAccStride * G;
+  TRG_TRY(ws_get(ctx, kSlotCounters, 64 + 8, &cnt));
+  const size_t em_bytes = 256 + sizeof(EmState) + sizeof(double) * kAccStride * G + 4 * (size_t)G + 64;
   TRG_TRY(ws_get(ctx, kSlotEm, em_bytes, &em));
   const int K = cfg->max_em_iterations;
   TRG_TRY(ws_get(ctx, kSlotEmTrace, (sizeof(double) * 2 + 8) * (size_t)K, &tr));
@@ -492,10 +820,15 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   p.a.partials = static_cast<double*>(part);
   p.a.stamps = static_cast<uint32_t*>(stamps);
   p.a.counters = static_cast<unsigned long long*>(cnt);
+  p.a.pmax = reinterpret_cast<const double*>(static_cast<char*>(cnt) + 64);
+  p.acc = static_cast<long long*>(accv);
+  p.a.acc_stride = (size_t)J;
   p.moments = static_cast<double*>(mom);
   p.bar = static_cast<unsigned*>(em);
   p.st = reinterpret_cast<EmState*>(static_cast<char*>(em) + 64);
   p.cta_acc = reinterpret_cast<double*>(static_cast<char*>(em) + 256);
+  p.sync = p.bar;  // [0..1] grid barrier, [2] flag, [3] arrivals
+  p.smtab = reinterpret_cast<unsigned*>(p.cta_acc + (size_t)kAccStride * G);
   p.crit_before = static_cast<double*>(tr);
   p.crit_after = p.crit_before + K;
   p.evals = reinterpret_cast<unsigned long long*>(p.crit_after + K);
@@ -522,12 +855,16 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   for (int k = 0; k < 9; ++k) st.Rt[k] = cfg->initial_R[k];
   for (int k = 0; k < 3; ++k) st.Rt[9 + k] = cfg->initial_t[k];
   TRG_CU(cudaMemsetAsync(em, 0, 64, ctx->stream));
-  TRG_CU(cudaMemsetAsync(cnt, 0, 64, ctx->stream));
+  TRG_CU(cudaMemsetAsync(cnt, 0, 64 + 8, ctx->stream));
+  if (accv)
+    TRG_CU(cudaMemsetAsync(accv, 0, sizeof(long long) * 2 * 12 * (size_t)J, ctx->stream));
   TRG_CU(trg_memcpy(ctx, p.st, &st, sizeof st, cudaMemcpyHostToDevice));
-  if (n > 0) k_check_finite<<<64, 256, 0, ctx->stream>>>(src_dev, 3 * n, status);
+  // non-finite check + max |coordinate| (the accumulators' scale)
+  TRG_TRY(launch_absmax(ctx, src_dev, n, reinterpret_cast<unsigned long long*>(static_cast<char*>(cnt) + 64),
+                        status));
   k_extent<<<1, 256, 0, ctx->stream>>>(tree->nodes, J, p.st, target_diag, cfg->translation_tol,
                                        meta, diag_dev);
-  ctx->launches += 2;
+  ctx->launches += 1;
   job->p = p;
   job->G = G;
   job->J = J;
@@ -540,8 +877,10 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
 
 int em_launch(trg_ctx* ctx, EmJob* job, int seg) {
   if (job->p.seg >= 0) job->p.seg = seg;
+  // per-launch handover words (grid barrier, flag, arrivals)
+  TRG_CU(cudaMemsetAsync(job->p.sync, 0, 64, ctx->stream));
   void* args[] = {&job->p};
-  TRG_CU(launch_persistent(ctx, job->kernel, job->G, kAssocBlock, args, job->smem));
+  TRG_CU(launch_persistent(ctx, job->kernel, job->G, job->block, args, job->smem));
   ctx->launches += 1;
   return TRG_OK;
 }

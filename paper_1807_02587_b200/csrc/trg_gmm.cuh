@@ -19,7 +19,7 @@ struct GComp {
 static_assert(sizeof(GComp) == 240, "GComp layout");
 
 // set_floored_cov (gmm.cpp:143-150) into a GComp.
-__device__ __forceinline__ int comp_set_cov(GComp& g, const double sc[3][3], double floor_value,
+static __device__ __noinline__ int comp_set_cov(GComp& g, const double sc[3][3], double floor_value,
                                             const double* warm = nullptr) {
   double lam[3], ax[3][3], cov[3][3];
   const int rc = eig_sym3_floored(sc, floor_value, lam, ax, warm);
@@ -61,7 +61,7 @@ __device__ __forceinline__ void write_dnode_from_comp(DNode& d, double* cov9, co
 
 // refresh_eig (gmm.cpp:31-35) of a tree node from its cov.
 // warm: start the eigensolve from the node's current axes (calibration).
-__device__ __forceinline__ int refresh_node(DNode& d, const double* cov9, bool warm = false) {
+static __device__ __noinline__ int refresh_node(DNode& d, const double* cov9, bool warm = false) {
   double m[3][3], lam[3], ax[3][3];
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j) m[i][j] = cov9[3 * i + j];

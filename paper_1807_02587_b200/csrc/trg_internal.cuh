@@ -8,6 +8,7 @@
 
 #include "../../include/treereg_b200.h"
 #include "trg_math.cuh"
+#include "trg_fx.cuh"
 
 namespace trg {
 
@@ -252,6 +253,11 @@ struct AssocParams {
   const double* pts;  // N*3 AoS
   size_t n;
   const double* Rt;  // device: R[9], t[3] (nullable => identity)
+  // tree path: exact fixed-point accumulators acc[J][NM][3] (trg_fx.cuh)
+  long long* acc;
+  size_t acc_stride;   // node stride of the planar limbs (>= n_nodes)
+  const double* pmax;  // device: max |coordinate| of pts (the accumulators' scale)
+  // dense path (flat mixture): per-(component, chunk) rows, stamped
   double* partials;  // [J][G][NM]
   uint32_t* stamps;  // [J][G]
   uint32_t epoch;
@@ -259,14 +265,18 @@ struct AssocParams {
   int* point_node;               // nullable
   double* point_w;               // nullable
   int* status;
-  int dbg_mode;                  // 0 normal; experiments: 1 skip reduction, 2 skip descent
   // nodes [0, n_snodes) read from a shared-memory copy (the calling kernel
   // stages them): the tree's upper levels, visited by every point
   const trg::DNode* snodes;
   int n_snodes;
+  Timeline* tl;  // probes only (TRG_ASSOC_PROBE)
 };
 int launch_associate(trg_ctx* ctx, const AssocParams& p, int nm, double* moments /*[J][nm]*/,
                      int grid);
+// max |coordinate| of a device cloud into *pmax_bits (bits of a double >= 0;
+// the caller zeroes it first); also flags non-finite coordinates (status).
+int launch_absmax(trg_ctx* ctx, const double* pts, size_t n, unsigned long long* pmax_bits,
+                  int* status);
 int assoc_grid(trg_ctx* ctx, int nm);
 // Per-node fixed-order combine of epoch-stamped partial rows -> out[J][nm].
 int launch_combine(trg_ctx* ctx, const double* partials, const uint32_t* stamps, uint32_t epoch,

@@ -440,7 +440,9 @@ static __device__ void warp_solve_normal_eq(const double* v, int nvp, SolveOut* 
   }
   __syncwarp();
   double x[6], trinv, mind;
+  if (tl && lane == 0) tl_mark_any(tl, 7004);
   warp_ldlt_solve6_tr(ata_s, v + 21, x, &trinv, &mind, ls);
+  if (tl && lane == 0) tl_mark_any(tl, 7005);
   if (lane == 0) {
     o->nvp = nvp;
     o->degenerate = 0;
@@ -476,9 +478,9 @@ static __device__ void warp_solve_normal_eq(const double* v, int nvp, SolveOut* 
   __syncwarp();
   if (s_need_eig) {
     double ev[6];
-    if (tl && lane == 0) tl_mark(tl, 7001);
+    if (tl && lane == 0) tl_mark_any(tl, 7001);
     warp_eig6(ata_s, ev, w);
-    if (tl && lane == 0) tl_mark(tl, 7002);
+    if (tl && lane == 0) tl_mark_any(tl, 7002);
     if (lane == 0) {
       o->eig_sweeps = w.sweeps;
       const double lmin = ev[0], lmax = ev[5];
@@ -488,7 +490,7 @@ static __device__ void warp_solve_normal_eq(const double* v, int nvp, SolveOut* 
     }
   }
   if (lane == 0 && !o->degenerate) small_angle_rotation(o->omega, o->dR);
-  if (tl && lane == 0) tl_mark(tl, 7003);
+  if (tl && lane == 0) tl_mark_any(tl, 7003);
   __syncwarp();
 }
 
