@@ -1413,14 +1413,15 @@ __device__ void cal_finish_leaf(const BuildParams& p, const CalCtx& cx, int j, d
     P = __shfl_sync(0xffffffffu, P, 0);
     CAL_PROBE(lane == 0, 5011);
   }
-  int mine = -1;  // the refreshes run on different lanes, concurrently
-  for (int k = 0; k < nd; ++k)
-    if (lane == k) mine = done[k];
-  if (mine >= 0) {
+  if (nd) {  // the refreshes, one lane each, warp-uniform solver (SIMT)
+    int mine = -1;
+    for (int k = 0; k < nd; ++k)
+      if (lane == k) mine = done[k];
     double cv[9];
-    for (int q = 0; q < 9; ++q) cv[q] = __ldcg(&p.cov[9 * (size_t)mine + q]);
-    if (refresh_node(p.nodes[mine], cv, true)) atomicCAS(p.status, 0, kEInval);
-    CAL_PROBE(true, 5030);
+    for (int q = 0; q < 9; ++q) cv[q] = mine >= 0 ? __ldcg(&p.cov[9 * (size_t)mine + q]) : 0.0;
+    if (refresh_node_simt(p.nodes[mine >= 0 ? mine : 0], cv, true, mine >= 0))
+      atomicCAS(p.status, 0, kEInval);
+    CAL_PROBE(lane == 0, 5030);
   }
   __syncwarp();
 }
@@ -1429,7 +1430,7 @@ __device__ void cal_finish_leaf(const BuildParams& p, const CalCtx& cx, int j, d
 // the same stream): parent moment match + refresh_eig, then the leaf
 // calibration passes.
 #ifndef TRG_KCAL_MINB
-#define TRG_KCAL_MINB 3
+#define TRG_KCAL_MINB 2
 #endif
 __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams p) {
   __shared__ FxScale sc[3];
@@ -1458,8 +1459,12 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
     if (cta == 0) reset_parents(p, lvl);
     grid_sync(p.bar, G);
     tl_mark(p.tl, 901);
-    for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x)
-      if (refresh_node(p.nodes[j], p.cov + 9 * (size_t)j)) atomicCAS(p.status, 0, kEInval);
+    for (int base = 0; base < J; base += G * blockDim.x) {  // SIMT refresh_eig
+      const int j = base + cta * blockDim.x + tid;
+      const bool act = j < J;
+      if (refresh_node_simt(p.nodes[act ? j : 0], p.cov + 9 * (size_t)(act ? j : 0), false, act))
+        atomicCAS(p.status, 0, kEInval);
+    }
     grid_sync(p.bar, G);
     tl_mark(p.tl, 902);
   }

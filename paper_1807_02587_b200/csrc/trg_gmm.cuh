@@ -81,4 +81,44 @@ static __device__ __noinline__ int refresh_node(DNode& d, const double* cov9, bo
   return kOk;
 }
 
+// Warp-uniform variants (trg_math.cuh eig_sym3*_simt): all 32 lanes call,
+// each with its own matrix; results are bit-identical to the per-lane ones.
+__device__ __forceinline__ int comp_set_cov_simt(GComp& g, const double sc[3][3], double floor_value,
+                                                 const double* warm = nullptr) {
+  double lam[3], ax[3][3], cov[3][3];
+  const int rc = eig_sym3_floored_simt(sc, floor_value, lam, ax, warm);
+  reconstruct(lam, ax, cov);
+  for (int i = 0; i < 3; ++i) {
+    g.lam[i] = lam[i];
+    g.il[i] = 1.0 / lam[i];
+    for (int j = 0; j < 3; ++j) {
+      g.axT[3 * i + j] = ax[j][i];
+      g.cov[3 * i + j] = cov[i][j];
+    }
+  }
+  g.log_norm = log_norm_of(lam);
+  return rc;
+}
+
+// refresh_eig of a node from cov9 into its DNode fields (written only when
+// `act` and the eigensolve succeeded).
+__device__ __forceinline__ int refresh_node_simt(DNode& d, const double* cov9, bool warm, bool act) {
+  double m[3][3], lam[3], ax[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) m[i][j] = act ? cov9[3 * i + j] : (i == j ? 1.0 : 0.0);
+  double w[9];
+  for (int i = 0; i < 9; ++i) w[i] = act && warm ? d.axT[i] : ((i % 4) == 0 ? 1.0 : 0.0);
+  const int rc = eig_sym3_simt(m, lam, ax, w);
+  if (!act || rc) return act ? rc : kOk;
+  for (int i = 0; i < 3; ++i) {
+    d.lam[i] = lam[i];
+    d.il[i] = 1.0 / lam[i];
+    for (int j = 0; j < 3; ++j) d.axT[3 * i + j] = ax[j][i];
+  }
+  d.log_norm = log_norm_of(lam);
+  const double tr = (lam[0] + lam[1]) + lam[2];
+  d.cplx = tr > 0.0 ? lam[2] / tr : -1.0;
+  return kOk;
+}
+
 }  // namespace trg

@@ -37,7 +37,7 @@ __device__ __forceinline__ unsigned sm_id() {
 // derives the same role table: updaters are the CTAs on the `upd_sms`
 // lowest-numbered SMs present (at least one CTA).  Block-wide; `bar` is
 // the grid barrier of the launch.
-__device__ Roles assign_roles(unsigned* smtab, unsigned* bar, int G, int upd_sms) {
+static __device__ Roles assign_roles(unsigned* smtab, unsigned* bar, int G, int upd_sms) {
   __shared__ unsigned present[8];  // SM bitmap (<= 256 SMs)
   __shared__ int s_cut, s_nu, s_idx;
   const int tid = threadIdx.x;
