@@ -48,8 +48,18 @@ def test_full_size_tree(ctx, name):
         assert np.array_equal(h[k], G[k]), k
     assert _relerr_rows(h["weight"][:, None], G["weight"][:, None]) <= 1e-4
     assert np.abs(h["mean"] - G["mean"]).max() <= 1e-4 * np.abs(G["mean"]).max()
-    assert _relerr_rows(h["cov"], G["cov"]) <= 1e-4
-    assert _relerr_rows(h["lambdas"], G["lambdas"]) <= 1e-4
+    # covariances and eigenvalues within 1e-4 relative, plus the rounding
+    # floor of a scatter formed from raw moments (m2/m0 - mu mu^T): a leaf of
+    # coincident points far from the origin (C3: |mu| ~ 50 m) has a
+    # covariance that IS that noise clamped at the 1e-12 floor in both
+    # implementations (as tests/test_random_sweep_gpu.py)
+    cs = np.linalg.norm(G["cov"].reshape(len(G["cov"]), -1), axis=1)
+    noise = 64 * np.finfo(float).eps * (np.sum(G["mean"] ** 2, axis=1) + cs)
+    dc = np.linalg.norm((h["cov"] - G["cov"]).reshape(len(cs), -1), axis=1)
+    assert np.all(dc <= 1e-4 * cs + noise), np.max(dc / np.maximum(cs, 1e-300))
+    ls = np.linalg.norm(G["lambdas"], axis=1)
+    dl = np.linalg.norm(h["lambdas"] - G["lambdas"], axis=1)
+    assert np.all(dl <= 1e-4 * ls + noise)
 
 
 @pytest.mark.parametrize("name", ["c2_kinect77k_L3", "c3_lidar72k_L3"])
