@@ -162,6 +162,11 @@ uint64_t trg_kernel_launches(trg_ctx* ctx);
 void trg_ctx_transfer_bytes(trg_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 /* CUDA stream (cudaStream_t) all work of this context is ordered on. */
 void* trg_ctx_stream(trg_ctx* ctx);
+/* Orders this context's stream after the work queued so far on `stream`
+ * (a cudaStream_t of the caller, e.g. the one that produced a device cloud
+ * passed with *_on_device = 1).  Device inputs must be complete -- or their
+ * producer's stream handed here -- before a call reads them. */
+int trg_ctx_wait_stream(trg_ctx* ctx, void* stream);
 
 /* ---- model ------------------------------------------------------------ */
 int trg_tree_capacity(int max_level);

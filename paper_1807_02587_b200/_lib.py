@@ -84,6 +84,7 @@ SIGNATURES = {
     "trg_ctx_set_sm_budget": (C.c_int, [C.c_void_p, C.c_int]),
     "trg_kernel_launches": (C.c_uint64, [C.c_void_p]),
     "trg_ctx_stream": (C.c_void_p, [C.c_void_p]),
+    "trg_ctx_wait_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "trg_ctx_transfer_bytes": (None, [C.c_void_p, u64p, u64p]),
     "trg_tree_capacity": (C.c_int, [C.c_int]),
     "trg_tree_upload": (C.c_int, [C.c_void_p, C.POINTER(TreeC), C.POINTER(C.c_void_p)]),

@@ -20,6 +20,7 @@
 //   register_icp_pt2pt      registration.hpp:64-66 -> trg_register_clouds (icp)
 //   build_flat_gmm          gmm.hpp:74-76          -> trg_build_flat_gmm
 //   responsibilities_dense  association.hpp:44-47  -> trg_responsibilities_dense
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -58,20 +59,35 @@ void check(int rc, const char* where) {
   if (rc != TRG_OK) raise(rc, where);
 }
 
-// One context per process (device from TRG_DEVICE, default 0).
+// One context PER THREAD (device from TRG_DEVICE, default 0): a context owns
+// a stream, growable workspaces and pinned buffers, so the reference's free
+// functions -- callable from several threads at once -- must not share one.
+std::atomic<unsigned long long> g_launches{0};  // finished threads' kernel launches
+
+struct CtxHolder {
+  trg_ctx* c = nullptr;
+  ~CtxHolder() {
+    if (!c) return;
+    g_launches += trg_kernel_launches(c);
+    trg_ctx_destroy(c);
+  }
+};
+
 trg_ctx* ctx() {
-  static trg_ctx* c = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  thread_local CtxHolder h;
+  if (!h.c) {
     const char* d = std::getenv("TRG_DEVICE");
-    check(trg_ctx_create(d ? std::atoi(d) : 0, &c), "trg_ctx_create");
-    if (std::getenv("TRG_ADAPTER_REPORT"))
-      std::atexit([] {
-        std::fprintf(stderr, "trg adapter: %llu kernel launches on the B200 path\n",
-                     static_cast<unsigned long long>(trg_kernel_launches(c)));
-      });
-  });
-  return c;
+    check(trg_ctx_create(d ? std::atoi(d) : 0, &h.c), "trg_ctx_create");
+    static std::once_flag once;
+    std::call_once(once, [] {
+      if (std::getenv("TRG_ADAPTER_REPORT"))
+        std::atexit([] {
+          std::fprintf(stderr, "trg adapter: %llu kernel launches on the B200 path\n",
+                       static_cast<unsigned long long>(g_launches.load()));
+        });
+    });
+  }
+  return h.c;
 }
 
 // PointCloud::points is std::vector<Eigen::Vector3d>: 3 contiguous doubles

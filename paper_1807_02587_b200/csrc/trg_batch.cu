@@ -1,7 +1,9 @@
 // trg_register_batch: independent frame pairs (BASELINE config C5) run as
 // concurrent registrations.  Each worker owns an SM-budgeted sub-context
 // (own stream, workspace and scratch tree; persistent grids sized to
-// device_sms / streams SMs, so all workers' grids are co-resident) and pulls
+// device_sms / streams SMs: the budgets sum to the device, so the grids are
+// normally co-resident -- not guaranteed for plain launches, hence the spin
+// guards of trg_internal.cuh, which fail a call instead of hanging) and pulls
 // pair indices from a shared counter.  Host work per pair is launch/staging
 // only; the GPU overlaps one pair's latency-bound phases (grid barriers,
 // eigen-solves, calibration climbs) with the others' E-step tiles.

@@ -163,6 +163,14 @@ cudaError_t set_dynamic_smem(const void* kernel, size_t bytes) {
   return e;
 }
 
+// Whole-device contexts launch cooperatively: the driver guarantees every
+// CTA is resident, which the grid barriers and role handovers need.
+// SM-budgeted worker contexts (trg_register_batch) launch plainly so several
+// run at once; their budgets sum to at most the device's SMs, which makes
+// co-residency LIKELY but not guaranteed (the block scheduler may place a
+// grid's CTAs unevenly).  Every spin-wait therefore carries a 10 s guard
+// (spin_guard, trg_internal.cuh): a grid that cannot become resident traps
+// and the call returns TRG_ECUDA instead of hanging the device.
 cudaError_t launch_persistent(trg_ctx* ctx, const void* kernel, int G, int block, void** args,
                               size_t smem) {
   if (ctx->sms < ctx->device_sms)
@@ -305,6 +313,7 @@ int trg_ctx_destroy(trg_ctx* ctx) {
     cudaEventDestroy(ctx->side_done);
     cudaStreamDestroy(ctx->side);
   }
+  if (ctx->ext_ready) cudaEventDestroy(ctx->ext_ready);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TRG_OK;
@@ -341,6 +350,19 @@ void trg_ctx_transfer_bytes(trg_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
 }
 uint64_t trg_kernel_launches(trg_ctx* ctx) { return ctx->launches; }
 void* trg_ctx_stream(trg_ctx* ctx) { return (void*)ctx->stream; }
+int trg_ctx_wait_stream(trg_ctx* ctx, void* stream) {
+  if (!ctx) {
+    set_error("ctx_wait_stream: null context");
+    return TRG_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (s == ctx->stream) return TRG_OK;
+  TRG_CU(cudaSetDevice(ctx->device));
+  if (!ctx->ext_ready) TRG_CU(cudaEventCreateWithFlags(&ctx->ext_ready, cudaEventDisableTiming));
+  TRG_CU(cudaEventRecord(ctx->ext_ready, s));
+  TRG_CU(cudaStreamWaitEvent(ctx->stream, ctx->ext_ready, 0));
+  return TRG_OK;
+}
 
 int trg_tree_capacity(int max_level) {
   int cap = 0, p = 1;

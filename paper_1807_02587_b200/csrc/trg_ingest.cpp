@@ -178,7 +178,9 @@ void read_ply(const std::string& buf, int want, std::vector<double>& out) {
   if (ax[0] < 0 || ax[1] < 0 || ax[2] < 0) fail("vertex element lacks float x/y/z properties", pos);
   for (const auto& e : elems) {
     const bool is_vx = &e == vx;
-    if (is_vx) out.reserve(3 * e.count);
+    // a hostile header may claim any count: reserve no more than the rest of
+    // the buffer could possibly hold (>= 1 byte per value)
+    if (is_vx) out.reserve(3 * std::min<size_t>(e.count, buf.size() - std::min(buf.size(), pos)));
     for (size_t r = 0; r < e.count; ++r) {
       const size_t row_at = pos;
       double xyz[3] = {0.0, 0.0, 0.0};
@@ -258,6 +260,9 @@ int trg_read_cloud(const char* path, int format, double** xyz, size_t* n) {
   } catch (const Fail& f) {
     trg::set_error(std::string(path) + ": " + f.what + " (byte " + std::to_string(f.offset) + ")");
     return TRG_ERUNTIME;  // ParseError is a std::runtime_error (cloud_io.hpp:18)
+  } catch (const std::exception& e) {  // e.g. bad_alloc / length_error: never escape the C-ABI
+    trg::set_error(std::string(path) + ": " + e.what());
+    return TRG_ERUNTIME;
   }
   *n = pts.size() / 3;
   *xyz = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(pts.size(), 1)));

@@ -84,6 +84,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Spin-wait guard: a wait that exceeds 10 s can only be a grid whose CTAs
+// are not all resident (e.g. SM-budgeted batch workers sharing the device):
+// trap (the launch fails with an error the host reports) instead of hanging.
+__device__ __forceinline__ void spin_guard(unsigned long long t0) {
+  if (gtimer() - t0 > 10000000000ull) __trap();
+}
 __device__ __forceinline__ void tl_mark_any(Timeline* tl, int label) {
   const int i = atomicAdd(&tl->n, 1);
   if (i < 1024) {
@@ -112,6 +118,7 @@ struct trg_ctx {
   bool own_stream = true;         // false: a shard context on its parent's stream
   cudaStream_t side = nullptr;    // copy stream: a pinned source cloud's H2D under the build
   cudaEvent_t side_done = nullptr;
+  cudaEvent_t ext_ready = nullptr;  // trg_ctx_wait_stream
   static constexpr int kSlots = 32;
   void* slot_ptr[kSlots] = {};
   size_t slot_size[kSlots] = {};
@@ -241,7 +248,8 @@ cudaError_t set_dynamic_smem(const void* kernel, size_t bytes);
 // Whole-device contexts use a cooperative launch (co-residency checked by
 // the driver).  SM-budgeted contexts (trg_ctx_set_sm_budget) use a plain
 // launch so several contexts' persistent kernels run concurrently: their
-// budgets sum to at most the device's SMs, so every grid stays co-resident.
+// budgets sum to at most the device's SMs, which makes co-residency likely
+// but not guaranteed -- every spin-wait is guarded (spin_guard).
 cudaError_t launch_persistent(trg_ctx* ctx, const void* kernel, int G, int block, void** args,
                               size_t smem = 0);
 

@@ -100,9 +100,11 @@ __device__ __forceinline__ void wait_flag(const unsigned* flag, unsigned s) {
   if (threadIdx.x == 0) {
     volatile const unsigned* f = flag;
     unsigned ns = 32;
+    const unsigned long long t0 = gtimer();
     while (*f < s) {
       __nanosleep(ns);
       ns = ns < 128 ? 2 * ns : 128;
+      spin_guard(t0);
     }
     __threadfence();
   }
@@ -114,7 +116,11 @@ __device__ __forceinline__ void wait_count(const unsigned* cnt, unsigned target)
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile const unsigned* f = cnt;
-    while (*f < target) __nanosleep(32);
+    const unsigned long long t0 = gtimer();
+    while (*f < target) {
+      __nanosleep(32);
+      spin_guard(t0);
+    }
     __threadfence();
   }
   __syncthreads();

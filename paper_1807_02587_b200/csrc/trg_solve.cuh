@@ -26,9 +26,11 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks) {
       // back off (32 ns doubling to 256 ns): a spinning CTA steals issue
       // slots from the SM's working CTAs during long tile passes
       unsigned ns = 32;
+      const unsigned long long t0 = gtimer();
       while (vb[1] == gen) {
         __nanosleep(ns);
         ns = ns < 256 ? 2 * ns : 256;
+        spin_guard(t0);
       }
     }
     __threadfence();

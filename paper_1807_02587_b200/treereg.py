@@ -241,13 +241,18 @@ def _points(cloud) -> np.ndarray:
     return p
 
 
-def _cloud_ptr(cloud):
-    """(pointer, n, on_device) for a numpy (host) or torch CUDA tensor."""
+def _cloud_ptr(cloud, ctx):
+    """(pointer, n, on_device) for a numpy (host) or torch CUDA tensor.  A
+    CUDA tensor may still be in production on torch's current stream: the
+    context's stream waits for it (trg_ctx_wait_stream) before any kernel of
+    the call reads it."""
     if hasattr(cloud, "is_cuda") and cloud.is_cuda:
         if cloud.dtype.__str__() != "torch.float64" or cloud.dim() != 2 or cloud.shape[1] != 3:
             raise InvalidArgument("device point cloud must be a contiguous (N, 3) float64 tensor")
         if not cloud.is_contiguous():
             raise InvalidArgument("device point cloud must be contiguous")
+        import torch
+        _chk(_lib.lib().trg_ctx_wait_stream(ctx.h, C.c_void_p(torch.cuda.current_stream(cloud.device).cuda_stream)))
         return C.c_void_p(cloud.data_ptr()), int(cloud.shape[0]), 1, cloud
     p = _points(cloud)
     return p.ctypes.data_as(C.c_void_p), len(p), 0, p
@@ -383,7 +388,7 @@ def build_tree(cloud, config: ModelConfig = ModelConfig(),
                ctx: Context | None = None) -> GmmTree:
     """gmm.hpp:69-70 build_tree, on the GPU."""
     ctx = ctx or default_context()
-    ptr, n, on_dev, _keep = _cloud_ptr(cloud)
+    ptr, n, on_dev, _keep = _cloud_ptr(cloud, ctx)
     cfg = config.c()
     h = C.c_void_p()
     d = BuildDiagC()
@@ -426,7 +431,7 @@ def associate_adaptive(cloud, tree: GmmTree, t: RigidTransform = None,
     """association.hpp:54-56 associate_adaptive on the GPU.  With
     ``per_point`` also returns each point's (deposit node, path weight)."""
     t = t or RigidTransform.identity()
-    ptr, n, on_dev, _keep = _cloud_ptr(cloud)
+    ptr, n, on_dev, _keep = _cloud_ptr(cloud, tree.ctx)
     J = tree.size()
     m0, m1 = np.zeros(J), np.zeros((J, 3))
     m2 = np.zeros((J, 3, 3)) if with_m2 else None
@@ -448,9 +453,21 @@ def associate_adaptive(cloud, tree: GmmTree, t: RigidTransform = None,
 
 # ------------------------------------------------------------------ M-step
 @dataclass
-class VirtualPointSet:  # mstep.hpp:27-32 (moments + the model they refer to)
+class VirtualPointSet:  # mstep.hpp:21-32
+    """The virtual points make_virtual_points produced on the device: per
+    point pi* and mu* and the index of its component in ``tree`` (the
+    reference's VirtualPoint::component), plus the moments they came from."""
     moments: MomentSet
     tree: GmmTree
+    index: np.ndarray = None    # [n] component (node) index
+    pi_star: np.ndarray = None  # [n]
+    mu_star: np.ndarray = None  # [n, 3]
+
+    def size(self) -> int:
+        return 0 if self.index is None else len(self.index)
+
+    def empty(self) -> bool:
+        return self.size() == 0
 
 
 @dataclass
@@ -465,13 +482,24 @@ class MStepSolution:  # mstep.hpp:54-61
 
 
 def make_virtual_points(moments: MomentSet, tree: GmmTree) -> VirtualPointSet:
-    """mstep.hpp:46-47.  The filter (m0 > 1e-8 N, pi* = m0/N, mu* = m1/m0)
-    runs on the device inside solve_mstep; validation mirrors mstep.cpp:11-17."""
+    """mstep.hpp:46-47 on the GPU (trg_make_virtual_points, k_make_vps): the
+    order-preserving filter m0 > 1e-8 N with pi* = m0 / N, mu* = m1 / m0
+    (mstep.cpp:8-30); validation mirrors mstep.cpp:11-17."""
     if moments.components() != tree.size():
         raise InvalidArgument("make_virtual_points: moment/component count mismatch")
     if moments.total_points == 0:
         raise InvalidArgument("make_virtual_points: no points were associated")
-    return VirtualPointSet(moments, tree)
+    J = moments.components()
+    m0 = np.ascontiguousarray(moments.m0, dtype=np.float64)
+    m1 = np.ascontiguousarray(moments.m1, dtype=np.float64)
+    idx = np.zeros(J, np.int32)
+    pi = np.zeros(J)
+    mu = np.zeros((J, 3))
+    n = C.c_int(0)
+    _chk(_lib.lib().trg_make_virtual_points(tree.ctx.h, J, _d(m0), _d(m1), int(moments.total_points),
+                                            idx.ctypes.data_as(_lib.ip), _d(pi), _d(mu), C.byref(n)))
+    k = int(n.value)
+    return VirtualPointSet(moments, tree, idx[:k].copy(), pi[:k].copy(), mu[:k].copy())
 
 
 def solve_mstep(vps: VirtualPointSet) -> MStepSolution:
@@ -523,7 +551,7 @@ def _result_buffers(cfg: RegistrationConfig):
 def register_with_tree(tree: GmmTree, source, config: RegistrationConfig = RegistrationConfig(),
                        target_diag: float = 0.0) -> RegistrationResult:
     """registration.hpp:59-62, EM loop resident on the GPU."""
-    ptr, n, on_dev, _keep = _cloud_ptr(source)
+    ptr, n, on_dev, _keep = _cloud_ptr(source, tree.ctx)
     r, cb, ca, ev = _result_buffers(config)
     cfg = config.c()
     _chk(_lib.lib().trg_register_with_tree(tree.ctx.h, tree.h, ptr, n, on_dev, C.byref(cfg),
@@ -535,8 +563,8 @@ def register_clouds(target, source, config: RegistrationConfig = RegistrationCon
                     ctx: Context | None = None) -> RegistrationResult:
     """registration.hpp:53-55 (adaptive:L / tree:L): build + EM on the GPU."""
     ctx = ctx or default_context()
-    pt, nt, dev_t, _k1 = _cloud_ptr(target)
-    ps, ns, dev_s, _k2 = _cloud_ptr(source)
+    pt, nt, dev_t, _k1 = _cloud_ptr(target, ctx)
+    ps, ns, dev_s, _k2 = _cloud_ptr(source, ctx)
     if dev_t != dev_s:
         raise InvalidArgument("register_clouds: target and source must live on the same side")
     r, cb, ca, ev = _result_buffers(config)
@@ -559,8 +587,8 @@ def register_batch(targets, sources, config: RegistrationConfig = RegistrationCo
     tp, tn = (C.c_void_p * max(1, n))(), (C.c_size_t * max(1, n))()
     sp, sn = (C.c_void_p * max(1, n))(), (C.c_size_t * max(1, n))()
     for i in range(n):
-        pt, nt, dt, k1 = _cloud_ptr(targets[i])
-        ps, ns, ds, k2 = _cloud_ptr(sources[i])
+        pt, nt, dt, k1 = _cloud_ptr(targets[i], ctx)
+        ps, ns, ds, k2 = _cloud_ptr(sources[i], ctx)
         keep += [k1, k2]
         sides |= {dt, ds}
         tp[i], tn[i], sp[i], sn[i] = pt.value, nt, ps.value, ns
@@ -600,7 +628,7 @@ def build_flat_gmm(cloud, j: int, config: ModelConfig = ModelConfig(),
     """gmm.hpp:74-76 build_flat_gmm on the GPU: the J components come back as
     a depth-1 GmmTree of J roots (``.host()`` gives the component arrays)."""
     ctx = ctx or default_context()
-    ptr, n, on_dev, _keep = _cloud_ptr(cloud)
+    ptr, n, on_dev, _keep = _cloud_ptr(cloud, ctx)
     cfg = config.c()
     h = C.c_void_p()
     d = BuildDiagC()
@@ -616,7 +644,7 @@ def responsibilities_dense(cloud, components: GmmTree, t: "RigidTransform" = Non
     """association.hpp:44-47 responsibilities_dense: every node of
     `components` (a flat mixture or any tree's nodes) against every point."""
     t = t or RigidTransform.identity()
-    ptr, n, on_dev, _keep = _cloud_ptr(cloud)
+    ptr, n, on_dev, _keep = _cloud_ptr(cloud, components.ctx)
     J = components.size()
     m0, m1 = np.zeros(J), np.zeros((J, 3))
     m2 = np.zeros((J, 3, 3)) if with_m2 else None
@@ -720,7 +748,7 @@ def _shard_arrays(clouds, comm: Comm):
     ptr = (C.c_void_p * len(clouds))()
     cnt = (C.c_size_t * len(clouds))()
     for i, c in enumerate(clouds):
-        p, n, d, k = _cloud_ptr(c)
+        p, n, d, k = _cloud_ptr(c, comm.ctx)
         keep.append(k)
         sides.add(d)
         ptr[i], cnt[i] = p.value, n

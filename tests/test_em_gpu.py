@@ -32,6 +32,24 @@ def test_solve_mstep_matches_reference(ctx, name):
     assert np.abs(sol.delta.rotation - g["solve_R"]).max() <= 1e-9
 
 
+@pytest.mark.parametrize("name", golden_names())
+def test_make_virtual_points_on_device(ctx, name):
+    """make_virtual_points (mstep.cpp:8-30) on the GPU: the order-preserving
+    m0 > 1e-8 N filter, pi* = m0 / N and mu* = m1 / m0 (IEEE divisions:
+    bit-exact)."""
+    tr = _tr()
+    g = load_golden(name)
+    tree = tr.GmmTree.from_host(g["tree"], ctx)
+    N = int(g["lc001_counts"][0])
+    m0, m1 = np.asarray(g["lc001_m0"]), np.asarray(g["lc001_m1"]).reshape(-1, 3)
+    vps = tr.make_virtual_points(tr.MomentSet(m0, m1, None, N), tree)
+    keep = np.nonzero(m0 > 1e-8 * N)[0]
+    assert np.array_equal(vps.index, keep)
+    assert np.array_equal(vps.pi_star, m0[keep] / N)
+    assert np.array_equal(vps.mu_star, m1[keep] / m0[keep][:, None])
+    assert vps.size() == int(g["solve_scalars"][3])
+
+
 def test_solve_mstep_degenerate(ctx):
     tr = _tr()
     g = load_golden("blobs1k_L2")
