@@ -14,7 +14,10 @@ on the source), as the paper times it.
            region (host wall clock around each synchronous call).
 * N > 1  : one process per GPU (torchrun), every rank registers its own copy of
            the C2 pair (independent pairs shard with no collective), weak
-           scaling; value = N*K / max-over-ranks time.
+           scaling; value = N*K / max-over-ranks time.  The `c4` item is the
+           1M-point scene point-sharded over the N ranks (NCCL all-reduces of
+           the per-node records each exchange step; strong scaling).
+* configs: the C1 and C3 pairs beside the headline (N = 1).
 * --impl reference: the reference's own CPU implementation (oracle/_ref =
            /root/reference sources built with the test shims) on the host's
            cores, same workload and metric; rank 0 only.
@@ -109,6 +112,13 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
+def config_dict(wl: str, world: int):
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": wl, "pairs_per_rank_per_step": 1,
+            "l2": "GPU arm: flushed (256 MB write) before every timed step; CPU arm: n/a",
+            "parallelism": f"independent pairs, one per rank per step, x{world} ranks, no collectives"}
+
+
 def algorithmic_bytes(diag, n_target: int, n_source: int, J: int, em_iters: int):
     """FP64 (s = 8), entry = idx 4 B + w 8 B + point 24 B.
     Build: per round 36 passes over E_l entries + the partition write of
@@ -175,7 +185,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": wl, "l2": "inputs 3.7 MB < L2; CPU run"},
+        "data": "synthetic", "config": config_dict(wl, args.gpus),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"{args.steps} full registrations (build+EM) of the {args.config.upper()} pair"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -271,9 +281,7 @@ def run_b200(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl, "pairs_per_rank_per_step": 1,
-                   "l2": "flushed (256 MB write) before every timed step",
-                   "parallelism": f"batch-sharded pairs x{world}, no collectives"},
+        "config": config_dict(wl, world),
         "tree_build_mpoints_per_s": world * len(tg) / t_build / 1e6,
         "phase_ms": {"build": 1e3 * t_build, "em": 1e3 * t_em,
                      "em_iterations": res.iterations, "converged": res.converged},
@@ -292,8 +300,13 @@ def run_b200(args):
     }
     if args.batch > 0:
         out["batched"] = run_batched(args, tr, ctx, cfg, dist, dev, world)
-    if args.c4 and (world == 1 or os.environ.get("TRG_BENCH_C4_SHARDED") == "1"):
-        out["c4"] = run_c4(args, tr, ctx, dist, dev, world)
+    if args.c4:
+        try:
+            out["c4"] = run_c4(args, tr, ctx, dist, dev, world)
+        except Exception as e:  # the headline line must survive a failing side item
+            out["c4"] = {"error": f"{type(e).__name__}: {e}"}
+    if args.extra and world == 1:
+        out["configs"] = {c: run_small(tr, ctx, dev, c, args.steps) for c in ("c1", "c3") if c != args.config}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.config)
     if rank == 0:
@@ -306,10 +319,12 @@ def run_b200(args):
 def run_c4(args, tr, ctx, dist, dev, world):
     """BASELINE C4: synthetic_scene(1M, seed 4), depth-4 tree, pose
     random_rigid_transform({8 deg, 0.03, seed 4}).  One GPU: the single-launch
-    path.  N GPUs (opt-in, TRG_BENCH_C4_SHARDED=1): every rank holds a
-    contiguous 1/N block of both clouds and runs the point-sharded path
-    (per-node records all-reduced over NCCL); the value is registrations of
-    the whole cloud per second (strong scaling)."""
+    path.  N GPUs: every rank holds a contiguous 1/N block of both clouds and
+    runs the point-sharded path (per-node records, leaf and EM moments
+    all-reduced over NCCL each exchange step); the value is registrations of
+    the whole cloud per second (strong scaling).  `parity`: the transform
+    against the reference's own register_clouds on this pose
+    (tests/golden/c4_scene1M_L4.npz), 1e-4 rad / 1e-4 x extent."""
     import torch
     pts = tr.synthetic("scene", 1_000_000, 4)
     T = tr.random_rigid_transform(8.0, 0.03, 4)
@@ -336,9 +351,19 @@ def run_c4(args, tr, ctx, dist, dev, world):
         res = step()
         builds.append(res.model_build_seconds)
     torch.cuda.synchronize()
-    dt = max_over_ranks(time.perf_counter() - t0, dist, dev)
+    dt_all = max_over_ranks(time.perf_counter() - t0, dist, dev)
     ang = float(np.degrees(np.arccos(np.clip((np.trace(res.transform.rotation.T @ T.rotation) - 1) / 2,
                                              -1, 1))))
+    parity = None
+    try:
+        z = np.load(os.path.join(ROOT, "tests", "golden", "c4_scene1M_L4.npz"))
+        ext = float(np.linalg.norm(pts.max(0) - pts.min(0)))
+        dr = float(np.arccos(np.clip((np.trace(res.transform.rotation.T @ z["rc_R"]) - 1) / 2, -1, 1)))
+        dt = float(np.linalg.norm(res.transform.translation - z["rc_t"]))
+        parity = {"vs": "reference register_clouds (golden)", "rot_rad": dr, "trans": dt,
+                  "ok": bool(dr <= 1e-4 and dt <= 1e-4 * ext and res.iterations == int(z["rc_meta"][0]))}
+    except Exception as e:  # fixture missing: report, don't fail
+        parity = {"vs": "unavailable", "error": str(e)}
     roof = None
     if world == 1:  # the HBM fraction is meaningful at C4 (entries exceed L2)
         diag = tr.BuildDiagnostics()
@@ -354,11 +379,11 @@ def run_c4(args, tr, ctx, dist, dev, world):
     return {"workload": "C4 synthetic_scene(1M, seed 4), adaptive:4" +
                         (f", point-sharded over {world} GPUs (NCCL)" if world > 1 else ", one GPU"),
             "scaling": "strong" if world > 1 else None,
-            "value": reps / dt, "unit": UNIT, "ms_per_registration": 1e3 * dt / reps,
+            "value": reps / dt_all, "unit": UNIT, "ms_per_registration": 1e3 * dt_all / reps,
             "timing": "host wall clock around synchronous registrations, max over ranks",
             "tree_build_mpoints_per_s": len(pts) / float(np.median(builds)) / 1e6,
             "em_iterations": res.iterations, "converged": res.converged,
-            "rot_err_deg_vs_gt": ang, "roofline": roof,
+            "rot_err_deg_vs_gt": ang, "parity": parity, "roofline": roof, "ranks": world,
             "note": "the reference's own register_clouds does not converge on this pose either "
                     "(50 iterations, same answer: tests/test_c4_gpu.py)"}
 
@@ -392,18 +417,23 @@ def run_batched(args, tr, ctx, cfg, dist, dev, world):
             "converged": sum(r.converged for r in res), "median_rot_err_deg_vs_gt": float(np.median(errs))}
 
 
-def cpu_baseline(cfg_name):
-    """The reference implementation (oracle/_ref) on this host's cores, one
-    full registration of the same pair (a bounded ~5-10 s sample)."""
+def cpu_baseline(cfg_name, samples: int = 5):
+    """The reference implementation (oracle/_ref) on this host's cores: one
+    warm-up registration of the same pair, then the median of `samples`
+    timed ones (a bounded ~10 s sample), plus one serial (1-thread) run."""
     try:
         from oracle.oracle import Ref
         tg, sr, gt, L, wl = workload(cfg_name)
         ref = Ref()
         cores = os.cpu_count() or 1
         ref.set_threads(cores)
-        t0 = time.perf_counter()
-        ref.register_clouds(tg, sr, level=L)
-        dt = time.perf_counter() - t0
+        ref.register_clouds(tg, sr, level=L)  # warm-up
+        ts = []
+        for _ in range(samples):
+            t0 = time.perf_counter()
+            ref.register_clouds(tg, sr, level=L)
+            ts.append(time.perf_counter() - t0)
+        dt = float(np.median(ts))
         # SURVEY 8d: the reference's serial run beside the all-cores one
         ref.set_threads(1)
         t0 = time.perf_counter()
@@ -411,13 +441,44 @@ def cpu_baseline(cfg_name):
         dt1 = time.perf_counter() - t0
         ref.set_threads(cores)
         return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "reference",
-                "sample": f"1 full registration (build+EM) of the {cfg_name.upper()} pair, "
-                          f"{cores} threads, {dt:.2f} s",
+                "sample": f"median of {samples} full registrations (build+EM) of the {cfg_name.upper()} "
+                          f"pair after 1 warm-up, {cores} threads: {dt:.3f} s "
+                          f"(min {min(ts):.3f}, max {max(ts):.3f})",
                 "serial": {"value": 1.0 / dt1, "unit": UNIT, "cores": 1,
                            "sample": f"the same registration on 1 thread, {dt1:.2f} s"}}
     except Exception as e:  # the oracle build is test infrastructure; report, don't fail
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                 "sample": f"unavailable: {e}"}
+
+
+def run_small(tr, ctx, dev, cfg_name, steps):
+    """BASELINE configs[0] (C1) / [2] (C3) beside the headline: device-resident
+    registrations, CUDA events on the library's stream, L2 flushed per step."""
+    import torch
+    tg, sr, gt, L, wl = workload(cfg_name)
+    cfg = tr.RegistrationConfig(variant=tr.Variant("adaptive", L))
+    tg_d = torch.from_numpy(tg).to(dev).contiguous()
+    sr_d = torch.from_numpy(sr).to(dev).contiguous()
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        res = tr.register_clouds(tg_d, sr_d, cfg, ctx)
+    ms, bs = [], []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = tr.register_clouds(tg_d, sr_d, cfg, ctx)
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        bs.append(res.model_build_seconds)
+    ang = float(np.degrees(np.arccos(np.clip((np.trace(res.transform.rotation.T @ gt.rotation) - 1) / 2, -1, 1))))
+    return {"workload": wl, "value": 1e3 * steps / sum(ms), "unit": UNIT,
+            "ms_per_step": sum(ms) / steps, "build_ms": 1e3 * float(np.median(bs)),
+            "em_iterations": res.iterations, "converged": res.converged, "rot_err_deg_vs_gt": ang}
 
 
 def main():
@@ -430,7 +491,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=32, help="C5 slice: pairs per rank (0 = skip)")
     ap.add_argument("--streams", type=int, default=4, help="concurrent registrations per GPU")
-    ap.add_argument("--c4", type=int, default=1, help="add the C4 (1M points, depth 4) line item")
+    ap.add_argument("--c4", type=int, default=1, help="add the C4 (1M points, depth 4) line item "
+                    "(point-sharded over NCCL when N > 1)")
+    ap.add_argument("--extra", type=int, default=1, help="add the C1 and C3 line items (N = 1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -10,9 +10,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# TRG_LIB_VARIANT=<name> loads libtrg_cuda_<name>.so (A/B experiments only)
-LIB_PATH = os.path.join(HERE, "libtrg_cuda.so" if not os.environ.get("TRG_LIB_VARIANT")
-                        else f"libtrg_cuda_{os.environ['TRG_LIB_VARIANT']}.so")
+LIB_PATH = os.path.join(HERE, "libtrg_cuda.so")
+# host-only companion (include/treereg_b200_host.h): ingest + synthetic inputs
+HOST_LIB_PATH = os.path.join(HERE, "libtrg_host.so")
 
 dp = C.POINTER(C.c_double)
 ip = C.POINTER(C.c_int)
@@ -132,6 +132,13 @@ SIGNATURES = {
     "trg_register_clouds": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                       C.c_size_t, C.c_int, C.POINTER(RegConfigC),
                                       C.POINTER(RegResultC)]),
+    "trg_debug_build_timeline": (C.c_int, [C.c_void_p, u64p, ip, C.c_int]),
+    "trg_debug_solve": (C.c_int, [C.c_void_p, dp, C.c_int, dp]),
+    "trg_debug_eig": (C.c_int, [C.c_void_p, C.c_int, dp, C.c_int, dp, dp, ip]),
+}
+
+HOST_SIGNATURES = {
+    "trg_host_last_error": (C.c_char_p, []),
     "trg_synthetic": (C.c_int, [C.c_char_p, C.c_size_t, C.c_uint64, dp]),
     "trg_unit_normalize": (C.c_int, [dp, C.c_size_t]),
     "trg_bbox_diagonal": (C.c_double, [dp, C.c_size_t]),
@@ -145,9 +152,6 @@ SIGNATURES = {
     "trg_synth_kinect_pair_ex": (C.c_int, [C.c_uint64, C.c_double, C.c_double, C.c_double, dp, dp,
                                            dp, dp]),
     "trg_synth_lidar_pair": (C.c_int, [C.c_uint64, dp, dp, dp, dp]),
-    "trg_debug_build_timeline": (C.c_int, [C.c_void_p, u64p, ip, C.c_int]),
-    "trg_debug_solve": (C.c_int, [C.c_void_p, dp, C.c_int, dp]),
-    "trg_debug_eig": (C.c_int, [C.c_void_p, C.c_int, dp, C.c_int, dp, dp, ip]),
 }
 
 _LIB = None
@@ -172,3 +176,25 @@ def lib():
 
 def last_error() -> str:
     return lib().trg_last_error().decode(errors="replace")
+
+
+_HOST = None
+
+
+def host_lib():
+    """Load libtrg_host.so (no device code) once."""
+    global _HOST
+    if _HOST is None:
+        if not os.path.exists(HOST_LIB_PATH):
+            raise ImportError(f"{HOST_LIB_PATH} is not built (run `make -C {HERE}`)")
+        L = C.CDLL(HOST_LIB_PATH)
+        for name, (res, args) in HOST_SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _HOST = L
+    return _HOST
+
+
+def host_last_error() -> str:
+    return host_lib().trg_host_last_error().decode(errors="replace")

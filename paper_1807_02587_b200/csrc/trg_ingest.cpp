@@ -17,11 +17,16 @@
 #include <string>
 #include <vector>
 
-#include "../../include/treereg_b200.h"
+#include "../../include/treereg_b200.h"  // status codes
+#include "../../include/treereg_b200_host.h"
 
 namespace trg {
-void set_error(const std::string& msg);
-}
+// the host library's own last-error message (trg_host_last_error)
+thread_local std::string g_host_error;
+static void set_error(const std::string& msg) { g_host_error = msg; }
+}  // namespace trg
+
+extern "C" const char* trg_host_last_error(void) { return trg::g_host_error.c_str(); }
 
 namespace {
 

@@ -20,7 +20,8 @@
 #include <string>
 #include <vector>
 
-#include "../../include/treereg_b200.h"
+#include "../../include/treereg_b200.h"  // status codes
+#include "../../include/treereg_b200_host.h"
 
 namespace {
 

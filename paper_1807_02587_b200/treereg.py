@@ -41,8 +41,8 @@ class CudaError(RuntimeError):
     pass
 
 
-def _raise(rc: int):
-    msg = _lib.last_error()
+def _raise(rc: int, host: bool = False):
+    msg = _lib.host_last_error() if host else _lib.last_error()
     if rc == _lib.TRG_EINVAL:
         raise InvalidArgument(msg)
     if rc == _lib.TRG_EDOMAIN:
@@ -59,6 +59,11 @@ def _raise(rc: int):
 def _chk(rc: int):
     if rc != 0:
         _raise(rc)
+
+
+def _chk_host(rc: int):
+    if rc != 0:
+        _raise(rc, host=True)
 
 
 def _d(a: np.ndarray):
@@ -796,44 +801,44 @@ def read_cloud(path, fmt: str = "auto") -> np.ndarray:
     code = {"auto": 0, "ply_ascii": 1, "ply_binary": 2, "xyz": 3}[fmt]
     p = dp()
     n = C.c_size_t()
-    _chk(_lib.lib().trg_read_cloud(str(path).encode(), code, C.byref(p), C.byref(n)))
+    _chk_host(_lib.host_lib().trg_read_cloud(str(path).encode(), code, C.byref(p), C.byref(n)))
     try:
         return np.ctypeslib.as_array(p, shape=(n.value * 3,)).reshape(n.value, 3).copy() \
             if n.value else np.zeros((0, 3))
     finally:
-        _lib.lib().trg_free_cloud(p)
+        _lib.host_lib().trg_free_cloud(p)
 
 
 def subsample(cloud, n: int, seed: int) -> np.ndarray:
     """cloud_io subsample: n points in index order, reference-identical picks."""
     p = _points(cloud)
     out = np.zeros((int(n), 3))
-    _chk(_lib.lib().trg_subsample(_d(p), len(p), int(n), seed, _d(out)))
+    _chk_host(_lib.host_lib().trg_subsample(_d(p), len(p), int(n), seed, _d(out)))
     return out
 
 
 def synthetic(kind: str, n: int, seed: int) -> np.ndarray:
     """synthetic.cpp generators (bit-identical restatement)."""
     out = np.zeros((n, 3))
-    _chk(_lib.lib().trg_synthetic(kind.encode(), n, seed, _d(out)))
+    _chk_host(_lib.host_lib().trg_synthetic(kind.encode(), n, seed, _d(out)))
     return out
 
 
 def unit_normalized(cloud) -> np.ndarray:
     p = _points(cloud).copy()
-    _chk(_lib.lib().trg_unit_normalize(_d(p), len(p)))
+    _chk_host(_lib.host_lib().trg_unit_normalize(_d(p), len(p)))
     return p
 
 
 def bbox_diagonal(cloud) -> float:
     p = _points(cloud)
-    return float(_lib.lib().trg_bbox_diagonal(_d(p), len(p)))
+    return float(_lib.host_lib().trg_bbox_diagonal(_d(p), len(p)))
 
 
 def random_rigid_transform(rot_range_deg: float, trans_range: float, seed: int,
                            trial: int = 0) -> RigidTransform:
     R, t = np.zeros((3, 3)), np.zeros(3)
-    _chk(_lib.lib().trg_random_rigid_transform(rot_range_deg, trans_range, seed, trial, _d(R),
+    _chk_host(_lib.host_lib().trg_random_rigid_transform(rot_range_deg, trans_range, seed, trial, _d(R),
                                                _d(t)))
     return RigidTransform(R, t)
 
@@ -841,7 +846,7 @@ def random_rigid_transform(rot_range_deg: float, trans_range: float, seed: int,
 def kinect_pair(seed: int):
     """C2: 320x240 Kinect-style frame pair -> (target, source, gt source->target)."""
     tg, sr, R, t = np.zeros((76800, 3)), np.zeros((76800, 3)), np.zeros((3, 3)), np.zeros(3)
-    _chk(_lib.lib().trg_synth_kinect_pair(seed, _d(tg), _d(sr), _d(R), _d(t)))
+    _chk_host(_lib.host_lib().trg_synth_kinect_pair(seed, _d(tg), _d(sr), _d(R), _d(t)))
     return tg, sr, RigidTransform(R, t)
 
 
@@ -850,7 +855,7 @@ def kinect_sequence(seed: int, frames: int, step_rot_deg: float = 2.0, step_tran
     mapping frame k into frame 0)."""
     out = np.zeros((frames, 76800, 3))
     R, t = np.zeros((frames, 3, 3)), np.zeros((frames, 3))
-    _chk(_lib.lib().trg_synth_kinect_sequence(seed, frames, step_rot_deg, step_trans, _d(out), _d(R),
+    _chk_host(_lib.host_lib().trg_synth_kinect_sequence(seed, frames, step_rot_deg, step_trans, _d(out), _d(R),
                                               _d(t)))
     return out, [RigidTransform(R[k], t[k]) for k in range(frames)]
 
@@ -858,5 +863,5 @@ def kinect_sequence(seed: int, frames: int, step_rot_deg: float = 2.0, step_tran
 def lidar_pair(seed: int):
     """C3: HDL-32-style sweep pair -> (target, source, gt source->target)."""
     tg, sr, R, t = np.zeros((72000, 3)), np.zeros((72000, 3)), np.zeros((3, 3)), np.zeros(3)
-    _chk(_lib.lib().trg_synth_lidar_pair(seed, _d(tg), _d(sr), _d(R), _d(t)))
+    _chk_host(_lib.host_lib().trg_synth_lidar_pair(seed, _d(tg), _d(sr), _d(R), _d(t)))
     return tg, sr, RigidTransform(R, t)

@@ -9,8 +9,8 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    src = open(os.path.join(ROOT, "include", "treereg_b200.h")).read()
+def declared_symbols(header="treereg_b200.h"):
+    src = open(os.path.join(ROOT, "include", header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(trg_[a-z0-9_]+)\s*\(", src)))
 
@@ -28,6 +28,19 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in declared_symbols() if not hasattr(L, s)]
     assert not missing, missing
     assert set(declared_symbols()) == set(_lib.SIGNATURES)
+
+
+def test_host_library_exports_its_header():
+    """libtrg_host.so (ingest + synthetic inputs, no device code) exports
+    exactly include/treereg_b200_host.h; the product library does not carry
+    those host ports."""
+    from paper_1807_02587_b200 import _lib
+    H = ctypes.CDLL(_lib.HOST_LIB_PATH)
+    host = declared_symbols("treereg_b200_host.h")
+    assert host and not [s for s in host if not hasattr(H, s)]
+    assert set(host) == set(_lib.HOST_SIGNATURES)
+    P = ctypes.CDLL(_lib.LIB_PATH)
+    assert not [s for s in host if s != "trg_host_last_error" and hasattr(P, s)]
 
 
 def test_no_cpu_fallback_without_gpu():
