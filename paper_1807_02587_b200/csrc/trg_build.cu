@@ -138,6 +138,7 @@ struct BuildParams {
   double* xcal;       // [capacity][10] calibration leaf moments (exchanged)
 };
 
+
 // ----------------------------------------------------------------- helpers
 
 __device__ __forceinline__ void comp_to_regs(const GComp& c, double r[18]) {
@@ -496,38 +497,76 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
 }
 
 // ----------------------------------------------------------------- node work
-// M-step for candidate c of node k (thread `comp` of the last arriver).
-__device__ void node_mstep(const BuildParams& p, int k, int c, const double* red, int comp) {
-  GComp* comps = p.nf.comps + ((size_t)k * 2 + c) * 8;
+#ifdef TRG_RP_PROBE
+#define UPROBE(lab) if (k == 0 && (threadIdx.x & 31) == 0) tl_mark_any(p.tl, lab)
+#else
+#define UPROBE(lab)
+#endif
+// M-steps of node k (m_step gmm.cpp:208-232), the whole warp: lane
+// 8 c + j fits component j of candidate c (when candidate c ran an EM
+// iteration this phase).  The eigensolves are warp-uniform (SIMT Jacobi,
+// bit-identical per lane to the scalar solver): divergent per-lane solves
+// serialise.  All 32 lanes must call.
+__device__ void node_mstep_warp(const BuildParams& p, const Phase& ph, int k, const double* red) {
+  const int lane = threadIdx.x & 31;
+  const int c = (lane >> 3) & 1, comp = lane & 7;
+  bool act = lane < 16 && ph.mode[c] == 1;
+  GComp& g = p.nf.comps[((size_t)k * 2 + c) * 8 + comp];
   const double* ac = red + kOffEm + c * 81;
-  double total = 0.0;
-  for (int j = 0; j < 8; ++j) total += __ldcg(ac + j * 10);
-  if (!(total > 0.0)) {
-    atomicCAS(p.status, 0, kERuntime);  // m_step: no responsibility mass
+  double total = 0.0, a[10];
+  if (act) {
+    for (int j = 0; j < 8; ++j) total += __ldcg(ac + j * 10);
+    if (!(total > 0.0)) {
+      atomicCAS(p.status, 0, kERuntime);  // m_step: no responsibility mass
+      act = false;
+    }
+  }
+  if (act) {
+    for (int q = 0; q < 10; ++q) a[q] = __ldcg(ac + comp * 10 + q);
+    if (a[0] <= total * 1e-12) {
+      g.w = 0.0;
+      act = false;
+    }
+  }
+  double sc[3][3], warm[9];
+  double fl = 1.0;
+  if (act) {
+    const double m0 = a[0];
+    const double d[3] = {a[1] / m0, a[2] / m0, a[3] / m0};
+    const double m2[3][3] = {{a[4], a[5], a[6]}, {a[5], a[7], a[8]}, {a[6], a[8], a[9]}};
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) sc[i][j] = m2[i][j] / m0 - d[i] * d[j];
+    g.w = m0 / total;
+    g.lw = log(g.w);
+    const double* mean = p.nf.mean + 3 * k;
+    for (int i = 0; i < 3; ++i) g.mean[i] = __ldcg(&mean[i]) + d[i];
+    // the eigensolve starts from the component's previous axes: EM moves the
+    // covariance a little per iteration, so the warm Jacobi needs ~1 sweep
+    for (int i = 0; i < 9; ++i) warm[i] = __ldcg(&g.axT[i]);
+    fl = __ldcg(&p.nf.floorv[k]);
+  } else {
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) sc[i][j] = i == j ? 1.0 : 0.0;
+    for (int i = 0; i < 9; ++i) warm[i] = (i % 4) == 0 ? 1.0 : 0.0;
+  }
+  GComp r;
+  UPROBE(7110);
+  const int rc = comp_set_cov_simt(r, sc, fl, warm);
+  UPROBE(7111);
+  if (!act) return;
+  if (rc) {
+    atomicCAS(p.status, 0, kEInval);
     return;
   }
-  double a[10];
-  for (int q = 0; q < 10; ++q) a[q] = __ldcg(ac + comp * 10 + q);
-  GComp& g = comps[comp];
-  if (a[0] <= total * 1e-12) {
-    g.w = 0.0;
-    return;
+  for (int i = 0; i < 9; ++i) {
+    g.axT[i] = r.axT[i];
+    g.cov[i] = r.cov[i];
   }
-  const double m0 = a[0];
-  const double d[3] = {a[1] / m0, a[2] / m0, a[3] / m0};
-  const double m2[3][3] = {{a[4], a[5], a[6]}, {a[5], a[7], a[8]}, {a[6], a[8], a[9]}};
-  double sc[3][3];
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) sc[i][j] = m2[i][j] / m0 - d[i] * d[j];
-  g.w = m0 / total;
-  g.lw = log(g.w);
-  const double* mean = p.nf.mean + 3 * k;
-  for (int i = 0; i < 3; ++i) g.mean[i] = __ldcg(&mean[i]) + d[i];
-  // the eigensolve starts from the component's previous axes: EM moves the
-  // covariance a little per iteration, so the warm Jacobi needs ~1 sweep
-  double warm[9];
-  for (int i = 0; i < 9; ++i) warm[i] = __ldcg(&g.axT[i]);
-  if (comp_set_cov(g, sc, __ldcg(&p.nf.floorv[k]), warm)) atomicCAS(p.status, 0, kEInval);
+  for (int i = 0; i < 3; ++i) {
+    g.lam[i] = r.lam[i];
+    g.il[i] = r.il[i];
+  }
+  g.log_norm = r.log_norm;
 }
 
 // Candidate init (fit_candidate gmm.cpp:319-326) for component `comp`.
@@ -578,6 +617,7 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
                                  const double* red, int round) {
   const int lane = threadIdx.x & 31;
   const NodeFit& nf = p.nf;
+  UPROBE(7100);
   if (ph.mom1 && lane == 0) {
     const double mass = __ldcg(red + kOffMom1);
     nf.mass[k] = mass;
@@ -653,11 +693,11 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
     p.ll_trace[((size_t)(p.st->exp_base + k) * 2 + c) * (I + 1) + slot] = ll;
   }
   // M-steps: lanes 0-7 candidate 0, lanes 8-15 candidate 1
-  if (lane < 16) {
-    const int c = lane >> 3;
-    if (ph.mode[c] == 1) node_mstep(p, k, c, red, lane & 7);
-  }
   __syncwarp();
+  UPROBE(7101);
+  if (ph.mode[0] == 1 || ph.mode[1] == 1) node_mstep_warp(p, ph, k, red);
+  __syncwarp();
+  UPROBE(7102);
   if (lane < 2 && ph.mode[lane] == 2) {
     const int c = lane;
     nf.final_ll[2 * k + c] = __ldcg(red + kOffFin + 9 * c);
@@ -1197,7 +1237,19 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
             }
           }
           last = __shfl_sync(0xffffffffu, last, 0);
-          if (last) node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
+#ifdef TRG_RP_PROBE
+          const bool probe = ph_i == TRG_RP_PROBE && k == 0 && lane == 0;
+          if (probe) tl_mark_any(p.tl, 7000 + round * 10);
+#endif
+          if (last) {
+#ifdef TRG_RP_PROBE
+            if (probe) tl_mark_any(p.tl, 7001 + round * 10);
+#endif
+            node_update_warp(p, ph, k, par, p.nodered + (size_t)k * kRec, round);
+#ifdef TRG_RP_PROBE
+            if (probe) tl_mark_any(p.tl, 7002 + round * 10);
+#endif
+          }
         }
         if (sharded) {
           grid_sync(p.bar, G);
