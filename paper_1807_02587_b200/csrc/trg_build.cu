@@ -119,7 +119,7 @@ struct BuildParams {
   double* cta_drift;    // [G]
   unsigned* cal_arrive;  // [capacity + 1]; slot capacity: leaf arrivals of a calibration pass
   unsigned long long* drift_bits;  // [2] per-pass max drift (bits of a double >= 0)
-  int* layout_scratch;  // [6 * 8 * Kmax]
+  int* layout_scratch;  // [7 * 8 * Kmax]
   double* ll_trace;     // [capacity][2][em_iters + 1] per expansion, both candidates
   int* kept_exp;        // [capacity] kept candidate per expansion
   unsigned* bar;
@@ -254,10 +254,12 @@ struct BuildSmem {
   int item_off[192];
   int item_kind[192];
   int tnode, tstart, tlen, tidx;
-  double ent[4][kTile];  // the tile's entries (x, y, z, w), staged once per tile
+  alignas(16) double ent[4][kTile + 2];  // the tile's entries (x, y, z, w): one bulk copy per tile
+  uint64_t mbar;                          // completion of the tile's bulk copies
+  unsigned mphase;                        // its phase parity (thread 0's copy)
   double sred[kTile / 32][11][33];  // per-warp cross-lane sums of tile_comp_pass (padded rows)
   double nref[3], nmean[3], seed[3];
-  GComp comp[2][8];
+  alignas(16) GComp comp[2][8];
   int cand_list[2];
   int ncand;
   int surv[8];
@@ -752,23 +754,36 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
 __device__ void load_tile_ctx(const BuildParams& p, BuildSmem& sm, const Phase& ph, int par,
                               int t) {
   const int tid = threadIdx.x;
-  // every thread reads the tile's (node, start, len) (broadcast loads) so the
-  // entry loads below issue without waiting for a block barrier
+  // every thread reads the tile's (node, start, len) (broadcast loads)
   const int k = __ldcg(&p.tile_node[par][t]);
   const int tstart = __ldcg(&p.tile_start[par][t]);
   const int tlen = __ldcg(&p.tile_len[par][t]);
+  const bool need_comps = ph.mode[0] || ph.mode[1] || ph.pcount;
+  // The tile's entries (x, y, z, w) and the node's 2 x 8 component table go
+  // to shared memory as bulk copies (TMA engine, cp.async.bulk) completing on
+  // the CTA's mbarrier: one thread issues them and the block's threads fetch
+  // the node context meanwhile.  Segments start at even entries (the layout
+  // pads them) so every copy is 16-byte aligned; the odd tail element copied
+  // past a tile is never read.
   if (tid == 0) {
     sm.tidx = t;
     sm.tnode = k;
     sm.tstart = tstart;
     sm.tlen = tlen;
-  }
-  if (!ph.pwrite && tid < tlen) {
-    const int e = tstart + tid;
-    sm.ent[0][tid] = __ldcg(&p.ex[par][e]);  // (other CTAs wrote them: L2, not L1)
-    sm.ent[1][tid] = __ldcg(&p.ey[par][e]);
-    sm.ent[2][tid] = __ldcg(&p.ez[par][e]);
-    sm.ent[3][tid] = __ldcg(&p.ew[par][e]);
+    const unsigned eb = (!ph.pwrite) ? (unsigned)((tlen + 1) & ~1) * 8u : 0u;
+    const unsigned cb = need_comps ? 16u * (unsigned)sizeof(GComp) : 0u;
+    if (eb + cb) {
+      fence_proxy_async_shared();  // the previous tile's generic reads come first
+      fence_proxy_async_global();  // other CTAs' writes (ordered by a grid barrier)
+      mbar_arrive_tx(&sm.mbar, 4u * eb + cb);
+      if (eb) {
+        bulk_g2s(sm.ent[0], p.ex[par] + tstart, eb, &sm.mbar);
+        bulk_g2s(sm.ent[1], p.ey[par] + tstart, eb, &sm.mbar);
+        bulk_g2s(sm.ent[2], p.ez[par] + tstart, eb, &sm.mbar);
+        bulk_g2s(sm.ent[3], p.ew[par] + tstart, eb, &sm.mbar);
+      }
+      if (cb) bulk_g2s(&sm.comp[0][0], p.nf.comps + (size_t)k * 16, cb, &sm.mbar);
+    }
   }
   if (tid < 3) {
     if (ph.mom1) {
@@ -788,7 +803,7 @@ __device__ void load_tile_ctx(const BuildParams& p, BuildSmem& sm, const Phase& 
     sm.nmean[tid] = __ldcg(&p.nf.mean[3 * k + tid]);
     if (ph.fps) sm.seed[tid] = __ldcg(&p.nf.seeds[24 * k + 3 * (ph.fps - 1) + tid]);
   }
-  if (tid == 0) {
+  if (tid == 32) {
     int nc = 0;
     for (int c = 0; c < 2; ++c)
       if (ph.mode[c]) sm.cand_list[nc++] = c;
@@ -799,15 +814,11 @@ __device__ void load_tile_ctx(const BuildParams& p, BuildSmem& sm, const Phase& 
       for (int s = 0; s < sm.ns; ++s) sm.surv[s] = __ldcg(&p.nf.surv[8 * k + s]);
     }
   }
-  const bool need_comps = ph.mode[0] || ph.mode[1] || ph.pcount;
-  if (need_comps) {
-    // 2 x 8 components
-    constexpr int kD = (int)(sizeof(GComp) / sizeof(double));
-    const double* src = reinterpret_cast<const double*>(p.nf.comps + (size_t)k * 16);
-    double* dst = reinterpret_cast<double*>(&sm.comp[0][0]);
-    for (int i = tid; i < 16 * kD; i += blockDim.x) dst[i] = __ldcg(src + i);
+  if (!ph.pwrite || need_comps) {
+    mbar_wait(&sm.mbar, sm.mphase);
   }
   __syncthreads();
+  if (tid == 0 && (!ph.pwrite || need_comps)) sm.mphase ^= 1u;
 }
 
 // Partition write (gmm.cpp:441-442): stable compaction of one tile into the
@@ -905,6 +916,7 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
   int* ccnt = ngate + 8 * K;      // [NC] entry count -> E2 offset
   int* ctil = ccnt + 8 * K;       // [NC] tile count -> T2 offset
   int* cidx = ctil + 8 * K;       // [NC] (k << 3 | s)
+  int* codd = cidx + 8 * K;       // [NC] 1 when the child's entry count is odd
   for (int k = tid; k < K; k += nt) nbase[k] = p.nf.ok[k] ? p.nf.ns[k] : 0;
   __syncthreads();
   const int NC = block_exscan(nbase, K, wtmp);
@@ -935,7 +947,8 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
       const int cnt = p.nf.next_seg[8 * k + s2];  // child entry count (from pcount)
       const bool gate = !last && !(p.nf.smass[8 * k + s2] < p.min_points);
       cgate[c] = gate ? 1 : 0;
-      ccnt[c] = gate ? cnt : 0;
+      ccnt[c] = gate ? (cnt + 1) & ~1 : 0;  // segments start at even entries (16-byte bulk copies)
+      codd[c] = gate ? cnt & 1 : 0;
       ctil[c] = gate ? (cnt + kTile - 1) / kTile : 0;
       cidx[c] = (k << 3) | s2;
     }
@@ -947,6 +960,7 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
   const int K2 = block_exscan(cgate, NC, wtmp);
   const int E2 = block_exscan(ccnt, NC, wtmp);
   const int T2 = block_exscan(ctil, NC, wtmp);
+  const int pad2 = block_exscan(codd, NC, wtmp);  // E2 - pad2 = the entries (E_l)
   if (tid == 0) {
     sOvf = (!last && (K2 > p.Kmax || E2 > p.Emax || T2 > p.Tmax)) ? 1 : 0;
   }
@@ -996,7 +1010,7 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
     st->Ep[npar] = E2;
     st->Tp[npar] = T2;
     if (round + 1 < 8) {
-      st->E_round[round + 1] = (unsigned long long)E2;
+      st->E_round[round + 1] = (unsigned long long)(E2 - pad2);
       st->K_round[round + 1] = K2;
     }
     if (last || K2 == 0) {
@@ -1164,6 +1178,12 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
   BuildState* st = p.st;
   const bool sharded = p.seg >= 0;
   if (sharded && (__ldcg(&st->done) || __ldcg(&st->status_overflow))) return;
+  if (tid == 0) {
+    mbar_init(&sm.mbar, 1);
+    mbar_fence_init();
+    sm.mphase = 0u;
+  }
+  __syncthreads();
   tl_mark(p.tl, -1);
   // Sharded segments: exchange point xp = the per-node reduction of a phase.
   // Segment q finishes exchange point q-1 (node updates from the all-reduced
@@ -1700,7 +1720,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
   };
   size_t o_e[2][4], o_rn[2][5], o_tl[2][3];
   for (int b = 0; b < 2; ++b) {
-    for (int q = 0; q < 4; ++q) o_e[b][q] = carve(sizeof(double) * E);
+    for (int q = 0; q < 4; ++q) o_e[b][q] = carve(sizeof(double) * (E + 2));  // + bulk-copy tail
     for (int q = 0; q < 5; ++q) o_rn[b][q] = carve(sizeof(int) * K);
     for (int q = 0; q < 3; ++q) o_tl[b][q] = carve(sizeof(int) * T);
   }
@@ -1719,7 +1739,7 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
                o_md = carve(sizeof(double) * E), o_emit = carve(sizeof(double) * 8 * E),
                o_calm = carve(sizeof(double) * 10 * cap), o_bar = carve(64),
                o_cacc = carve(sizeof(long long) * 3 * 30 * (size_t)cap), o_pmax = carve(64),
-               o_lay = carve(sizeof(int) * 48 * K),
+               o_lay = carve(sizeof(int) * 56 * K),
                o_llt = carve(sizeof(double) * (size_t)cap * 2 * (cfg->em_iterations_per_node + 1)),
                o_kex = carve(sizeof(int) * (size_t)cap),
                o_car = carve(sizeof(unsigned) * ((size_t)cap + 1)), o_dbits = carve(16),
