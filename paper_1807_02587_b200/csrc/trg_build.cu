@@ -410,28 +410,35 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
       double a[11];
 #pragma unroll
       for (int q = 0; q < 11; ++q) a[q] = 0.0;
-      for (int e = lane; e < tlen; e += 32) {
-        const double w = sm.ent[3][e];
-        const double g = G.gam[item][e] * w;
-        if (k == 0) a[10] += G.lt[ci][e];
-        if (mode == 1) {
-          if (g > 0.0) {
-            const double d0 = sm.ent[0][e] - n0, d1 = sm.ent[1][e] - n1, d2 = sm.ent[2][e] - n2;
-            a[0] += g;
-            a[1] += g * d0;
-            a[2] += g * d1;
-            a[3] += g * d2;
-            a[4] += g * (d0 * d0);
-            a[5] += g * (d0 * d1);
-            a[6] += g * (d0 * d2);
-            a[7] += g * (d1 * d1);
-            a[8] += g * (d1 * d2);
-            a[9] += g * (d2 * d2);
-          }
-        } else {
-          a[0] += g;  // mode 2: child mass (gmm.cpp:355)
+      // Per lane the entries e = lane, lane + 32, ... in order (two per
+      // iteration for ILP); uniform control flow (mode and k are per warp; a
+      // zero responsibility adds exact zeros, so no per-entry test).
+      if (mode == 1) {
+        auto acc = [&](int e) {
+          const double g = G.gam[item][e] * sm.ent[3][e];
+          const double d0 = sm.ent[0][e] - n0, d1 = sm.ent[1][e] - n1, d2 = sm.ent[2][e] - n2;
+          a[0] += g;
+          a[1] += g * d0;
+          a[2] += g * d1;
+          a[3] += g * d2;
+          a[4] += g * (d0 * d0);
+          a[5] += g * (d0 * d1);
+          a[6] += g * (d0 * d2);
+          a[7] += g * (d1 * d1);
+          a[8] += g * (d1 * d2);
+          a[9] += g * (d2 * d2);
+        };
+        int e = lane;
+        for (; e + 32 < tlen; e += 64) {
+          acc(e);
+          acc(e + 32);
         }
+        if (e < tlen) acc(e);
+      } else {
+        for (int e = lane; e < tlen; e += 32) a[0] += G.gam[item][e] * sm.ent[3][e];  // child mass (gmm.cpp:355)
       }
+      if (k == 0)
+        for (int e = lane; e < tlen; e += 32) a[10] += G.lt[ci][e];
       // Cross-lane sums through shared memory: lane q adds value q of all
       // 32 lanes in the halving tree (16, 8, 4, 2, 1) - the very tree lane
       // 0 of an xor butterfly computes, so the sums are bit-identical to it,
