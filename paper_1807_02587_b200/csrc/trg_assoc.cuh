@@ -36,9 +36,8 @@ __device__ __forceinline__ double node_score(const DNode* __restrict__ g, double
 
 // Score for the descent without an early return, so the <= 8 sibling
 // evaluations are straight-line code; `bad` collects the non-PD error.
-__device__ __forceinline__ double node_score_nb(const DNode* __restrict__ g, double y0, double y1,
-                                                double y2, bool& bad) {
-  const double w = g->weight;
+__device__ __forceinline__ double node_score_nb(const DNode* __restrict__ g, double w, double y0,
+                                                double y1, double y2, bool& bad) {
   const double lam2 = g->lam[2];
   const double q = fast_q(g->mean, g->axT, g->il, y0, y1, y2);
   const double sc = __dmul_rn(w, trg_exp(__fma_rn(-0.5, q, g->log_norm)));
@@ -77,7 +76,8 @@ __device__ __forceinline__ Descent descend(const DNode* __restrict__ nodes, cons
     bool bad = false;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const double v = node_score_nb(sib + (k < count ? k : 0), y0, y1, y2, bad);
+      const int kk = k < count ? k : 0;
+      const double v = node_score_nb(sib + kk, sib[kk].weight, y0, y1, y2, bad);
       sc[k] = k < count ? v : 0.0;
     }
     if (bad) atomicCAS(status, 0, kEDomain);  // log_density: covariance is not PD

@@ -513,9 +513,8 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
 #endif
 // M-steps of node k (m_step gmm.cpp:208-232), the whole warp: lane
 // 8 c + j fits component j of candidate c (when candidate c ran an EM
-// iteration this phase).  The eigensolves are warp-uniform (SIMT Jacobi,
-// bit-identical per lane to the scalar solver): divergent per-lane solves
-// serialise.  All 32 lanes must call.
+// iteration this phase), all lanes of the warp in one pass of the
+// closed-form eigensolver (eig3_cf).
 __device__ void node_mstep_warp(const BuildParams& p, const Phase& ph, int k, const double* red) {
   const int lane = threadIdx.x & 31;
   const int c = (lane >> 3) & 1, comp = lane & 7;
@@ -537,7 +536,7 @@ __device__ void node_mstep_warp(const BuildParams& p, const Phase& ph, int k, co
       act = false;
     }
   }
-  double sc[3][3], warm[9];
+  double sc[3][3];
   double fl = 1.0;
   if (act) {
     const double m0 = a[0];
@@ -549,18 +548,24 @@ __device__ void node_mstep_warp(const BuildParams& p, const Phase& ph, int k, co
     g.lw = log(g.w);
     const double* mean = p.nf.mean + 3 * k;
     for (int i = 0; i < 3; ++i) g.mean[i] = __ldcg(&mean[i]) + d[i];
-    // the eigensolve starts from the component's previous axes: EM moves the
-    // covariance a little per iteration, so the warm Jacobi needs ~1 sweep
-    for (int i = 0; i < 9; ++i) warm[i] = __ldcg(&g.axT[i]);
     fl = __ldcg(&p.nf.floorv[k]);
   } else {
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) sc[i][j] = i == j ? 1.0 : 0.0;
-    for (int i = 0; i < 9; ++i) warm[i] = (i % 4) == 0 ? 1.0 : 0.0;
   }
   GComp r;
   UPROBE(7110);
-  const int rc = comp_set_cov_simt(r, sc, fl, warm);
+#ifdef TRG_RP_PROBE
+  const long long c0 = clock64();
+#endif
+  const int rc = comp_set_cov_cf(r, sc, fl);
+#ifdef TRG_RP_PROBE
+  const long long c1 = clock64();
+  if (k == 0 && (threadIdx.x & 31) == 0) {
+    const int i = atomicAdd(&p.tl->n, 1);
+    if (i < 1024) { p.tl->lab[i] = 7199; p.tl->t[i] = (unsigned long long)(c1 - c0); }
+  }
+#endif
   UPROBE(7111);
   if (!act) return;
   if (rc) {
@@ -1371,12 +1376,21 @@ __device__ __forceinline__ int cal_arrive(const BuildParams& p, const CalCtx& cx
   return par;
 }
 
-// Sum of v over lanes [0, cc) of the warp in lane (= child) order, the
-// reference's serial loop order; the result is uniform.
-__device__ __forceinline__ double child_sum(double v, int cc) {
-  double t = 0.0;
-  for (int q = 0; q < cc; ++q) t += __shfl_sync(0xffffffffu, v, q);
-  return t;
+// Sums of v[i] over lanes [0, cc) of the warp, each in lane (= child)
+// order -- the reference's serial loop order; the N sums interleave (one
+// shuffle round per child for all of them) and the results are uniform.
+template <int N>
+__device__ __forceinline__ void child_sums(const double (&v)[N], int cc, double (&out)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) out[i] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double x = __shfl_sync(0xffffffffu, v[i], q);
+      if (q < cc) out[i] += x;
+    }
+  }
 }
 
 // Internal node P, all children final, by one warp (lane c holds child c):
@@ -1394,7 +1408,10 @@ __device__ void cal_internal(const BuildParams& p, const CalCtx& cx, int P, doub
   for (int k = 0; k < 3; ++k) cm[k] = own ? __ldcg(&p.nodes[ci].mean[k]) : 0.0;
 #pragma unroll
   for (int k = 0; k < 9; ++k) cv[k] = own ? __ldcg(&p.cov[9 * (size_t)ci + k]) : 0.0;
-  const double b = child_sum(cb, cc);  // branch (gmm.cpp:547-556) = the octet's share sum
+  const double bv[1] = {cb};
+  double bb[1];
+  child_sums<1>(bv, cc, bb);
+  const double b = bb[0];  // branch (gmm.cpp:547-556) = the octet's share sum
   if (lane == 0) cx.branch[P] = b;
   if (b > 0.0 && own) {  // reweight (gmm.cpp:557-566); a shadowed octet keeps its shares
     const double nw = cb / b;
@@ -1402,19 +1419,28 @@ __device__ void cal_internal(const BuildParams& p, const CalCtx& cx, int P, doub
     cw = nw;
     p.nodes[ci].weight = nw;
   }
-  const double w = child_sum(cw, cc);
+  const double wv[4] = {cw, __dmul_rn(cw, cm[0]), __dmul_rn(cw, cm[1]), __dmul_rn(cw, cm[2])};
+  double wm[4];
+  child_sums<4>(wv, cc, wm);
+  const double w = wm[0];
   if (!(w > 0.0)) return;
   double mu[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) mu[k] = child_sum(__dmul_rn(cw, cm[k]), cc) / w;
+  for (int k = 0; k < 3; ++k) mu[k] = wm[1 + k] / w;
   const double d[3] = {cm[0] - mu[0], cm[1] - mu[1], cm[2] - mu[2]};
+  double t[9], cs[9];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const double v = child_sum(__dmul_rn(cw, __dadd_rn(cv[3 * r + q], __dmul_rn(d[r], d[q]))), cc);
-      if (lane == 3 * r + q) p.cov[9 * (size_t)P + 3 * r + q] = v / w;
-    }
+    for (int q = 0; q < 3; ++q)
+      t[3 * r + q] = __dmul_rn(cw, __dadd_rn(cv[3 * r + q], __dmul_rn(d[r], d[q])));
+  child_sums<9>(t, cc, cs);
+  if (lane < 9) {
+    double v = cs[0];
+#pragma unroll
+    for (int q = 1; q < 9; ++q) v = lane == q ? cs[q] : v;
+    p.cov[9 * (size_t)P + lane] = v / w;
+  }
   if (lane < 3) p.nodes[P].mean[lane] = mu[lane];
 }
 
@@ -1441,9 +1467,7 @@ __device__ void cal_leaf(const BuildParams& p, const CalCtx& cx, int j, const do
   GComp g;
   g.w = nd.weight;
   for (int q = 0; q < 3; ++q) g.mean[q] = mu[q];
-  double w[9];
-  for (int q = 0; q < 9; ++q) w[q] = nd.axT[q];
-  if (comp_set_cov(g, S2, cov_floor(S2, p.eps, p.abs_floor), w)) atomicCAS(p.status, 0, kEInval);
+  if (comp_set_cov_cf(g, S2, cov_floor(S2, p.eps, p.abs_floor))) atomicCAS(p.status, 0, kEInval);
   double dc[3][3];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) dc[r][c] = g.cov[3 * r + c] - before[r][c];
@@ -1492,13 +1516,13 @@ __device__ void cal_finish_leaf(const BuildParams& p, const CalCtx& cx, int j, d
     P = __shfl_sync(0xffffffffu, P, 0);
     CAL_PROBE(lane == 0, 5011);
   }
-  if (nd) {  // the refreshes, one lane each, warp-uniform solver (SIMT)
+  if (nd) {  // the refreshes, one lane each (closed-form solver)
     int mine = -1;
     for (int k = 0; k < nd; ++k)
       if (lane == k) mine = done[k];
     double cv[9];
     for (int q = 0; q < 9; ++q) cv[q] = mine >= 0 ? __ldcg(&p.cov[9 * (size_t)mine + q]) : 0.0;
-    if (refresh_node_simt(p.nodes[mine >= 0 ? mine : 0], cv, true, mine >= 0))
+    if (refresh_node_cf(p.nodes[mine >= 0 ? mine : 0], cv, mine >= 0))
       atomicCAS(p.status, 0, kEInval);
     CAL_PROBE(lane == 0, 5030);
   }
@@ -1538,10 +1562,10 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
     if (cta == 0) reset_parents(p, lvl);
     grid_sync(p.bar, G);
     tl_mark(p.tl, 901);
-    for (int base = 0; base < J; base += G * blockDim.x) {  // SIMT refresh_eig
+    for (int base = 0; base < J; base += G * blockDim.x) {  // refresh_eig
       const int j = base + cta * blockDim.x + tid;
       const bool act = j < J;
-      if (refresh_node_simt(p.nodes[act ? j : 0], p.cov + 9 * (size_t)(act ? j : 0), false, act))
+      if (refresh_node_cf(p.nodes[act ? j : 0], p.cov + 9 * (size_t)(act ? j : 0), act))
         atomicCAS(p.status, 0, kEInval);
     }
     grid_sync(p.bar, G);

@@ -81,12 +81,12 @@ static __device__ __noinline__ int refresh_node(DNode& d, const double* cov9, bo
   return kOk;
 }
 
-// Warp-uniform variants (trg_math.cuh eig_sym3*_simt): all 32 lanes call,
-// each with its own matrix; results are bit-identical to the per-lane ones.
-__device__ __forceinline__ int comp_set_cov_simt(GComp& g, const double sc[3][3], double floor_value,
-                                                 const double* warm = nullptr) {
+// Closed-form variants (trg_math.cuh eig_sym3*_cf): set_floored_cov of the
+// M-steps and leaf refits, refresh_eig of the calibration's parents.  No
+// warp collectives: any set of lanes may call.
+__device__ __forceinline__ int comp_set_cov_cf(GComp& g, const double sc[3][3], double floor_value) {
   double lam[3], ax[3][3], cov[3][3];
-  const int rc = eig_sym3_floored_simt(sc, floor_value, lam, ax, warm);
+  const int rc = eig_sym3_floored_cf(sc, floor_value, lam, ax);
   reconstruct(lam, ax, cov);
   for (int i = 0; i < 3; ++i) {
     g.lam[i] = lam[i];
@@ -102,13 +102,11 @@ __device__ __forceinline__ int comp_set_cov_simt(GComp& g, const double sc[3][3]
 
 // refresh_eig of a node from cov9 into its DNode fields (written only when
 // `act` and the eigensolve succeeded).
-__device__ __forceinline__ int refresh_node_simt(DNode& d, const double* cov9, bool warm, bool act) {
+__device__ __forceinline__ int refresh_node_cf(DNode& d, const double* cov9, bool act) {
   double m[3][3], lam[3], ax[3][3];
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j) m[i][j] = act ? cov9[3 * i + j] : (i == j ? 1.0 : 0.0);
-  double w[9];
-  for (int i = 0; i < 9; ++i) w[i] = act && warm ? d.axT[i] : ((i % 4) == 0 ? 1.0 : 0.0);
-  const int rc = eig_sym3_simt(m, lam, ax, w);
+  const int rc = eig_sym3_cf(m, lam, ax);
   if (!act || rc) return act ? rc : kOk;
   for (int i = 0; i < 3; ++i) {
     d.lam[i] = lam[i];

@@ -18,10 +18,14 @@ __global__ void k_eig_selftest(int n, const double* in, int count, double* evals
     }
   } else {
     // n == 3: strict eig_sym3 (geometry.cpp:40-79); n == -3: floored at 1e-4
+    // (Jacobi); n == 33 / -33: the same with the closed-form solver
     double m[3][3], lam[3], ax[3][3];
     for (int r = 0; r < 3; ++r)
       for (int c = 0; c < 3; ++c) m[r][c] = in[9 * i + 3 * r + c];
-    status3[i] = n == 3 ? eig_sym3(m, lam, ax) : eig_sym3_floored(m, 1e-4, lam, ax);
+    status3[i] = n == 3    ? eig_sym3(m, lam, ax)
+                 : n == -3 ? eig_sym3_floored(m, 1e-4, lam, ax)
+                 : n == 33 ? eig_sym3_cf(m, lam, ax)
+                           : eig_sym3_floored_cf(m, 1e-4, lam, ax);
     for (int r = 0; r < 3; ++r) {
       evals[3 * i + r] = lam[r];
       for (int c = 0; c < 3; ++c) evecs[9 * i + 3 * r + c] = ax[r][c];

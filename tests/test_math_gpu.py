@@ -81,3 +81,43 @@ def test_warp_solve_matches_numpy(ctx):
         x = np.linalg.solve(m, b)
         assert np.allclose(out[:6], x, rtol=1e-8, atol=1e-8 * np.abs(x).max())
         assert abs(out[6] - cond) <= 1e-8 * cond
+
+
+def test_closed_form_eig3_matches_jacobi(ctx, port):
+    """The closed-form 3x3 solver (eig3_cf, used by the M-steps, the leaf
+    refits and the calibration's parent refreshes) against the Jacobi oracle:
+    eigenvalues to 1e-13 of the spread (tiny floored eigenvalues to 1e-11
+    relative), eigenvectors of separated eigenvalues to 1e-9, the same sign
+    and handedness conventions, a valid orthonormal basis always; and the
+    quantities the densities use (log-normaliser, the quadratic form) agree
+    even inside near-degenerate eigenspaces."""
+    rng = np.random.default_rng(7)
+    mats = _spd(rng, 400, 3)
+    mats[:10] = np.eye(3) * 2.5  # ties
+    mats[10:20] = np.diag([2.0, 5.0, 3.0])
+    for i in range(20, 60):  # planar and linear patches, near-degenerate pairs
+        q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+        lam = [1e-2, 1e-2 * (1 + 10.0 ** rng.uniform(-12, -3)), 10.0 ** rng.uniform(-7, -4)]
+        mats[i] = q @ np.diag(rng.permutation(lam)) @ q.T
+    mats[60:70] *= 1e-9  # tiny scales
+    mats[70:80] *= 1e6
+    for n, floored in ((33, False), (-33, True)):
+        ev, vec, st = _dev_eig(ctx, n, mats)
+        for i, m in enumerate(mats):
+            lam, ax = port.eig_sym3(m, floored=floored, floor_value=1e-4)
+            assert st[i] == 0
+            e, v = ev[i], vec[i]
+            spread = abs(lam[0])
+            assert np.all(np.abs(lam - e) <= 1e-14 * spread + 1e-300), (i, lam, e)
+            assert np.abs(v.T @ v - np.eye(3)).max() <= 1e-13
+            assert np.linalg.det(v) > 0
+            gap = np.array([min(abs(lam[l] - lam[(l + 1) % 3]), abs(lam[l] - lam[(l + 2) % 3]))
+                            for l in range(3)])
+            sep = gap > 1e-5 * spread
+            d = np.abs(ax - v).max(axis=0)
+            assert np.all(d[sep] <= 1e-9), (i, d, lam)
+            # the density's quadratic form is basis-independent
+            x = rng.standard_normal(3) * np.sqrt(spread)
+            qa = np.sum((ax.T @ x) ** 2 / np.maximum(lam, 1e-300))
+            qb = np.sum((v.T @ x) ** 2 / np.maximum(e, 1e-300))
+            assert abs(qa - qb) <= 1e-9 * abs(qa) + 1e-300

@@ -28,3 +28,9 @@ for r in range(3):
     a, b = t[lab == 7001 + 10 * r][0], t[lab == 7002 + 10 * r][0]
     m = (t >= a) & (t <= b) & (lab >= 7100)
     print("round", r, " ".join("%d:%.2f" % (l, x - a) for l, x in zip(lab[m], t[m])))
+# raw SM cycles of the M-step eigensolve (label 7199 carries cycles, not ns)
+t2 = np.zeros(1024, np.uint64)
+l2 = np.zeros(1024, np.int32)
+from paper_1807_02587_b200 import _lib  # noqa: E402
+n = _lib.lib().trg_debug_build_timeline(ctx.h, t2.ctypes.data_as(_lib.u64p), l2.ctypes.data_as(_lib.ip), 1024)
+print("eig cycles", t2[:n][l2[:n] == 7199][:12])
