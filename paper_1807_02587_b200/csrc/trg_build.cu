@@ -593,7 +593,9 @@ __device__ void cand_init(const BuildParams& p, int k, int c, const double seed[
   const double* S = p.nf.scatter + 9 * k;
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j) cs[i][j] = S[3 * i + j] / 4.0;
-  if (comp_set_cov(g, cs, p.nf.floorv[k])) atomicCAS(p.status, 0, kEInval);
+  // the initial axes only feed densities (basis-independent), so the
+  // closed-form solver serves; the corner seeds keep the Jacobi's basis
+  if (comp_set_cov_cf(g, cs, p.nf.floorv[k])) atomicCAS(p.status, 0, kEInval);
 }
 
 // Winner of an argmax field (score, entry index) of node k: its score, and
@@ -2184,17 +2186,31 @@ int build_sharded_dev(trg_comm* c, const double* const* dev, const size_t* n,
       xaa[i] = job[i].p.xarg_all;
       xc[i] = job[i].p.xcal;
     }
-    const size_t kmax = (size_t)job[0].p.Kmax;
+    // Exchanges are sized to the live nodes: the round's expanding nodes K_r
+    // (read back once per round, after the segment that ran the previous
+    // round's layout) and the tree's J for the calibration.
+    size_t kr = 1;
     for (int q = 0; q < nseg; ++q) {
       for (int i = 0; i < S; ++i) TRG_TRY(build_launch(c->shard_ctx[i], &job[i], q));
       if (q + 1 == nseg) break;
-      TRG_TRY(comm_allreduce_sum(c, red.data(), kmax * kRec));
-      if (q % XP <= 7) TRG_TRY(comm_allgather(c, xa.data(), xaa.data(), kmax * 8));  // mom1 / FPS
+      if (q % XP == 0 && q > 0) {
+        int k2 = 0;
+        TRG_CU(cudaMemcpyAsync(&k2, &job[0].p.st->Kp[(q / XP) & 1], sizeof(int),
+                               cudaMemcpyDeviceToHost, c->shard_ctx[0]->stream));
+        TRG_CU(cudaStreamSynchronize(c->shard_ctx[0]->stream));
+        kr = (size_t)std::max(0, std::min(k2, job[0].p.Kmax));
+      }
+      TRG_TRY(comm_allreduce_sum(c, red.data(), kr * kRec));
+      if (q % XP <= 7) TRG_TRY(comm_allgather(c, xa.data(), xaa.data(), (size_t)job[0].p.Kmax * 8));  // mom1 / FPS
     }
-    const size_t cap = (size_t)job[0].p.capacity;
+    int jn = 0;
+    TRG_CU(cudaMemcpyAsync(&jn, &job[0].p.st->J, sizeof(int), cudaMemcpyDeviceToHost,
+                           c->shard_ctx[0]->stream));
+    TRG_CU(cudaStreamSynchronize(c->shard_ctx[0]->stream));
+    const size_t nj = (size_t)std::max(0, std::min(jn, job[0].p.capacity));
     for (int s = 0; s <= 40; ++s) {
       for (int i = 0; i < S; ++i) TRG_TRY(calibrate_launch(c->shard_ctx[i], &job[i], s));
-      if (s < 40) TRG_TRY(comm_allreduce_sum(c, xc.data(), cap * 10));
+      if (s < 40) TRG_TRY(comm_allreduce_sum(c, xc.data(), nj * 10));
     }
     // consensus on errors / overflow (a shard that overflowed stopped early,
     // so the others' results are void too)
