@@ -122,7 +122,7 @@ struct BuildParams {
   int* layout_scratch;  // [7 * 8 * Kmax]
   double* ll_trace;     // [capacity][2][em_iters + 1] per expansion, both candidates
   int* kept_exp;        // [capacity] kept candidate per expansion
-  unsigned* bar;
+  unsigned* bar;  // [0]: k_build's grid barrier, [8]: k_calibrate's (other grid size)
   BuildState* st;
   Timeline* tl;
   int* status;
@@ -1107,12 +1107,27 @@ __device__ int phase_items(const Phase& ph, int* off, int* kind) {
 // lane-strided then butterfly: fixed order, deterministic.
 __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k, int off,
                                             int kind) {
+  // (the record loads are issued in batches of 8 ahead of their uses: the
+  // cache-global loads are ordered volatile asm, so a load-then-add loop
+  // would wait a full L2 round trip per tile; the sums keep their order)
+  constexpr int B = 8;
   const int lane = threadIdx.x & 31;
   const int t0 = p.rn[par].tile0[k], nt = p.rn[par].ntiles[k];
   double* out = p.nodered + (size_t)k * kRec;
+  const double* rec0 = p.partial + (size_t)t0 * kRec;
   if (kind == 0) {
     double v = 0.0;
-    for (int q = lane; q < nt; q += 32) v += __ldcg(p.partial + (size_t)(t0 + q) * kRec + off);
+    for (int q0 = lane; q0 < nt; q0 += 32 * B) {
+      double b[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int q = q0 + 32 * u;
+        b[u] = q < nt ? __ldcg(rec0 + (size_t)q * kRec + off) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        if (q0 + 32 * u < nt) v += b[u];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) out[off] = v;
@@ -1123,11 +1138,17 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
     const int s = off, ns = __ldcg(&p.nf.ns[k]);
     if (s >= ns) return;
     const int comp = __ldcg(&p.nf.surv[8 * k + s]);
-    const double* cnt = p.partial + (size_t)t0 * kRec + kOffCnt + comp;
+    const double* cnt = rec0 + kOffCnt + comp;
     const int per = (nt + 31) / 32;
     const int q0 = min(nt, lane * per), q1 = min(nt, q0 + per);
     double loc = 0.0;
-    for (int q = q0; q < q1; ++q) loc += __ldcg(cnt + (size_t)q * kRec);
+    for (int qb = q0; qb < q1; qb += B) {
+      double b[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) b[u] = qb + u < q1 ? __ldcg(cnt + (size_t)(qb + u) * kRec) : 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u) loc += b[u];
+    }
     double inc = loc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1135,16 +1156,30 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
       if (lane >= o) inc += y;
     }
     double base = inc - loc;
-    for (int q = q0; q < q1; ++q) {
-      p.tile_base[(size_t)(t0 + q) * 8 + s] = base;
-      base += __ldcg(cnt + (size_t)q * kRec);
+    for (int qb = q0; qb < q1; qb += B) {
+      double b[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) b[u] = qb + u < q1 ? __ldcg(cnt + (size_t)(qb + u) * kRec) : 0.0;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        if (qb + u < q1) p.tile_base[(size_t)(t0 + qb + u) * 8 + s] = base;
+        base += b[u];
+      }
     }
     if (lane == 31) p.nf.next_seg[8 * k + s] = (int)inc;  // child entry count
   } else {
     double bs = -INFINITY, bi = 1e300;
-    for (int q = lane; q < nt; q += 32)
-      argmax_merge(bs, bi, __ldcg(p.partial + (size_t)(t0 + q) * kRec + off),
-                   __ldcg(p.partial + (size_t)(t0 + q) * kRec + off + 1));
+    for (int q0 = lane; q0 < nt; q0 += 32 * B) {
+      double sc[B], ix[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int q = q0 + 32 * u;
+        sc[u] = q < nt ? __ldcg(rec0 + (size_t)q * kRec + off) : -INFINITY;
+        ix[u] = q < nt ? __ldcg(rec0 + (size_t)q * kRec + off + 1) : 1e300;
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) argmax_merge(bs, bi, sc[u], ix[u]);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
@@ -1263,12 +1298,9 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
           if (sharded) continue;
           unsigned last = 0;
           if (lane == 0) {
-            __threadfence();
-            last = (atomicAdd(&p.fdone[k], 1u) == (unsigned)NI - 1) ? 1u : 0u;
-            if (last) {
-              p.fdone[k] = 0u;
-              __threadfence();
-            }
+            // release this item's sum, acquire the node's other items
+            last = (atom_add_acq_rel(&p.fdone[k], 1u) == (unsigned)NI - 1) ? 1u : 0u;
+            if (last) p.fdone[k] = 0u;  // (ordered before the next phase by the grid barrier)
           }
           last = __shfl_sync(0xffffffffu, last, 0);
 #ifdef TRG_RP_PROBE
@@ -1366,10 +1398,8 @@ __device__ __forceinline__ int cal_arrive(const BuildParams& p, const CalCtx& cx
   const int par = __ldcg(&p.nodes[i].parent);
   const int slot = par >= 0 ? par : p.capacity;
   const int need = par >= 0 ? __ldcg(&p.nodes[par].child_count) : cx.root_count;
-  __threadfence();
-  const unsigned old = atomicAdd(&cx.arrive[slot], 1u);
+  const unsigned old = atom_add_acq_rel(&cx.arrive[slot], 1u);  // release mine, acquire siblings'
   if (old + 1 != (unsigned)need) return -1;
-  __threadfence();
   cx.arrive[slot] = 0u;
   if (par < 0) {  // top octet (gmm.cpp:567-571)
     cal_reweight(p, cx.branch, 0, cx.root_count, drift);
@@ -1562,7 +1592,7 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
   if (!sharded || p.seg == 0) {
     tl_mark(p.tl, 900);
     if (cta == 0) reset_parents(p, lvl);
-    grid_sync(p.bar, G);
+    grid_sync(p.bar + 8, G);
     tl_mark(p.tl, 901);
     for (int base = 0; base < J; base += G * blockDim.x) {  // refresh_eig
       const int j = base + cta * blockDim.x + tid;
@@ -1570,7 +1600,7 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
       if (refresh_node_cf(p.nodes[act ? j : 0], p.cov + 9 * (size_t)(act ? j : 0), act))
         atomicCAS(p.status, 0, kEInval);
     }
-    grid_sync(p.bar, G);
+    grid_sync(p.bar + 8, G);
     tl_mark(p.tl, 902);
   }
   // ------------------------------------------------ leaf calibration
@@ -1615,7 +1645,7 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
       if (pass == TRG_PROBE_PASS && tid == 0 && cta % 32 == 0) tl_mark_any(p.tl, 5103);
 #endif
       assoc_fx_pass<10>(a, nullptr, sc, G * WPB, cta * WPB + warp);
-      grid_sync(p.bar, G);
+      grid_sync(p.bar + 8, G);
       tl_mark(p.tl, 1000 + pass * 10 + 1);
       if (sharded) {
         // this shard's leaf moments, for the all-reduce (rows zeroed for
@@ -1658,7 +1688,7 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
     for (int off = 16; off > 0; off >>= 1) drift = smax(drift, __shfl_xor_sync(0xffffffffu, drift, off));
     if (lane == 0 && drift > 0.0)
       atomicMax(&p.drift_bits[pass & 1], (unsigned long long)__double_as_longlong(drift));
-    grid_sync(p.bar, G);
+    grid_sync(p.bar + 8, G);
     tl_mark(p.tl, 1000 + pass * 10 + 2);
     if (cta == 0 && tid == 0) {
       st->drift = __longlong_as_double((long long)__ldcg(&p.drift_bits[pass & 1]));

@@ -14,8 +14,8 @@
 //   workers:  wait flag >= step  ->  point pass  ->  fence, arrive (+1)
 //   updaters: wait arrivals == n_work * (step + 1)  ->  serial math  ->
 //             fence, flag = step + 1
-// (fence + counter/flag = release/acquire; the acquiring side's fence also
-// drops stale L1 lines, as in grid_sync).
+// (counter/flag updates are GPU-scope releases, the waits acquire loads,
+// which also drop stale L1 lines, as in grid_sync).
 #pragma once
 #include "trg_solve.cuh"
 
@@ -97,16 +97,14 @@ static __device__ Roles assign_roles(unsigned* smtab, unsigned* bar, int G, int 
 // Workers: wait until the updaters published step `s` (flag >= s).
 __device__ __forceinline__ void wait_flag(const unsigned* flag, unsigned s) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile const unsigned* f = flag;
+  if (threadIdx.x == 0 && ld_acquire_u32(flag) < s) {
     unsigned ns = 32;
     const unsigned long long t0 = gtimer();
-    while (*f < s) {
+    while (ld_acquire_u32(flag) < s) {
       __nanosleep(ns);
       ns = ns < 128 ? 2 * ns : 128;
       spin_guard(t0);
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -114,32 +112,27 @@ __device__ __forceinline__ void wait_flag(const unsigned* flag, unsigned s) {
 // Updaters: wait until `target` worker arrivals are counted.
 __device__ __forceinline__ void wait_count(const unsigned* cnt, unsigned target) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile const unsigned* f = cnt;
+  if (threadIdx.x == 0 && ld_acquire_u32(cnt) < target) {
     const unsigned long long t0 = gtimer();
-    while (*f < target) {
+    while (ld_acquire_u32(cnt) < target) {
       __nanosleep(32);
       spin_guard(t0);
     }
-    __threadfence();
   }
   __syncthreads();
 }
 
 // Workers: this CTA's point pass is complete (all its threads' writes and
-// reductions are ordered before the arrival).
+// reductions are ordered before the arrival by the CTA barrier; the release
+// publishes them).
 __device__ __forceinline__ void arrive_count(unsigned* cnt) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(cnt, 1u);
-  }
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
 }
 
-// Updater 0: publish step s.
+// Updater 0: publish step s (its CTA's writes ordered before by the caller).
 __device__ __forceinline__ void publish_flag(unsigned* flag, unsigned s) {
-  __threadfence();
-  atomicExch(flag, s);
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(s) : "memory");
 }
 
 }  // namespace trg

