@@ -20,6 +20,7 @@ extern "C" int trg_register_batch(trg_ctx* ctx, int n_pairs, const double* const
                                   const size_t* n_targets, const double* const* sources,
                                   const size_t* n_sources, int on_device,
                                   const trg_reg_config* cfg, int streams, trg_reg_result* out) {
+  trg::NvtxRange nvtx_range_("trg_register_batch");
   if (!ctx || n_pairs < 0 || (n_pairs > 0 && (!targets || !n_targets || !sources || !n_sources ||
                                                !cfg || !out))) {
     set_error("register_batch: bad argument");

@@ -2099,6 +2099,7 @@ int check_model_config(const trg_model_config* cfg) { return validate_model_conf
 extern "C" int trg_build_tree(trg_ctx* ctx, const double* xyz, size_t n, int xyz_on_device,
                               const trg_model_config* cfg, trg_tree_dev** out,
                               trg_build_diag* diag) {
+  trg::NvtxRange nvtx_range_("trg_build_tree");
   // validate_config gmm.cpp:465-477, validate_cloud :479-484
   TRG_TRY(validate_model_config(cfg));
   if (n == 0 || !xyz) {
@@ -2307,6 +2308,7 @@ int build_sharded_dev(trg_comm* c, const double* const* dev, const size_t* n,
 extern "C" int trg_build_tree_sharded(trg_comm* comm, const double* const* xyz, const size_t* n,
                                       int on_device, const trg_model_config* cfg,
                                       trg_tree_dev** out, trg_build_diag* diag) {
+  trg::NvtxRange nvtx_range_("trg_build_tree_sharded");
   if (!comm || !xyz || !n || !out) {
     set_error("build_tree_sharded: bad argument");
     return TRG_EINVAL;

@@ -391,6 +391,7 @@ __global__ void k_refresh_nodes(DNode* nodes, const double* cov, int J, int* fir
 static int tree_upload(trg_ctx* ctx, const trg_tree* h, bool refresh, trg_tree_dev** out);
 
 int trg_tree_upload(trg_ctx* ctx, const trg_tree* h, trg_tree_dev** out) {
+  trg::NvtxRange nvtx_range_("trg_tree_upload");
   return tree_upload(ctx, h, false, out);
 }
 
@@ -468,6 +469,7 @@ static int tree_upload(trg_ctx* ctx, const trg_tree* h, bool refresh, trg_tree_d
 }
 
 int trg_tree_download(trg_ctx* ctx, const trg_tree_dev* t, trg_tree* h) {
+  trg::NvtxRange nvtx_range_("trg_tree_download");
   if (!t || !h) {
     set_error("trg_tree_download: null argument");
     return TRG_EINVAL;
@@ -515,6 +517,7 @@ int trg_associate(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, siz
                   int xyz_on_device, const double R[9], const double t[3],
                   const trg_assoc_config* cfg, trg_moments* out, int* point_node,
                   double* point_weight) {
+  trg::NvtxRange nvtx_range_("trg_associate");
   // association.cpp:43-50 validate_inputs, :95-102
   if (n == 0) {
     set_error("association: empty point cloud");

@@ -1092,6 +1092,7 @@ extern "C" {
 
 int trg_solve_mstep(trg_ctx* ctx, const trg_tree_dev* tree, const double* m0, const double* m1,
                     uint64_t total_points, trg_mstep_solution* out) {
+  trg::NvtxRange nvtx_range_("trg_solve_mstep");
   if (!tree || tree->n_nodes == 0) {
     set_error("make_virtual_points: moment/component count mismatch");
     return TRG_EINVAL;
@@ -1139,6 +1140,7 @@ int trg_solve_mstep(trg_ctx* ctx, const trg_tree_dev* tree, const double* m0, co
 int trg_make_virtual_points(trg_ctx* ctx, int n_components, const double* m0, const double* m1,
                             uint64_t total_points, int* index, double* pi_star, double* mu_star,
                             int* n_out) {
+  trg::NvtxRange nvtx_range_("trg_make_virtual_points");
   if (total_points == 0) {
     set_error("make_virtual_points: no points were associated");
     return TRG_EINVAL;
@@ -1186,6 +1188,7 @@ int trg_make_virtual_points(trg_ctx* ctx, int n_components, const double* m0, co
 int trg_solve_mstep_vps(trg_ctx* ctx, int n_vps, const double* pi_star, const double* mu_star,
                         const double* comp_mean, const double* comp_lambdas,
                         const double* comp_axes, trg_mstep_solution* out) {
+  trg::NvtxRange nvtx_range_("trg_solve_mstep_vps");
   if (n_vps < 0) {
     set_error("solve_mstep: bad virtual point count");
     return TRG_EINVAL;
@@ -1240,6 +1243,7 @@ int trg_solve_mstep_vps(trg_ctx* ctx, int n_vps, const double* pi_star, const do
 int trg_register_with_tree(trg_ctx* ctx, const trg_tree_dev* tree, const double* xyz, size_t n,
                            int xyz_on_device, const trg_reg_config* cfg, double target_diag,
                            trg_reg_result* out) {
+  trg::NvtxRange nvtx_range_("trg_register_with_tree");
   if (n == 0 || !xyz) {
     set_error("register: bad source cloud");
     return TRG_EINVAL;
@@ -1339,6 +1343,7 @@ static int register_tree_async(trg_ctx* ctx, const double* tgt, size_t n_target,
 int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target,
                         const double* source, size_t n_source, int on_device,
                         const trg_reg_config* cfg, trg_reg_result* out) {
+  trg::NvtxRange nvtx_range_("trg_register_clouds");
   if (n_target == 0 || n_source == 0 || !target || !source) {
     set_error("register: empty cloud");
     return TRG_EINVAL;
@@ -1401,6 +1406,7 @@ extern "C" int trg_register_clouds_sharded(trg_comm* comm, const double* const* 
                                            const size_t* n_target, const double* const* source,
                                            const size_t* n_source, int on_device,
                                            const trg_reg_config* cfg, trg_reg_result* out) {
+  trg::NvtxRange nvtx_range_("trg_register_clouds_sharded");
   if (!comm || !target || !source || !n_target || !n_source || !out) {
     set_error("register_sharded: bad argument");
     return TRG_EINVAL;

@@ -561,6 +561,7 @@ using namespace trg;
 extern "C" int trg_build_flat_gmm(trg_ctx* ctx, const double* xyz, size_t n, int xyz_on_device,
                                   size_t J, const trg_model_config* cfg, trg_tree_dev** out,
                                   trg_build_diag* diag) {
+  trg::NvtxRange nvtx_range_("trg_build_flat_gmm");
   if (!ctx || !cfg || !out) {
     set_error("build_flat_gmm: bad argument");
     return TRG_EINVAL;
@@ -580,6 +581,7 @@ extern "C" int trg_responsibilities_dense(trg_ctx* ctx, const trg_tree_dev* comp
                                           size_t n, int xyz_on_device, const double R[9],
                                           const double t[3], double outlier_floor,
                                           trg_moments* out) {
+  trg::NvtxRange nvtx_range_("trg_responsibilities_dense");
   // association.cpp:43-50 validate_inputs
   if (n == 0 || !xyz) {
     set_error("association: empty point cloud");

@@ -10,6 +10,18 @@
 #include "trg_math.cuh"
 #include "trg_fx.cuh"
 
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges cost nothing without a tool attached
+
+namespace trg {
+// NVTX range over one C-ABI call (visible in Nsight Systems / ncu --nvtx).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace trg
+
 namespace trg {
 
 // ---------------------------------------------------------------- errors
