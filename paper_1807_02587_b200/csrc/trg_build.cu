@@ -350,29 +350,42 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
   const int nc = pcount ? 1 : sm.ncand;
   const int tlen = sm.tlen;
   auto& G = sm.u.g;
-  // ---- (1)
+  // ---- (1a) component per warp, entries over the lanes: the component's
+  // parameters stay in registers for the whole tile (one shared-memory read
+  // per component instead of per entry); the log-densities go to the gam
+  // rows, which (1b) then turns into responsibilities in place.
+  for (int item = warp; item < nc * 8; item += kTile / 32) {
+    const int ci = item >> 3, k = item & 7;
+    const int cand = pcount ? sm.kept : sm.cand_list[ci];
+    // gmm.cpp:176-178 log w + log_density (-inf when w == 0), without
+    // branches: the value is selected, the domain error (log_density on a
+    // non-PD covariance) flagged once per component
+    double r[18];
+    comp_to_regs(sm.comp[cand][k], r);
+    const bool live = r[0] > 0.0, pd = r[16] > 0.0;
+    if (lane == 0 && live && !pd && tlen > 0) atomicCAS(p.status, 0, kEDomain);
+#pragma unroll 4
+    for (int e = lane; e < tlen; e += 32) {
+      const double v =
+          r[1] + __fma_rn(-0.5, fast_q(r + 2, r + 5, r + 14, sm.ent[0][e], sm.ent[1][e], sm.ent[2][e]), r[17]);
+      G.gam[item][e] = (live && pd) ? v : -INFINITY;
+    }
+  }
+  __syncthreads();
+  // ---- (1b) entry per thread: max / sum / log in component order exactly
+  // like the reference
   if (tid < tlen) {
-    const double x0 = sm.ent[0][tid], x1 = sm.ent[1][tid], x2 = sm.ent[2][tid], w = sm.ent[3][tid];
+    const double w = sm.ent[3][tid];
     for (int ci = 0; ci < nc; ++ci) {
       const int cand = pcount ? sm.kept : sm.cand_list[ci];
       const int mode = pcount ? 3 : (cand == 0 ? ph.mode[0] : ph.mode[1]);  // (no local-memory index)
       double lg[8];
       double m = -INFINITY;
-      bool nonpd = false;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        // gmm.cpp:176-178 log w + log_density (-inf when w == 0), without
-        // branches: the value is selected, the domain error (log_density on
-        // a non-PD covariance) flagged once below
-        double r[18];
-        comp_to_regs(sm.comp[cand][k], r);
-        const double v = r[1] + __fma_rn(-0.5, fast_q(r + 2, r + 5, r + 14, x0, x1, x2), r[17]);
-        const bool live = r[0] > 0.0, pd = r[16] > 0.0;
-        nonpd |= live && !pd;
-        lg[k] = (live && pd) ? v : -INFINITY;
+        lg[k] = G.gam[ci * 8 + k][tid];
         m = fmax(m, lg[k]);
       }
-      if (nonpd) atomicCAS(p.status, 0, kEDomain);
       const bool fin = isfinite(m);
       double ek[8], s = 0.0;
 #pragma unroll
