@@ -24,7 +24,7 @@ __device__ __forceinline__ double node_score(const DNode* __restrict__ g, double
                                              double y2, int* status) {
   const double w = g->weight;
   const double lam2 = g->lam[2];
-  const double q = fast_q(g->mean, g->axT, g->il, y0, y1, y2);
+  const double q = fast_q(g->mean, g->prec, y0, y1, y2);
   const double sc = __dmul_rn(w, trg_exp(__fma_rn(-0.5, q, g->log_norm)));
   if (!(w > 0.0)) return 0.0;
   if (!(lam2 > 0.0)) {
@@ -39,7 +39,7 @@ __device__ __forceinline__ double node_score(const DNode* __restrict__ g, double
 __device__ __forceinline__ double node_score_nb(const DNode* __restrict__ g, double w, double y0,
                                                 double y1, double y2, bool& bad) {
   const double lam2 = g->lam[2];
-  const double q = fast_q(g->mean, g->axT, g->il, y0, y1, y2);
+  const double q = fast_q(g->mean, g->prec, y0, y1, y2);
   const double sc = __dmul_rn(w, trg_exp(__fma_rn(-0.5, q, g->log_norm)));
   const bool live = w > 0.0;
   bad = bad || (live && !(lam2 > 0.0));

@@ -141,16 +141,17 @@ struct BuildParams {
 
 // ----------------------------------------------------------------- helpers
 
-__device__ __forceinline__ void comp_to_regs(const GComp& c, double r[18]) {
+// The scoring fields of a component: w, log w, mean, precision, log_norm,
+// 1/lam_min (positive iff the covariance is PD).
+__device__ __forceinline__ void comp_to_regs(const GComp& c, double r[13]) {
   r[0] = c.w;
   r[1] = c.lw;
 #pragma unroll
   for (int i = 0; i < 3; ++i) r[2 + i] = c.mean[i];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) r[5 + i] = c.axT[i];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) r[14 + i] = c.il[i];
-  r[17] = c.log_norm;
+  for (int i = 0; i < 6; ++i) r[5 + i] = c.prec[i];
+  r[11] = c.log_norm;
+  r[12] = c.il[2];
 }
 
 // Deterministic block sum of NV values per thread; results in out[0..NV) (smem).
@@ -360,14 +361,14 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     // gmm.cpp:176-178 log w + log_density (-inf when w == 0), without
     // branches: the value is selected, the domain error (log_density on a
     // non-PD covariance) flagged once per component
-    double r[18];
+    double r[13];
     comp_to_regs(sm.comp[cand][k], r);
-    const bool live = r[0] > 0.0, pd = r[16] > 0.0;
+    const bool live = r[0] > 0.0, pd = r[12] > 0.0;
     if (lane == 0 && live && !pd && tlen > 0) atomicCAS(p.status, 0, kEDomain);
 #pragma unroll 4
     for (int e = lane; e < tlen; e += 32) {
       const double v =
-          r[1] + __fma_rn(-0.5, fast_q(r + 2, r + 5, r + 14, sm.ent[0][e], sm.ent[1][e], sm.ent[2][e]), r[17]);
+          r[1] + __fma_rn(-0.5, fast_q(r + 2, r + 5, sm.ent[0][e], sm.ent[1][e], sm.ent[2][e]), r[11]);
       G.gam[item][e] = (live && pd) ? v : -INFINITY;
     }
   }
@@ -593,6 +594,7 @@ __device__ void node_mstep_warp(const BuildParams& p, const Phase& ph, int k, co
     g.lam[i] = r.lam[i];
     g.il[i] = r.il[i];
   }
+  for (int i = 0; i < 6; ++i) g.prec[i] = r.prec[i];
   g.log_norm = r.log_norm;
 }
 
@@ -1527,6 +1529,7 @@ __device__ void cal_leaf(const BuildParams& p, const CalCtx& cx, int j, const do
     nd.lam[i] = g.lam[i];
     nd.il[i] = 1.0 / g.lam[i];
   }
+  for (int i = 0; i < 6; ++i) nd.prec[i] = g.prec[i];
   nd.log_norm = g.log_norm;
   const double tr = (g.lam[0] + g.lam[1]) + g.lam[2];
   nd.cplx = tr > 0.0 ? g.lam[2] / tr : -1.0;

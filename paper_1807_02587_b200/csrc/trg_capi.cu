@@ -417,6 +417,7 @@ static int tree_upload(trg_ctx* ctx, const trg_tree* h, bool refresh, trg_tree_d
       for (int k = 0; k < 3; ++k) d.axT[3 * r + k] = refresh ? (r == k) : h->axes[9 * i + 3 * k + r];
     }
     for (int r = 0; r < 3; ++r) d.il[r] = 1.0 / d.lam[r];
+    set_prec(d.axT, d.il, d.prec);
     d.pad = 0.0;
     d.log_norm = refresh ? 0.0 : h->log_norm[i];
     d.weight = h->weight[i];

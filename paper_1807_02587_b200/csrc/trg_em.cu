@@ -1205,6 +1205,7 @@ int trg_solve_mstep_vps(trg_ctx* ctx, int n_vps, const double* pi_star, const do
       d.il[r] = 1.0 / d.lam[r];
       for (int k = 0; k < 3; ++k) d.axT[3 * r + k] = comp_axes[9 * v + 3 * k + r];
     }
+    set_prec(d.axT, d.il, d.prec);
     pimu[4 * v] = pi_star[v];
     for (int k = 0; k < 3; ++k) pimu[4 * v + 1 + k] = mu_star[3 * v + k];
   }

@@ -132,7 +132,7 @@ __device__ __forceinline__ double flat_logp(const FlatParams& p, int k, double x
   const double lwk = p.lw[k];
   if (!(lwk > -INFINITY)) return -INFINITY;
   const DNode& g = p.nodes[k];
-  const double q = fast_q(g.mean, g.axT, g.il, x0, x1, x2);
+  const double q = fast_q(g.mean, g.prec, x0, x1, x2);
   return lwk + __fma_rn(-0.5, q, g.log_norm);
 }
 

@@ -15,8 +15,9 @@ struct GComp {
   double log_norm;
   double cov[9];
   double il[3];  // 1 / lam
+  double prec[6];  // precision matrix for fast_q (set_prec)
 };
-static_assert(sizeof(GComp) == 240, "GComp layout");
+static_assert(sizeof(GComp) == 288, "GComp layout");
 
 // set_floored_cov (gmm.cpp:143-150) into a GComp.
 static __device__ __noinline__ int comp_set_cov(GComp& g, const double sc[3][3], double floor_value,
@@ -34,6 +35,7 @@ static __device__ __noinline__ int comp_set_cov(GComp& g, const double sc[3][3],
     }
   }
   g.log_norm = log_norm_of(lam);
+  set_prec(g.axT, g.il, g.prec);
   return kOk;
 }
 
@@ -48,6 +50,7 @@ __device__ __forceinline__ void write_dnode_from_comp(DNode& d, double* cov9, co
     d.lam[i] = g.lam[i];
     d.il[i] = 1.0 / g.lam[i];
   }
+  for (int i = 0; i < 6; ++i) d.prec[i] = g.prec[i];
   d.pad = 0.0;
   d.log_norm = g.log_norm;
   d.weight = w;
@@ -76,6 +79,7 @@ static __device__ __noinline__ int refresh_node(DNode& d, const double* cov9, bo
     for (int j = 0; j < 3; ++j) d.axT[3 * i + j] = ax[j][i];
   }
   d.log_norm = log_norm_of(lam);
+  set_prec(d.axT, d.il, d.prec);
   const double tr = (lam[0] + lam[1]) + lam[2];
   d.cplx = tr > 0.0 ? lam[2] / tr : -1.0;
   return kOk;
@@ -97,6 +101,7 @@ __device__ __forceinline__ int comp_set_cov_cf(GComp& g, const double sc[3][3], 
     }
   }
   g.log_norm = log_norm_of(lam);
+  set_prec(g.axT, g.il, g.prec);
   return rc;
 }
 
@@ -114,6 +119,7 @@ __device__ __forceinline__ int refresh_node_cf(DNode& d, const double* cov9, boo
     for (int j = 0; j < 3; ++j) d.axT[3 * i + j] = ax[j][i];
   }
   d.log_norm = log_norm_of(lam);
+  set_prec(d.axT, d.il, d.prec);
   const double tr = (lam[0] + lam[1]) + lam[2];
   d.cplx = tr > 0.0 ? lam[2] / tr : -1.0;
   return kOk;
