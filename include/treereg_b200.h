@@ -116,6 +116,11 @@ typedef struct {
   double* ll_traces;
   int ll_trace_capacity;
   int n_expansions;
+  /* trg_build_flat_gmm only: the flat fit's per-iteration log-likelihoods
+   * (gmm.cpp:729-734, em_iterations_per_node * max_level values) are written
+   * contiguously at ll_traces when ll_trace_capacity *
+   * (em_iterations_per_node + 1) holds them; their count goes here. */
+  int flat_trace_len;
 } trg_build_diag;
 
 /* treereg::MStepSolution, mstep.hpp:54-61 */

@@ -57,7 +57,8 @@ class BuildDiagC(C.Structure):
     _fields_ = [("entries_per_round", C.c_uint64 * 8), ("expanded_per_round", C.c_int * 8),
                 ("calibration_passes", C.c_int), ("calibration_drift", C.c_double),
                 ("calib_density_evaluations", C.c_uint64), ("ll_traces", dp),
-                ("ll_trace_capacity", C.c_int), ("n_expansions", C.c_int)]
+                ("ll_trace_capacity", C.c_int), ("n_expansions", C.c_int),
+                ("flat_trace_len", C.c_int)]
 
 
 class MStepSolutionC(C.Structure):

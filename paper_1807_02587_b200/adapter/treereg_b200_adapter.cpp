@@ -20,6 +20,7 @@
 //   register_icp_pt2pt      registration.hpp:64-66 -> trg_register_clouds (icp)
 //   build_flat_gmm          gmm.hpp:74-76          -> trg_build_flat_gmm
 //   responsibilities_dense  association.hpp:44-47  -> trg_responsibilities_dense
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -370,9 +371,17 @@ std::vector<GaussianComponent> build_flat_gmm(const PointCloud& cloud, std::size
   if (!cloud.all_finite()) throw std::invalid_argument("point cloud has non-finite coordinates");
   const trg_model_config mc = model_cfg(config);
   DevTree dt;
-  check(trg_build_flat_gmm(ctx(), xyz(cloud), cloud.size(), 0, j, &mc, &dt.h, nullptr),
+  // the flat fit's per-iteration log-likelihoods (gmm.cpp:729-734)
+  const int iters = std::max(1, config.em_iterations_per_node * config.max_level);
+  std::vector<double> trace(static_cast<size_t>(iters));
+  trg_build_diag d{};
+  d.ll_traces = trace.data();
+  d.ll_trace_capacity = (iters + config.em_iterations_per_node) / (config.em_iterations_per_node + 1);
+  check(trg_build_flat_gmm(ctx(), xyz(cloud), cloud.size(), 0, j, &mc, &dt.h,
+                           diagnostics != nullptr ? &d : nullptr),
         "build_flat_gmm");
-  if (diagnostics != nullptr) diagnostics->node_ll_traces.emplace_back();
+  if (diagnostics != nullptr)
+    diagnostics->node_ll_traces.emplace_back(trace.begin(), trace.begin() + d.flat_trace_len);
   return download(dt.h).nodes;
 }
 

@@ -545,10 +545,21 @@ int flat_build(trg_ctx* ctx, const double* dev, size_t n, size_t J, const trg_mo
   tree->max_level = 1;
   tree->root_count = (int)J;
   if (diag) {
+    double* traces = diag->ll_traces;
+    const int tcap = diag->ll_trace_capacity;
     *diag = trg_build_diag{};
     diag->entries_per_round[0] = n;
     diag->expanded_per_round[0] = 1;
-    diag->n_expansions = 0;  // the flat fit's trace has em_iterations * max_level values
+    diag->n_expansions = 0;
+    diag->ll_traces = traces;
+    diag->ll_trace_capacity = tcap;
+    if (traces && iters > 0 &&
+        (size_t)tcap * (size_t)(cfg->em_iterations_per_node + 1) >= (size_t)iters) {
+      TRG_CU(cudaMemcpyAsync(traces, p.ll_trace, sizeof(double) * (size_t)iters,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+      TRG_CU(cudaStreamSynchronize(ctx->stream));
+      diag->flat_trace_len = iters;
+    }
   }
   *out = tree;
   return TRG_OK;

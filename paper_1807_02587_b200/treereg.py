@@ -637,10 +637,17 @@ def build_flat_gmm(cloud, j: int, config: ModelConfig = ModelConfig(),
     cfg = config.c()
     h = C.c_void_p()
     d = BuildDiagC()
+    iters = max(1, config.em_iterations_per_node * config.max_level)
+    trace = np.zeros(iters)
+    if diagnostics is not None:  # one row of em_iterations_per_node + 1 values per capacity unit
+        d.ll_traces = _d(trace)
+        d.ll_trace_capacity = -(-iters // (config.em_iterations_per_node + 1))
     _chk(_lib.lib().trg_build_flat_gmm(ctx.h, ptr, n, on_dev, int(j), C.byref(cfg), C.byref(h),
                                        C.byref(d)))
     if diagnostics is not None:
         diagnostics.entries_per_round = [int(d.entries_per_round[0])]
+        # gmm.cpp:729-734: the flat fit's EM log-likelihood trace
+        diagnostics.node_ll_traces = [trace[:d.flat_trace_len].copy()]
     return GmmTree(h, ctx)
 
 

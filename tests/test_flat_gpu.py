@@ -28,9 +28,15 @@ def _relerr_rows(a, b):
 def test_flat_build_matches_reference(ctx, name):
     tr = _tr()
     g = load_flat(name)
+    diag = tr.BuildDiagnostics()
     mix = tr.build_flat_gmm(g["points"], int(g["J"]), tr.ModelConfig(rng_seed=int(g["seed"])),
-                            ctx=ctx)
+                            diag, ctx=ctx)
     h, G = mix.host(), g["mix"]
+    # the flat fit's EM log-likelihood trace (gmm.cpp:729-734, BuildDiagnostics)
+    assert len(diag.node_ll_traces) == 1
+    ll = np.asarray(diag.node_ll_traces[0])
+    assert ll.shape == g["ll_trace"].shape
+    assert np.abs(ll - g["ll_trace"]).max() <= 1e-8 * np.abs(g["ll_trace"]).max()
     assert len(h["weight"]) == int(g["J"])
     assert np.array_equal(h["weight"] == 0.0, G["weight"] == 0.0)  # same dormant set
     live = G["weight"] > 0
