@@ -321,111 +321,136 @@ static __device__ void warp_eig6(const double* in, double ev[6], Eig6Smem& w) {
   __syncwarp();
 }
 
-// solve_mstep (mstep.cpp:76-98) from the reduced normal equations, by one
-// warp: parallel eigenvalues for the condition estimate, then LDLT + exp map
-// on lane 0.  Result in *o (valid after the call on all lanes).
-// ldlt_solve6_tr (trg_math.cuh: LDLT with diagonal pivoting, the shim's
-// Eigen::LDLT) by one warp through shared memory: the same operations per
-// element in the same order, the pivot swaps as one symmetric permutation,
-// each step's column of L and trailing update in parallel, the two
-// triangular solves on lane 0, L^-1 by columns in parallel for tr(A^-1).
-struct Ldlt6Smem {
-  double a[36], l[36], m[36], d[6], y[6];
+// ldlt_solve6_tr (trg_math.cuh: LDLT with diagonal pivoting -- first largest
+// |a_ii| -- the shim's Eigen::LDLT), the two triangular solves and tr(A^-1)
+// = sum_k (1/d_k) sum_{i<=k} (L^-1)_ki^2, on ONE thread with everything in
+// registers: the row/column exchanges are compare-selects over the static
+// candidates, so no shared-memory round trip sits on the dependency chain
+// (the warp-parallel shared-memory version it replaces spent ~14 us per EM
+// iteration on its ~100 serialised steps).
+__device__ __forceinline__ void ldlt_solve6_tr_reg(const double* A, const double* b, double x[6],
+                                                   double* trace_inv, double* min_pivot) {
+  double a[6][6], l[6][6], d[6];
   int perm[6];
-};
-
-static __device__ void warp_ldlt_solve6_tr(const double* A, const double* b, double x[6],
-                                           double* trace_inv, double* min_pivot, Ldlt6Smem& w) {
-  const int lane = threadIdx.x & 31;
-  for (int e = lane; e < 36; e += 32) {
-    w.a[e] = A[e];
-    w.l[e] = (e / 6 == e % 6) ? 1.0 : 0.0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    perm[i] = i;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      a[i][j] = A[i * 6 + j];
+      l[i][j] = i == j ? 1.0 : 0.0;
+    }
   }
-  if (lane < 6) w.perm[lane] = lane;
-  __syncwarp();
+#pragma unroll
   for (int k = 0; k < 6; ++k) {
-    int p = k;  // every lane finds the same pivot (first largest |a_ii|)
+    int p = k;
+    double best = fabs(a[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i) {
+      const double v = fabs(a[i][i]);
+      if (v > best) {
+        best = v;
+        p = i;
+      }
+    }
+    // exchange rows / columns k <-> p of a, rows k <-> p of L's first k columns
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i) {
+      const bool sw = p == i;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        const double t = a[k][j];
+        a[k][j] = sw ? a[i][j] : t;
+        a[i][j] = sw ? t : a[i][j];
+      }
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        const double t = a[j][k];
+        a[j][k] = sw ? a[j][i] : t;
+        a[j][i] = sw ? t : a[j][i];
+      }
+#pragma unroll
+      for (int j = 0; j < k; ++j) {
+        const double t = l[k][j];
+        l[k][j] = sw ? l[i][j] : t;
+        l[i][j] = sw ? t : l[i][j];
+      }
+      const int tp = perm[k];
+      perm[k] = sw ? perm[i] : tp;
+      perm[i] = sw ? tp : perm[i];
+    }
+    const double dk = a[k][k];
+    d[k] = dk;
+#pragma unroll
+    for (int i = k + 1; i < 6; ++i) l[i][k] = (dk != 0.0) ? a[i][k] / dk : 0.0;
+#pragma unroll
     for (int i = k + 1; i < 6; ++i)
-      if (fabs(w.a[i * 6 + i]) > fabs(w.a[p * 6 + p])) p = i;
-    if (p != k) {  // warp-uniform: rows and columns k <-> p, and L's rows below k
-      double v0 = 0.0, v1 = 0.0, lk = 0.0, lp = 0.0;
-      const auto sg = [&](int i) { return i == k ? p : (i == p ? k : i); };
-      v0 = w.a[sg(lane / 6) * 6 + sg(lane % 6)];
-      if (lane + 32 < 36) v1 = w.a[sg((lane + 32) / 6) * 6 + sg((lane + 32) % 6)];
-      if (lane < k) {
-        lk = w.l[k * 6 + lane];
-        lp = w.l[p * 6 + lane];
-      }
-      __syncwarp();
-      w.a[lane] = v0;
-      if (lane + 32 < 36) w.a[lane + 32] = v1;
-      if (lane < k) {
-        w.l[k * 6 + lane] = lp;
-        w.l[p * 6 + lane] = lk;
-      }
-      if (lane == 0) {
-        const int t = w.perm[k];
-        w.perm[k] = w.perm[p];
-        w.perm[p] = t;
-      }
-      __syncwarp();
-    }
-    const double dk = w.a[k * 6 + k];
-    if (lane == 0) w.d[k] = dk;
-    if (lane > k && lane < 6) w.l[lane * 6 + k] = (dk != 0.0) ? w.a[lane * 6 + k] / dk : 0.0;
-    __syncwarp();
-    for (int e = lane; e < 36; e += 32) {
-      const int i = e / 6, j = e % 6;
-      if (i > k && j > k) w.a[e] = w.a[e] - w.l[i * 6 + k] * dk * w.l[j * 6 + k];
-    }
-    __syncwarp();
+#pragma unroll
+      for (int j = k + 1; j < 6; ++j) a[i][j] = a[i][j] - l[i][k] * dk * l[j][k];
   }
-  // M = L^{-1}: lane j < 6 builds column j
-  if (lane < 6) {
-    const int j = lane;
-    double mc[6];
-    for (int i = 0; i < 6; ++i) mc[i] = (i == j) ? 1.0 : 0.0;
+  // the triangular solves (permuted right-hand side)
+  double y[6], z[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double v = b[0];
+#pragma unroll
+    for (int q = 1; q < 6; ++q) v = perm[i] == q ? b[q] : v;
+    y[i] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double s2 = y[i];
+#pragma unroll
+    for (int j = 0; j < i; ++j) s2 -= l[i][j] * y[j];
+    y[i] = s2;
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) y[i] = (d[i] != 0.0) ? y[i] / d[i] : 0.0;
+#pragma unroll
+  for (int i = 5; i >= 0; --i) {
+    double s2 = y[i];
+#pragma unroll
+    for (int j = i + 1; j < 6; ++j) s2 -= l[j][i] * z[j];
+    z[i] = s2;
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double v = z[0];
+#pragma unroll
+    for (int q = 1; q < 6; ++q) v = perm[q] == i ? z[q] : v;
+    x[i] = v;
+  }
+  // tr(A^{-1}) = sum_k (1/d_k) sum_{i <= k} M_ki^2 with M = L^{-1}, in k order
+  double m[6][6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) m[i][j] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
     for (int i = j + 1; i < 6; ++i) {
-      double s = 0.0;
-      for (int k = j; k < i; ++k) s -= w.l[i * 6 + k] * mc[k];
-      mc[i] = s;
+      double s2 = 0.0;
+#pragma unroll
+      for (int k = j; k < i; ++k) s2 -= l[i][k] * m[k][j];
+      m[i][j] = s2;
     }
-    for (int i = 0; i < 6; ++i) w.m[i * 6 + j] = mc[i];
   }
-  if (lane == 0) {  // the triangular solves
-    double y[6], z[6];
-    for (int i = 0; i < 6; ++i) y[i] = b[w.perm[i]];
-    for (int i = 0; i < 6; ++i) {
-      double s = y[i];
-      for (int j = 0; j < i; ++j) s -= w.l[i * 6 + j] * y[j];
-      y[i] = s;
-    }
-    for (int i = 0; i < 6; ++i) y[i] = (w.d[i] != 0.0) ? y[i] / w.d[i] : 0.0;
-    for (int i = 5; i >= 0; --i) {
-      double s = y[i];
-      for (int j = i + 1; j < 6; ++j) s -= w.l[j * 6 + i] * z[j];
-      z[i] = s;
-    }
-    for (int i = 0; i < 6; ++i) w.y[w.perm[i]] = z[i];
-  }
-  __syncwarp();
-  // tr(A^{-1}) = sum_k (1/d_k) sum_{i <= k} M_ki^2, in k order
-  double sk = 0.0;
-  if (lane < 6)
-    for (int i = 0; i <= lane; ++i) sk += w.m[lane * 6 + i] * w.m[lane * 6 + i];
-  double tr = 0.0, mind = w.d[0];
+  double tr = 0.0, mind = d[0];
+#pragma unroll
   for (int k = 0; k < 6; ++k) {
-    const double s = __shfl_sync(0xffffffffu, sk, k);
-    const double dk = w.d[k];
-    mind = dk < mind ? dk : mind;
-    tr += (dk > 0.0) ? s / dk : INFINITY;
+    double sk = 0.0;
+#pragma unroll
+    for (int i = 0; i <= k; ++i) sk += m[k][i] * m[k][i];
+    mind = d[k] < mind ? d[k] : mind;
+    tr += (d[k] > 0.0) ? sk / d[k] : INFINITY;
   }
-  for (int i = 0; i < 6; ++i) x[i] = w.y[i];
   *trace_inv = tr;
   *min_pivot = mind;
-  __syncwarp();
 }
 
+// solve_mstep (mstep.cpp:76-98) from the reduced normal equations, by one
+// warp: LDLT + tr(A^-1) on lane 0 (the condition bracket tr(A) tr(A^-1)),
+// the warp-parallel 6x6 Jacobi only when the bracket straddles 1e12, then
+// the exp map.  Result in *o (valid after the call on all lanes).
 static __device__ void warp_solve_normal_eq(const double* v, int nvp, SolveOut* o, Eig6Smem& w,
                                             Timeline* tl = nullptr, bool exact_cond = true) {
   const int lane = threadIdx.x & 31;
@@ -440,16 +465,15 @@ static __device__ void warp_solve_normal_eq(const double* v, int nvp, SolveOut* 
   }
   __shared__ double ata_s[36];
   __shared__ int s_need_eig;
-  __shared__ Ldlt6Smem ls;
   for (int e = lane; e < 36; e += 32) {
     const int i = e / 6, j = e % 6;
     const int a = i < j ? i : j, b = i < j ? j : i;
     ata_s[e] = v[a * 6 - a * (a - 1) / 2 + (b - a)];
   }
   __syncwarp();
-  double x[6], trinv, mind;
+  double x[6], trinv = 0.0, mind = 0.0;
   if (tl && lane == 0) tl_mark_any(tl, 7004);
-  warp_ldlt_solve6_tr(ata_s, v + 21, x, &trinv, &mind, ls);
+  if (lane == 0) ldlt_solve6_tr_reg(ata_s, v + 21, x, &trinv, &mind);
   if (tl && lane == 0) tl_mark_any(tl, 7005);
   if (lane == 0) {
     o->nvp = nvp;
