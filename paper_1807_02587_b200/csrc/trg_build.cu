@@ -1286,7 +1286,9 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
         continue;
       }
       if (mine) {
-        // (a) tile pass
+        // (a) tile pass (the phase's reduction items are listed first, off the
+        // critical path: the lists live outside the tile scratch)
+        if (tid == 0) sm.nitems = phase_items(ph, sm.item_off, sm.item_kind);
         const int T = __ldcg(&st->Tp[par]);
         int ntl = 0, nent = 0;
         for (int t = cta; t < T; t += G) {
@@ -1303,8 +1305,6 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
         tl_mark(p.tl, round * 100 + ph_i);
         // (b) per-node reduction of the tile records (+ node update when the
         // whole cloud is here)
-        if (tid == 0) sm.nitems = phase_items(ph, sm.item_off, sm.item_kind);
-        __syncthreads();
         const int NI = sm.nitems;
         const int K = __ldcg(&st->Kp[par]);
         for (int it = cta * (kTile / 32) + warp; it < K * NI; it += G * (kTile / 32)) {
