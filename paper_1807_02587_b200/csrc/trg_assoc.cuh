@@ -260,7 +260,8 @@ __device__ __forceinline__ void stage_nodes_bulk(DNode* snodes, const DNode* nod
     fence_proxy_async_global();
     bulk_g2s_issue(snodes, nodes, (unsigned)(S * sizeof(DNode)), bar);
   }
-  mbar_wait(bar, phase);
+  if (threadIdx.x == 0) mbar_wait(bar, phase);
+  __syncthreads();
   phase ^= 1u;
 }
 

@@ -105,6 +105,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void spin_guard(unsigned long long t0) {
   if (gtimer() - t0 > 10000000000ull) __trap();
 }
+// The same, reading the clock only every 64th poll (the polls stay cheap:
+// a polling thread shares its SM's issue slots with working CTAs).
+__device__ __forceinline__ void spin_guard_every(unsigned long long t0, unsigned& polls) {
+  if ((++polls & 63u) == 0u) spin_guard(t0);
+}
 __device__ __forceinline__ void tl_mark_any(Timeline* tl, int label) {
   const int i = atomicAdd(&tl->n, 1);
   if (i < 1024) {

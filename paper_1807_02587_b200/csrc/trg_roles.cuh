@@ -98,12 +98,12 @@ static __device__ Roles assign_roles(unsigned* smtab, unsigned* bar, int G, int 
 __device__ __forceinline__ void wait_flag(const unsigned* flag, unsigned s) {
   __syncthreads();
   if (threadIdx.x == 0 && ld_acquire_u32(flag) < s) {
-    unsigned ns = 32;
+    unsigned ns = 32, polls = 0;
     const unsigned long long t0 = gtimer();
     while (ld_acquire_u32(flag) < s) {
       __nanosleep(ns);
       ns = ns < 128 ? 2 * ns : 128;
-      spin_guard(t0);
+      spin_guard_every(t0, polls);
     }
   }
   __syncthreads();
@@ -114,9 +114,10 @@ __device__ __forceinline__ void wait_count(const unsigned* cnt, unsigned target)
   __syncthreads();
   if (threadIdx.x == 0 && ld_acquire_u32(cnt) < target) {
     const unsigned long long t0 = gtimer();
+    unsigned polls = 0;
     while (ld_acquire_u32(cnt) < target) {
       __nanosleep(32);
-      spin_guard(t0);
+      spin_guard_every(t0, polls);
     }
   }
   __syncthreads();

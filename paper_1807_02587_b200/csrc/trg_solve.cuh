@@ -32,12 +32,12 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks) {
     const unsigned old = atom_add_acq_rel(&bar[0], 1u);
     const unsigned target = (old / nblocks + 1u) * nblocks;
     if (old + 1u != target) {
-      unsigned ns = 32;
+      unsigned ns = 32, polls = 0;
       const unsigned long long t0 = gtimer();
       while ((int)(ld_acquire_u32(&bar[0]) - target) < 0) {
         __nanosleep(ns);
         ns = ns < 128 ? 2 * ns : 128;
-        spin_guard(t0);
+        spin_guard_every(t0, polls);
       }
     }
   }
