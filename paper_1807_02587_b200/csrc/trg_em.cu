@@ -978,13 +978,23 @@ __global__ void k_bbox(const double* __restrict__ p, size_t n, double* part, uns
     last = atomicAdd(cnt, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last && threadIdx.x < 32) {
+    // the partials over the lanes of one warp (min / max are exact in any
+    // order), then a shuffle reduction
     __threadfence();
-    for (int b = 0; b < (int)gridDim.x; ++b)
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32)
       for (int k = 0; k < 3; ++k) {
         l[k] = smin(l[k], __ldcg(&part[6 * b + k]));
         h[k] = smax(h[k], __ldcg(&part[6 * b + 3 + k]));
       }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      for (int k = 0; k < 3; ++k) {
+        l[k] = smin(l[k], __shfl_xor_sync(0xffffffffu, l[k], o));
+        h[k] = smax(h[k], __shfl_xor_sync(0xffffffffu, h[k], o));
+      }
+  }
+  if (last && threadIdx.x == 0) {
     double s = (h[0] - l[0]) * (h[0] - l[0]);
     s += (h[1] - l[1]) * (h[1] - l[1]);
     s += (h[2] - l[2]) * (h[2] - l[2]);
