@@ -72,6 +72,13 @@ typedef struct {
   double initial_R[9];     /* identity */
   double initial_t[3];     /* zero */
   trg_model_config model_config;
+  /* Not in the reference (0 there, the parity mode): 1 = the EM's
+   * association scores in FP32 (SURVEY 7.2 fast path; adaptive:L / tree:L
+   * only): the point-minus-mean differences stay FP64, the quadratic form,
+   * log-scores and normalisation are FP32, the deposits FP64.  Stop nodes can
+   * differ from the reference's where the top two sibling log-scores are
+   * within ~1e-5; transforms agree within the north_star tolerance. */
+  int fast_scoring;
 } trg_reg_config;
 
 /* Host-side tree: treereg::GmmTree (gmm.hpp:56-67) + cached eigen data of

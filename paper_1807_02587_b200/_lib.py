@@ -37,7 +37,8 @@ class RegConfigC(C.Structure):
     _fields_ = [("variant_kind", C.c_int), ("variant_param", C.c_int), ("lambda_c", C.c_double),
                 ("max_em_iterations", C.c_int), ("rotation_tol", C.c_double),
                 ("translation_tol", C.c_double), ("initial_R", C.c_double * 9),
-                ("initial_t", C.c_double * 3), ("model_config", ModelConfigC)]
+                ("initial_t", C.c_double * 3), ("model_config", ModelConfigC),
+                ("fast_scoring", C.c_int)]
 
 
 class TreeC(C.Structure):

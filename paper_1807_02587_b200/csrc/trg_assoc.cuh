@@ -247,6 +247,133 @@ __device__ void assoc_fx_pass(const AssocParams& p, const double* Rt_smem, const
   }
 }
 
+// ------------------------------------------------------------ FP32 fast path
+// (trg_reg_config.fast_scoring) The EM's descent with FP32
+// scores: per node a 64-byte record (mean kept FP64 so the point-minus-mean
+// difference is exact to FP64 rounding, precision matrix and log(w) +
+// log_norm in FP32), the argmax and normaliser in the log domain (the
+// maximum's sibling has score ratio 1, the path weight is 1 / sum of
+// exp(ls_k - max)), the reference's underflow rules as log-thresholds.
+struct __align__(16) FNode {
+  double mean[3];
+  float prec[6];   // fast_q's packed precision matrix
+  float lwn;       // log(weight) + log_norm; -inf when weight == 0 (or not PD)
+  float cplx;      // node complexity (-1: no positive trace)
+  int first_child;
+  short child_count;
+  short bad;       // weight > 0 but the covariance is not PD (log_density throws)
+};
+static_assert(sizeof(FNode) == 64, "FNode layout");
+
+__device__ __forceinline__ void fnode_from(const DNode& d, FNode& f) {
+  for (int i = 0; i < 3; ++i) f.mean[i] = d.mean[i];
+  for (int i = 0; i < 6; ++i) f.prec[i] = (float)d.prec[i];
+  const bool live = d.weight > 0.0, pd = d.lam[2] > 0.0;
+  f.lwn = (live && pd) ? (float)(log(d.weight) + d.log_norm) : -INFINITY;
+  f.cplx = (float)d.cplx;
+  f.first_child = d.first_child;
+  f.child_count = (short)d.child_count;
+  f.bad = (live && !pd) ? 1 : 0;
+}
+
+__device__ __forceinline__ Descent descend_f32(const FNode* __restrict__ nodes, const FNode* snodes,
+                                               int n_snodes, int root_count, int depth,
+                                               float lambda_c, double y0, double y1, double y2,
+                                               int* status) {
+  Descent r{-1, 1.0, 0};
+  int node = -1;
+  for (int l = 0; l < depth; ++l) {
+    const FNode* cur = node < n_snodes ? snodes + node : nodes + node;
+    const int first = node < 0 ? 0 : cur->first_child;
+    const int count = node < 0 ? root_count : cur->child_count;
+    const FNode* sib = first + count <= n_snodes ? snodes + first : nodes + first;
+    float ls[8];
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const FNode& g = sib[k < count ? k : 0];
+      const float d0 = (float)(y0 - g.mean[0]), d1 = (float)(y1 - g.mean[1]), d2 = (float)(y2 - g.mean[2]);
+      const float u0 = fmaf(g.prec[2], d2, fmaf(g.prec[1], d1, g.prec[0] * d0));
+      const float u1 = fmaf(g.prec[4], d2, g.prec[3] * d1);
+      const float q = fmaf(d0, u0, fmaf(d1, u1, g.prec[5] * d2 * d2));
+      bad = bad || (k < count && g.bad);
+      ls[k] = k < count ? fmaf(-0.5f, q, g.lwn) : -INFINITY;
+    }
+    if (bad) atomicCAS(status, 0, kEDomain);  // log_density: covariance is not PD
+    float m = ls[0];
+    int best = 0;
+#pragma unroll
+    for (int k = 1; k < 8; ++k)
+      if (ls[k] > m) {  // strict '>' : lowest index wins ties
+        m = ls[k];
+        best = k;
+      }
+    float s = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += __expf(ls[k] - m);
+    r.evals += count;
+    const float logsum = m + __logf(s);  // NaN when every score is -inf
+    if (l == 0 && !(logsum > -690.7755f)) {  // sum <= 1e-300: outlier
+      r.node = -1;
+      return r;
+    }
+    if (!(logsum > -744.44f)) break;  // the FP64 sum would underflow to 0: keep the current node
+    node = first + best;
+    r.path *= (double)(1.0f / s);
+    const FNode* nd = sib + best;
+    if (nd->child_count == 0) break;
+    if (nd->cplx < 0.0f) {
+      atomicCAS(status, 0, kEDomain);  // node_complexity: no positive trace
+      break;
+    }
+    if (nd->cplx <= lambda_c) break;
+  }
+  r.node = node;
+  return r;
+}
+
+// assoc_fx_pass with the FP32 descent (same windows, deposits and counters).
+template <int NM>
+__device__ void assoc_fx_pass_f32(const AssocParams& p, const FNode* fnodes, const FNode* fstage,
+                                  const double* Rt_smem, const FxScale* sc, int nwarps, int gwarp) {
+  constexpr int kOrd[10] = {0, 1, 1, 1, 2, 2, 2, 2, 2, 2};
+  const int lane = threadIdx.x & 31;
+  unsigned long long my_out = 0, my_ev = 0;
+  const size_t nwin = (p.n + 31) / 32;
+  const float lc = (float)p.lambda_c;
+  for (size_t w = gwarp; w < nwin; w += nwarps) {
+    const size_t i = w * 32 + lane;
+    int key = -1;
+    double v[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) v[m] = 0.0;
+    if (i < p.n) {
+      double y0, y1, y2;
+      apply_rt(Rt_smem, p.pts[3 * i], p.pts[3 * i + 1], p.pts[3 * i + 2], y0, y1, y2);
+      const Descent d = descend_f32(fnodes, fstage, p.n_snodes, p.root_count, p.depth, lc, y0, y1,
+                                    y2, p.status);
+      my_ev += d.evals;
+      if (d.node < 0) {
+        ++my_out;
+      } else {
+        key = d.node;
+        deposit_values<NM>(d.path, y0, y1, y2, v);
+      }
+    }
+    __syncwarp();
+    warp_run_deposit<NM>(key, v, p.acc, p.acc_stride, sc, kOrd);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    my_out += __shfl_xor_sync(0xffffffffu, my_out, off);
+    my_ev += __shfl_xor_sync(0xffffffffu, my_ev, off);
+  }
+  if (lane == 0 && (my_out | my_ev)) {
+    atomicAdd(&p.counters[0], my_out);
+    atomicAdd(&p.counters[1], my_ev);
+  }
+}
+
 // Stages nodes [0, S) into shared memory with one bulk copy (TMA engine),
 // completing on `bar` (phase bit `phase`, flipped on return).  Block-wide;
 // the nodes may have been rewritten by other CTAs before the caller's last

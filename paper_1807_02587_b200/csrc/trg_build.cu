@@ -1965,6 +1965,8 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
                                                p.tile_node[0], p.tile_start[0], p.tile_len[0],
                                                ctx->status, p.pmax_bits);
   ctx->launches += 1;
+  // the calibration's association reads a spatially sorted copy (trg_sort.cu)
+  TRG_TRY(morton_sorted_copy(ctx, pts, n, p.a.pmax, kSlotBuild2, kSlotBuild3, &p.a.pts));
   job->p = p;
   job->tree = tree;
   job->G = G;

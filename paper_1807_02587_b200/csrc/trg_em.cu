@@ -47,6 +47,10 @@ struct EmParams {
   // Queued behind an asynchronous build (register_clouds): the tree's size
   // comes from the build's published meta (nothing to do unless meta->ok).
   const TreeMeta* meta;
+  // FP32 fast path (trg_reg_config.fast_scoring): the tree as FNode records,
+  // converted by the launch's own CTAs before its first grid barrier
+  FNode* fnodes;
+  int fast;
 };
 
 constexpr int kAccStride = kNormalEq + 2;
@@ -432,6 +436,12 @@ __global__ void __launch_bounds__(kEmBlock, TRG_KEM_MINB) k_em_tree(EmParams p) 
   const size_t S = p.a.acc_stride;
   unsigned* flag = p.sync + 2;
   unsigned* arrived = p.sync + 3;
+  if (p.fast)  // the FP32 records, ordered before use by assign_roles' grid barrier
+    for (int j = blockIdx.x * blockDim.x + tid; j < J; j += G * blockDim.x) {
+      FNode f;
+      fnode_from(p.a.nodes[j], f);
+      p.fnodes[j] = f;
+    }
   const Roles r = assign_roles(p.smtab, p.sync, G, 1);
   if (r.upd && r.idx != 0) return;  // the solver's SM stays free of E-step work
   EmState* st = p.st;
@@ -443,8 +453,21 @@ __global__ void __launch_bounds__(kEmBlock, TRG_KEM_MINB) k_em_tree(EmParams p) 
     }
     __syncthreads();
     DNode* stage = reinterpret_cast<DNode*>(k_em_stage);
+    FNode* fstage = reinterpret_cast<FNode*>(k_em_stage);
     unsigned mphase = 0;
-    stage_nodes_bulk(stage, p.a.nodes, n_snodes, &mbar, mphase);  // the model is fixed
+    if (p.fast) {  // the model is fixed: its upper levels staged once
+      if (n_snodes > 0) {
+        if (tid == 0) {
+          fence_proxy_async_global();
+          bulk_g2s_issue(fstage, p.fnodes, (unsigned)(n_snodes * sizeof(FNode)), &mbar);
+          mbar_wait(&mbar, mphase);
+        }
+        __syncthreads();
+        mphase ^= 1u;
+      }
+    } else {
+      stage_nodes_bulk(stage, p.a.nodes, n_snodes, &mbar, mphase);
+    }
     AssocParams a = p.a;
     a.n_nodes = J;
     a.root_count = root_count;
@@ -461,7 +484,10 @@ __global__ void __launch_bounds__(kEmBlock, TRG_KEM_MINB) k_em_tree(EmParams p) 
       __syncthreads();
       a.acc = p.acc + (size_t)(it & 1) * S * 12;
       a.counters = p.a.counters + 2 * (it & 1);
-      assoc_fx_pass<4>(a, rt, sc, r.n_work * WPB, r.idx * WPB + warp);
+      if (p.fast)
+        assoc_fx_pass_f32<4>(a, p.fnodes, fstage, rt, sc, r.n_work * WPB, r.idx * WPB + warp);
+      else
+        assoc_fx_pass<4>(a, rt, sc, r.n_work * WPB, r.idx * WPB + warp);
       arrive_count(arrived);
       if (sharded) return;  // one E-step per segment
     }
@@ -843,6 +869,12 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
     p.psum = static_cast<double*>(ps);
   }
   p.n_total = sharded ? n_total : (double)n;
+  p.fast = (!dense && cfg->fast_scoring) ? 1 : 0;
+  if (p.fast) {
+    void* fb = nullptr;
+    TRG_TRY(ws_get(ctx, kSlotBuild9, sizeof(FNode) * (size_t)std::max(J, 1), &fb));
+    p.fnodes = static_cast<FNode*>(fb);
+  }
   TRG_TRY(timeline_reset(ctx));
   p.epoch0 = ctx->epoch + 1;
   ctx->epoch += (uint32_t)K + 1;
@@ -862,6 +894,8 @@ int em_prepare(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, si
   // non-finite check + max |coordinate| (the accumulators' scale)
   TRG_TRY(launch_absmax(ctx, src_dev, n, reinterpret_cast<unsigned long long*>(static_cast<char*>(cnt) + 64),
                         status));
+  // the E-steps read a spatially sorted copy (trg_sort.cu)
+  if (!dense) TRG_TRY(morton_sorted_copy(ctx, src_dev, n, p.a.pmax, kSlotBuild4, kSlotBuild5, &p.a.pts));
   k_extent<<<1, 256, 0, ctx->stream>>>(tree->nodes, J, p.st, target_diag, cfg->translation_tol,
                                        meta, diag_dev);
   ctx->launches += 1;

@@ -201,6 +201,11 @@ enum Slot : int {
 };
 
 int ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);
+// trg_sort.cu: a Morton-ordered copy of a large cloud for the association
+// passes (locality of the descents and of the deposit runs)
+constexpr size_t kSortMinPoints = 262144;
+int morton_sorted_copy(trg_ctx* ctx, const double* pts, size_t n, const double* pmax, int slot_pts,
+                       int slot_tmp, const double** out);
 
 // Every host<->device copy of the library goes through here (byte counters
 // back the e2e h2d/d2h figures of bench.py).  Pinned host buffers are copied

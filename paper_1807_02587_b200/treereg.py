@@ -220,6 +220,9 @@ class RegistrationConfig:  # registration.hpp:27-36
     initial_transform: RigidTransform = field(default_factory=RigidTransform)
     model_config: ModelConfig = field(default_factory=ModelConfig)
     deterministic: bool = True
+    # not in the reference: FP32 association scoring in the EM (SURVEY 7.2 fast
+    # path; off = the reference's FP64 parity mode)
+    fast_scoring: bool = False
 
     def c(self) -> RegConfigC:
         r = RegConfigC()
@@ -235,6 +238,7 @@ class RegistrationConfig:  # registration.hpp:27-36
         for k in range(3):
             r.initial_t[k] = float(self.initial_transform.translation[k])
         r.model_config = self.model_config.c()
+        r.fast_scoring = 1 if self.fast_scoring else 0
         return r
 
 
