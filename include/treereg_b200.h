@@ -273,11 +273,14 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target, con
  * (registration.hpp:53-55) and a caller loops; this entry point is that
  * loop.  Pair i registers sources[i] (n_sources[i] points) to targets[i]
  * with `cfg` and fills out[i] (trace pointers as in trg_reg_result, may be
- * NULL).  `streams` pairs (1..16; 0 = 4) run concurrently, each on its own
- * worker thread, CUDA stream and 1/streams of the SMs; results equal
- * trg_register_clouds on each pair up to rounding (the per-CTA reduction
- * tree follows the grid size).  Returns TRG_OK or the
- * status of the lowest-index failing pair (out[] of the others is filled). */
+ * NULL).  Tree variants (adaptive / tree): `streams` = pairs in flight
+ * (1..24; 0 = 16); the pairs run in waves, each wave's tree builds as ONE
+ * cooperative launch (one CTA group per pair, group barriers) and its EM
+ * loops as one more.  Flat / ICP variants: `streams` pairs (1..16; 0 = 4)
+ * run concurrently, each on its own worker thread, CUDA stream and
+ * 1/streams of the SMs.  Either way every pair's result is bit-identical to
+ * trg_register_clouds on that pair.  Returns TRG_OK or the status of the
+ * lowest-index failing pair (out[] of the others is filled). */
 int trg_register_batch(trg_ctx* ctx, int n_pairs, const double* const* targets,
                        const size_t* n_targets, const double* const* sources,
                        const size_t* n_sources, int on_device, const trg_reg_config* cfg,

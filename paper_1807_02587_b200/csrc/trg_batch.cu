@@ -1,5 +1,8 @@
-// trg_register_batch: independent frame pairs (BASELINE config C5) run as
-// concurrent registrations.  Each worker owns an SM-budgeted sub-context
+// trg_register_batch: independent frame pairs (BASELINE config C5).
+// Tree variants (adaptive / tree): waves of pairs whose builds and EMs run
+// as single cooperative launches, one CTA group per pair
+// (register_batch_fused, trg_em.cu).  Flat / ICP variants run as concurrent
+// registrations: each worker owns an SM-budgeted sub-context
 // (own stream, workspace and scratch tree; persistent grids sized to
 // device_sms / streams SMs: the budgets sum to the device, so the grids are
 // normally co-resident -- not guaranteed for plain launches, hence the spin
@@ -26,12 +29,20 @@ extern "C" int trg_register_batch(trg_ctx* ctx, int n_pairs, const double* const
     set_error("register_batch: bad argument");
     return TRG_EINVAL;
   }
-  if (streams == 0) streams = 4;
-  if (streams < 1 || streams > 16) {
-    set_error("register_batch: streams must be in 1..16");
+  const bool fused =
+      cfg && (cfg->variant_kind == TRG_VARIANT_ADAPTIVE || cfg->variant_kind == TRG_VARIANT_TREE);
+  if (streams == 0) streams = fused ? kBatchInflightDefault : 4;
+  if (streams < 1 || streams > (fused ? kBatchInflightMax : 16)) {
+    set_error(fused ? "register_batch: pairs in flight must be in 1..24"
+                    : "register_batch: streams must be in 1..16");
     return TRG_EINVAL;
   }
   if (n_pairs == 0) return TRG_OK;
+  if (fused) {
+    TRG_CU(cudaSetDevice(ctx->device));
+    return register_batch_fused(ctx, n_pairs, targets, n_targets, sources, n_sources, on_device,
+                                cfg, streams, out);
+  }
   streams = std::min(streams, n_pairs);
   const int budget = std::max(1, ctx->device_sms / streams);
   while ((int)ctx->workers.size() < streams) {

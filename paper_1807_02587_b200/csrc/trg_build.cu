@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "trg_gmm.cuh"
@@ -1212,8 +1213,8 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
 
 // Writes this shard's argmax candidates of the phase (score + the entry's
 // point) for the all-gather (sharded mode).
-__device__ void write_xarg(const BuildParams& p, const Phase& ph, int par, int K) {
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+__device__ void write_xarg(const BuildParams& p, const Phase& ph, int par, int K, int G, int cta) {
+  const int gt = cta * blockDim.x + threadIdx.x, nt = G * blockDim.x;
   for (int k = gt; k < K; k += nt) {
     const double* red = p.nodered + (size_t)k * kRec;
     double* o = p.xarg + (size_t)k * 8;
@@ -1235,10 +1236,13 @@ __device__ void write_xarg(const BuildParams& p, const Phase& ph, int par, int K
 #ifndef TRG_KBUILD_MINB
 #define TRG_KBUILD_MINB 3
 #endif
-__global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p) {
+// The build of one cloud on a group of G CTAs (this CTA: `cta` of them);
+// every barrier and work split is over the group.  k_build runs it on the
+// whole grid, k_build on one group per cloud.
+__device__ __forceinline__ void build_run(const BuildParams& p, int G, int cta) {
   extern __shared__ __align__(16) unsigned char k_build_smem[];  // BuildSmem (> 48 KB static)
   BuildSmem& sm = *reinterpret_cast<BuildSmem*>(k_build_smem);
-  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   BuildState* st = p.st;
   const bool sharded = p.seg >= 0;
@@ -1335,7 +1339,7 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
         }
         if (sharded) {
           grid_sync(p.bar, G);
-          if (ph.mom1 || ph.fps) write_xarg(p, ph, par, K);
+          if (ph.mom1 || ph.fps) write_xarg(p, ph, par, K, G, cta);
           return;  // exchange point: the host all-reduces nodered / gathers xarg
         }
         grid_sync(p.bar, G);
@@ -1352,6 +1356,25 @@ __global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(BuildParams p)
     }
     if (__ldcg(&st->done) || __ldcg(&st->status_overflow)) break;
   }
+}
+
+// Clouds per launch: k_build / k_calibrate take a batch of independent
+// clouds, cloud i on CTAs [i * group, (i + 1) * group), its parameters in
+// the launch's parameter space (dynamically indexed constant bank, no local
+// copy).  A single build is a batch of one on the whole grid.  One kernel
+// per body on purpose: with -fmad=true ptxas contracts FP64 mul/add pairs
+// per compiled kernel, so two copies of the same body could round
+// differently, and batched and single registrations must agree bitwise.
+constexpr int kMaxBatch = kBatchInflightMax;
+struct BuildBatch {
+  int group, n;
+  BuildParams p[kMaxBatch];
+};
+static_assert(sizeof(BuildBatch) <= 32000, "kernel parameter space");
+
+__global__ void __launch_bounds__(kTile, TRG_KBUILD_MINB) k_build(const __grid_constant__ BuildBatch b) {
+  const int i = blockIdx.x / b.group;
+  if (i < b.n) build_run(b.p[i], b.group, blockIdx.x - i * b.group);
 }
 
 // Number of exchange points of a sharded build of depth L (k_build runs
@@ -1584,11 +1607,11 @@ __device__ void cal_finish_leaf(const BuildParams& p, const CalCtx& cx, int j, d
 #ifndef TRG_KCAL_MINB
 #define TRG_KCAL_MINB 2
 #endif
-__global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams p) {
+__device__ __forceinline__ void calibrate_run(const BuildParams& p, int G, int cta) {
   __shared__ FxScale sc[3];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ int lvl[9];
-  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   BuildState* st = p.st;
   const bool sharded = p.seg >= 0;
@@ -1721,6 +1744,11 @@ __global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(BuildParams 
     m.ok = __ldcg(p.status) == 0 ? 1 : 0;
     *p.meta = m;
   }
+}
+
+__global__ void __launch_bounds__(kTile, TRG_KCAL_MINB) k_calibrate(const __grid_constant__ BuildBatch b) {
+  const int i = blockIdx.x / b.group;
+  if (i < b.n) calibrate_run(b.p[i], b.group, blockIdx.x - i * b.group);
 }
 
 __global__ void k_init_entries(const double* __restrict__ pts, size_t n, double* ex, double* ey,
@@ -1976,9 +2004,19 @@ int build_prepare(trg_ctx* ctx, const double* pts, size_t n, const trg_model_con
 }
 
 // One k_build launch (seg = -1: the whole build; else one sharded segment).
+// A batch of one on G CTAs (only p[0] is read).
+std::unique_ptr<BuildBatch> single_batch(const BuildParams& p, int G) {
+  std::unique_ptr<BuildBatch> b(new BuildBatch);
+  b->group = G;
+  b->n = 1;
+  b->p[0] = p;
+  return b;
+}
+
 int build_launch(trg_ctx* ctx, BuildJob* job, int seg) {
   job->p.seg = seg;
-  void* args[] = {&job->p};
+  auto b = single_batch(job->p, job->G);
+  void* args[] = {b.get()};
   TRG_CU(launch_persistent(ctx, (const void*)k_build, job->G, kTile, args, sizeof(BuildSmem)));
   ctx->launches += 1;
   return TRG_OK;
@@ -1986,7 +2024,8 @@ int build_launch(trg_ctx* ctx, BuildJob* job, int seg) {
 
 int calibrate_launch(trg_ctx* ctx, BuildJob* job, int seg) {
   job->p.seg = seg;
-  void* args[] = {&job->p};
+  auto b = single_batch(job->p, job->Gc);
+  void* args[] = {b.get()};
   TRG_CU(launch_persistent(ctx, (const void*)k_calibrate, job->Gc, kTile, args,
                            sizeof(DNode) * kStageNodes));
   ctx->launches += 1;
@@ -2162,7 +2201,7 @@ struct AsyncBuild {
 };
 
 int build_async_start(trg_ctx* ctx, const double* dev, size_t n, const trg_model_config* cfg,
-                      AsyncBuild** h, trg_tree_dev** tree, const TreeMeta** meta) {
+                      AsyncBuild** h, trg_tree_dev** tree, const TreeMeta** meta, bool launch) {
   if (!*h) {  // first attempt: trg_build_tree's argument checks
     TRG_TRY(validate_model_config(cfg));
     if (n == 0 || !dev) {
@@ -2181,8 +2220,10 @@ int build_async_start(trg_ctx* ctx, const double* dev, size_t n, const trg_model
   AsyncBuild* b = *h;
   b->job = BuildJob{};
   TRG_TRY(build_prepare(ctx, dev, n, &b->cfg, b->al, nullptr, 0, &b->job));
-  TRG_TRY(build_launch(ctx, &b->job, -1));
-  TRG_TRY(calibrate_launch(ctx, &b->job, -1));
+  if (launch) {
+    TRG_TRY(build_launch(ctx, &b->job, -1));
+    TRG_TRY(calibrate_launch(ctx, &b->job, -1));
+  }
   *tree = b->job.tree;
   *meta = b->job.p.meta;
   return TRG_OK;
@@ -2208,6 +2249,32 @@ int build_async_finish(trg_ctx* ctx, AsyncBuild* b, trg_tree_dev** out, bool* re
 }
 
 void build_async_free(AsyncBuild* b) { delete b; }
+
+// The builds of m prepared clouds (build_async_start without launch) as one
+// k_build and one k_calibrate launch on ctx's stream, each cloud
+// on an equal group of the co-resident grid.
+int build_batch_launch(trg_ctx* ctx, AsyncBuild* const* hs, int m) {
+  if (m < 1 || m > kMaxBatch) {
+    set_error("build_batch_launch: bad batch size");
+    return TRG_EINVAL;
+  }
+  std::unique_ptr<BuildBatch> b(new BuildBatch);
+  b->n = m;
+  for (int k = 0; k < m; ++k) {
+    b->p[k] = hs[k]->job.p;
+    b->p[k].seg = -1;
+  }
+  void* args[] = {b.get()};
+  TRG_CU(set_dynamic_smem((const void*)k_build, sizeof(BuildSmem)));
+  b->group = persistent_grid(ctx, (const void*)k_build, kTile, sizeof(BuildSmem)) / m;
+  TRG_CU(launch_persistent(ctx, (const void*)k_build, b->group * m, kTile, args, sizeof(BuildSmem)));
+  const size_t cal_smem = sizeof(DNode) * kStageNodes;
+  TRG_CU(set_dynamic_smem((const void*)k_calibrate, cal_smem));
+  b->group = persistent_grid(ctx, (const void*)k_calibrate, kTile, cal_smem) / m;
+  TRG_CU(launch_persistent(ctx, (const void*)k_calibrate, b->group * m, kTile, args, cal_smem));
+  ctx->launches += 2;
+  return TRG_OK;
+}
 
 }  // namespace trg
 

@@ -4,10 +4,13 @@
 // point rows, single-block 6-DoF solve (K8), T <- delta o T, convergence and
 // degenerate-streak control -- with grid barriers between phases, so the
 // host never sees an iteration boundary.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <cmath>
 #include <cstdio>
+#include <memory>
+#include <string>
 #include <vector>
 
 #include "trg_dense.cuh"
@@ -411,7 +414,11 @@ __device__ __forceinline__ void em_apply_update(const SolveOut& so, double* rt, 
 #ifndef TRG_KEM_MINB
 #define TRG_KEM_MINB 2
 #endif
-__global__ void __launch_bounds__(kEmBlock, TRG_KEM_MINB) k_em_tree(EmParams p) {
+// The EM of one registration on a group of G CTAs (this CTA: `cta`).
+// by_sm: the solver is the CTA on the group's lowest SM, whose other CTAs
+// idle (a single registration on the whole grid: that SM keeps the serial
+// code resident); otherwise the group's CTA 0 (batches).
+__device__ __forceinline__ void em_tree_run(const EmParams& p, int G, int cta, bool by_sm) {
   __shared__ SolveSmem ss;
   __shared__ Eig6Smem e6;
   __shared__ SolveOut so;
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(kEmBlock, TRG_KEM_MINB) k_em_tree(EmParams p) 
   __shared__ __align__(8) uint64_t mbar;
   __shared__ int s_done, s_fails, s_conv, s_iters;
   extern __shared__ __align__(128) unsigned char k_em_stage[];
-  const int G = gridDim.x, tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5;
   constexpr int WPB = kEmBlock / 32;
   int J = p.a.n_nodes, root_count = p.a.root_count, n_snodes = p.a.n_snodes;
   if (p.meta) {
@@ -437,12 +444,12 @@ __global__ void __launch_bounds__(kEmBlock, TRG_KEM_MINB) k_em_tree(EmParams p) 
   unsigned* flag = p.sync + 2;
   unsigned* arrived = p.sync + 3;
   if (p.fast)  // the FP32 records, ordered before use by assign_roles' grid barrier
-    for (int j = blockIdx.x * blockDim.x + tid; j < J; j += G * blockDim.x) {
+    for (int j = cta * blockDim.x + tid; j < J; j += G * blockDim.x) {
       FNode f;
       fnode_from(p.a.nodes[j], f);
       p.fnodes[j] = f;
     }
-  const Roles r = assign_roles(p.smtab, p.sync, G, 1);
+  const Roles r = by_sm ? assign_roles(p.smtab, p.sync, G, 1) : roles_by_index(p.sync, G, cta);
   if (r.upd && r.idx != 0) return;  // the solver's SM stays free of E-step work
   EmState* st = p.st;
   if (!r.upd) {
@@ -626,6 +633,22 @@ __global__ void __launch_bounds__(kEmBlock, TRG_KEM_MINB) k_em_tree(EmParams p) 
     crit_trace(it);
     if (s_done) break;
   }
+}
+
+// Registrations per launch: k_em_tree takes a batch of independent EM runs,
+// run i on CTAs [i * group, (i + 1) * group) (trg_register_batch); a single
+// registration is a batch of one on the whole grid with SM-placed roles.
+// One kernel for both (see k_build: per-kernel FP64 contraction).
+constexpr int kMaxEmBatch = kBatchInflightMax;
+struct EmBatch {
+  int group, n, by_sm;
+  EmParams p[kMaxEmBatch];
+};
+static_assert(sizeof(EmBatch) <= 32000, "kernel parameter space");
+
+__global__ void __launch_bounds__(kEmBlock, TRG_KEM_MINB) k_em_tree(const __grid_constant__ EmBatch b) {
+  const int i = blockIdx.x / b.group;
+  if (i < b.n) em_tree_run(b.p[i], b.group, blockIdx.x - i * b.group, b.by_sm != 0);
 }
 
 // registration.cpp:140-151 tree_extent_estimate (single block; min/max are
@@ -914,6 +937,15 @@ int em_launch(trg_ctx* ctx, EmJob* job, int seg) {
   // per-launch handover words (grid barrier, flag, arrivals)
   TRG_CU(cudaMemsetAsync(job->p.sync, 0, 64, ctx->stream));
   void* args[] = {&job->p};
+  std::unique_ptr<EmBatch> b;
+  if (job->kernel == (const void*)k_em_tree) {  // a batch of one, SM-placed roles
+    b.reset(new EmBatch);
+    b->group = job->G;
+    b->n = 1;
+    b->by_sm = 1;
+    b->p[0] = job->p;
+    args[0] = b.get();
+  }
   TRG_CU(launch_persistent(ctx, job->kernel, job->G, job->block, args, job->smem));
   ctx->launches += 1;
   return TRG_OK;
@@ -1541,3 +1573,198 @@ extern "C" int trg_register_clouds_sharded(trg_comm* comm, const double* const* 
   out->model_build_seconds = ms * 1e-3;
   return rc;
 }
+
+// ------------------------------------------------------------ batched pairs
+// trg_register_batch for the tree variants (BASELINE config C5): the pairs
+// run in waves of up to kBatchInflightMax.  Each pair of a wave has a worker context
+// (own stream, workspace, scratch tree, status words) that stages its
+// clouds, its target's bbox and its build state; the wave's builds are then
+// ONE k_build_batch + ONE k_calibrate_batch launch and its EMs ONE
+// k_em_tree launch on the batch context's stream, every pair on its own
+// CTA group of the co-resident (cooperative) grid with group barriers.  The
+// results are bit-identical to trg_register_clouds (group size does not
+// enter any result: tests/test_grid_invariance_gpu.py).
+namespace trg {
+
+namespace batch_detail {
+
+int em_batch_launch(trg_ctx* ctx, EmJob* const* js, int m) {
+  std::unique_ptr<EmBatch> b(new EmBatch);
+  b->n = m;
+  b->by_sm = 0;
+  for (int k = 0; k < m; ++k) b->p[k] = js[k]->p;
+  const size_t smem = sizeof(DNode) * kStageNodes;
+  TRG_CU(set_dynamic_smem((const void*)k_em_tree, smem));
+  b->group = persistent_grid(ctx, (const void*)k_em_tree, kEmBlock, smem) / m;
+  if (b->group < 2) {
+    set_error("register_batch: too many pairs in flight for the device");
+    return TRG_EINVAL;
+  }
+  void* args[] = {b.get()};
+  TRG_CU(launch_persistent(ctx, (const void*)k_em_tree, b->group * m, kEmBlock, args, smem));
+  ctx->launches += 1;
+  return TRG_OK;
+}
+
+struct BatchSlot {
+  AsyncBuild* ab = nullptr;
+  trg_tree_dev* tree = nullptr;
+  const TreeMeta* meta = nullptr;
+  double* od = nullptr;
+  const double* tgt = nullptr;
+  const double* src = nullptr;
+  EmJob job;
+  cudaEvent_t b0 = nullptr, b1 = nullptr;  // build span (shared by the wave)
+};
+
+void slot_release(BatchSlot& s) {
+  if (s.job.e0) cudaEventDestroy(s.job.e0);
+  if (s.job.e1) cudaEventDestroy(s.job.e1);
+  if (s.b0) cudaEventDestroy(s.b0);
+  if (s.b1) cudaEventDestroy(s.b1);
+  s.job.e0 = s.job.e1 = s.b0 = s.b1 = nullptr;
+  if (s.ab) build_async_free(s.ab);
+  s.ab = nullptr;
+}
+
+// One wave: pairs [base, base + m) on workers 0..m-1.
+int batch_wave(trg_ctx* ctx, int base, int m, const double* const* targets,
+               const size_t* n_targets, const double* const* sources, const size_t* n_sources,
+               int on_device, const trg_reg_config* cfg, trg_reg_result* out,
+               std::vector<BatchSlot>& sl, std::vector<cudaEvent_t>& ev, cudaEvent_t ev_main) {
+  trg_model_config mc = cfg->model_config;
+  mc.max_level = cfg->variant_param;
+  std::vector<AsyncBuild*> abs(m);
+  std::vector<EmJob*> jobs(m);
+  // 1. per pair: clouds, target bbox, build state (worker streams)
+  for (int k = 0; k < m; ++k) {
+    trg_ctx* w = ctx->workers[k];
+    const int i = base + k;
+    BatchSlot& s = sl[k];
+    if (n_targets[i] == 0 || n_sources[i] == 0 || !targets[i] || !sources[i]) {
+      set_error("register: empty cloud");
+      return TRG_EINVAL;
+    }
+    TRG_TRY(stage_points_public(w, targets[i], n_targets[i], on_device, kSlotPoints, &s.tgt));
+    TRG_TRY(stage_points_public(w, sources[i], n_sources[i], on_device, kSlotPoints2, &s.src));
+    TRG_TRY(bbox_launch(w, s.tgt, n_targets[i], &s.od));
+    TRG_CU(cudaEventCreate(&s.b0));
+    TRG_CU(cudaEventCreate(&s.b1));
+    TRG_CU(cudaEventRecord(s.b0, w->stream));
+    w->build_into_scratch = true;
+    const int rc = build_async_start(w, s.tgt, n_targets[i], &mc, &s.ab, &s.tree, &s.meta, false);
+    w->build_into_scratch = false;
+    TRG_TRY(rc);
+    abs[k] = s.ab;
+    TRG_CU(cudaEventRecord(ev[k], w->stream));
+    TRG_CU(cudaStreamWaitEvent(ctx->stream, ev[k], 0));
+  }
+  // 2. the wave's builds: one k_build_batch + one k_calibrate_batch
+  TRG_TRY(build_batch_launch(ctx, abs.data(), m));
+  TRG_CU(cudaEventRecord(ev_main, ctx->stream));
+  // 3. EM state behind the builds (worker streams)
+  for (int k = 0; k < m; ++k) {
+    trg_ctx* w = ctx->workers[k];
+    BatchSlot& s = sl[k];
+    TRG_CU(cudaStreamWaitEvent(w->stream, ev_main, 0));
+    TRG_CU(cudaEventRecord(s.b1, w->stream));
+    TRG_TRY(em_prepare(w, s.tree, s.src, n_sources[base + k], cfg, 0.0, false, 0.0, &s.job, false,
+                       s.meta, s.od));
+    TRG_CU(cudaMemsetAsync(s.job.p.sync, 0, 64, w->stream));  // the launch's handover words
+    jobs[k] = &s.job;
+    TRG_CU(cudaEventRecord(ev[k], w->stream));
+    TRG_CU(cudaStreamWaitEvent(ctx->stream, ev[k], 0));
+  }
+  // 4. the wave's EMs: one k_em_tree
+  TRG_TRY(em_batch_launch(ctx, jobs.data(), m));
+  TRG_CU(cudaEventRecord(ev_main, ctx->stream));
+  // 5. collect (an entry-buffer overflow re-runs that pair alone, with the
+  // grown allocation its worker now holds)
+  int rc_all = TRG_OK;
+  for (int k = 0; k < m; ++k) {
+    trg_ctx* w = ctx->workers[k];
+    BatchSlot& s = sl[k];
+    const int i = base + k;
+    TRG_CU(cudaStreamWaitEvent(w->stream, ev_main, 0));
+    trg_tree_dev* built = nullptr;
+    bool retry = false;
+    int rc = build_async_finish(w, s.ab, &built, &retry);  // synchronises the worker stream
+    if (rc == TRG_OK && retry) {
+      cudaMemsetAsync(w->status2, 0, sizeof(int), w->stream);
+      rc = trg_register_clouds(w, targets[i], n_targets[i], sources[i], n_sources[i], on_device,
+                               cfg, &out[i]);
+    } else if (rc == TRG_OK) {
+      s.job.J = built->n_nodes;
+      rc = em_collect(w, &s.job, &out[i]);
+      s.job.e0 = s.job.e1 = nullptr;  // destroyed by em_collect
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, s.b0, s.b1);
+      if (rc == TRG_OK) out[i].model_build_seconds = ms * 1e-3;
+    } else {
+      cudaMemsetAsync(w->status2, 0, sizeof(int), w->stream);
+      if (rc == TRG_EINVAL && trg_last_error()[0] == 'b')
+        set_error("point cloud has non-finite coordinates or no mass");
+    }
+    if (rc != TRG_OK && rc_all == TRG_OK) {
+      rc_all = rc;
+      set_error("register_batch: pair " + std::to_string(i) + ": " + trg_last_error());
+    }
+  }
+  return rc_all;
+}
+
+}  // namespace batch_detail
+
+using namespace batch_detail;
+
+int register_batch_fused(trg_ctx* ctx, int n_pairs, const double* const* targets,
+                         const size_t* n_targets, const double* const* sources,
+                         const size_t* n_sources, int on_device, const trg_reg_config* cfg,
+                         int inflight, trg_reg_result* out) {
+  TRG_TRY(validate_reg_config(cfg));
+  inflight = std::min({inflight, n_pairs, kBatchInflightMax, kMaxEmBatch});
+  while ((int)ctx->workers.size() < inflight) {
+    trg_ctx* w = nullptr;
+    TRG_TRY(trg_ctx_create(ctx->device, &w));
+    ctx->workers.push_back(w);
+  }
+  // full-device workers: their workspaces are sized for a whole-grid run
+  for (int k = 0; k < inflight; ++k) TRG_TRY(trg_ctx_set_sm_budget(ctx->workers[k], ctx->device_sms));
+  // inputs the caller produced on its own stream must be complete
+  TRG_CU(cudaStreamSynchronize(ctx->stream));
+  std::vector<uint64_t> l0(inflight), h0(inflight), d0(inflight);
+  for (int k = 0; k < inflight; ++k) {
+    l0[k] = ctx->workers[k]->launches;
+    h0[k] = ctx->workers[k]->bytes_h2d;
+    d0[k] = ctx->workers[k]->bytes_d2h;
+  }
+  std::vector<cudaEvent_t> ev(inflight, nullptr);
+  cudaEvent_t ev_main = nullptr;
+  int rc = TRG_OK;
+  for (int k = 0; k < inflight && rc == TRG_OK; ++k)
+    if (cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming) != cudaSuccess) rc = TRG_ECUDA;
+  if (rc == TRG_OK && cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming) != cudaSuccess)
+    rc = TRG_ECUDA;
+  for (int base = 0; base < n_pairs && rc == TRG_OK; base += inflight) {
+    const int m = std::min(inflight, n_pairs - base);
+    std::vector<BatchSlot> sl(m);
+    rc = batch_wave(ctx, base, m, targets, n_targets, sources, n_sources, on_device, cfg, out, sl,
+                    ev, ev_main);
+    if (rc != TRG_OK) {  // nothing queued may outlive the call
+      cudaStreamSynchronize(ctx->stream);
+      for (int k = 0; k < m; ++k) cudaStreamSynchronize(ctx->workers[k]->stream);
+    }
+    for (auto& s : sl) slot_release(s);
+  }
+  for (auto e : ev)
+    if (e) cudaEventDestroy(e);
+  if (ev_main) cudaEventDestroy(ev_main);
+  for (int k = 0; k < inflight; ++k) {
+    ctx->launches += ctx->workers[k]->launches - l0[k];
+    ctx->bytes_h2d += ctx->workers[k]->bytes_h2d - h0[k];
+    ctx->bytes_d2h += ctx->workers[k]->bytes_d2h - d0[k];
+  }
+  return rc;
+}
+
+}  // namespace trg

@@ -94,6 +94,19 @@ static __device__ Roles assign_roles(unsigned* smtab, unsigned* bar, int G, int 
   return r;
 }
 
+// Roles of a CTA group by index (one launch running several independent
+// groups): the group's CTA 0 updates, the rest work.  Block-wide; the group
+// barrier orders what the CTAs wrote before the call.
+static __device__ Roles roles_by_index(unsigned* bar, int G, int cta) {
+  grid_sync(bar, G);
+  Roles r;
+  r.upd = cta == 0;
+  r.idx = r.upd ? 0 : cta - 1;
+  r.n_upd = 1;
+  r.n_work = G - 1;
+  return r;
+}
+
 // Workers: wait until the updaters published step `s` (flag >= s).
 __device__ __forceinline__ void wait_flag(const unsigned* flag, unsigned s) {
   __syncthreads();

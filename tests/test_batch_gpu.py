@@ -1,5 +1,5 @@
-"""trg_register_batch (BASELINE config C5: independent frame pairs run as
-concurrent SM-budgeted registrations) against the reference's own
+"""trg_register_batch (BASELINE config C5: independent frame pairs; tree
+variants as waves of single launches with one CTA group per pair) against the reference's own
 register_clouds results (golden fixtures) and against one-pair calls.
 Tolerances as north_star: 1e-4 rad rotation, 1e-4 x extent translation."""
 import numpy as np
@@ -58,7 +58,10 @@ def test_batch_errors(ctx):
     with pytest.raises(tr.InvalidArgument, match="pair 1"):
         tr.register_batch([g["points"]] * 3, [g["src"], bad, g["src"]], cfg, ctx, 2)
     with pytest.raises(tr.InvalidArgument):
-        tr.register_batch([g["points"]], [g["src"]], cfg, ctx, 17)
+        tr.register_batch([g["points"]], [g["src"]], cfg, ctx, 25)  # > 24 pairs in flight
+    with pytest.raises(tr.InvalidArgument):  # flat / ICP: <= 16 worker threads
+        tr.register_batch([g["points"]], [g["src"]], tr.RegistrationConfig(variant=tr.Variant("icp", 0)),
+                          ctx, 17)
     assert tr.register_batch([], [], cfg, ctx) == []
 
 

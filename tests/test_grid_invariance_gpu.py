@@ -64,3 +64,42 @@ def test_bitwise_batch_vs_single(ctx):
     for (t, s, _), r in zip(pairs, res):
         one = tr.register_clouds(t, s, cfg, ctx)
         assert _reg_key(r) == _reg_key(one)
+
+
+@pytest.mark.parametrize("inflight", [2, 5, 16])
+def test_bitwise_fused_batch_waves(ctx, inflight):
+    """register_batch's fused path (tree variants): waves of `inflight` pairs,
+    each wave's builds and EMs as single launches with one CTA group per pair
+    (2: three waves 2 + 2 + 1; 5: one wave; 16: one wave of 5 on big groups)
+    -- every pair bit-identical to its own register_clouds, eval counts
+    included."""
+    tr = _tr()
+    pairs = [tr.kinect_pair(k) for k in (3, 4, 5, 6, 7)]
+    cfg = tr.RegistrationConfig(variant=tr.Variant("adaptive", 3))
+    res = tr.register_batch([p[0] for p in pairs], [p[1] for p in pairs], cfg, ctx, inflight)
+    for (t, s, _), r in zip(pairs, res):
+        one = tr.register_clouds(t, s, cfg, ctx)
+        assert _reg_key(r) == _reg_key(one)
+        assert list(r.eval_counts) == list(one.eval_counts)
+        assert np.array_equal(r.criterion_trace, one.criterion_trace)
+
+
+def test_fused_batch_entry_overflow_retry():
+    """A fresh context sizes the entry buffers for L <= 3 growth (12 x N); a
+    depth-4 build outgrows them: the pair that overflowed is re-run alone
+    with the grown buffers, and the batch still equals register_clouds."""
+    tr = _tr()
+    names = ["scene3k_L3", "kinect4k_L3", "lumpy2k_L2"]
+    gs = [load_golden(n) for n in names]
+    cfg = tr.RegistrationConfig(variant=tr.Variant("adaptive", 4))
+    ctx = tr.Context(0)
+    try:
+        res = tr.register_batch([g["points"] for g in gs], [g["src"] for g in gs], cfg, ctx, 3)
+    finally:
+        ctx.close()
+    ctx1 = tr.Context(0)
+    try:
+        for g, r in zip(gs, res):
+            assert _reg_key(r) == _reg_key(tr.register_clouds(g["points"], g["src"], cfg, ctx1))
+    finally:
+        ctx1.close()
