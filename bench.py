@@ -390,9 +390,10 @@ def run_c4(args, tr, ctx, dist, dev, world):
 
 def run_batched(args, tr, ctx, cfg, dist, dev, world):
     """C5 slice: `--batch` independent Kinect-sized pairs per rank (pair k
-    uses noise and pose seed k), device-resident, through trg_register_batch with
-    `--streams` concurrent SM-budgeted registrations.  Timed with CUDA
-    events around each whole batch, max over ranks."""
+    uses noise and pose seed k), device-resident, through trg_register_batch:
+    waves of `--streams` pairs in flight (0 = library default, 24), each wave's
+    builds and EMs as single launches with one CTA group per pair.  Timed by
+    the host clock around whole synchronous batches, max over ranks."""
     import torch
     rank = dist.get_rank() if dist is not None else 0
     pairs = [tr.kinect_pair(1 + rank * args.batch + k) for k in range(args.batch)]
@@ -411,7 +412,7 @@ def run_batched(args, tr, ctx, cfg, dist, dev, world):
     errs = [float(np.degrees(np.arccos(np.clip((np.trace(r.transform.rotation.T @ p[2].rotation) - 1) / 2,
                                                -1, 1)))) for r, p in zip(res, pairs)]
     return {"workload": f"C5 slice: {args.batch} independent C2-style Kinect pairs per rank (seeds k)",
-            "pairs_per_rank": args.batch, "streams": args.streams, "reps": reps,
+            "pairs_per_rank": args.batch, "pairs_in_flight": args.streams or 24, "reps": reps,
             "value": world * args.batch * reps / dt, "unit": UNIT,
             "ms_per_batch": 1e3 * dt / reps, "timing": "host wall clock around synchronous batches",
             "converged": sum(r.converged for r in res), "median_rot_err_deg_vs_gt": float(np.median(errs))}
@@ -489,8 +490,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--batch", type=int, default=32, help="C5 slice: pairs per rank (0 = skip)")
-    ap.add_argument("--streams", type=int, default=4, help="concurrent registrations per GPU")
+    ap.add_argument("--batch", type=int, default=256, help="C5 slice: pairs per rank (0 = skip)")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="C5 slice: pairs in flight per GPU (0 = library default)")
     ap.add_argument("--c4", type=int, default=1, help="add the C4 (1M points, depth 4) line item "
                     "(point-sharded over NCCL when N > 1)")
     ap.add_argument("--extra", type=int, default=1, help="add the C1 and C3 line items (N = 1)")

@@ -274,7 +274,7 @@ int trg_register_clouds(trg_ctx* ctx, const double* target, size_t n_target, con
  * loop.  Pair i registers sources[i] (n_sources[i] points) to targets[i]
  * with `cfg` and fills out[i] (trace pointers as in trg_reg_result, may be
  * NULL).  Tree variants (adaptive / tree): `streams` = pairs in flight
- * (1..24; 0 = 16); the pairs run in waves, each wave's tree builds as ONE
+ * (1..24; 0 = 24); the pairs run in waves, each wave's tree builds as ONE
  * cooperative launch (one CTA group per pair, group barriers) and its EM
  * loops as one more.  Flat / ICP variants: `streams` pairs (1..16; 0 = 4)
  * run concurrently, each on its own worker thread, CUDA stream and

@@ -262,7 +262,7 @@ int build_async_start(trg_ctx* ctx, const double* dev, size_t n, const trg_model
 int build_batch_launch(trg_ctx* ctx, AsyncBuild* const* hs, int m);
 // trg_register_batch of tree-variant pairs: waves of `inflight` pairs, each
 // wave's builds and EMs as single launches (trg_em.cu)
-constexpr int kBatchInflightDefault = 16, kBatchInflightMax = 24;
+constexpr int kBatchInflightDefault = 24, kBatchInflightMax = 24;
 int register_batch_fused(trg_ctx* ctx, int n_pairs, const double* const* targets,
                          const size_t* n_targets, const double* const* sources,
                          const size_t* n_sources, int on_device, const trg_reg_config* cfg,
