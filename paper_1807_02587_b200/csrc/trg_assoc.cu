@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(kAssocBlock) k_assoc(AssocParams p) {
   __syncthreads();
   p.snodes = sn;
   const int wpb = kAssocBlock / 32;
-  assoc_fx_pass<NM>(p, p.Rt ? rt : nullptr, sc, gridDim.x * wpb, blockIdx.x * wpb + (threadIdx.x >> 5));
+  assoc_fx_pass<NM>(p, p.Rt ? rt : nullptr, sc, gridDim.x * wpb, (threadIdx.x >> 5) * gridDim.x + blockIdx.x);
 }
 
 // acc[J][NM][3] -> out[J][NM] (doubles), one thread per value.

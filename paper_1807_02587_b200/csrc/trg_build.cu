@@ -1684,7 +1684,9 @@ __device__ __forceinline__ void calibrate_run(const BuildParams& p, int G, int c
 #ifdef TRG_ASSOC_PROBE
       if (pass == TRG_PROBE_PASS && tid == 0 && cta % 32 == 0) tl_mark_any(p.tl, 5103);
 #endif
-      assoc_fx_pass<10>(a, nullptr, sc, G * WPB, cta * WPB + warp);
+      // warp-major window order: the windows beyond one per warp land on
+      // different SMs (the pass is bound by each SM's share of the descents)
+      assoc_fx_pass<10>(a, nullptr, sc, G * WPB, warp * G + cta);
       grid_sync(p.bar + 8, G);
       tl_mark(p.tl, 1000 + pass * 10 + 1);
       if (sharded) {

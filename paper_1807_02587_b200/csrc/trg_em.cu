@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kAssocBlock, 2) k_register(EmParams p) {
         if (it > 0) crit_trace(it - 1, sc_prev);
       } else {
         const int ctas = defer ? G - 1 : G, c = defer ? cta - 1 : cta;
-        assoc_fx_pass<4>(a, rt, sc, ctas * WPB, c * WPB + warp);
+        assoc_fx_pass<4>(a, rt, sc, ctas * WPB, warp * ctas + c);
       }
       grid_sync(p.bar, G);
       tl_mark(p.tl, 2000 + it * 10 + 1);
@@ -492,9 +492,11 @@ __device__ __forceinline__ void em_tree_run(const EmParams& p, int G, int cta, b
       a.acc = p.acc + (size_t)(it & 1) * S * 12;
       a.counters = p.a.counters + 2 * (it & 1);
       if (p.fast)
-        assoc_fx_pass_f32<4>(a, p.fnodes, fstage, rt, sc, r.n_work * WPB, r.idx * WPB + warp);
+        assoc_fx_pass_f32<4>(a, p.fnodes, fstage, rt, sc, r.n_work * WPB, warp * r.n_work + r.idx);
       else
-        assoc_fx_pass<4>(a, rt, sc, r.n_work * WPB, r.idx * WPB + warp);
+        // warp-major window order: every worker CTA gets windows, spread over
+        // the SMs (CTA-major left the last CTAs idle when windows < warps)
+        assoc_fx_pass<4>(a, rt, sc, r.n_work * WPB, warp * r.n_work + r.idx);
       arrive_count(arrived);
       if (sharded) return;  // one E-step per segment
     }
