@@ -246,7 +246,7 @@ struct BuildSmem {
       double am[2];
     } s;
     struct {                 // tile_comp_pass (entry-per-thread E-step)
-      double gam[16][kTile];  // responsibilities, component-major
+      double gam[16][kTile];  // responsibilities (w * gamma outside the partition), component-major
       double lt[2][kTile];    // w * log-likelihood per entry and candidate
       int best;               // heaviest survivor (partition fallback)
     } g;
@@ -398,8 +398,16 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
       // gamma_k = exp(log_k - log_total) = e_k / s (gmm.cpp:189, 354): one
       // reciprocal per entry instead of a second exp per component
       const double rs = fin ? rcp_sum(s) : 0.0;
+      // the moment passes use the weighted responsibility w * gamma (stored
+      // instead of gamma: one shared-memory load less per entry and
+      // component in (2), the same rounded product); the partition uses gamma
+      if (pcount) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) G.gam[ci * 8 + k][tid] = ek[k] * rs;
+        for (int k = 0; k < 8; ++k) G.gam[ci * 8 + k][tid] = ek[k] * rs;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) G.gam[ci * 8 + k][tid] = (ek[k] * rs) * w;
+      }
       // the per-iteration log-likelihood only feeds the diagnostics trace
       // (gmm.cpp:240); the final pass (mode 2) always needs it (gmm.cpp:394)
       const bool want_ll = mode == 2 || (mode == 1 && p.want_traces);
@@ -430,7 +438,7 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
       // zero responsibility adds exact zeros, so no per-entry test).
       if (mode == 1) {
         auto acc = [&](int e) {
-          const double g = G.gam[item][e] * sm.ent[3][e];
+          const double g = G.gam[item][e];  // w * gamma
           const double d0 = sm.ent[0][e] - n0, d1 = sm.ent[1][e] - n1, d2 = sm.ent[2][e] - n2;
           a[0] += g;
           a[1] += g * d0;
@@ -450,7 +458,7 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
         }
         if (e < tlen) acc(e);
       } else {
-        for (int e = lane; e < tlen; e += 32) a[0] += G.gam[item][e] * sm.ent[3][e];  // child mass (gmm.cpp:355)
+        for (int e = lane; e < tlen; e += 32) a[0] += G.gam[item][e];  // child mass w * gamma (gmm.cpp:355)
       }
       if (k == 0)
         for (int e = lane; e < tlen; e += 32) a[10] += G.lt[ci][e];
