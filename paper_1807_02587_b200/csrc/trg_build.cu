@@ -101,7 +101,7 @@ struct BuildParams {
   int* tile_start[2];
   int* tile_len[2];
   NodeFit nf;
-  double* partial;    // [Tmax][kRec]
+  double* partial;    // [kRec][Tmax] field-major: a field of a node's consecutive tiles is contiguous
   double* nodered;    // [Kmax][kRec] per-node reduced record
   unsigned* fdone;    // [Kmax] fields reduced (per phase)
   TreeMeta* meta;     // published by k_calibrate for work queued behind the build
@@ -141,6 +141,19 @@ struct BuildParams {
 
 
 // ----------------------------------------------------------------- helpers
+
+// One tile's partial record in the field-major buffer (field f of tile t at
+// partial[f * Tmax + t]): the tile pass writes its fields, the per-node
+// reduction then reads each field over the node's consecutive tiles with
+// coalesced loads (tile-major records made every load a separate sector:
+// 4x the bytes, from DRAM once the buffer outgrows L2).  Concurrently
+// processed tiles are adjacent, so the scattered 8-byte writes still
+// complete whole sectors in L2.
+struct TileRec {
+  double* base;   // partial + t
+  size_t stride;  // Tmax
+  __device__ __forceinline__ double& operator[](int f) const { return base[(size_t)f * stride]; }
+};
 
 // The scoring fields of a component: w, log w, mean, precision, log_norm,
 // 1/lam_min (positive iff the covariance is PD).
@@ -273,7 +286,7 @@ struct BuildSmem {
 // ----------------------------------------------------------------- tile work
 // Thread-per-entry passes: list_moments 1/2 and one FPS round.
 __device__ void tile_entry_pass(const BuildParams& p, BuildSmem& sm, const Phase& ph, int par,
-                                double* rec) {
+                                TileRec rec) {
   const int tid = threadIdx.x;
   const int e = sm.tstart + tid;
   const bool act = tid < sm.tlen;
@@ -347,7 +360,7 @@ __device__ void tile_entry_pass(const BuildParams& p, BuildSmem& sm, const Phase
 //      (mode 1), masses (mode 2) or survivor-normalised partition (mode 3),
 //      then a fixed butterfly over the lanes.
 __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase& ph, int par,
-                               double* rec, bool pcount) {
+                               TileRec rec, bool pcount) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nc = pcount ? 1 : sm.ncand;
   const int tlen = sm.tlen;
@@ -1139,7 +1152,8 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
   const int lane = threadIdx.x & 31;
   const int t0 = p.rn[par].tile0[k], nt = p.rn[par].ntiles[k];
   double* out = p.nodered + (size_t)k * kRec;
-  const double* rec0 = p.partial + (size_t)t0 * kRec;
+  const double* rec0 = p.partial + t0;  // field f of tile t0 + q: rec0[f * Tmax + q]
+  const size_t TS = (size_t)p.Tmax;
   if (kind == 0) {
     double v = 0.0;
     for (int q0 = lane; q0 < nt; q0 += 32 * B) {
@@ -1147,7 +1161,7 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         const int q = q0 + 32 * u;
-        b[u] = q < nt ? __ldcg(rec0 + (size_t)q * kRec + off) : 0.0;
+        b[u] = q < nt ? __ldcg(rec0 + (size_t)off * TS + q) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < B; ++u)
@@ -1163,14 +1177,14 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
     const int s = off, ns = __ldcg(&p.nf.ns[k]);
     if (s >= ns) return;
     const int comp = __ldcg(&p.nf.surv[8 * k + s]);
-    const double* cnt = rec0 + kOffCnt + comp;
+    const double* cnt = rec0 + (size_t)(kOffCnt + comp) * TS;
     const int per = (nt + 31) / 32;
     const int q0 = min(nt, lane * per), q1 = min(nt, q0 + per);
     double loc = 0.0;
     for (int qb = q0; qb < q1; qb += B) {
       double b[B];
 #pragma unroll
-      for (int u = 0; u < B; ++u) b[u] = qb + u < q1 ? __ldcg(cnt + (size_t)(qb + u) * kRec) : 0.0;
+      for (int u = 0; u < B; ++u) b[u] = qb + u < q1 ? __ldcg(cnt + qb + u) : 0.0;
 #pragma unroll
       for (int u = 0; u < B; ++u) loc += b[u];
     }
@@ -1184,7 +1198,7 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
     for (int qb = q0; qb < q1; qb += B) {
       double b[B];
 #pragma unroll
-      for (int u = 0; u < B; ++u) b[u] = qb + u < q1 ? __ldcg(cnt + (size_t)(qb + u) * kRec) : 0.0;
+      for (int u = 0; u < B; ++u) b[u] = qb + u < q1 ? __ldcg(cnt + qb + u) : 0.0;
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         if (qb + u < q1) p.tile_base[(size_t)(t0 + qb + u) * 8 + s] = base;
@@ -1199,8 +1213,8 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         const int q = q0 + 32 * u;
-        sc[u] = q < nt ? __ldcg(rec0 + (size_t)q * kRec + off) : -INFINITY;
-        ix[u] = q < nt ? __ldcg(rec0 + (size_t)q * kRec + off + 1) : 1e300;
+        sc[u] = q < nt ? __ldcg(rec0 + (size_t)off * TS + q) : -INFINITY;
+        ix[u] = q < nt ? __ldcg(rec0 + (size_t)(off + 1) * TS + q) : 1e300;
       }
 #pragma unroll
       for (int u = 0; u < B; ++u) argmax_merge(bs, bi, sc[u], ix[u]);
@@ -1306,7 +1320,7 @@ __device__ __forceinline__ void build_run(const BuildParams& p, int G, int cta) 
         int ntl = 0, nent = 0;
         for (int t = cta; t < T; t += G) {
           load_tile_ctx(p, sm, ph, par, t);
-          double* rec = p.partial + (size_t)t * kRec;
+          const TileRec rec{p.partial + t, (size_t)p.Tmax};
           tile_entry_pass(p, sm, ph, par, rec);
           if (ph.mode[0] || ph.mode[1]) tile_comp_pass(p, sm, ph, par, rec, false);
           if (ph.pcount) tile_comp_pass(p, sm, ph, par, rec, true);
