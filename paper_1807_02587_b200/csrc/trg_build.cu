@@ -948,11 +948,25 @@ __device__ int block_exscan(int* a, int n, int* wtmp /* >= 33 ints smem */) {
   return total;
 }
 
+// Last index i in [0, n) with a[i] <= v (a non-decreasing, a[0] <= v).
+__device__ __forceinline__ int upper_index(const int* a, int n, int v) {
+  int lo = 0, hi = n;  // a[lo] <= v < a[hi] (a[n] = +inf)
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 // Layout (CTA 0, all threads): create this round's child tree nodes, choose
 // the next round's expanding set (mass gate gmm.cpp:621-623), its entry
 // segments and tiles.  Children are numbered node by node, survivor by
 // survivor, exactly like build_tree's push_back order (gmm.cpp:629-641).
-__device__ void round_layout(const BuildParams& p, int par, int round, int* scratch) {
+// Work is spread per child and per tile (a child finds its node, a tile its
+// child, by binary search in the exclusive scans); the scratch arrays live
+// in the idle tile scratch when they fit, else in global memory.
+__device__ void round_layout(const BuildParams& p, BuildSmem& sm, int par, int round,
+                             int* gscratch) {
   BuildState* st = p.st;
   const int tid = threadIdx.x, nt = blockDim.x;
   __shared__ int wtmp[33];
@@ -961,14 +975,15 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
   const int J0 = st->J;
   const int npar = par ^ 1;
   const bool last = round + 1 >= p.L;
-  // (1) child-id base per expanding node
-  int* nbase = scratch;           // [K]
+  int* scratch = (size_t)(K + 6 * 8 * K) * sizeof(int) <= sizeof(sm.u)
+                     ? reinterpret_cast<int*>(&sm.u) : gscratch;
+  int* nbase = scratch;           // [K] child-id base per expanding node
   int* cgate = scratch + K;       // [NC] gated flag -> K2 position
   int* ngate = cgate + 8 * K;     // [NC] gated flag (kept)
-  int* ccnt = ngate + 8 * K;      // [NC] entry count -> E2 offset
+  int* ccnt = ngate + 8 * K;      // [NC] padded entry count -> E2 offset
   int* ctil = ccnt + 8 * K;       // [NC] tile count -> T2 offset
-  int* cidx = ctil + 8 * K;       // [NC] (k << 3 | s)
-  int* codd = cidx + 8 * K;       // [NC] 1 when the child's entry count is odd
+  int* clen = ctil + 8 * K;       // [NC] entry count
+  int* codd = clen + 8 * K;       // [NC] 1 when the child's entry count is odd
   for (int k = tid; k < K; k += nt) nbase[k] = p.nf.ok[k] ? p.nf.ns[k] : 0;
   __syncthreads();
   const int NC = block_exscan(nbase, K, wtmp);
@@ -980,35 +995,33 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
     if (tid == 0) atomicCAS(p.status, 0, kERuntime);
     return;
   }
-  // (2) create child nodes, link parents; gather per-child gate/count/tiles
-  for (int k = tid; k < K; k += nt) {
-    const int ns = p.nf.ok[k] ? p.nf.ns[k] : 0;
-    if (ns == 0) continue;
+  // (2) one child per thread: create the tree node, link the parent; the
+  // child's gate / entry count / tiles
+  for (int c = tid; c < NC; c += nt) {
+    const int k = upper_index(nbase, K, c), s2 = c - nbase[k];
+    const int ns = p.nf.ns[k];
     const int parent = p.rn[par].tree_id[k];
     const int id0 = J0 + nbase[k];
-    if (parent >= 0) {
+    if (s2 == 0 && parent >= 0) {
       p.nodes[parent].first_child = id0;
       p.nodes[parent].child_count = ns;
     }
     const int kept = p.nf.kept[k];
-    for (int s2 = 0; s2 < ns; ++s2) {
-      const int c = nbase[k] + s2;
-      const GComp& g = p.nf.comps[((size_t)k * 2 + kept) * 8 + p.nf.surv[8 * k + s2]];
-      const double w = p.nf.smass[8 * k + s2] / p.nf.stotal[k];
-      write_dnode_from_comp(p.nodes[id0 + s2], p.cov + 9 * (size_t)(id0 + s2), g, w, round, parent);
-      const int cnt = p.nf.next_seg[8 * k + s2];  // child entry count (from pcount)
-      const bool gate = !last && !(p.nf.smass[8 * k + s2] < p.min_points);
-      cgate[c] = gate ? 1 : 0;
-      ccnt[c] = gate ? (cnt + 1) & ~1 : 0;  // segments start at even entries (16-byte bulk copies)
-      codd[c] = gate ? cnt & 1 : 0;
-      ctil[c] = gate ? (cnt + kTile - 1) / kTile : 0;
-      cidx[c] = (k << 3) | s2;
-    }
+    const GComp& g = p.nf.comps[((size_t)k * 2 + kept) * 8 + p.nf.surv[8 * k + s2]];
+    const double sm_c = p.nf.smass[8 * k + s2];
+    const double w = sm_c / p.nf.stotal[k];
+    write_dnode_from_comp(p.nodes[id0 + s2], p.cov + 9 * (size_t)(id0 + s2), g, w, round, parent);
+    const int cnt = p.nf.next_seg[8 * k + s2];  // child entry count (from pcount)
+    const bool gate = !last && !(sm_c < p.min_points);
+    cgate[c] = gate ? 1 : 0;
+    ngate[c] = gate ? 1 : 0;
+    ccnt[c] = gate ? (cnt + 1) & ~1 : 0;  // segments start at even entries (16-byte bulk copies)
+    codd[c] = gate ? cnt & 1 : 0;
+    ctil[c] = gate ? (cnt + kTile - 1) / kTile : 0;
+    clen[c] = gate ? cnt : 0;
   }
   __syncthreads();
   // (3) next round's expanding list: positions, entry offsets, tile offsets
-  for (int c = tid; c < NC; c += nt) ngate[c] = cgate[c];
-  __syncthreads();
   const int K2 = block_exscan(cgate, NC, wtmp);
   const int E2 = block_exscan(ccnt, NC, wtmp);
   const int T2 = block_exscan(ctil, NC, wtmp);
@@ -1029,25 +1042,26 @@ __device__ void round_layout(const BuildParams& p, int par, int round, int* scra
     return;
   }
   for (int c = tid; c < NC; c += nt) {
-    const int k = cidx[c] >> 3, s2 = cidx[c] & 7;
+    const int k = upper_index(nbase, K, c), s2 = c - nbase[k];
     if (!ngate[c]) {
       p.nf.next_seg[8 * k + s2] = -1;
       continue;
     }
-    const int k2 = cgate[c], e2 = ccnt[c], t2 = ctil[c];
-    const int cnt = p.nf.next_seg[8 * k + s2];
-    const int ntl = (cnt + kTile - 1) / kTile;
+    const int k2 = cgate[c], e2 = ccnt[c], cnt = clen[c];
     p.rn[npar].tree_id[k2] = J0 + c;
     p.rn[npar].seg[k2] = e2;
     p.rn[npar].len[k2] = cnt;
-    p.rn[npar].tile0[k2] = t2;
-    p.rn[npar].ntiles[k2] = ntl;
-    for (int q = 0; q < ntl; ++q) {
-      p.tile_node[npar][t2 + q] = k2;
-      p.tile_start[npar][t2 + q] = e2 + q * kTile;
-      p.tile_len[npar][t2 + q] = min(kTile, cnt - q * kTile);
-    }
+    p.rn[npar].tile0[k2] = ctil[c];
+    p.rn[npar].ntiles[k2] = (cnt + kTile - 1) / kTile;
     p.nf.next_seg[8 * k + s2] = e2;
+  }
+  // (4) the next round's tiles, one per thread: its child by binary search
+  // over the tile offsets (ungated children own no tiles)
+  for (int t = tid; t < T2; t += nt) {
+    const int c = upper_index(ctil, NC, t), q = t - ctil[c];
+    p.tile_node[npar][t] = cgate[c];
+    p.tile_start[npar][t] = ccnt[c] + q * kTile;
+    p.tile_len[npar][t] = min(kTile, clen[c] - q * kTile);
   }
   __syncthreads();
   if (tid == 0) {
@@ -1293,7 +1307,7 @@ __device__ __forceinline__ void build_run(const BuildParams& p, int G, int cta) 
       const bool mine = !sharded || xp == p.seg;  // this launch runs the phase's work
       if (ph.layout) {
         if (mine) {
-          if (cta == 0) round_layout(p, par, round, p.layout_scratch);
+          if (cta == 0) round_layout(p, sm, par, round, p.layout_scratch);
           grid_sync(p.bar, G);
           tl_mark(p.tl, round * 100 + ph_i);
         }

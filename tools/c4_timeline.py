@@ -1,5 +1,5 @@
 """Device timeline of one C4 build (1M points, L=4): per-round tile / reduce
-time and the calibration stages."""
+time and the calibration stages (`phases`: per phase)."""
 import collections
 import sys
 sys.path.insert(0, ".")
@@ -15,10 +15,12 @@ tgd = torch.from_numpy(tg).cuda()
 for _ in range(2):
     tree = tr.build_tree(tgd, tr.ModelConfig(max_level=4), None, ctx)
 t, lab = marks(ctx)
+per_phase = len(sys.argv) > 1 and sys.argv[1] == "phases"
 g = collections.defaultdict(float)
 for i in range(1, len(t)):
     k = group(int(lab[i]))
-    k = k.rsplit(" phase", 1)[0]
+    if not per_phase:
+        k = k.rsplit(" phase", 1)[0]
     g[k] += t[i] - t[i - 1]
 print("span us %.0f" % (t[-1] - t[0]))
 for k, v in sorted(g.items()):
