@@ -557,16 +557,24 @@ __device__ void node_mstep_warp(const BuildParams& p, const Phase& ph, int k, co
   bool act = lane < 16 && ph.mode[c] == 1;
   GComp& g = p.nf.comps[((size_t)k * 2 + c) * 8 + comp];
   const double* ac = red + kOffEm + c * 81;
-  double total = 0.0, a[10];
+  // every operand in one round trip (the loads do not depend on the tests)
+  double tv[8], a[10], mn[3], flv = 1.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) tv[j] = lane < 16 ? __ldcg(ac + j * 10) : 0.0;
+#pragma unroll
+  for (int q = 0; q < 10; ++q) a[q] = lane < 16 ? __ldcg(ac + comp * 10 + q) : 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) mn[i] = lane < 16 ? __ldcg(&p.nf.mean[3 * k + i]) : 0.0;
+  if (lane < 16) flv = __ldcg(&p.nf.floorv[k]);
+  double total = 0.0;
   if (act) {
-    for (int j = 0; j < 8; ++j) total += __ldcg(ac + j * 10);
+    for (int j = 0; j < 8; ++j) total += tv[j];
     if (!(total > 0.0)) {
       atomicCAS(p.status, 0, kERuntime);  // m_step: no responsibility mass
       act = false;
     }
   }
   if (act) {
-    for (int q = 0; q < 10; ++q) a[q] = __ldcg(ac + comp * 10 + q);
     if (a[0] <= total * 1e-12) {
       g.w = 0.0;
       act = false;
@@ -582,9 +590,8 @@ __device__ void node_mstep_warp(const BuildParams& p, const Phase& ph, int k, co
       for (int j = 0; j < 3; ++j) sc[i][j] = m2[i][j] / m0 - d[i] * d[j];
     g.w = m0 / total;
     g.lw = log(g.w);
-    const double* mean = p.nf.mean + 3 * k;
-    for (int i = 0; i < 3; ++i) g.mean[i] = __ldcg(&mean[i]) + d[i];
-    fl = __ldcg(&p.nf.floorv[k]);
+    for (int i = 0; i < 3; ++i) g.mean[i] = mn[i] + d[i];
+    fl = flv;
   } else {
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) sc[i][j] = i == j ? 1.0 : 0.0;
@@ -739,7 +746,7 @@ __device__ void node_update_warp(const BuildParams& p, const Phase& ph, int k, i
     cand_init(p, k, 1, seed, lane);
   }
   // ll traces (BuildDiagnostics::node_ll_traces, gmm.cpp:240, 361)
-  if (lane < 2 && ph.mode[lane] != 0) {
+  if (p.want_traces && lane < 2 && ph.mode[lane] != 0) {
     const int c = lane, I = p.em_iters;
     const int slot = ph.mode[c] == 1 ? ph.em_it[c] - 1 : I;
     const double ll = ph.mode[c] == 1 ? __ldcg(red + kOffEm + 81 * c + 80) : __ldcg(red + kOffFin + 9 * c);
