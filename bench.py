@@ -396,9 +396,10 @@ def run_batched(args, tr, ctx, cfg, dist, dev, world):
     the host clock around whole synchronous batches, max over ranks."""
     import torch
     rank = dist.get_rank() if dist is not None else 0
-    pairs = [tr.kinect_pair(1 + rank * args.batch + k) for k in range(args.batch)]
-    tg = [torch.from_numpy(p[0]).to(dev).contiguous() for p in pairs]
-    sr = [torch.from_numpy(p[1]).to(dev).contiguous() for p in pairs]
+    # the pairs are rendered on the device (bit-identical to tr.kinect_pair)
+    pairs = [tr.kinect_pair_device(1 + rank * args.batch + k, ctx) for k in range(args.batch)]
+    tg = [p[0] for p in pairs]
+    sr = [p[1] for p in pairs]
     for _ in range(1):
         tr.register_batch(tg, sr, cfg, ctx, args.streams)
     torch.cuda.synchronize()

@@ -286,6 +286,21 @@ int trg_register_batch(trg_ctx* ctx, int n_pairs, const double* const* targets,
                        const size_t* n_sources, int on_device, const trg_reg_config* cfg,
                        int streams, trg_reg_result* out);
 
+/* ---- synthetic frames on the device (no reference
+ *      counterpart: the C2 / C3 / C5 generators are new).  The ray casting
+ *      of trg_synth_kinect_pair / trg_synth_lidar_pair (libtrg_host.so) as
+ *      one thread per pixel / beam, from the poses, noise draws and beam
+ *      directions trg_synth_*_pair_plan returns: bit-identical frames.
+ *      R, t: frames x 9 / 3 host doubles (sensor -> world); noise: frames x
+ *      76,800 (Kinect, scaled by noise_scale x the axial sigma) resp. frames
+ *      x 72,000 (LiDAR, x 0.02 m) host doubles, or NULL for noise-free
+ *      frames; dir_tables: 4,564 host doubles; out: DEVICE buffer of frames
+ *      x points x 3 doubles, written in order on ctx's stream. */
+int trg_render_kinect_frames(trg_ctx* ctx, int frames, const double* R, const double* t,
+                             const double* noise, double noise_scale, double* out);
+int trg_render_lidar_frames(trg_ctx* ctx, int frames, const double* R, const double* t,
+                            const double* noise, const double* dir_tables, double* out);
+
 /* ---- point-sharded execution (no reference counterpart:
  *      the reference is single-process).  A large cloud is split into
  *      contiguous blocks, one per shard; entries never move between shards.

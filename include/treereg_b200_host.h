@@ -54,6 +54,20 @@ int trg_synth_kinect_sequence(uint64_t seed, int frames, double step_rot_deg, do
 /* HDL-32-style sweep pair (72,000 points each). */
 int trg_synth_lidar_pair(uint64_t seed, double* target, double* source, double R_gt[9],
                          double t_gt[3]);
+/* The sequential parts of the two pair generators, for the device renderer
+ * (trg_render_kinect_frames / trg_render_lidar_frames, libtrg_cuda.so): the
+ * sensor poses of both frames (R[f]: 9 doubles sensor -> world, t[f]: 3),
+ * the noise draws of both frames in pixel / beam order (noise: 2 x 76,800
+ * resp. 2 x 72,000 doubles), the LiDAR beam direction tables (dir_tables:
+ * 4,564 doubles: cos / sin of the 2,250 azimuths, cos / sin of the 32
+ * elevations) and the ground truth.  Rendering from them reproduces
+ * trg_synth_kinect_pair_ex(seed, noise_scale, rot, trans, ...) /
+ * trg_synth_lidar_pair(seed, ...) bit for bit. */
+int trg_synth_kinect_pair_plan(uint64_t seed, double rot_range_deg, double trans_range,
+                               double R[18], double t[6], double* noise, double R_gt[9],
+                               double t_gt[3]);
+int trg_synth_lidar_pair_plan(uint64_t seed, double R[18], double t[6], double* noise,
+                              double* dir_tables, double R_gt[9], double t_gt[3]);
 
 #ifdef __cplusplus
 }

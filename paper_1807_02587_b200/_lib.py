@@ -128,6 +128,8 @@ SIGNATURES = {
     "trg_register_clouds_sharded": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
                                               C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int,
                                               C.c_void_p, C.c_void_p]),
+    "trg_render_kinect_frames": (C.c_int, [C.c_void_p, C.c_int, dp, dp, dp, C.c_double, C.c_void_p]),
+    "trg_render_lidar_frames": (C.c_int, [C.c_void_p, C.c_int, dp, dp, dp, dp, C.c_void_p]),
     "trg_register_batch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
                                      C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int,
                                      C.c_void_p, C.c_int, C.c_void_p]),
@@ -154,6 +156,8 @@ HOST_SIGNATURES = {
     "trg_synth_kinect_pair_ex": (C.c_int, [C.c_uint64, C.c_double, C.c_double, C.c_double, dp, dp,
                                            dp, dp]),
     "trg_synth_lidar_pair": (C.c_int, [C.c_uint64, dp, dp, dp, dp]),
+    "trg_synth_kinect_pair_plan": (C.c_int, [C.c_uint64, C.c_double, C.c_double, dp, dp, dp, dp, dp]),
+    "trg_synth_lidar_pair_plan": (C.c_int, [C.c_uint64, dp, dp, dp, dp, dp, dp]),
 }
 
 _LIB = None

@@ -269,6 +269,7 @@ struct BuildSmem {
   int item_off[192];
   int item_kind[192];
   int tnode, tstart, tlen, tidx;
+  int probe;  // TRG_TILE_PROBE: this CTA's tiles of the probed phase are marked
   alignas(16) double ent[4][kTile + 2];  // the tile's entries (x, y, z, w): one bulk copy per tile
   uint64_t mbar;                          // completion of the tile's bulk copies
   unsigned mphase;                        // its phase parity (thread 0's copy)
@@ -284,6 +285,14 @@ struct BuildSmem {
 };
 
 // ----------------------------------------------------------------- tile work
+#ifdef TRG_TILE_PROBE
+#ifndef TRG_TILE_PROBE_ROUND
+#define TRG_TILE_PROBE_ROUND 0
+#endif
+#define TPROBE(lab) if (sm.probe && threadIdx.x == 0) tl_mark_any(p.tl, lab)
+#else
+#define TPROBE(lab)
+#endif
 // Thread-per-entry passes: list_moments 1/2 and one FPS round.
 __device__ void tile_entry_pass(const BuildParams& p, BuildSmem& sm, const Phase& ph, int par,
                                 TileRec rec) {
@@ -387,6 +396,7 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     }
   }
   __syncthreads();
+  TPROBE(8003);
   // ---- (1b) entry per thread: max / sum / log in component order exactly
   // like the reference
   if (tid < tlen) {
@@ -436,6 +446,7 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     G.best = best;
   }
   __syncthreads();
+  TPROBE(8004);
   // ---- (2)
   if (!pcount) {
     for (int item = warp; item < nc * 8; item += kTile / 32) {
@@ -1337,10 +1348,16 @@ __device__ __forceinline__ void build_run(const BuildParams& p, int G, int cta) 
         // (a) tile pass (the phase's reduction items are listed first, off the
         // critical path: the lists live outside the tile scratch)
         if (tid == 0) sm.nitems = phase_items(ph, sm.item_off, sm.item_kind);
+#ifdef TRG_TILE_PROBE
+        if (tid == 0) sm.probe = cta == 0 && ph_i == TRG_TILE_PROBE && round == TRG_TILE_PROBE_ROUND;
+        TPROBE(8000);
+#endif
         const int T = __ldcg(&st->Tp[par]);
         int ntl = 0, nent = 0;
         for (int t = cta; t < T; t += G) {
+          TPROBE(8001);
           load_tile_ctx(p, sm, ph, par, t);
+          TPROBE(8002);
           const TileRec rec{p.partial + t, (size_t)p.Tmax};
           tile_entry_pass(p, sm, ph, par, rec);
           if (ph.mode[0] || ph.mode[1]) tile_comp_pass(p, sm, ph, par, rec, false);
@@ -1348,6 +1365,7 @@ __device__ __forceinline__ void build_run(const BuildParams& p, int G, int cta) 
           ++ntl;
           nent += sm.tlen;
           __syncthreads();
+          TPROBE(8009);
         }
         grid_sync(p.bar, G);
         tl_mark(p.tl, round * 100 + ph_i);

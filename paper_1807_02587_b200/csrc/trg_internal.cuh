@@ -198,6 +198,7 @@ enum Slot : int {
   kSlotHostEmInit,    // host slots only: pinned EmState initialiser (no staging sync)
   kSlotHostBuildInit, // host slots only: pinned BuildState initialiser
   kSlotHostCollect,   // host slots only: a call's results, fetched with one synchronisation
+  kSlotRender,        // frame renderer (trg_render.cu): poses, noise draws, direction tables
 };
 
 int ws_get(trg_ctx* ctx, int slot, size_t bytes, void** out);

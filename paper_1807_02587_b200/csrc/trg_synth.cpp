@@ -22,6 +22,7 @@
 
 #include "../../include/treereg_b200.h"  // status codes
 #include "../../include/treereg_b200_host.h"
+#include "trg_raycast.h"
 
 namespace {
 
@@ -258,75 +259,9 @@ V3 apply(const double R[9], const double t[3], V3 p) {
 }
 
 // ------------------------------------------------------- ray casting (new)
-constexpr double kInf = std::numeric_limits<double>::infinity();
-
-struct Ray {
-  V3 o, d;
-};
-
-// Axis-aligned box, inside (room: ray starts inside) or outside hit.
-double hit_box_outside(const Ray& r, V3 lo, V3 hi) {
-  double t0 = 0.0, t1 = kInf;
-  const double o[3] = {r.o.x, r.o.y, r.o.z}, d[3] = {r.d.x, r.d.y, r.d.z};
-  const double l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
-  for (int k = 0; k < 3; ++k) {
-    if (std::fabs(d[k]) < 1e-15) {
-      if (o[k] < l[k] || o[k] > h[k]) return kInf;
-      continue;
-    }
-    double a = (l[k] - o[k]) / d[k], b = (h[k] - o[k]) / d[k];
-    if (a > b) std::swap(a, b);
-    t0 = std::max(t0, a);
-    t1 = std::min(t1, b);
-    if (t0 > t1) return kInf;
-  }
-  return t0 > 1e-9 ? t0 : kInf;
-}
-
-double hit_box_inside(const Ray& r, V3 lo, V3 hi) {
-  double t = kInf;
-  const double o[3] = {r.o.x, r.o.y, r.o.z}, d[3] = {r.d.x, r.d.y, r.d.z};
-  const double l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
-  for (int k = 0; k < 3; ++k) {
-    if (d[k] > 0) t = std::min(t, (h[k] - o[k]) / d[k]);
-    if (d[k] < 0) t = std::min(t, (l[k] - o[k]) / d[k]);
-  }
-  return t;
-}
-
-double hit_sphere(const Ray& r, V3 c, double rad) {
-  const V3 oc = sub(r.o, c);
-  const double a = dot(r.d, r.d);  // ray directions are not unit length
-  const double b = dot(oc, r.d), cc = dot(oc, oc) - rad * rad;
-  const double disc = b * b - a * cc;
-  if (disc < 0) return kInf;
-  const double t = (-b - std::sqrt(disc)) / a;
-  return t > 1e-9 ? t : kInf;
-}
-
-// Parallelogram corner + a*eu + b*ev, a,b in [0,1].
-double hit_panel(const Ray& r, V3 corner, V3 eu, V3 ev) {
-  const V3 n{eu.y * ev.z - eu.z * ev.y, eu.z * ev.x - eu.x * ev.z, eu.x * ev.y - eu.y * ev.x};
-  const double dn = dot(r.d, n);
-  if (std::fabs(dn) < 1e-15) return kInf;
-  const double t = dot(sub(corner, r.o), n) / dn;
-  if (!(t > 1e-9)) return kInf;
-  const V3 p = sub(add(r.o, mul(t, r.d)), corner);
-  const double uu = dot(eu, eu), vv = dot(ev, ev), uv = dot(eu, ev);
-  const double pu = dot(p, eu), pv = dot(p, ev);
-  const double det = uu * vv - uv * uv;
-  const double a = (pu * vv - pv * uv) / det, b = (pv * uu - pu * uv) / det;
-  return (a >= 0 && a <= 1 && b >= 0 && b <= 1) ? t : kInf;
-}
-
-// Closed room: synthetic_scene's layout scaled x2 (metres), y up.
-double cast_room(const Ray& r) {
-  double t = hit_box_inside(r, {0, 0, 0}, {4, 2.4, 3});
-  t = std::min(t, hit_box_outside(r, {2.4, 0.0, 1.8}, {3.2, 0.7, 2.6}));
-  t = std::min(t, hit_sphere(r, {1.1, 0.6, 1.0}, 0.44));
-  t = std::min(t, hit_panel(r, {1.8, 0.0, 0.2}, {1.0, 0.0, 0.3}, {0.0, 0.8, 0.6}));
-  return t;
-}
+// The scenes and the per-pixel / per-beam casts live in trg_raycast.h, shared
+// with the device renderer (trg_render.cu): the same operations in the same
+// order on both sides.
 
 // Camera-to-world pose for a Kinect frame: looks from (3.4,1.5,2.6) at the
 // room corner area.  Camera axes: x right, y down, z forward.
@@ -344,80 +279,50 @@ void look_at(V3 eye, V3 target, double R[9], double t[3]) {
   t[0] = eye.x; t[1] = eye.y; t[2] = eye.z;
 }
 
+// The axial-noise draws of one frame: one N(0, 1) per pixel in pixel order
+// (a fresh distribution per frame, as render_kinect draws them).
+void frame_normals(Rng& rng, std::size_t n, double* out) {
+  std::normal_distribution<double> g(0.0, 1.0);
+  for (std::size_t i = 0; i < n; ++i) out[i] = g(rng);
+}
+
 // Renders one 320x240 frame from camera pose (Rwc, twc); points in camera
 // coordinates, axial noise sigma_z = 0.0012 + 0.0019 (z - 0.4)^2.
 void render_kinect(const double Rwc[9], const double twc[3], Rng& rng, double* out,
                    double noise_scale) {
-  const double fx = 262.5, fy = 262.5, cx = 159.5, cy = 119.5;
   std::normal_distribution<double> g(0.0, 1.0);
   std::size_t k = 0;
   for (int v = 0; v < 240; ++v)
-    for (int u = 0; u < 320; ++u) {
-      const V3 dc{(u - cx) / fx, (v - cy) / fy, 1.0};
-      const V3 dw{Rwc[0] * dc.x + Rwc[1] * dc.y + Rwc[2] * dc.z,
-                  Rwc[3] * dc.x + Rwc[4] * dc.y + Rwc[5] * dc.z,
-                  Rwc[6] * dc.x + Rwc[7] * dc.y + Rwc[8] * dc.z};
-      const Ray r{{twc[0], twc[1], twc[2]}, dw};
-      const double t = cast_room(r);  // z = t since dc.z == 1
-      const double z = std::isfinite(t) ? t : 6.0;
-      const double sz = 0.0012 + 0.0019 * (z - 0.4) * (z - 0.4);
-      const double zn = z + noise_scale * sz * g(rng);
-      out[k++] = dc.x * zn;
-      out[k++] = dc.y * zn;
-      out[k++] = zn;
-    }
+    for (int u = 0; u < 320; ++u, k += 3) trg_rc::kinect_pixel(Rwc, twc, u, v, g(rng), noise_scale, out + k);
 }
 
-// HDL-32 street: ground z = 0, building boxes, poles, enclosing cylinder.
-double cast_street(const Ray& r) {
-  double t = kInf;
-  if (r.d.z < 0) t = -r.o.z / r.d.z;
-  static const double boxes[][6] = {
-      {8, -20, 0, 20, -9, 9},  {-25, -22, 0, -10, -8, 14}, {-6, 10, 0, 12, 24, 7},
-      {25, 6, 0, 40, 18, 11},  {-40, 12, 0, -28, 30, 16},  {-18, -45, 0, 5, -34, 10},
-      {30, -30, 0, 44, -16, 8}, {3, -6, 0, 5, -4, 1.2}};
-  for (const auto& b : boxes)
-    t = std::min(t, hit_box_outside(r, {b[0], b[1], b[2]}, {b[3], b[4], b[5]}));
-  static const double poles[][3] = {{6, 4, 0.15}, {-5, 5, 0.2}, {14, -3, 0.15},
-                                    {-12, -4, 0.25}, {2, 12, 0.15}, {-3, -14, 0.2}};
-  for (const auto& p : poles) {  // vertical cylinders of height 6 m
-    const double ox = r.o.x - p[0], oy = r.o.y - p[1];
-    const double a = r.d.x * r.d.x + r.d.y * r.d.y;
-    if (a < 1e-15) continue;
-    const double b = ox * r.d.x + oy * r.d.y, c = ox * ox + oy * oy - p[2] * p[2];
-    const double disc = b * b - a * c;
-    if (disc < 0) continue;
-    const double tc = (-b - std::sqrt(disc)) / a;
-    if (tc > 1e-9 && r.o.z + tc * r.d.z <= 6.0) t = std::min(t, tc);
+// HDL-32 beam directions: azimuth a (2250 steps of 0.16 deg), elevation b
+// (32 beams from -30.67 deg by 1.3333 deg); cos / sin tables [cos 2250 | sin
+// 2250 | cos 32 | sin 32] (libm on the host; the device renderer takes them)
+void lidar_tables(double* tab) {
+  constexpr double kDeg = 0.017453292519943295;
+  for (int a = 0; a < 2250; ++a) {
+    const double az = a * 0.16 * kDeg;
+    tab[a] = std::cos(az);
+    tab[2250 + a] = std::sin(az);
   }
-  {  // enclosing cylinder r = 60 (every ray returns)
-    const double a = r.d.x * r.d.x + r.d.y * r.d.y;
-    const double b = r.o.x * r.d.x + r.o.y * r.d.y, c = r.o.x * r.o.x + r.o.y * r.o.y - 3600.0;
-    const double tc = (-b + std::sqrt(b * b - a * c)) / a;
-    t = std::min(t, tc);
+  for (int b = 0; b < 32; ++b) {
+    const double el = (-30.67 + 1.3333 * b) * kDeg;
+    tab[4500 + b] = std::cos(el);
+    tab[4532 + b] = std::sin(el);
   }
-  return t;
 }
 
 void render_lidar(const double Rws[9], const double tws[3], Rng& rng, double* out) {
   std::normal_distribution<double> g(0.0, 1.0);
-  constexpr double kDeg = 0.017453292519943295;
+  double tab[4564];
+  lidar_tables(tab);
   std::size_t k = 0;
-  for (int a = 0; a < 2250; ++a) {
-    const double az = a * 0.16 * kDeg;
-    for (int b = 0; b < 32; ++b) {
-      const double el = (-30.67 + 1.3333 * b) * kDeg;
-      const V3 ds{std::cos(el) * std::cos(az), std::cos(el) * std::sin(az), std::sin(el)};
-      const V3 dw{Rws[0] * ds.x + Rws[1] * ds.y + Rws[2] * ds.z,
-                  Rws[3] * ds.x + Rws[4] * ds.y + Rws[5] * ds.z,
-                  Rws[6] * ds.x + Rws[7] * ds.y + Rws[8] * ds.z};
-      const Ray r{{tws[0], tws[1], tws[2]}, dw};
-      const double range = cast_street(r) + 0.02 * g(rng);
-      out[k++] = ds.x * range;
-      out[k++] = ds.y * range;
-      out[k++] = ds.z * range;
+  for (int a = 0; a < 2250; ++a)
+    for (int b = 0; b < 32; ++b, k += 3) {
+      const trg_rc::V3 ds{tab[4500 + b] * tab[a], tab[4500 + b] * tab[2250 + a], tab[4532 + b]};
+      trg_rc::lidar_beam(Rws, tws, ds, g(rng), out + k);
     }
-  }
 }
 
 // Relative pose: source frame -> target frame, given both sensor->world poses.
@@ -494,20 +399,73 @@ int trg_random_rigid_transform(double rot_deg, double trans, uint64_t seed, int 
   return TRG_OK;
 }
 
-int trg_synth_kinect_pair_ex(uint64_t seed, double noise_scale, double rot_deg, double trans,
-                             double* target, double* source, double R_gt[9], double t_gt[3]) {
-  double R1[9], t1[3];
+}  // extern "C"
+
+namespace {
+// Camera poses of a Kinect pair: camera 2 = camera 1 moved by
+// random_rigid_transform({rot_deg, trans}, trial 0) in its own frame.
+void kinect_pair_poses(uint64_t seed, double rot_deg, double trans, double R1[9], double t1[3],
+                       double R2[9], double t2[3]) {
   look_at({3.4, 1.5, 2.6}, {1.2, 0.7, 0.9}, R1, t1);
   double dR[9], dt[3];
   rigid(rot_deg, trans, seed, 0, dR, dt);
-  double R2[9], t2[3];  // camera 2 = camera 1 moved by (dR, dt) in its own frame
   matmul(R1, dR, R2);
   for (int i = 0; i < 3; ++i)
     t2[i] = t1[i] + R1[3 * i] * dt[0] + R1[3 * i + 1] * dt[1] + R1[3 * i + 2] * dt[2];
+}
+
+// Sensor poses of a LiDAR pair: 1 m forward + 2 deg yaw, then a small
+// random perturbation.
+void lidar_pair_poses(uint64_t seed, double R1[9], double t1[3], double R2[9], double t2[3]) {
+  constexpr double kDeg = 0.017453292519943295;
+  for (int k = 0; k < 9; ++k) R1[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  t1[0] = 0.0;
+  t1[1] = 0.0;
+  t1[2] = 1.8;
+  const double c = std::cos(2.0 * kDeg), s = std::sin(2.0 * kDeg);
+  const double Rego[9] = {c, -s, 0, s, c, 0, 0, 0, 1};
+  double dR[9], dt[3];
+  rigid(1.0, 0.05, seed, 0, dR, dt);
+  matmul(Rego, dR, R2);
+  t2[0] = 1.0 + dt[0];
+  t2[1] = dt[1];
+  t2[2] = 1.8 + dt[2];
+}
+}  // namespace
+
+extern "C" {
+
+int trg_synth_kinect_pair_ex(uint64_t seed, double noise_scale, double rot_deg, double trans,
+                             double* target, double* source, double R_gt[9], double t_gt[3]) {
+  double R1[9], t1[3], R2[9], t2[3];
+  kinect_pair_poses(seed, rot_deg, trans, R1, t1, R2, t2);
   Rng rng(splitmix64(seed + 0x4b696e656374ull));
   render_kinect(R1, t1, rng, target, noise_scale);
   render_kinect(R2, t2, rng, source, noise_scale);
   relative(R1, t1, R2, t2, R_gt, t_gt);
+  return TRG_OK;
+}
+
+int trg_synth_kinect_pair_plan(uint64_t seed, double rot_deg, double trans, double Rwc[18],
+                               double twc[6], double* noise, double R_gt[9], double t_gt[3]) {
+  if (!Rwc || !twc || !noise || !R_gt || !t_gt) return TRG_EINVAL;
+  kinect_pair_poses(seed, rot_deg, trans, Rwc, twc, Rwc + 9, twc + 3);
+  Rng rng(splitmix64(seed + 0x4b696e656374ull));
+  frame_normals(rng, 76800, noise);
+  frame_normals(rng, 76800, noise + 76800);
+  relative(Rwc, twc, Rwc + 9, twc + 3, R_gt, t_gt);
+  return TRG_OK;
+}
+
+int trg_synth_lidar_pair_plan(uint64_t seed, double Rws[18], double tws[6], double* noise,
+                              double* dir_tables, double R_gt[9], double t_gt[3]) {
+  if (!Rws || !tws || !noise || !dir_tables || !R_gt || !t_gt) return TRG_EINVAL;
+  lidar_pair_poses(seed, Rws, tws, Rws + 9, tws + 3);
+  Rng rng(splitmix64(seed + 0x4c69444152ull));
+  frame_normals(rng, 72000, noise);
+  frame_normals(rng, 72000, noise + 72000);
+  lidar_tables(dir_tables);
+  relative(Rws, tws, Rws + 9, tws + 3, R_gt, t_gt);
   return TRG_OK;
 }
 
@@ -543,19 +501,8 @@ int trg_synth_kinect_pair(uint64_t seed, double* target, double* source, double 
 
 int trg_synth_lidar_pair(uint64_t seed, double* target, double* source, double R_gt[9],
                          double t_gt[3]) {
-  constexpr double kDeg = 0.017453292519943295;
-  double R1[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-  const double t1[3] = {0.0, 0.0, 1.8};
-  // ego motion: 1 m forward + 2 deg yaw, then a small random perturbation
-  const double c = std::cos(2.0 * kDeg), s = std::sin(2.0 * kDeg);
-  const double Rego[9] = {c, -s, 0, s, c, 0, 0, 0, 1};
-  double dR[9], dt[3];
-  rigid(1.0, 0.05, seed, 0, dR, dt);
-  double R2[9], t2[3];
-  matmul(Rego, dR, R2);
-  t2[0] = 1.0 + dt[0];
-  t2[1] = dt[1];
-  t2[2] = 1.8 + dt[2];
+  double R1[9], t1[3], R2[9], t2[3];
+  lidar_pair_poses(seed, R1, t1, R2, t2);
   Rng rng(splitmix64(seed + 0x4c69444152ull));
   render_lidar(R1, t1, rng, target);
   render_lidar(R2, t2, rng, source);

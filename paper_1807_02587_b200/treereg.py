@@ -871,6 +871,53 @@ def kinect_sequence(seed: int, frames: int, step_rot_deg: float = 2.0, step_tran
     return out, [RigidTransform(R[k], t[k]) for k in range(frames)]
 
 
+def _render_frames(kind: str, seed: int, ctx, noise_scale: float, rot_range_deg: float,
+                   trans_range: float):
+    import torch
+    ctx = ctx or default_context()
+    n = 76800 if kind == "kinect" else 72000
+    R, t = np.zeros((2, 3, 3)), np.zeros((2, 3))
+    noise = np.zeros(2 * n)
+    Rg, tg = np.zeros((3, 3)), np.zeros(3)
+    H = _lib.host_lib()
+    tab = None
+    if kind == "kinect":
+        _chk_host(H.trg_synth_kinect_pair_plan(seed, rot_range_deg, trans_range, _d(R), _d(t), _d(noise),
+                                               _d(Rg), _d(tg)))
+    else:
+        tab = np.zeros(4564)
+        _chk_host(H.trg_synth_lidar_pair_plan(seed, _d(R), _d(t), _d(noise), _d(tab), _d(Rg), _d(tg)))
+    dev = torch.device("cuda", ctx.device)
+    out = torch.empty((2, n, 3), dtype=torch.float64, device=dev)
+    # the buffer's previous users on torch's stream finish first; torch's
+    # stream then waits for the render
+    _chk(_lib.lib().trg_ctx_wait_stream(ctx.h, C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    if kind == "kinect":
+        _chk(_lib.lib().trg_render_kinect_frames(ctx.h, 2, _d(R), _d(t), _d(noise), noise_scale,
+                                                 C.c_void_p(out.data_ptr())))
+    else:
+        _chk(_lib.lib().trg_render_lidar_frames(ctx.h, 2, _d(R), _d(t), _d(noise), _d(tab),
+                                                C.c_void_p(out.data_ptr())))
+    torch.cuda.current_stream(dev).wait_stream(torch.cuda.ExternalStream(ctx.stream, device=dev))
+    return out[0], out[1], RigidTransform(Rg, tg)
+
+
+def kinect_pair_device(seed: int, ctx: Context | None = None, noise_scale: float = 1.0,
+                       rot_range_deg: float = 5.0, trans_range: float = 0.05):
+    """kinect_pair rendered on the GPU: the poses and the
+    noise draws from the host generator (trg_synth_kinect_pair_plan), the
+    76,800 rays per frame cast on the device (trg_render_kinect_frames) ->
+    (target, source) as CUDA (N, 3) float64 tensors, bit-identical to
+    kinect_pair(seed), and the ground truth."""
+    return _render_frames("kinect", seed, ctx, noise_scale, rot_range_deg, trans_range)
+
+
+def lidar_pair_device(seed: int, ctx: Context | None = None):
+    """lidar_pair rendered on the GPU (trg_render_lidar_frames), bit-identical
+    to lidar_pair(seed)."""
+    return _render_frames("lidar", seed, ctx, 1.0, 0.0, 0.0)
+
+
 def lidar_pair(seed: int):
     """C3: HDL-32-style sweep pair -> (target, source, gt source->target)."""
     tg, sr, R, t = np.zeros((72000, 3)), np.zeros((72000, 3)), np.zeros((3, 3)), np.zeros(3)
