@@ -1373,14 +1373,20 @@ __device__ __forceinline__ void build_run(const BuildParams& p, int G, int cta) 
         // whole cloud is here)
         const int NI = sm.nitems;
         const int K = __ldcg(&st->Kp[par]);
-        for (int it = cta * (kTile / 32) + warp; it < K * NI; it += G * (kTile / 32)) {
-          const int k = it / NI, f = it % NI;
-          reduce_item(p, par, k, sm.item_off[f], sm.item_kind[f]);
+        // F consecutive fields per warp item, F chosen so that every warp has
+        // at most one item: a warp that completes a node runs its update
+        // (~5 us), and a second item queued behind it would delay that other
+        // node's update in turn
+        const int nw = G * (kTile / 32);
+        const int F = max(1, (K * NI + nw - 1) / nw), IPN = (NI + F - 1) / F;
+        for (int it = cta * (kTile / 32) + warp; it < K * IPN; it += nw) {
+          const int k = it / IPN, f0 = (it % IPN) * F, f1 = min(f0 + F, NI);
+          for (int f = f0; f < f1; ++f) reduce_item(p, par, k, sm.item_off[f], sm.item_kind[f]);
           if (sharded) continue;
           unsigned last = 0;
           if (lane == 0) {
-            // release this item's sum, acquire the node's other items
-            last = (atom_add_acq_rel(&p.fdone[k], 1u) == (unsigned)NI - 1) ? 1u : 0u;
+            // release this item's sums, acquire the node's other items
+            last = (atom_add_acq_rel(&p.fdone[k], 1u) == (unsigned)IPN - 1) ? 1u : 0u;
             if (last) p.fdone[k] = 0u;  // (ordered before the next phase by the grid barrier)
           }
           last = __shfl_sync(0xffffffffu, last, 0);
