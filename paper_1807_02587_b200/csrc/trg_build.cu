@@ -1671,8 +1671,12 @@ __device__ void cal_finish_leaf(const BuildParams& p, const CalCtx& cx, int j, d
 // Second persistent kernel of the build (launched right behind k_build on
 // the same stream): parent moment match + refresh_eig, then the leaf
 // calibration passes.
+// Three CTAs per SM (80 registers): the association windows are bound by
+// each SM's share of the descents, and 24 warps per SM hide their latency
+// better than 16 (C2 stage 1 22.4 -> 19.3 us per pass); the leaf refits'
+// spills cost less (stage 2 +0.8 us).
 #ifndef TRG_KCAL_MINB
-#define TRG_KCAL_MINB 2
+#define TRG_KCAL_MINB 3
 #endif
 __device__ __forceinline__ void calibrate_run(const BuildParams& p, int G, int cta) {
   __shared__ FxScale sc[3];
