@@ -378,8 +378,9 @@ __device__ void assoc_fx_pass_f32(const AssocParams& p, const FNode* fnodes, con
 // completing on `bar` (phase bit `phase`, flipped on return).  Block-wide;
 // the nodes may have been rewritten by other CTAs before the caller's last
 // grid barrier.
-__device__ __forceinline__ void stage_nodes_bulk(DNode* snodes, const DNode* nodes, int S,
-                                                 uint64_t* bar, unsigned& phase) {
+// In two halves, so that a caller can overlap the copy with other loads.
+__device__ __forceinline__ void stage_nodes_issue(DNode* snodes, const DNode* nodes, int S,
+                                                  uint64_t* bar) {
   if (S <= 0) return;
   __syncthreads();  // every reader of the previous stage is done
   if (threadIdx.x == 0) {
@@ -387,9 +388,17 @@ __device__ __forceinline__ void stage_nodes_bulk(DNode* snodes, const DNode* nod
     fence_proxy_async_global();
     bulk_g2s_issue(snodes, nodes, (unsigned)(S * sizeof(DNode)), bar);
   }
+}
+__device__ __forceinline__ void stage_nodes_wait(int S, uint64_t* bar, unsigned& phase) {
+  if (S <= 0) return;
   if (threadIdx.x == 0) mbar_wait(bar, phase);
   __syncthreads();
   phase ^= 1u;
+}
+__device__ __forceinline__ void stage_nodes_bulk(DNode* snodes, const DNode* nodes, int S,
+                                                 uint64_t* bar, unsigned& phase) {
+  stage_nodes_issue(snodes, nodes, S, bar);
+  stage_nodes_wait(S, bar, phase);
 }
 
 // Node j's NM values from the planar accumulators.

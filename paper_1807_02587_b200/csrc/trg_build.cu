@@ -1743,15 +1743,20 @@ __device__ __forceinline__ void calibrate_run(const BuildParams& p, int G, int c
     if (pass == TRG_PROBE_PASS && tid == 0 && cta % 32 == 0) tl_mark_any(p.tl, 5100);
 #endif
     if (run_s1) {
+      // the upper levels (stage 2 rewrote them) are copied while the drift
+      // test's load is in flight
+      stage_nodes_issue(cal_stage, p.nodes, n_stage, &mbar);
+      bool stop = false;
       if (pass > 0) {
         const double dprev = __longlong_as_double((long long)__ldcg(&p.drift_bits[(pass - 1) & 1]));
-        if (!(dprev > 1e-13)) {  // gmm.cpp:652
-          if (sharded && cta == 0 && tid == 0) st->cal_done = 1;
-          break;
-        }
+        stop = !(dprev > 1e-13);  // gmm.cpp:652
+      }
+      stage_nodes_wait(n_stage, &mbar, mphase);  // (no copy may outlive the CTA)
+      if (stop) {
+        if (sharded && cta == 0 && tid == 0) st->cal_done = 1;
+        break;
       }
       if (cta == 0 && tid == 0) p.drift_bits[pass & 1] = 0ull;
-      stage_nodes_bulk(cal_stage, p.nodes, n_stage, &mbar, mphase);  // stage 2 rewrote them
 #ifdef TRG_ASSOC_PROBE
       if (pass == TRG_PROBE_PASS && tid == 0 && cta % 32 == 0) tl_mark_any(p.tl, 5103);
 #endif
