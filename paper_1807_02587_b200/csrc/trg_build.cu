@@ -1486,24 +1486,34 @@ struct CalCtx {
 
 __device__ __forceinline__ void cal_reweight(const BuildParams& p, const double* branch, int first,
                                              int count, double& drift) {
-  double s = 0.0;
-  for (int c = 0; c < count; ++c) s += __ldcg(&branch[first + c]);
-  if (!(s > 0.0)) return;  // shadowed octet: keep the fitted shares
-  for (int c = 0; c < count; ++c) {
-    const double w = __ldcg(&branch[first + c]) / s;
-    drift = smax(drift, fabs(__ldcg(&p.nodes[first + c].weight) - w));
-    p.nodes[first + c].weight = w;
+  double b[8], wo[8];  // every operand in one round trip (count <= 8)
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    b[c] = c < count ? __ldcg(&branch[first + c]) : 0.0;
+    wo[c] = c < count ? __ldcg(&p.nodes[first + c].weight) : 0.0;
   }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c < count) s += b[c];
+  if (!(s > 0.0)) return;  // shadowed octet: keep the fitted shares
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c < count) {
+      const double w = b[c] / s;
+      drift = smax(drift, fabs(wo[c] - w));
+      p.nodes[first + c].weight = w;
+    }
 }
 
-// Node i is final for this pass: arrive on its parent.  Returns the parent
-// when this arrival completed it (its node work is then this thread's), -1
-// otherwise (or after reweighting the top octet).
-__device__ __forceinline__ int cal_arrive(const BuildParams& p, const CalCtx& cx, int i,
+// A node is final for this pass: arrive on its parent `par` (-1: the top
+// octet), which has `need` children (both loaded by the caller ahead of
+// time, off the climb's critical path).  Returns the parent when this
+// arrival completed it (its node work is then this thread's), -1 otherwise
+// (or after reweighting the top octet).
+__device__ __forceinline__ int cal_arrive(const BuildParams& p, const CalCtx& cx, int par, int need,
                                           double& drift) {
-  const int par = __ldcg(&p.nodes[i].parent);
   const int slot = par >= 0 ? par : p.capacity;
-  const int need = par >= 0 ? __ldcg(&p.nodes[par].child_count) : cx.root_count;
   const unsigned old = atom_add_acq_rel(&cx.arrive[slot], 1u);  // release mine, acquire siblings'
   if (old + 1 != (unsigned)need) return -1;
   cx.arrive[slot] = 0u;
@@ -1534,9 +1544,12 @@ __device__ __forceinline__ void child_sums(const double (&v)[N], int cc, double 
 // Internal node P, all children final, by one warp (lane c holds child c):
 // branch mass, octet reweight, moment match of P (no eigensolve).  Every
 // sum runs in child order.
-__device__ void cal_internal(const BuildParams& p, const CalCtx& cx, int P, double& drift) {
+__device__ void cal_internal(const BuildParams& p, const CalCtx& cx, int P, double& drift,
+                             int& ppar, int& pneed) {
   const int lane = threadIdx.x & 31;
   const int f = __ldcg(&p.nodes[P].first_child), cc = __ldcg(&p.nodes[P].child_count);
+  ppar = __ldcg(&p.nodes[P].parent);  // for the next arrival (with the children's loads)
+  pneed = ppar >= 0 ? __ldcg(&p.nodes[ppar].child_count) : cx.root_count;
   const bool own = lane < cc;
   const int ci = f + (own ? lane : 0);
   const double cb = own ? __ldcg(&cx.branch[ci]) : 0.0;
@@ -1638,20 +1651,22 @@ __device__ void cal_leaf(const BuildParams& p, const CalCtx& cx, int j, const do
 // Leaf j final (its warp; lane 0 did the refit): climb as long as this warp
 // completes ancestors, then the refresh_eig of every node it matched, one
 // lane each.
-__device__ void cal_finish_leaf(const BuildParams& p, const CalCtx& cx, int j, double& drift) {
+__device__ void cal_finish_leaf(const BuildParams& p, const CalCtx& cx, int j, int par, int need,
+                                double& drift) {
   const int lane = threadIdx.x & 31;
   int done[8];
   int nd = 0;
   int P = -1;
-  if (lane == 0) P = cal_arrive(p, cx, j, drift);
+  if (lane == 0) P = cal_arrive(p, cx, par, need, drift);
   P = __shfl_sync(0xffffffffu, P, 0);
   CAL_PROBE(lane == 0 && j % 16 == 0, 5003);
   while (P >= 0) {
-    cal_internal(p, cx, P, drift);
+    int ppar, pneed;
+    cal_internal(p, cx, P, drift, ppar, pneed);
     __syncwarp();
     CAL_PROBE(lane == 0, 5010);
     done[nd++] = P;
-    if (lane == 0) P = cal_arrive(p, cx, P, drift);
+    if (lane == 0) P = cal_arrive(p, cx, ppar, pneed, drift);
     P = __shfl_sync(0xffffffffu, P, 0);
     CAL_PROBE(lane == 0, 5011);
   }
@@ -1786,7 +1801,10 @@ __device__ __forceinline__ void calibrate_run(const BuildParams& p, int G, int c
     }
     double drift = 0.0;
     for (int j = warp * G + cta; j < J; j += G * WPB) {  // a warp per leaf, spread over SMs
-      if (__ldcg(&p.nodes[j].child_count) != 0) continue;  // leaves only
+      const int cc_j = __ldcg(&p.nodes[j].child_count), par_j = __ldcg(&p.nodes[j].parent);
+      if (cc_j != 0) continue;  // leaves only
+      // the parent's child count for the arrival, loaded under the refit
+      const int need_j = par_j >= 0 ? __ldcg(&p.nodes[par_j].child_count) : cx.root_count;
       if (lane == 0) {
         CAL_PROBE(j % 16 == 0, 5000);
         double m[10];
@@ -1800,7 +1818,7 @@ __device__ __forceinline__ void calibrate_run(const BuildParams& p, int G, int c
         CAL_PROBE(j % 16 == 0, 5002);
       }
       __syncwarp();
-      cal_finish_leaf(p, cx, j, drift);
+      cal_finish_leaf(p, cx, j, par_j, need_j, drift);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) drift = smax(drift, __shfl_xor_sync(0xffffffffu, drift, off));
