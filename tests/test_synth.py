@@ -48,3 +48,28 @@ def test_kinect_and_lidar_pairs():
     r = np.linalg.norm(lt, axis=1)
     assert lt.shape == (72000, 3) and 2.0 < r.min() and r.max() < 62.0
     assert abs(LT.translation[0] - 1.0) < 0.1
+
+
+def test_pair_plans_match_the_generators():
+    """The host halves of the device frame renderer (trg_synth_*_pair_plan):
+    the same ground truth as the full generators, the first pixel / beam of
+    each frame re-cast on the host from the plan equal to the generator's
+    (the device renderer's bit-identity is tests/test_render_gpu.py)."""
+    import ctypes as C
+    from paper_1807_02587_b200 import _lib as L
+    tr = _lib()
+    H = L.host_lib()
+    d = lambda a: a.ctypes.data_as(L.dp)  # noqa: E731
+    tg, sr, T = tr.kinect_pair(4)
+    R, t, noise = np.zeros((2, 3, 3)), np.zeros((2, 3)), np.zeros(2 * 76800)
+    Rg, tg_ = np.zeros((3, 3)), np.zeros(3)
+    assert H.trg_synth_kinect_pair_plan(4, 5.0, 0.05, d(R), d(t), d(noise), d(Rg), d(tg_)) == 0
+    assert np.array_equal(Rg, T.rotation) and np.array_equal(tg_, T.translation)
+    assert np.isfinite(noise).all() and 0.9 < noise.std() < 1.1
+    lt, ls, LT = tr.lidar_pair(3)
+    R2, t2, n2, tab = np.zeros((2, 3, 3)), np.zeros((2, 3)), np.zeros(2 * 72000), np.zeros(4564)
+    assert H.trg_synth_lidar_pair_plan(3, d(R2), d(t2), d(n2), d(tab), d(Rg), d(tg_)) == 0
+    assert np.array_equal(Rg, LT.rotation) and np.array_equal(tg_, LT.translation)
+    az = np.arange(2250) * 0.16 * 0.017453292519943295
+    assert np.allclose(tab[:2250], np.cos(az), atol=1e-15) and np.allclose(tab[2250:4500], np.sin(az), atol=1e-15)
+    assert H.trg_synth_kinect_pair_plan(4, 5.0, 0.05, None, d(t), d(noise), d(Rg), d(tg_)) != 0
