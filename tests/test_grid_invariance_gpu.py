@@ -103,3 +103,26 @@ def test_fused_batch_entry_overflow_retry():
             assert _reg_key(r) == _reg_key(tr.register_clouds(g["points"], g["src"], cfg, ctx1))
     finally:
         ctx1.close()
+
+
+@pytest.mark.parametrize("variant", [("adaptive", 3), ("tree", 2)])
+def test_fused_batch_mixed_sizes_host_inputs(ctx, variant):
+    """One wave of clouds of different sizes (3k / 4k / 10k / 76.8k points),
+    host (numpy) inputs, both tree variants: every pair bit-identical to its
+    own register_clouds."""
+    tr = _tr()
+    gs = [load_golden(n) for n in ("scene3k_L3", "kinect4k_L3", "blobs1k_L2")]
+    tgs = [g["points"] for g in gs]
+    srs = [g["src"] for g in gs]
+    lt = tr.unit_normalized(tr.synthetic("lumpy", 10000, 1))
+    tgs.append(lt)
+    srs.append(tr.random_rigid_transform(15.0, 0.05, 1)(lt))
+    kt, ks, _ = tr.kinect_pair(9)
+    tgs.append(kt)
+    srs.append(ks)
+    cfg = tr.RegistrationConfig(variant=tr.Variant(*variant))
+    res = tr.register_batch(tgs, srs, cfg, ctx, 5)
+    for t, s, r in zip(tgs, srs, res):
+        one = tr.register_clouds(t, s, cfg, ctx)
+        assert _reg_key(r) == _reg_key(one)
+        assert list(r.eval_counts) == list(one.eval_counts)
