@@ -1180,7 +1180,7 @@ __device__ __forceinline__ void reduce_item(const BuildParams& p, int par, int k
   // (the record loads are issued in batches of 8 ahead of their uses: the
   // cache-global loads are ordered volatile asm, so a load-then-add loop
   // would wait a full L2 round trip per tile; the sums keep their order)
-  constexpr int B = 8;
+  constexpr int B = 16;
   const int lane = threadIdx.x & 31;
   const int t0 = p.rn[par].tile0[k], nt = p.rn[par].ntiles[k];
   double* out = p.nodered + (size_t)k * kRec;
