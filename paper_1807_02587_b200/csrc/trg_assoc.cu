@@ -55,9 +55,8 @@ __global__ void k_absmax(const double* __restrict__ p, size_t n3, unsigned long 
     bad |= !isfinite(v);
     m = fmax(m, fabs(v));
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(bits, (unsigned long long)__double_as_longlong(m));
+  m = block_max_nonneg(m);  // one atomic per block (per-warp atomics serialised on one word)
+  if (threadIdx.x == 0 && m > 0.0) atomicMax(bits, (unsigned long long)__double_as_longlong(m));
   if (bad && status) atomicCAS(status, 0, kEInval);
 }
 

@@ -1867,10 +1867,8 @@ __global__ void k_init_entries(const double* __restrict__ pts, size_t n, double*
       tile_len[t] = (int)min((size_t)kTile, n - i);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) am = fmax(am, __shfl_xor_sync(0xffffffffu, am, o));
-  if ((threadIdx.x & 31) == 0 && am > 0.0)
-    atomicMax(pmax_bits, (unsigned long long)__double_as_longlong(am));
+  am = block_max_nonneg(am);  // one atomic per block (per-warp atomics serialised on one word)
+  if (threadIdx.x == 0 && am > 0.0) atomicMax(pmax_bits, (unsigned long long)__double_as_longlong(am));
 }
 
 }  // namespace trg

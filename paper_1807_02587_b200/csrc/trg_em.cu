@@ -1014,7 +1014,7 @@ int run_em(trg_ctx* ctx, const trg_tree_dev* tree, const double* src_dev, size_t
 // bit-identical to the reference for any reduction order.
 __global__ void k_bbox(const double* __restrict__ p, size_t n, double* part, unsigned* cnt,
                        double* out) {
-  __shared__ double lo[3][256], hi[3][256];
+  __shared__ double wl[8][3], wh[8][3];  // per-warp partials (256 threads)
   __shared__ bool last;
   double l[3] = {p[0], p[1], p[2]}, h[3] = {p[0], p[1], p[2]};
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
@@ -1024,23 +1024,29 @@ __global__ void k_bbox(const double* __restrict__ p, size_t n, double* part, uns
       l[k] = (v < l[k]) ? v : l[k];
       h[k] = (h[k] < v) ? v : h[k];
     }
-  for (int k = 0; k < 3; ++k) {
-    lo[k][threadIdx.x] = l[k];
-    hi[k][threadIdx.x] = h[k];
-  }
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s)
-      for (int k = 0; k < 3; ++k) {
-        lo[k][threadIdx.x] = smin(lo[k][threadIdx.x], lo[k][threadIdx.x + s]);
-        hi[k][threadIdx.x] = smax(hi[k][threadIdx.x], hi[k][threadIdx.x + s]);
-      }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
+  // min / max are exact in any order: shuffles within the warp, then the
+  // eight warps' partials
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
     for (int k = 0; k < 3; ++k) {
-      part[6 * blockIdx.x + k] = lo[k][0];
-      part[6 * blockIdx.x + 3 + k] = hi[k][0];
+      l[k] = smin(l[k], __shfl_xor_sync(0xffffffffu, l[k], o));
+      h[k] = smax(h[k], __shfl_xor_sync(0xffffffffu, h[k], o));
+    }
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < 3; ++k) {
+      wl[threadIdx.x >> 5][k] = l[k];
+      wh[threadIdx.x >> 5][k] = h[k];
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      for (int k = 0; k < 3; ++k) {
+        l[k] = smin(l[k], wl[w][k]);
+        h[k] = smax(h[k], wh[w][k]);
+      }
+    for (int k = 0; k < 3; ++k) {
+      part[6 * blockIdx.x + k] = l[k];
+      part[6 * blockIdx.x + 3 + k] = h[k];
     }
     __threadfence();
     last = atomicAdd(cnt, 1u) == gridDim.x - 1;

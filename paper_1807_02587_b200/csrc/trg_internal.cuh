@@ -110,6 +110,21 @@ __device__ __forceinline__ void spin_guard(unsigned long long t0) {
 __device__ __forceinline__ void spin_guard_every(unsigned long long t0, unsigned& polls) {
   if ((++polls & 63u) == 0u) spin_guard(t0);
 }
+// Max of non-negative doubles over the block (result in thread 0; exact, so
+// any order); block size a multiple of 32, at most 1024.
+__device__ __forceinline__ double block_max_nonneg(double v) {
+  __shared__ double wm[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  return v;
+}
 __device__ __forceinline__ void tl_mark_any(Timeline* tl, int label) {
   const int i = atomicAdd(&tl->n, 1);
   if (i < 1024) {
