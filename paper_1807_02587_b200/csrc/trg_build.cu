@@ -270,6 +270,9 @@ struct BuildSmem {
   int item_kind[192];
   int tnode, tstart, tlen, tidx;
   int probe;  // TRG_TILE_PROBE: this CTA's tiles of the probed phase are marked
+#ifdef TRG_TILE_PROBE
+  long long pclk[10];
+#endif
   alignas(16) double ent[4][kTile + 2];  // the tile's entries (x, y, z, w): one bulk copy per tile
   uint64_t mbar;                          // completion of the tile's bulk copies
   unsigned mphase;                        // its phase parity (thread 0's copy)
@@ -289,7 +292,9 @@ struct BuildSmem {
 #ifndef TRG_TILE_PROBE_ROUND
 #define TRG_TILE_PROBE_ROUND 0
 #endif
-#define TPROBE(lab) if (sm.probe && threadIdx.x == 0) tl_mark_any(p.tl, lab)
+// raw SM clocks into shared memory (no atomics inside the tile), flushed
+// after the tile as labels 8100 + i carrying cycles since mark 8001
+#define TPROBE(lab) if (sm.probe && threadIdx.x == 0) sm.pclk[(lab) - 8000] = clock64()
 #else
 #define TPROBE(lab)
 #endif
@@ -388,12 +393,14 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
     comp_to_regs(sm.comp[cand][k], r);
     const bool live = r[0] > 0.0, pd = r[12] > 0.0;
     if (lane == 0 && live && !pd && tlen > 0) atomicCAS(p.status, 0, kEDomain);
+    if (item == 0) TPROBE(8005);
 #pragma unroll 4
     for (int e = lane; e < tlen; e += 32) {
       const double v =
           r[1] + __fma_rn(-0.5, fast_q(r + 2, r + 5, sm.ent[0][e], sm.ent[1][e], sm.ent[2][e]), r[11]);
       G.gam[item][e] = (live && pd) ? v : -INFINITY;
     }
+    if (item == 0) TPROBE(8006);
   }
   __syncthreads();
   TPROBE(8003);
@@ -481,6 +488,7 @@ __device__ void tile_comp_pass(const BuildParams& p, BuildSmem& sm, const Phase&
           acc(e + 32);
         }
         if (e < tlen) acc(e);
+        if (item == 0) TPROBE(8007);
       } else {
         for (int e = lane; e < tlen; e += 32) a[0] += G.gam[item][e];  // child mass w * gamma (gmm.cpp:355)
       }
@@ -1366,6 +1374,17 @@ __device__ __forceinline__ void build_run(const BuildParams& p, int G, int cta) 
           nent += sm.tlen;
           __syncthreads();
           TPROBE(8009);
+#ifdef TRG_TILE_PROBE
+          if (sm.probe && tid == 0)
+            for (int q = 0; q < 10; ++q)
+              if (q != 0) {
+                const int i = atomicAdd(&p.tl->n, 1);
+                if (i < 1024) {
+                  p.tl->lab[i] = 8100 + q;
+                  p.tl->t[i] = (unsigned long long)(sm.pclk[q] - sm.pclk[1]);
+                }
+              }
+#endif
         }
         grid_sync(p.bar, G);
         tl_mark(p.tl, round * 100 + ph_i);
