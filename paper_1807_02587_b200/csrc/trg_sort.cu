@@ -56,11 +56,11 @@ __global__ void k_gather_points(const double* __restrict__ pts, const unsigned* 
 // A Morton-ordered copy of pts (n points) in workspace slot `slot_pts`
 // (scratch: `slot_tmp`), queued on the context's stream; *out points to it.
 // pmax: the cloud's max |coordinate| on the device (already computed on the
-// stream).  Clouds below kSortMinPoints are used as they are.
+// stream).  Clouds in (kSortMaxSmall, kSortMinPoints) are used as they are.
 int morton_sorted_copy(trg_ctx* ctx, const double* pts, size_t n, const double* pmax, int slot_pts,
                        int slot_tmp, const double** out) {
   *out = pts;
-  if (n < kSortMinPoints || n > 0xffffffffull) return TRG_OK;
+  if ((n > kSortMaxSmall && n < kSortMinPoints) || n < 64 || n > 0xffffffffull) return TRG_OK;
   size_t temp = 0;
   unsigned* null = nullptr;
   TRG_CU(cub::DeviceRadixSort::SortPairs(nullptr, temp, null, null, null, null, (int)n, 0, 30,
