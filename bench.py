@@ -300,14 +300,20 @@ def run_b200(args):
         "clocks": clk.summary(),
     }
     if args.batch > 0:
-        out["batched"] = run_batched(args, tr, ctx, cfg, dist, dev, world)
+        try:
+            out["batched"] = run_batched(args, tr, ctx, cfg, dist, dev, world)
+        except Exception as e:  # the headline line must survive a failing side item
+            out["batched"] = {"error": f"{type(e).__name__}: {e}"}
     if args.c4:
         try:
             out["c4"] = run_c4(args, tr, ctx, dist, dev, world)
         except Exception as e:  # the headline line must survive a failing side item
             out["c4"] = {"error": f"{type(e).__name__}: {e}"}
     if args.extra and world == 1:
-        out["configs"] = {c: run_small(tr, ctx, dev, c, args.steps) for c in ("c1", "c3") if c != args.config}
+        try:
+            out["configs"] = {c: run_small(tr, ctx, dev, c, args.steps) for c in ("c1", "c3") if c != args.config}
+        except Exception as e:
+            out["configs"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.config)
     if rank == 0:
