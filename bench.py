@@ -420,7 +420,7 @@ def run_batched(args, tr, ctx, cfg, dist, dev, world):
     errs = [float(np.degrees(np.arccos(np.clip((np.trace(r.transform.rotation.T @ p[2].rotation) - 1) / 2,
                                                -1, 1)))) for r, p in zip(res, pairs)]
     out = {"workload": f"C5 slice: {args.batch} independent C2-style Kinect pairs per rank (seeds k)",
-           "pairs_per_rank": args.batch, "pairs_in_flight": args.streams or 24, "reps": reps,
+           "pairs_per_rank": args.batch, "pairs_in_flight": min(args.streams or 24, args.batch), "reps": reps,
            "value": world * args.batch * reps / dt, "unit": UNIT,
            "ms_per_batch": 1e3 * dt / reps, "timing": "host wall clock around synchronous batches",
            "converged": sum(r.converged for r in res), "median_rot_err_deg_vs_gt": float(np.median(errs))}
