@@ -1730,6 +1730,11 @@ int register_batch_fused(trg_ctx* ctx, int n_pairs, const double* const* targets
                          const size_t* n_sources, int on_device, const trg_reg_config* cfg,
                          int inflight, trg_reg_result* out) {
   TRG_TRY(validate_reg_config(cfg));
+  for (int i = 0; i < n_pairs; ++i)  // argument errors before any work
+    if (n_targets[i] == 0 || n_sources[i] == 0 || !targets[i] || !sources[i]) {
+      set_error("register_batch: pair " + std::to_string(i) + ": register: empty cloud");
+      return TRG_EINVAL;
+    }
   inflight = std::min({inflight, n_pairs, kBatchInflightMax, kMaxEmBatch});
   while ((int)ctx->workers.size() < inflight) {
     trg_ctx* w = nullptr;
@@ -1753,17 +1758,25 @@ int register_batch_fused(trg_ctx* ctx, int n_pairs, const double* const* targets
     if (cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming) != cudaSuccess) rc = TRG_ECUDA;
   if (rc == TRG_OK && cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming) != cudaSuccess)
     rc = TRG_ECUDA;
-  for (int base = 0; base < n_pairs && rc == TRG_OK; base += inflight) {
+  // every wave runs (the other pairs' results are filled when one fails);
+  // the call returns the status of the lowest-index failing pair
+  std::string first_msg;
+  for (int base = 0; base < n_pairs && rc != TRG_ECUDA; base += inflight) {
     const int m = std::min(inflight, n_pairs - base);
     std::vector<BatchSlot> sl(m);
-    rc = batch_wave(ctx, base, m, targets, n_targets, sources, n_sources, on_device, cfg, out, sl,
-                    ev, ev_main);
-    if (rc != TRG_OK) {  // nothing queued may outlive the call
+    const int rw = batch_wave(ctx, base, m, targets, n_targets, sources, n_sources, on_device, cfg,
+                              out, sl, ev, ev_main);
+    if (rw != TRG_OK) {  // nothing queued may outlive the call
       cudaStreamSynchronize(ctx->stream);
       for (int k = 0; k < m; ++k) cudaStreamSynchronize(ctx->workers[k]->stream);
+      if (rc == TRG_OK) {
+        rc = rw;
+        first_msg = trg_last_error();
+      }
     }
     for (auto& s : sl) slot_release(s);
   }
+  if (rc != TRG_OK && !first_msg.empty()) set_error(first_msg);
   for (auto e : ev)
     if (e) cudaEventDestroy(e);
   if (ev_main) cudaEventDestroy(ev_main);

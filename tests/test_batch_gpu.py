@@ -88,3 +88,22 @@ def test_register_sequence_matches_reference(ctx):
     for k in range(5):
         assert rotation_angle_between(traj[k].rotation, z["traj_R"][k]) <= 4e-4
         assert np.linalg.norm(traj[k].translation - z["traj_t"][k]) <= 4e-4 * ext
+
+
+def test_batch_failure_in_a_later_wave(ctx):
+    """A pair that fails in one wave (non-finite source) while later waves
+    still run: the error names the lowest failing pair; an empty cloud is an
+    argument error before any work; the context stays usable."""
+    tr = _tr()
+    g = load_golden("scene3k_L3")
+    bad = g["src"].copy()
+    bad[3, 0] = np.inf
+    cfg = tr.RegistrationConfig(variant=tr.Variant("adaptive", 3))
+    srcs = [g["src"], bad, g["src"], g["src"]]
+    with pytest.raises(tr.InvalidArgument, match="pair 1"):
+        tr.register_batch([g["points"]] * 4, srcs, cfg, ctx, 2)
+    with pytest.raises(tr.InvalidArgument, match="empty cloud"):
+        tr.register_batch([g["points"], g["points"][:0]], [g["src"], g["src"]], cfg, ctx, 2)
+    res = tr.register_batch([g["points"]] * 2, [g["src"]] * 2, cfg, ctx, 2)
+    one = tr.register_clouds(g["points"], g["src"], cfg, ctx)
+    assert all(np.array_equal(r.transform.rotation, one.transform.rotation) for r in res)
