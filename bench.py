@@ -390,6 +390,8 @@ def run_c4(args, tr, ctx, dist, dev, world):
             "timing": "host wall clock around synchronous registrations, max over ranks",
             "tree_build_mpoints_per_s": len(pts) / float(np.median(builds)) / 1e6,
             "em_iterations": res.iterations, "converged": res.converged,
+            "em_ms": 1e3 * res.em_seconds,
+            "ms_per_em_iteration": 1e3 * res.em_seconds / max(1, res.iterations),
             "rot_err_deg_vs_gt": ang, "parity": parity, "roofline": roof, "ranks": world,
             "note": "the reference's own register_clouds does not converge on this pose either "
                     "(50 iterations, same answer: tests/test_c4_gpu.py)"}
